@@ -1,0 +1,318 @@
+"""ORACLE TEST INFRASTRUCTURE — not product code.
+
+ctypes binding of oracle/_ref/librtnlinv_ref.so: the UNMODIFIED reference
+(/root/reference/proj/src, compiled in place by oracle/Makefile) behind the flat
+wrapper oracle/ref_capi.cpp. Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this module.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_DIR = os.path.join(HERE, "_ref")
+LIB_PATH = os.path.join(REF_DIR, "librtnlinv_ref.so")
+REFERENCE_SRC = "/root/reference/proj"
+
+
+class RefError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class _Plan(ctypes.Structure):
+    _fields_ = [
+        ("N", ctypes.c_int), ("G", ctypes.c_int), ("Gc", ctypes.c_int), ("J", ctypes.c_int),
+        ("newton_steps", ctypes.c_int), ("alpha0", ctypes.c_float), ("alpha_q", ctypes.c_float),
+        ("alpha_min", ctypes.c_float), ("cg_tol", ctypes.c_float), ("cg_max_iter", ctypes.c_int),
+        ("cg_iter_budget", ctypes.c_int), ("prev_damping", ctypes.c_float), ("gamma", ctypes.c_double),
+    ]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_int), ("A", ctypes.c_int), ("sched_l", ctypes.c_int), ("sched_o", ctypes.c_int),
+                ("chain", ctypes.c_int), ("normalize", ctypes.c_int), ("delay_samples", ctypes.c_double)]
+
+
+def build(quiet=True):
+    """Compile the reference in place (needs /root/reference; the GPU box uses the prebuilt .so)."""
+    if not os.path.isdir(REFERENCE_SRC):
+        return os.path.exists(LIB_PATH)
+    out = subprocess.run(["make", "-C", HERE, "-j8"], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + out.stdout[-4000:] + out.stderr[-4000:])
+    return True
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            build()
+        _lib = ctypes.CDLL(LIB_PATH)
+        _lib.ref_last_error.restype = ctypes.c_char_p
+    return _lib
+
+
+def _fp(a):
+    return None if a is None else a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def _dp(a):
+    return None if a is None else a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _ip(a):
+    return None if a is None else a.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+
+
+def _chk(code):
+    if code != 0:
+        raise RefError(code, lib().ref_last_error().decode())
+
+
+def _c64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.complex64))
+
+
+def plan_c(plan) -> _Plan:
+    return _Plan(plan.N, plan.G, plan.Gc, plan.J, plan.newton_steps, plan.alpha0, plan.alpha_q, plan.alpha_min,
+                 plan.cg_tol, plan.cg_max_iter, plan.cg_iter_budget, plan.prev_damping, plan.gamma)
+
+
+def make_plan(N, J):
+    from paper_1701_08361_b200 import ReconPlan
+    p = _Plan()
+    _chk(lib().ref_make_plan(N, J, ctypes.byref(p)))
+    return ReconPlan(N=p.N, gamma=p.gamma, G=p.G, Gc=p.Gc, J=p.J, newton_steps=p.newton_steps, alpha0=p.alpha0,
+                     alpha_q=p.alpha_q, alpha_min=p.alpha_min, cg_tol=p.cg_tol, cg_max_iter=p.cg_max_iter,
+                     cg_iter_budget=p.cg_iter_budget, prev_damping=p.prev_damping)
+
+
+# ---- synthetic acquisition / pre stage -------------------------------------------------
+def phantom_series(J, F, K, U, N, noise=0.0, seed=7):
+    """frames of default_phantom(J, seed): samples (F, J, K, 2N) complex64, angles (F, K)"""
+    S = 2 * N
+    samples = np.zeros((F, J, K, S), np.complex64)
+    angles = np.zeros((F, K), np.float64)
+    _chk(lib().ref_phantom_series(J, F, K, U, N, ctypes.c_double(noise), ctypes.c_uint64(seed), _fp(samples),
+                                  _dp(angles)))
+    return samples, angles
+
+
+def grid_adjoint(plan, samples, angles):
+    samples = _c64(samples)
+    angles = np.ascontiguousarray(angles, np.float64)
+    J, K, S = samples.shape
+    z = np.zeros((J, plan.G, plan.G), np.complex64)
+    _chk(lib().ref_grid_adjoint(ctypes.byref(plan_c(plan)), _fp(samples), _dp(angles), J, K, S, _fp(z)))
+    return z
+
+
+def build_psf(plan, angles, S):
+    angles = np.ascontiguousarray(angles, np.float64)
+    P = np.zeros((plan.G, plan.G), np.complex64)
+    _chk(lib().ref_build_psf(ctypes.byref(plan_c(plan)), _dp(angles), len(angles), S, _fp(P)))
+    return P
+
+
+def compress_series(samples, angles, Jv, ncal):
+    samples = _c64(samples)
+    angles = np.ascontiguousarray(angles, np.float64)
+    F, Jp, K, S = samples.shape
+    out = np.zeros((F, Jv, K, S), np.complex64)
+    energy = ctypes.c_double(0)
+    _chk(lib().ref_compress_series(_fp(samples), _dp(angles), F, Jp, K, S, Jv, ncal, _fp(out),
+                                   ctypes.byref(energy)))
+    return out, energy.value
+
+
+def bandlimited_truth_rss(J, seed, n, N):
+    out = np.zeros((N, N), np.complex64)
+    _chk(lib().ref_bandlimited_truth_rss(J, ctypes.c_uint64(seed), n, N, _fp(out)))
+    return out
+
+
+def nrmse_scaled(got, want, interior=0.45):
+    got, want = _c64(got), _c64(want)
+    v = ctypes.c_double(0)
+    _chk(lib().ref_nrmse_scaled(_fp(got), _fp(want), got.shape[0], ctypes.c_double(interior), ctypes.byref(v)))
+    return v.value
+
+
+# ---- primitives ------------------------------------------------------------------------------
+def fft(x, sign):
+    a = _c64(x).copy()
+    _chk(lib().ref_fft(_fp(a), a.shape[0], sign))
+    return a
+
+
+def fft_counts():
+    out = (ctypes.c_uint64 * 4)()
+    lib().ref_fft_counts(out)
+    return list(out)
+
+
+def fft_reset_counts():
+    lib().ref_fft_reset_counts()
+
+
+def make_weights_inv(Gc, G):
+    out = np.zeros((Gc, Gc), np.complex64)
+    _chk(lib().ref_make_weights_inv(Gc, G, _fp(out)))
+    return out
+
+
+def apply_W_inv(chat, winv, G):
+    chat, winv = _c64(chat), _c64(winv)
+    out = np.zeros((G, G), np.complex64)
+    _chk(lib().ref_apply_W_inv(_fp(chat), _fp(winv), chat.shape[0], G, _fp(out)))
+    return out
+
+
+def apply_W_invH(u, winv, Gc):
+    u, winv = _c64(u), _c64(winv)
+    out = np.zeros((Gc, Gc), np.complex64)
+    _chk(lib().ref_apply_W_invH(_fp(u), _fp(winv), u.shape[0], Gc, _fp(out)))
+    return out
+
+
+def toeplitz_apply(x, P):
+    a = _c64(x).copy()
+    _chk(lib().ref_toeplitz_apply(_fp(a), _fp(_c64(P)), a.shape[0]))
+    return a
+
+
+def make_step_cache(plan, x, P):
+    rho = np.zeros((plan.G, plan.G), np.complex64)
+    coils = np.zeros((plan.J, plan.G, plan.G), np.complex64)
+    _chk(lib().ref_make_step_cache(ctypes.byref(plan_c(plan)), _fp(_c64(x)), _fp(_c64(P)), _fp(rho), _fp(coils)))
+    return rho, coils
+
+
+def apply_normal(plan, x, dx, P, A=1):
+    out = np.zeros_like(_c64(dx))
+    _chk(lib().ref_apply_normal(ctypes.byref(plan_c(plan)), _fp(_c64(x)), _fp(_c64(dx)), _fp(_c64(P)), A, _fp(out)))
+    return out
+
+
+def cg_solve(plan, x, rhs, P, alpha, tol, max_iter):
+    out = np.zeros_like(_c64(rhs))
+    iters = ctypes.c_int(0)
+    res = np.zeros(max(max_iter, 1), np.float64)
+    _chk(lib().ref_cg_solve(ctypes.byref(plan_c(plan)), _fp(_c64(x)), _fp(_c64(rhs)), _fp(_c64(P)),
+                            ctypes.c_float(alpha), ctypes.c_float(tol), max_iter, _fp(out), ctypes.byref(iters),
+                            _dp(res)))
+    return out, iters.value, res[:iters.value].copy()
+
+
+def newton_step(plan, x, reg, alpha, z, P, cg_tol, cg_max_iter):
+    xx = _c64(x).copy()
+    iters = ctypes.c_int(0)
+    r0 = ctypes.c_double(0)
+    _chk(lib().ref_newton_step(ctypes.byref(plan_c(plan)), _fp(xx), _fp(_c64(reg)), ctypes.c_float(alpha),
+                               _fp(_c64(z)), _fp(_c64(P)), ctypes.c_float(cg_tol), cg_max_iter, ctypes.byref(iters),
+                               ctypes.byref(r0)))
+    return xx, iters.value, r0.value
+
+
+def initial_estimate(plan):
+    out = np.zeros(plan.G * plan.G + plan.J * plan.Gc * plan.Gc, np.complex64)
+    _chk(lib().ref_initial_estimate(ctypes.byref(plan_c(plan)), _fp(out)))
+    return out
+
+
+def reconstruct_frame(plan, z, P, init, reg=None, A=1):
+    img = np.zeros((plan.N, plan.N), np.complex64)
+    est = np.zeros_like(_c64(init))
+    per = np.zeros(max(plan.newton_steps, 1), np.int32)
+    secs = ctypes.c_double(0)
+    _chk(lib().ref_reconstruct_frame(ctypes.byref(plan_c(plan)), _fp(_c64(z)), _fp(_c64(P)), _fp(_c64(init)),
+                                     _fp(None if reg is None else _c64(reg)), A, _fp(img), _fp(est), _ip(per),
+                                     ctypes.byref(secs)))
+    return img, est, per[:plan.newton_steps].tolist(), secs.value
+
+
+def reconstruct_series(plan, samples, angles, T=1, A=1, sched=(1, 1), chain=True, normalize=True, plain=False):
+    samples = _c64(samples)
+    angles = np.ascontiguousarray(angles, np.float64)
+    F, J, K, S = samples.shape
+    M = plan.newton_steps
+    images = np.zeros((F, plan.N, plan.N), np.complex64)
+    audit = np.zeros((F, 5 + M), np.int32)
+    seqs = np.zeros((F, 3), np.uint64)
+    cg = np.zeros(F, np.int32)
+    secs = np.zeros(F, np.float64)
+    scale = ctypes.c_double(0)
+    o = _Opts(T, A, sched[0], sched[1], int(chain), int(normalize), 0.0)
+    _chk(lib().ref_reconstruct_series(ctypes.byref(plan_c(plan)), ctypes.byref(o), _fp(samples), _dp(angles), F, K,
+                                      S, int(plain), _fp(images), _ip(audit),
+                                      seqs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), _ip(cg), _dp(secs),
+                                      ctypes.byref(scale)))
+    return dict(images=images, audit=audit, seqs=seqs, cg_iters=cg, seconds=secs, data_scale=scale.value)
+
+
+# ---- decomposition / autotune --------------------------------------------------------------
+def partition_channels(J, A):
+    out = np.zeros(2 * max(A, 1), np.int32)
+    _chk(lib().ref_partition_channels(J, A, _ip(out)))
+    return [(int(out[2 * a]), int(out[2 * a + 1])) for a in range(A)]
+
+
+def h_choose(n, m, M, l, o, completed, late=None, delay_ms=30):
+    comp = np.ascontiguousarray(np.asarray(completed, np.int32))
+    lt = None if late is None else np.ascontiguousarray(np.asarray(list(late) + [-1], np.int32))
+    out = ctypes.c_int(0)
+    _chk(lib().ref_h_choose(n, m, M, l, o, _ip(comp), len(comp), _ip(lt), delay_ms, ctypes.byref(out)))
+    return out.value
+
+
+def legal_configs(total):
+    buf = np.zeros(2 * 128, np.int32)
+    n = lib().ref_legal_configs(total, _ip(buf), 128)
+    if n < 0:
+        raise RefError(-n, lib().ref_last_error().decode())
+    return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(n)]
+
+
+def frames_bucket(frames):
+    out = ctypes.c_int(0)
+    _chk(lib().ref_frames_bucket(frames, ctypes.byref(out)))
+    return out.value
+
+
+def _records(db):
+    rows = np.zeros((max(len(db), 1), 6), np.int32)
+    ms = np.zeros(max(len(db), 1), np.float64)
+    for i, r in enumerate(db):
+        rows[i] = [r[0], r[1], r[2], r[3], r[4], r[5]]
+        ms[i] = r[6]
+    return rows, ms
+
+
+def select_config(key, db):
+    rows, ms = _records(db)
+    k = np.asarray(key, np.int32)
+    out = np.zeros(2, np.int32)
+    _chk(lib().ref_select_config(_ip(k), _ip(rows), _dp(ms), len(db), _ip(out)))
+    return int(out[0]), int(out[1])
+
+
+def learn_step(key, db, total=8):
+    rows, ms = _records(db)
+    k = np.asarray(key, np.int32)
+    out = np.zeros(2, np.int32)
+    _chk(lib().ref_learn_step(_ip(k), _ip(rows), _dp(ms), len(db), total, _ip(out)))
+    return int(out[0]), int(out[1])

@@ -1,0 +1,368 @@
+"""B200-native NLINV (arXiv 1701.08361) hot path — Python host mirror.
+
+The product is the sm_100a library ``librtnlinv_b200.so`` (built in-tree by
+``build.py``) behind the C ABI ``include/rtnlinv_b200.h``. This module binds that
+ABI with ctypes and mirrors the reference's C++ operator / frame API
+(proj/include/rtnlinv/nlinv.hpp, fft.hpp) with the same names, argument meaning
+and error types, so the parity tests read like the reference's own tests.
+
+There is no CPU fallback: importing works anywhere, but every compute call goes
+through the CUDA library and raises ``RuntimeError`` when it is missing or no
+GPU is visible.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librtnlinv_b200.so")
+
+__all__ = [
+    "ReconPlan", "Context", "UsageError", "DataError", "SolverError", "DecompFault",
+    "make_plan", "raw_plan", "make_weights_inv", "fft_forward", "fft_inverse",
+    "fft_counts", "fft_reset_counts", "FftCtx", "est_dim", "est_split", "est_join",
+    "initial_estimate", "load_library", "library_loaded",
+]
+
+
+# ---- error taxonomy (types.hpp:12-25) --------------------------------------------
+class UsageError(RuntimeError):
+    pass
+
+
+class DataError(RuntimeError):
+    pass
+
+
+class SolverError(RuntimeError):
+    pass
+
+
+class DecompFault(RuntimeError):
+    pass
+
+
+_ERRORS = {2: UsageError, 3: DataError, 4: SolverError}
+
+
+class _Plan(ctypes.Structure):
+    _fields_ = [
+        ("N", ctypes.c_int), ("G", ctypes.c_int), ("Gc", ctypes.c_int), ("J", ctypes.c_int),
+        ("newton_steps", ctypes.c_int), ("alpha0", ctypes.c_float), ("alpha_q", ctypes.c_float),
+        ("alpha_min", ctypes.c_float), ("cg_tol", ctypes.c_float), ("cg_max_iter", ctypes.c_int),
+        ("cg_iter_budget", ctypes.c_int), ("prev_damping", ctypes.c_float), ("gamma", ctypes.c_double),
+    ]
+
+
+@dataclass
+class ReconPlan:
+    """rtnlinv::ReconPlan (planner.hpp:21-35) with the reference defaults."""
+    N: int = 0
+    gamma: float = 1.5
+    G: int = 0
+    Gc: int = 0
+    J: int = 1
+    newton_steps: int = 6
+    alpha0: float = 1.0
+    alpha_q: float = 0.5
+    alpha_min: float = 1e-6
+    cg_tol: float = 1e-3
+    cg_max_iter: int = 200
+    cg_iter_budget: int = 0
+    prev_damping: float = 1.0
+
+    def to_c(self) -> _Plan:
+        return _Plan(self.N, self.G, self.Gc, self.J, self.newton_steps, self.alpha0, self.alpha_q,
+                     self.alpha_min, self.cg_tol, self.cg_max_iter, self.cg_iter_budget,
+                     self.prev_damping, self.gamma)
+
+    @property
+    def D(self) -> int:
+        return est_dim(self)
+
+
+def raw_plan(G: int, J: int) -> ReconPlan:
+    """The tests' raw plan: N = G/2, Gc = G/4 (test_nlinv.cpp:22-29)."""
+    return ReconPlan(N=G // 2, G=G, Gc=G // 4, J=J)
+
+
+def _even_ceil(x: float) -> int:
+    import math
+    v = int(math.ceil(x - 1e-9))
+    return v + 1 if v % 2 else v
+
+
+def make_plan(N: int, J: int) -> ReconPlan:
+    """make_plan without a lookup table: G = even_ceil(3N), Gc = floor(G/4) (planner.cpp:126-140)."""
+    G = _even_ceil(2.0 * 1.5 * N)
+    return ReconPlan(N=N, J=J, G=G, gamma=G / (2.0 * N), Gc=G // 4)
+
+
+# ---- library loading ------------------------------------------------------------
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load the sm_100a library (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"CUDA library not built: {path} (run python -m paper_1701_08361_b200.build)")
+    lib = ctypes.CDLL(path)
+    f = ctypes.POINTER(ctypes.c_float)
+    d = ctypes.POINTER(ctypes.c_double)
+    i = ctypes.POINTER(ctypes.c_int)
+    vp = ctypes.c_void_p
+    sig = {
+        "rtn_abi_version": ([], ctypes.c_int),
+        "rtn_last_error": ([], ctypes.c_char_p),
+        "rtn_grid_supported": ([ctypes.c_int], ctypes.c_int),
+        "rtn_device_count": ([], ctypes.c_int),
+        "rtn_ctx_create": ([ctypes.POINTER(_Plan), ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
+        "rtn_ctx_destroy": ([vp], None),
+        "rtn_fft2": ([f, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+        "rtn_fft_set_ctx": ([ctypes.c_int], None),
+        "rtn_fft_get_ctx": ([], ctypes.c_int),
+        "rtn_fft_counts": ([ctypes.POINTER(ctypes.c_uint64)], None),
+        "rtn_fft_reset_counts": ([], None),
+        "rtn_make_weights_inv": ([ctypes.c_int, ctypes.c_int, f], ctypes.c_int),
+        "rtn_set_psf": ([vp, f], ctypes.c_int),
+        "rtn_set_data": ([vp, f], ctypes.c_int),
+        "rtn_apply_W_inv": ([vp, f, f], ctypes.c_int),
+        "rtn_apply_W_invH": ([vp, f, f], ctypes.c_int),
+        "rtn_toeplitz_apply": ([vp, f], ctypes.c_int),
+        "rtn_make_step_cache": ([vp, f, f, f], ctypes.c_int),
+        "rtn_apply_normal": ([vp, f, f], ctypes.c_int),
+        "rtn_cg_solve": ([vp, f, ctypes.c_float, ctypes.c_float, ctypes.c_int, f, i, d], ctypes.c_int),
+        "rtn_newton_step": ([vp, f, f, ctypes.c_float, ctypes.c_float, ctypes.c_int, i, d], ctypes.c_int),
+        "rtn_reconstruct_frame": ([vp, f, f, f, f, i, d], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def library_loaded() -> bool:
+    return _lib is not None
+
+
+def _check(status: int):
+    if status == 0:
+        return
+    msg = _lib.rtn_last_error().decode(errors="replace")
+    raise _ERRORS.get(status, RuntimeError)(msg)
+
+
+def _fp(a: Optional[np.ndarray]):
+    if a is None:
+        return None
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def _c64(a, shape=None) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.complex64))
+    if shape is not None and a.size != int(np.prod(shape)):
+        raise UsageError(f"expected {int(np.prod(shape))} complex entries, got {a.size}")
+    return a
+
+
+# ---- Estimate layout (nlinv.hpp:21-24) -------------------------------------------
+def est_dim(plan: ReconPlan) -> int:
+    return plan.G * plan.G + plan.J * plan.Gc * plan.Gc
+
+
+def est_split(e: np.ndarray, plan: ReconPlan):
+    """flat estimate -> (rho G x G, chat J x Gc x Gc) views"""
+    G, Gc, J = plan.G, plan.Gc, plan.J
+    return e[:G * G].reshape(G, G), e[G * G:].reshape(J, Gc, Gc)
+
+
+def est_join(rho: np.ndarray, chat: np.ndarray) -> np.ndarray:
+    return np.concatenate([np.asarray(rho, np.complex64).ravel(), np.asarray(chat, np.complex64).ravel()])
+
+
+def initial_estimate(plan: ReconPlan) -> np.ndarray:
+    """rho = 1 on the field-of-view window, coils 0 (nlinv.cpp:60-70)"""
+    G = plan.G
+    L = G // 2
+    lo = (G - L) // 2
+    rho = np.zeros((G, G), np.complex64)
+    rho[lo:lo + L, lo:lo + L] = 1.0
+    return est_join(rho, np.zeros((plan.J, plan.Gc, plan.Gc), np.complex64))
+
+
+# ---- fft.hpp -----------------------------------------------------------------------
+class FftCtx:
+    other, normal_op, setup, bench = 0, 1, 2, 3
+
+
+def _fft(x: np.ndarray, sign: int) -> np.ndarray:
+    lib = load_library()
+    a = _c64(x).copy()
+    n = a.shape[0]
+    _check(lib.rtn_fft2(_fp(a), n, sign))
+    return a
+
+
+def fft_forward(x: np.ndarray) -> np.ndarray:
+    """centered unitary forward 2D transform (fft::forward)"""
+    return _fft(x, -1)
+
+
+def fft_inverse(x: np.ndarray) -> np.ndarray:
+    return _fft(x, +1)
+
+
+def fft_counts():
+    lib = load_library()
+    out = (ctypes.c_uint64 * 4)()
+    lib.rtn_fft_counts(out)
+    return {"other": out[0], "normal_op": out[1], "setup": out[2], "bench": out[3]}
+
+
+def fft_reset_counts():
+    load_library().rtn_fft_reset_counts()
+
+
+class CtxScope:
+    """fft::CtxScope"""
+
+    def __init__(self, ctx: int):
+        self.ctx = ctx
+
+    def __enter__(self):
+        lib = load_library()
+        self.prev = lib.rtn_fft_get_ctx()
+        lib.rtn_fft_set_ctx(self.ctx)
+
+    def __exit__(self, *exc):
+        load_library().rtn_fft_set_ctx(self.prev)
+
+
+def make_weights_inv(Gc: int, G: int) -> np.ndarray:
+    lib = load_library()
+    out = np.zeros((max(Gc, 1), max(Gc, 1)), np.complex64)
+    _check(lib.rtn_make_weights_inv(Gc, G, _fp(out)))
+    return out
+
+
+# ---- device context -------------------------------------------------------------------
+@dataclass
+class FrameResult:
+    image: np.ndarray
+    est: np.ndarray
+    cg_per_step: list = field(default_factory=list)
+    cg_iters: int = 0
+    seconds: float = 0.0
+
+
+class Context:
+    """One plan on one GPU: owns the device buffers and the CUDA stream."""
+
+    def __init__(self, plan: ReconPlan, device: int = 0):
+        self.lib = load_library()
+        self.plan = plan
+        self._h = ctypes.c_void_p()
+        c = plan.to_c()
+        _check(self.lib.rtn_ctx_create(ctypes.byref(c), device, ctypes.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            self.lib.rtn_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def D(self) -> int:
+        return est_dim(self.plan)
+
+    def set_psf(self, P):
+        P = _c64(P, (self.plan.G, self.plan.G))
+        _check(self.lib.rtn_set_psf(self._h, _fp(P)))
+
+    def set_data(self, z):
+        z = _c64(z, (self.plan.J, self.plan.G, self.plan.G))
+        _check(self.lib.rtn_set_data(self._h, _fp(z)))
+
+    def apply_W_inv(self, chat):
+        chat = _c64(chat, (self.plan.Gc, self.plan.Gc))
+        out = np.zeros((self.plan.G, self.plan.G), np.complex64)
+        _check(self.lib.rtn_apply_W_inv(self._h, _fp(chat), _fp(out)))
+        return out
+
+    def apply_W_invH(self, u):
+        u = _c64(u, (self.plan.G, self.plan.G))
+        out = np.zeros((self.plan.Gc, self.plan.Gc), np.complex64)
+        _check(self.lib.rtn_apply_W_invH(self._h, _fp(u), _fp(out)))
+        return out
+
+    def toeplitz_apply(self, x):
+        x = _c64(x, (self.plan.G, self.plan.G)).copy()
+        _check(self.lib.rtn_toeplitz_apply(self._h, _fp(x)))
+        return x.reshape(self.plan.G, self.plan.G)
+
+    def make_step_cache(self, x):
+        x = _c64(x, (self.D,))
+        G, J = self.plan.G, self.plan.J
+        rho = np.zeros((G, G), np.complex64)
+        coils = np.zeros((J, G, G), np.complex64)
+        _check(self.lib.rtn_make_step_cache(self._h, _fp(x), _fp(rho), _fp(coils)))
+        return rho, coils
+
+    def apply_normal(self, dx):
+        dx = _c64(dx, (self.D,))
+        out = np.zeros(self.D, np.complex64)
+        _check(self.lib.rtn_apply_normal(self._h, _fp(dx), _fp(out)))
+        return out
+
+    def cg_solve(self, rhs, alpha: float, tol: float, max_iter: int):
+        rhs = _c64(rhs, (self.D,))
+        x = np.zeros(self.D, np.complex64)
+        iters = ctypes.c_int(0)
+        res = np.zeros(max(max_iter, 1), np.float64)
+        _check(self.lib.rtn_cg_solve(self._h, _fp(rhs), alpha, tol, max_iter, _fp(x), ctypes.byref(iters),
+                                     res.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return x, iters.value, res[:iters.value].copy()
+
+    def newton_step(self, x, reg, alpha: float, cg_tol: float, cg_max_iter: int):
+        """returns (x_new, cg_iters, residual0); x is not modified"""
+        x = _c64(x, (self.D,)).copy()
+        reg = _c64(reg, (self.D,))
+        iters = ctypes.c_int(0)
+        r0 = ctypes.c_double(0)
+        _check(self.lib.rtn_newton_step(self._h, _fp(x), _fp(reg), alpha, cg_tol, cg_max_iter,
+                                        ctypes.byref(iters), ctypes.byref(r0)))
+        return x, iters.value, r0.value
+
+    def reconstruct_frame(self, init, reg=None) -> FrameResult:
+        init = _c64(init, (self.D,))
+        regc = None if reg is None else _c64(reg, (self.D,))
+        N = self.plan.N
+        img = np.zeros((N, N), np.complex64)
+        est = np.zeros(self.D, np.complex64)
+        per = (ctypes.c_int * max(self.plan.newton_steps, 1))()
+        secs = ctypes.c_double(0)
+        _check(self.lib.rtn_reconstruct_frame(self._h, _fp(init), _fp(regc), _fp(img), _fp(est), per,
+                                              ctypes.byref(secs)))
+        cg = [per[m] for m in range(self.plan.newton_steps)]
+        return FrameResult(img, est, cg, sum(cg), secs.value)

@@ -1,0 +1,51 @@
+"""Build the sm_100a extension in-tree (paper_1701_08361_b200/librtnlinv_b200.so).
+
+The product library is plain nvcc output (no torch extension): the C-ABI in
+include/rtnlinv_b200.h is its only interface. Flags: sm_100a only, -lineinfo for
+ncu source mapping, and deliberately NO fast-math / FTZ: the W^-1 weights reach
+the subnormal range (nlinv.cpp:101-117, test_nlinv.cpp:133-137).
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "librtnlinv_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+SOURCES = ["engine.cu", "capi.cpp"]
+FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++20",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=default",
+    "-shared", "-Xlinker", "-Bsymbolic",
+    "--expt-relaxed-constexpr",
+]
+
+
+def needs_build():
+    if not os.path.exists(OUT):
+        return True
+    t = os.path.getmtime(OUT)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps.append(os.path.join(HERE, "..", "include", "rtnlinv_b200.h"))
+    deps.append(os.path.abspath(__file__))
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def build(force=False, verbose=False):
+    if not force and not needs_build():
+        return OUT
+    cmd = [NVCC] + FLAGS + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", OUT + ".tmp", "-lcudart"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(OUT + ".tmp", OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(OUT)

@@ -1,0 +1,784 @@
+// Engine: device buffers, size dispatch and kernel sequencing for one plan.
+#include "engine.hpp"
+
+#include <atomic>
+#include <cstddef>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numbers>
+#include <string>
+
+#include "kernels_impl.cuh"
+
+namespace rtnb {
+
+// ------------------------------------------------------------------------------
+// errors, FFT accounting
+// ------------------------------------------------------------------------------
+
+void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(5, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+std::atomic<uint64_t> g_counts[4];
+thread_local int t_ctx = CTX_OTHER;
+}  // namespace
+
+int fft_current_ctx() { return t_ctx; }
+void fft_set_ctx(int c) { t_ctx = c; }
+void fft_book(int ctx, uint64_t n) { g_counts[ctx & 3].fetch_add(n, std::memory_order_relaxed); }
+uint64_t fft_count(int ctx) { return g_counts[ctx & 3].load(); }
+uint64_t fft_count_total() {
+  uint64_t t = 0;
+  for (auto& c : g_counts) t += c.load();
+  return t;
+}
+void fft_reset_counts() {
+  for (auto& c : g_counts) c.store(0);
+}
+
+// ------------------------------------------------------------------------------
+// small pointwise kernels for the op-level primitives
+// ------------------------------------------------------------------------------
+
+namespace {
+
+__global__ void k_pad_weight(const float2* __restrict__ chat, const float* __restrict__ winv, int Gc,
+                             int G, float2* __restrict__ out) {
+  const int off = G / 2 - Gc / 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < G * G; e += gridDim.x * blockDim.x) {
+    const int r = e / G - off, c = e % G - off;
+    float2 v = make_float2(0.f, 0.f);
+    if (r >= 0 && r < Gc && c >= 0 && c < Gc) {
+      const float w = winv[r * Gc + c];
+      const float2 x = chat[r * Gc + c];
+      v = make_float2(x.x * w, x.y * w);
+    }
+    out[e] = v;
+  }
+}
+
+__global__ void k_crop_weight(const float2* __restrict__ in, const float* __restrict__ winv, int Gc,
+                              int G, float2* __restrict__ out) {
+  const int off = G / 2 - Gc / 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < Gc * Gc; e += gridDim.x * blockDim.x) {
+    const int r = e / Gc, c = e % Gc;
+    const float2 x = in[(size_t)(r + off) * G + c + off];
+    const float w = winv[e];
+    out[e] = make_float2(x.x * w, x.y * w);
+  }
+}
+
+__global__ void k_mask(float2* __restrict__ x, int G) {
+  const int L = G / 2, lo = (G - L) / 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < G * G; e += gridDim.x * blockDim.x) {
+    const int r = e / G, c = e % G;
+    if (!(r >= lo && r < lo + L && c >= lo && c < lo + L)) x[e] = make_float2(0.f, 0.f);
+  }
+}
+
+__global__ void k_mul(float2* __restrict__ x, const float2* __restrict__ P, int n) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const float2 a = x[e], b = P[e];
+    x[e] = make_float2(__fsub_rn(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)),
+                       __fadd_rn(__fmul_rn(a.x, b.y), __fmul_rn(a.y, b.x)));
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------
+// size dispatch
+// ------------------------------------------------------------------------------
+
+struct Engine::Ops {
+  int G = 0, N1 = 0, N2 = 0, LPB = 0;
+  size_t smem = 0;
+  void (*colA)(cudaStream_t, int, Dims, const float*, const float2*, const float2*, float2*, int, int,
+               const DevState*, int) = nullptr;
+  void (*rows1)(cudaStream_t, int, Dims, int, const float2*, const float2*, const float2*, const float2*,
+                const float2*, float2*, float2*, const float2*, float2*, const DevState*, int) = nullptr;
+  void (*colsT)(cudaStream_t, int, Dims, const float2*, const float2*, float2*, const DevState*, int) = nullptr;
+  void (*rows2)(cudaStream_t, int, Dims, int, const float2*, const float2*, const float2*, const float2*,
+                const float2*, float2*, float2*, double*, DevState*, int) = nullptr;
+  void (*colsW)(cudaStream_t, int, Dims, ColsWArgs, const float*, const float2*, const float2*,
+                const float2*, const float2*, const float2*, int, double*, DevState*, CrScalars,
+                int) = nullptr;
+  void (*fft)(cudaStream_t, int, int, float2*, int, int, const float2*, float) = nullptr;
+};
+
+namespace {
+
+template <int N1, int N2>
+struct Inst {
+  using Geo = LineGeom<N1, N2, 16>;
+  static constexpr size_t kSmem = sizeof(float2) * Geo::SMEM_FLOAT2;
+
+  static void set_attrs() {
+    const int s = static_cast<int>(kSmem);
+    check_cuda(cudaFuncSetAttribute(k_colA<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colA");
+    check_cuda(cudaFuncSetAttribute(k_rows1<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr rows1");
+    check_cuda(cudaFuncSetAttribute(k_colsT<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsT");
+    check_cuda(cudaFuncSetAttribute(k_rows2<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr rows2");
+    check_cuda(cudaFuncSetAttribute(k_colsW<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsW");
+    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
+    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, +1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr ifft");
+  }
+
+  static Engine::Ops make();
+};
+
+}  // namespace
+
+template <int N1, int N2>
+Engine::Ops Inst<N1, N2>::make() {
+  Engine::Ops o;
+  o.G = N1 * N2;
+  o.N1 = N1;
+  o.N2 = N2;
+  o.LPB = Geo::LPB;
+  o.smem = kSmem;
+  o.colA = [](cudaStream_t s, int grid, Dims d, const float* winv, const float2* tw, const float2* chat,
+              float2* U, int r0, int nr, const DevState* st, int h) {
+    k_colA<Geo><<<grid, kThreads, kSmem, s>>>(d, winv, tw, chat, U, r0, nr, st, h);
+  };
+  o.rows1 = [](cudaStream_t s, int grid, Dims d, int mode, const float2* tw, const float2* U,
+               const float2* coils, const float2* rhom, const float2* drho, float2* V, float2* coils_out,
+               const float2* rho_src, float2* rhom_out, const DevState* st, int h) {
+    k_rows1<Geo><<<grid, kThreads, kSmem, s>>>(d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
+                                                rhom_out, st, h);
+  };
+  o.colsT = [](cudaStream_t s, int grid, Dims d, const float2* tw, const float2* P, float2* V,
+               const DevState* st, int h) {
+    k_colsT<Geo><<<grid, kThreads, kSmem, s>>>(d, tw, P, V, st, h);
+  };
+  o.rows2 = [](cudaStream_t s, int grid, Dims d, int mode, const float2* tw, const float2* V,
+               const float2* coils, const float2* rhom, const float2* z, float2* RC, float2* Y,
+               double* partials, DevState* st, int h) {
+    k_rows2<Geo><<<grid, kThreads, kSmem, s>>>(d, mode, tw, V, coils, rhom, z, RC, Y, partials, st, h);
+  };
+  o.colsW = [](cudaStream_t s, int grid, Dims d, ColsWArgs a, const float* winv, const float2* tw,
+               const float2* Y, const float2* RC, const float2* coils, const float2* z, int nbw,
+               double* partials, DevState* st, CrScalars cr, int h) {
+    k_colsW<Geo><<<grid, kThreads, kSmem, s>>>(d, a, winv, tw, Y, RC, coils, z, nbw, partials, st, cr, h);
+  };
+  o.fft = [](cudaStream_t s, int grid, int sign, float2* data, int batch, int axis, const float2* tw,
+             float scale) {
+    if (sign < 0) {
+      k_fft_pass<Geo, -1><<<grid, kThreads, kSmem, s>>>(data, batch, axis, tw, scale);
+    } else {
+      k_fft_pass<Geo, +1><<<grid, kThreads, kSmem, s>>>(data, batch, axis, tw, scale);
+    }
+  };
+  return o;
+}
+
+namespace {
+
+struct Registry {
+  std::mutex mu;
+  std::vector<Engine::Ops> ops;
+  std::vector<std::pair<int, void (*)()>> attrs;  // per G, run once per device
+  std::vector<std::vector<int>> attrs_done;       // [device] -> list of G
+  bool tw_done[64] = {};
+  std::vector<std::pair<std::pair<int, int>, float2*>> twG;  // (device, G) -> table
+  std::vector<std::pair<std::pair<int, int>, double2*>> twD;  // (device, n*sign) -> direct table
+};
+
+Registry& registry() {
+  static Registry* r = [] {
+    auto* reg = new Registry;
+#define RTNB_INST(a, b)                                 \
+  reg->ops.push_back(Inst<a, b>::make());               \
+  reg->attrs.push_back({a * b, &Inst<a, b>::set_attrs});
+    RTNB_INST(4, 4)
+    RTNB_INST(4, 6)
+    RTNB_INST(4, 8)
+    RTNB_INST(6, 8)
+    RTNB_INST(8, 8)
+    RTNB_INST(8, 9)
+    RTNB_INST(8, 12)
+    RTNB_INST(8, 16)
+    RTNB_INST(10, 16)
+    RTNB_INST(12, 16)
+    RTNB_INST(16, 16)
+    RTNB_INST(16, 20)
+    RTNB_INST(16, 24)
+    RTNB_INST(16, 32)
+#undef RTNB_INST
+    return reg;
+  }();
+  return *r;
+}
+
+// per-device one-time setup: small-DFT constant table and kernel attributes for G
+const Engine::Ops* ops_for(int G, int dev) {
+  Registry& r = registry();
+  std::lock_guard<std::mutex> lock(r.mu);
+  const Engine::Ops* found = nullptr;
+  for (const auto& o : r.ops) {
+    if (o.G == G) found = &o;
+  }
+  if (!found) return nullptr;
+  if (dev < 0 || dev >= 64) fail(2, "device index out of range");
+  if (!r.tw_done[dev]) {
+    float2 tw[528];
+    for (int n = 1; n <= 32; ++n) {
+      for (int k = 0; k < n; ++k) {
+        const double a = -2.0 * std::numbers::pi * k / n;
+        tw[small_tw_offset(n) + k] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+      }
+    }
+    check_cuda(cudaMemcpyToSymbol(c_small_tw, tw, sizeof(tw)), "upload small twiddles");
+    r.tw_done[dev] = true;
+  }
+  if (r.attrs_done.size() <= static_cast<size_t>(dev)) r.attrs_done.resize(dev + 1);
+  bool done = false;
+  for (int g : r.attrs_done[dev]) done = done || g == G;
+  if (!done) {
+    for (auto& a : r.attrs) {
+      if (a.first == G) a.second();
+    }
+    r.attrs_done[dev].push_back(G);
+  }
+  return found;
+}
+
+float2* twiddles_for(int G, int dev) {
+  Registry& r = registry();
+  std::lock_guard<std::mutex> lock(r.mu);
+  for (auto& e : r.twG) {
+    if (e.first == std::make_pair(dev, G)) return e.second;
+  }
+  std::vector<float2> h(static_cast<size_t>(G));
+  for (int e = 0; e < G; ++e) {
+    const double a = -2.0 * std::numbers::pi * e / G;
+    h[static_cast<size_t>(e)] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+  }
+  float2* d = nullptr;
+  check_cuda(cudaMalloc(&d, sizeof(float2) * G), "twiddle alloc");
+  check_cuda(cudaMemcpy(d, h.data(), sizeof(float2) * G, cudaMemcpyHostToDevice), "twiddle upload");
+  r.twG.push_back({{dev, G}, d});
+  return d;
+}
+
+double2* direct_table(int n, int sign, int dev) {
+  Registry& r = registry();
+  std::lock_guard<std::mutex> lock(r.mu);
+  const int key = n * (sign < 0 ? -1 : 1);
+  for (auto& e : r.twD) {
+    if (e.first == std::make_pair(dev, key)) return e.second;
+  }
+  std::vector<double2> h(static_cast<size_t>(n));
+  for (int e = 0; e < n; ++e) {
+    const double a = (sign < 0 ? -2.0 : 2.0) * std::numbers::pi * e / n;
+    h[static_cast<size_t>(e)] = make_double2(std::cos(a), std::sin(a));
+  }
+  double2* d = nullptr;
+  check_cuda(cudaMalloc(&d, sizeof(double2) * n), "direct table alloc");
+  check_cuda(cudaMemcpy(d, h.data(), sizeof(double2) * n, cudaMemcpyHostToDevice), "direct table upload");
+  r.twD.push_back({{dev, key}, d});
+  return d;
+}
+
+int blocks_for(long long n, int cap) {
+  long long b = (n + kThreads - 1) / kThreads;
+  if (b < 1) b = 1;
+  return static_cast<int>(b > cap ? cap : b);
+}
+
+}  // namespace
+
+bool grid_supported(int G) {
+  for (const auto& o : registry().ops) {
+    if (o.G == G) return true;
+  }
+  return false;
+}
+
+void fft2_device(float2* data, int n, int batch, int sign, cudaStream_t s) {
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "get device");
+  const Engine::Ops* ops = (n % 2 == 0) ? ops_for(n, dev) : nullptr;
+  if (ops) {
+    const float2* tw = twiddles_for(n, dev);
+    const int grid = batch * ((n + ops->LPB - 1) / ops->LPB);
+    ops->fft(s, grid, sign, data, batch, 1, tw, 1.0f);
+    ops->fft(s, grid, sign, data, batch, 0, tw, 1.0f / n);
+  } else {
+    // direct centered DFT per line (any side, including odd; fft.cpp:37-40 convention)
+    const double2* tw = direct_table(n, sign, dev);
+    float2* tmp = nullptr;
+    check_cuda(cudaMallocAsync(&tmp, sizeof(float2) * n * n * batch, s), "fft tmp");
+    k_dft_direct<<<batch * n, 128, sizeof(float2) * n, s>>>(data, tmp, n, batch, 1, tw, 1.0f);
+    k_dft_direct<<<batch * n, 128, sizeof(float2) * n, s>>>(tmp, data, n, batch, 0, tw, 1.0f / n);
+    check_cuda(cudaFreeAsync(tmp, s), "fft tmp free");
+  }
+  check_cuda(cudaGetLastError(), "fft launch");
+}
+
+// ------------------------------------------------------------------------------
+// Engine
+// ------------------------------------------------------------------------------
+
+Engine::Engine(const Plan& plan, int device) : plan_(plan), dev_(device) {
+  if (plan.G < 2 || plan.G % 2 != 0) fail(2, "plan: grid side G must be even and >= 2");
+  if (plan.Gc < 1 || plan.Gc > plan.G) fail(2, "make_weights_inv: need 1 <= Gc <= G");
+  if (plan.J < 1) fail(2, "plan: need at least one channel");
+  if (plan.N < 1 || plan.N > plan.G) fail(2, "plan: image side N must be in [1, G]");
+  if (plan.newton_steps < 0 || plan.newton_steps > kMaxSteps) fail(2, "plan: newton_steps out of range");
+  check_cuda(cudaSetDevice(dev_), "set device");
+  ops_ = ops_for(plan.G, dev_);
+  if (!ops_) fail(2, "grid side " + std::to_string(plan.G) + " is not supported by the sm_100a line FFT");
+  dims_.G = plan.G;
+  dims_.Gc = plan.Gc;
+  dims_.J = plan.J;
+  dims_.L = plan.G / 2;
+  dims_.lo = (plan.G - dims_.L) / 2;
+  dims_.off = plan.G / 2 - plan.Gc / 2;
+  dims_.N = plan.N;
+  dims_.invG = 1.0f / static_cast<float>(plan.G);
+  D_ = plan.G * plan.G + plan.J * plan.Gc * plan.Gc;
+  check_cuda(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
+  alloc();
+}
+
+Engine::~Engine() {
+  cudaSetDevice(dev_);
+  cudaStreamSynchronize(s_);
+  void* bufs[] = {winv_, P_, z_, x_, xcg_, r_, p_, ap_, ar_, est_scratch_[0], est_scratch_[1],
+                  est_scratch_[2], coils_, rhom_, U_, V_, RC_, Y_, gbuf_, img_, partials_, st_, cr_buf_};
+  for (void* b : bufs) {
+    if (b) cudaFree(b);
+  }
+  if (st_host_) cudaFreeHost(st_host_);
+  if (s_) cudaStreamDestroy(s_);
+}
+
+void Engine::alloc() {
+  const size_t G2 = static_cast<size_t>(plan_.G) * plan_.G;
+  const size_t J = static_cast<size_t>(plan_.J);
+  const size_t L = static_cast<size_t>(dims_.L);
+  auto c2 = [](float2** p, size_t n, const char* w) {
+    check_cuda(cudaMalloc(p, sizeof(float2) * std::max<size_t>(n, 1)), w);
+    check_cuda(cudaMemset(*p, 0, sizeof(float2) * std::max<size_t>(n, 1)), w);
+  };
+  // W^-1 weights in double, stored as float (make_weights_inv, nlinv.cpp:101-117)
+  winv_host_.assign(static_cast<size_t>(plan_.Gc) * plan_.Gc, 0.f);
+  const int c = plan_.Gc / 2;
+  for (int r = 0; r < plan_.Gc; ++r) {
+    for (int q = 0; q < plan_.Gc; ++q) {
+      const double ky = (r - c) / static_cast<double>(plan_.G);
+      const double kx = (q - c) / static_cast<double>(plan_.G);
+      const double w = std::pow(1.0 + 880.0 * (kx * kx + ky * ky), 16.0);
+      winv_host_[static_cast<size_t>(r) * plan_.Gc + q] = static_cast<float>(1.0 / w);
+    }
+  }
+  check_cuda(cudaMalloc(&winv_, sizeof(float) * winv_host_.size()), "winv");
+  check_cuda(cudaMemcpy(winv_, winv_host_.data(), sizeof(float) * winv_host_.size(), cudaMemcpyHostToDevice),
+             "winv upload");
+  twG_ = twiddles_for(plan_.G, dev_);
+  c2(&P_, G2, "psf");
+  c2(&z_, J * G2, "z");
+  for (float2** b : {&x_, &xcg_, &r_, &p_, &ap_, &ar_, &est_scratch_[0], &est_scratch_[1], &est_scratch_[2]}) {
+    c2(b, static_cast<size_t>(D_), "estimate");
+  }
+  c2(&coils_, J * G2, "coils");
+  c2(&rhom_, G2, "rho");
+  c2(&U_, J * plan_.G * plan_.Gc, "U");
+  c2(&V_, J * L * plan_.G, "V");
+  c2(&RC_, J * L * L, "RC");
+  c2(&Y_, J * L * plan_.Gc, "Y");
+  c2(&gbuf_, G2, "scratch");
+  c2(&img_, static_cast<size_t>(plan_.N) * plan_.N, "image");
+  vec_grid_ = blocks_for(D_, 148 * 4);
+  nbr_ = blocks_for(static_cast<long long>(G2) / 4, 148);
+  const int max_grid = std::max(vec_grid_, plan_.J * ((plan_.G + ops_->LPB - 1) / ops_->LPB) + nbr_ + 8);
+  check_cuda(cudaMalloc(&partials_, sizeof(double) * 2 * max_grid), "partials");
+  check_cuda(cudaMalloc(&st_, sizeof(DevState)), "state");
+  check_cuda(cudaMemset(st_, 0, sizeof(DevState)), "state");
+  check_cuda(cudaMallocHost(&st_host_, sizeof(DevState)), "state mirror");
+  std::memset(st_host_, 0, sizeof(DevState));
+  ensure_cr_capacity(std::max({plan_.cg_max_iter, plan_.cg_iter_budget, 1}));
+}
+
+void Engine::ensure_cr_capacity(int max_iter) {
+  if (max_iter + 2 <= cr_cap_) return;
+  if (cr_buf_) {
+    check_cuda(cudaStreamSynchronize(s_), "sync");
+    cudaFree(cr_buf_);
+  }
+  cr_cap_ = max_iter + 2;
+  check_cuda(cudaMalloc(&cr_buf_, sizeof(double) * 3 * cr_cap_), "cr scalars");
+  check_cuda(cudaMemset(cr_buf_, 0, sizeof(double) * 3 * cr_cap_), "cr scalars");
+  cr_.rar = cr_buf_;
+  cr_.ap2 = cr_buf_ + cr_cap_;
+  cr_.rn = cr_buf_ + 2 * cr_cap_;
+}
+
+void Engine::sync() { check_cuda(cudaStreamSynchronize(s_), "stream sync"); }
+
+void Engine::read_state() {
+  check_cuda(cudaMemcpyAsync(st_host_, st_, sizeof(DevState), cudaMemcpyDeviceToHost, s_), "state read");
+  sync();
+}
+
+void Engine::raise_status(const char* where) {
+  if (st_host_->status == ST_SOLVER) fail(4, std::string(where) + ": iteration diverged or produced non-finite values");
+  if (st_host_->status != ST_OK) fail(st_host_->status, std::string(where) + ": device error");
+}
+
+void Engine::set_psf(const float* P) {
+  check_cuda(cudaMemcpyAsync(P_, P, sizeof(float2) * plan_.G * plan_.G, cudaMemcpyHostToDevice, s_), "psf upload");
+  sync();
+}
+void Engine::set_data(const float* z) {
+  check_cuda(cudaMemcpyAsync(z_, z, sizeof(float2) * plan_.J * plan_.G * plan_.G, cudaMemcpyHostToDevice, s_),
+             "data upload");
+  sync();
+}
+void Engine::set_psf_device(const float2* P) {
+  check_cuda(cudaMemcpyAsync(P_, P, sizeof(float2) * plan_.G * plan_.G, cudaMemcpyDeviceToDevice, s_), "psf copy");
+}
+void Engine::set_data_device(const float2* z) {
+  check_cuda(cudaMemcpyAsync(z_, z, sizeof(float2) * plan_.J * plan_.G * plan_.G, cudaMemcpyDeviceToDevice, s_),
+             "data copy");
+}
+
+// ---- enqueue helpers ---------------------------------------------------------
+
+void Engine::enq_step_begin(int m) {
+  k_step_begin<<<1, 32, 0, s_>>>(st_, m);
+}
+
+void Engine::enq_decode(const float2* est) {
+  const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
+  const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB;
+  ops_->colA(s_, J * tGc, dims_, winv_, twG_, est + static_cast<size_t>(G) * G, U_, 0, G, st_, 0);
+  ops_->rows1(s_, J * tG, dims_, R1_DECODE, twG_, U_, nullptr, nullptr, nullptr, nullptr, coils_, est, rhom_,
+              st_, 0);
+}
+
+void Engine::enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt) {
+  const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
+  const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
+  ops_->colA(s_, J * tGc, dims_, winv_, twG_, dx + static_cast<size_t>(G) * G, U_, dims_.lo, dims_.L, st_,
+             use_halt);
+  ops_->rows1(s_, J * tL, dims_, R1_OP, twG_, U_, coils_, rhom_, dx, V_, nullptr, nullptr, nullptr, st_, use_halt);
+  ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, use_halt);
+  ops_->rows2(s_, J * tL, dims_, R2_OP, twG_, V_, coils_, rhom_, z_, RC_, Y_, partials_, st_, use_halt);
+  ColsWArgs a{};
+  a.mode = cw_mode;
+  a.alpha = alpha;
+  a.dot_slot = dot_slot;
+  a.dx = dx;
+  a.out = out;
+  const int nbw = J * tGc;
+  ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RC_, coils_, z_, nbw, partials_, st_, cr_, use_halt);
+}
+
+void Engine::enq_setup(const float2* x, const float2* reg, float alpha) {
+  const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
+  const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
+  enq_decode(x);
+  ops_->rows1(s_, J * tL, dims_, R1_SETUP, twG_, U_, coils_, rhom_, nullptr, V_, nullptr, nullptr, nullptr, st_, 0);
+  ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, 0);
+  ops_->rows2(s_, J * tL, dims_, R2_SETUP, twG_, V_, coils_, rhom_, z_, RC_, Y_, partials_, st_, 0);
+  ColsWArgs a{};
+  a.mode = CW_SETUP;
+  a.a_x = static_cast<float>(-static_cast<double>(alpha));
+  a.a_reg = static_cast<float>(static_cast<double>(alpha) * plan_.prev_damping);
+  a.dot_slot = -1;
+  a.x = x;
+  a.reg = reg;
+  a.out = r_;
+  a.out2 = p_;
+  a.out3 = xcg_;
+  const int nbw = J * tGc;
+  ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RC_, coils_, z_, nbw, partials_, st_, cr_, 0);
+}
+
+void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
+  ensure_cr_capacity(cap);
+  enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1);
+  k_cr_prime<<<vec_grid_, kThreads, 0, s_>>>(D_, ap_, ar_, partials_, st_, cr_);
+  for (int it = 1; it <= cap; ++it) {
+    k_cr_xr<<<vec_grid_, kThreads, 0, s_>>>(D_, xcg_, r_, p_, ap_, partials_, st_, cr_, it, tol);
+    if (it == cap) break;
+    if (sync_each) {
+      read_state();
+      if (st_host_->status || st_host_->cr_halt) break;
+    }
+    enq_apply(r_, ar_, CW_OPALPHA, alpha, it, 1);
+    k_cr_pap<<<vec_grid_, kThreads, 0, s_>>>(D_, p_, ap_, r_, ar_, partials_, st_, cr_, it);
+  }
+}
+
+void Engine::enq_newton_step(int m, float2* x, const float2* reg, float alpha, float tol, int cap,
+                             bool sync_each) {
+  enq_step_begin(m);
+  {
+    fft_book(CTX_SETUP, 4ull * plan_.J);
+    enq_setup(x, reg, alpha);
+  }
+  if (cap >= 1) {
+    if (sync_each) {
+      read_state();
+      raise_status("cg_solve");
+    }
+    if (!sync_each || !st_host_->cr_halt) enq_cr(alpha, tol, cap, sync_each);
+  }
+  k_axpy1<<<vec_grid_, kThreads, 0, s_>>>(D_, x, xcg_, st_);
+}
+
+void Engine::enq_image(const float2* est, float2* img, float scale, bool apply_scale) {
+  enq_decode(est);
+  k_image<<<blocks_for(static_cast<long long>(plan_.N) * plan_.N, 148 * 4), kThreads, 0, s_>>>(
+      dims_, est, coils_, scale, apply_scale ? 1 : 0, img, st_);
+}
+
+// ---- op-level API -------------------------------------------------------------
+
+void Engine::apply_W_inv(const float* chat, float* out) {
+  const int G = plan_.G, Gc = plan_.Gc;
+  check_cuda(cudaMemcpyAsync(est_scratch_[0], chat, sizeof(float2) * Gc * Gc, cudaMemcpyHostToDevice, s_), "h2d");
+  k_pad_weight<<<blocks_for(G * G, 1024), kThreads, 0, s_>>>(est_scratch_[0], winv_, Gc, G, gbuf_);
+  fft2_device(gbuf_, G, 1, +1, s_);
+  fft_book(fft_current_ctx(), 1);
+  check_cuda(cudaMemcpyAsync(out, gbuf_, sizeof(float2) * G * G, cudaMemcpyDeviceToHost, s_), "d2h");
+  sync();
+}
+
+void Engine::apply_W_invH(const float* u, float* out) {
+  const int G = plan_.G, Gc = plan_.Gc;
+  check_cuda(cudaMemcpyAsync(gbuf_, u, sizeof(float2) * G * G, cudaMemcpyHostToDevice, s_), "h2d");
+  fft2_device(gbuf_, G, 1, -1, s_);
+  fft_book(fft_current_ctx(), 1);
+  k_crop_weight<<<blocks_for(Gc * Gc, 1024), kThreads, 0, s_>>>(gbuf_, winv_, Gc, G, est_scratch_[0]);
+  check_cuda(cudaMemcpyAsync(out, est_scratch_[0], sizeof(float2) * Gc * Gc, cudaMemcpyDeviceToHost, s_), "d2h");
+  sync();
+}
+
+void Engine::toeplitz_apply(float* x) {
+  const int G = plan_.G;
+  check_cuda(cudaMemcpyAsync(gbuf_, x, sizeof(float2) * G * G, cudaMemcpyHostToDevice, s_), "h2d");
+  k_mask<<<blocks_for(G * G, 1024), kThreads, 0, s_>>>(gbuf_, G);
+  fft2_device(gbuf_, G, 1, -1, s_);
+  k_mul<<<blocks_for(G * G, 1024), kThreads, 0, s_>>>(gbuf_, P_, G * G);
+  fft2_device(gbuf_, G, 1, +1, s_);
+  k_mask<<<blocks_for(G * G, 1024), kThreads, 0, s_>>>(gbuf_, G);
+  fft_book(fft_current_ctx(), 2);
+  check_cuda(cudaMemcpyAsync(x, gbuf_, sizeof(float2) * G * G, cudaMemcpyDeviceToHost, s_), "d2h");
+  sync();
+}
+
+void Engine::make_step_cache(const float* x, float* rho_out, float* coils_out) {
+  check_cuda(cudaMemcpyAsync(est_scratch_[2], x, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
+  check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
+  enq_decode(est_scratch_[2]);
+  fft_book(fft_current_ctx(), static_cast<uint64_t>(plan_.J));
+  const size_t G2 = static_cast<size_t>(plan_.G) * plan_.G;
+  if (rho_out) check_cuda(cudaMemcpyAsync(rho_out, rhom_, sizeof(float2) * G2, cudaMemcpyDeviceToHost, s_), "d2h");
+  if (coils_out) {
+    check_cuda(cudaMemcpyAsync(coils_out, coils_, sizeof(float2) * G2 * plan_.J, cudaMemcpyDeviceToHost, s_), "d2h");
+  }
+  sync();
+  have_cache_ = true;
+}
+
+void Engine::apply_normal(const float* dx, float* out) {
+  if (!have_cache_) fail(2, "apply_normal: no step cache (call make_step_cache first)");
+  check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
+  check_cuda(cudaMemcpyAsync(est_scratch_[0], dx, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
+  enq_apply(est_scratch_[0], est_scratch_[1], CW_OP, 0.f, -1, 0);
+  fft_book(fft_current_ctx(), 4ull * plan_.J);
+  check_cuda(cudaMemcpyAsync(out, est_scratch_[1], sizeof(float2) * D_, cudaMemcpyDeviceToHost, s_), "d2h");
+  read_state();
+  raise_status("apply_normal");
+}
+
+void Engine::cg_solve(const float* rhs, float alpha, float tol, int max_iter, float* x_out, int* iters,
+                      std::vector<double>* residuals) {
+  if (!have_cache_) fail(2, "cg_solve: no step cache (call make_step_cache first)");
+  // host-side entry checks mirror nlinv.cpp:182-186 exactly
+  double nsq = 0;
+  for (int i = 0; i < 2 * D_; ++i) nsq += static_cast<double>(rhs[i]) * rhs[i];
+  const double rhs_norm = std::sqrt(nsq);
+  if (!std::isfinite(rhs_norm)) fail(4, "cg_solve: right-hand side is not finite");
+  *iters = 0;
+  if (residuals) residuals->clear();
+  if (max_iter < 1 || rhs_norm == 0.0) {
+    std::memset(x_out, 0, sizeof(float2) * D_);
+    return;
+  }
+  ensure_cr_capacity(max_iter);
+  check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
+  check_cuda(cudaMemcpyAsync(r_, rhs, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
+  check_cuda(cudaMemcpyAsync(p_, r_, sizeof(float2) * D_, cudaMemcpyDeviceToDevice, s_), "d2d");
+  check_cuda(cudaMemsetAsync(xcg_, 0, sizeof(float2) * D_, s_), "zero");
+  enq_step_begin(0);
+  // the step record's rhs norm feeds the tolerance target
+  {
+    StepRec rec{};
+    rec.rhs_nrm2 = nsq;
+    check_cuda(cudaMemcpyAsync(reinterpret_cast<char*>(st_) + offsetof(DevState, steps), &rec, sizeof(rec),
+                               cudaMemcpyHostToDevice, s_),
+               "step record");
+    sync();
+  }
+  const int ctx = fft_current_ctx();
+  enq_cr(alpha, tol, max_iter, tol > 0.0f);
+  read_state();
+  raise_status("cg_solve");
+  const int n = st_host_->steps[0].iters;
+  fft_book(ctx, 4ull * plan_.J * static_cast<uint64_t>(n));
+  *iters = n;
+  if (residuals) {
+    std::vector<double> rn(static_cast<size_t>(cr_cap_));
+    check_cuda(cudaMemcpy(rn.data(), cr_.rn, sizeof(double) * cr_cap_, cudaMemcpyDeviceToHost), "residuals");
+    residuals->assign(rn.begin() + 1, rn.begin() + 1 + n);
+  }
+  check_cuda(cudaMemcpyAsync(x_out, xcg_, sizeof(float2) * D_, cudaMemcpyDeviceToHost, s_), "d2h");
+  sync();
+}
+
+void Engine::newton_step(float* x, const float* reg, float alpha, float tol, int cap, int* iters,
+                         double* residual0) {
+  check_cuda(cudaMemcpyAsync(x_, x, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
+  check_cuda(cudaMemcpyAsync(est_scratch_[1], reg, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
+  check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
+  const int ctx_n = CTX_NORMAL_OP;
+  enq_newton_step(0, x_, est_scratch_[1], alpha, tol, cap, true);
+  read_state();
+  raise_status("newton_step");
+  const StepRec& s = st_host_->steps[0];
+  *iters = s.iters;
+  *residual0 = std::sqrt(s.resid_win + s.resid_out);
+  fft_book(ctx_n, 4ull * plan_.J * static_cast<uint64_t>(s.iters));
+  check_cuda(cudaMemcpyAsync(x, x_, sizeof(float2) * D_, cudaMemcpyDeviceToHost, s_), "d2h");
+  sync();
+  have_cache_ = true;
+}
+
+// ---- frame pipeline -------------------------------------------------------------
+
+void Engine::enqueue_frame(float2* x_dev, const RegFn& reg_dev, float2* image_dev, float image_scale,
+                           bool apply_scale, FrameStats* stats) {
+  const int M = plan_.newton_steps;
+  check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
+  float alpha = plan_.alpha0;
+  int remaining = plan_.cg_iter_budget;
+  const bool budget = plan_.cg_iter_budget > 0;
+  spec_caps_.assign(static_cast<size_t>(M), 0);
+  for (int m = 0; m < M; ++m) {
+    int cap = plan_.cg_max_iter;
+    float tol = plan_.cg_tol;
+    if (budget) {
+      const int steps_left = M - m;
+      cap = (remaining + steps_left - 1) / steps_left;  // nlinv.cpp:301-306
+      tol = 0.0f;
+    }
+    const float2* reg = reg_dev(m);
+    enq_newton_step(m, x_dev, reg, alpha, tol, cap, !budget);
+    if (!budget) {
+      read_state();
+      raise_status("reconstruct_frame");
+      cap = st_host_->steps[m].iters;
+    }
+    spec_caps_[static_cast<size_t>(m)] = cap;
+    fft_book(CTX_NORMAL_OP, 4ull * plan_.J * static_cast<uint64_t>(cap));
+    if (budget) remaining -= cap;
+    alpha = std::max(alpha * plan_.alpha_q, plan_.alpha_min);
+  }
+  fft_book(CTX_SETUP, static_cast<uint64_t>(plan_.J));
+  enq_image(x_dev, image_dev, image_scale, apply_scale);
+  check_cuda(cudaMemcpyAsync(st_host_, st_, sizeof(DevState), cudaMemcpyDeviceToHost, s_), "state read");
+  check_cuda(cudaGetLastError(), "frame launch");
+  if (stats) {
+    stats->cg_per_step = spec_caps_;
+    stats->cg_iters = 0;
+    for (int c : spec_caps_) stats->cg_iters += c;
+  }
+}
+
+bool Engine::finish_frame(FrameStats* stats) {
+  sync();
+  raise_status("reconstruct_frame");
+  const int M = plan_.newton_steps;
+  bool ok = true;
+  for (int m = 0; m < M; ++m) {
+    if (st_host_->steps[m].iters != spec_caps_[static_cast<size_t>(m)] || st_host_->steps[m].zero_rhs) ok = false;
+  }
+  if (!ok) {
+    // undo the speculative booking; the synchronous re-run books the real counts
+    uint64_t n = 0;
+    for (int c : spec_caps_) n += static_cast<uint64_t>(c);
+    g_counts[CTX_NORMAL_OP].fetch_sub(4ull * plan_.J * n);
+    g_counts[CTX_SETUP].fetch_sub(4ull * plan_.J * M + plan_.J);
+  }
+  (void)stats;
+  return ok;
+}
+
+void Engine::run_frame_sync(float2* x_dev, const RegFn& reg_dev, float2* image_dev, float image_scale,
+                            bool apply_scale, FrameStats* stats) {
+  const int M = plan_.newton_steps;
+  check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
+  float alpha = plan_.alpha0;
+  int remaining = plan_.cg_iter_budget;
+  const bool budget = plan_.cg_iter_budget > 0;
+  std::vector<int> per;
+  for (int m = 0; m < M; ++m) {
+    int cap = plan_.cg_max_iter;
+    float tol = plan_.cg_tol;
+    if (budget) {
+      const int steps_left = M - m;
+      cap = (remaining + steps_left - 1) / steps_left;
+      tol = 0.0f;
+    }
+    enq_newton_step(m, x_dev, reg_dev(m), alpha, tol, cap, true);
+    read_state();
+    raise_status("reconstruct_frame");
+    const int it = st_host_->steps[m].iters;
+    fft_book(CTX_NORMAL_OP, 4ull * plan_.J * static_cast<uint64_t>(it));
+    per.push_back(it);
+    if (budget) remaining -= it;
+    alpha = std::max(alpha * plan_.alpha_q, plan_.alpha_min);
+  }
+  fft_book(CTX_SETUP, static_cast<uint64_t>(plan_.J));
+  enq_image(x_dev, image_dev, image_scale, apply_scale);
+  read_state();
+  raise_status("reconstruct_frame");
+  if (stats) {
+    stats->cg_per_step = per;
+    stats->cg_iters = 0;
+    for (int c : per) stats->cg_iters += c;
+  }
+}
+
+void Engine::reconstruct_frame(const float* init, const float* reg, float* image, float* est_out,
+                               FrameStats* stats) {
+  const auto t0 = std::chrono::steady_clock::now();
+  check_cuda(cudaMemcpyAsync(x_, init, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
+  check_cuda(cudaMemcpyAsync(est_scratch_[1], reg ? reg : init, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_),
+             "h2d");
+  float2* regp = est_scratch_[1];
+  const RegFn rf = [regp](int) -> const float2* { return regp; };
+  enqueue_frame(x_, rf, img_, 1.0f, false, stats);
+  if (!finish_frame(stats)) {
+    check_cuda(cudaMemcpyAsync(x_, init, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
+    run_frame_sync(x_, rf, img_, 1.0f, false, stats);
+  }
+  check_cuda(cudaMemcpyAsync(image, img_, sizeof(float2) * plan_.N * plan_.N, cudaMemcpyDeviceToHost, s_), "d2h");
+  if (est_out) check_cuda(cudaMemcpyAsync(est_out, x_, sizeof(float2) * D_, cudaMemcpyDeviceToHost, s_), "d2h");
+  sync();
+  have_cache_ = true;
+  if (stats) stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace rtnb

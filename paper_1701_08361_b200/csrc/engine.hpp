@@ -1,0 +1,175 @@
+// Host-side engine: one device context per (GPU, stream) that owns every device
+// buffer of a plan and enqueues the fused kernels of kernels_impl.cuh. The C-ABI
+// (capi.cpp) and the C++ drop-in API (api.cpp) are thin layers over this.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace rtnb {
+
+// Mirrors rtnlinv::ReconPlan (planner.hpp:21-35).
+struct Plan {
+  int N = 0;
+  int G = 0;
+  int Gc = 0;
+  int J = 1;
+  int newton_steps = 6;
+  float alpha0 = 1.0f;
+  float alpha_q = 0.5f;
+  float alpha_min = 1e-6f;
+  float cg_tol = 1e-3f;
+  int cg_max_iter = 200;
+  int cg_iter_budget = 0;
+  float prev_damping = 1.0f;
+  double gamma = 1.5;
+};
+
+// Typed failure carrying the reference's exit-code mapping (types.hpp:12-25,
+// rtnlinv_main.cpp:381-391): 2 usage, 3 data, 4 solver / decomposition fault.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+
+bool grid_supported(int G);
+
+// Logical transform accounting (fft.hpp:10-38): a 2D transform is booked against
+// the calling thread's context, whatever kernels implement it.
+enum FftCtx : int { CTX_OTHER = 0, CTX_NORMAL_OP = 1, CTX_SETUP = 2, CTX_BENCH = 3 };
+int fft_current_ctx();
+void fft_set_ctx(int c);
+void fft_book(int ctx, uint64_t n);
+uint64_t fft_count(int ctx);
+uint64_t fft_count_total();
+void fft_reset_counts();
+
+// centered unitary 2D transform of `batch` n x n images resident on the device
+void fft2_device(float2* data, int n, int batch, int sign, cudaStream_t s);
+
+struct FrameStats {
+  std::vector<int> cg_per_step;
+  int cg_iters = 0;
+  double seconds = 0;
+};
+
+class Engine {
+ public:
+  Engine(const Plan& plan, int device = 0);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  const Plan& plan() const { return plan_; }
+  int D() const { return D_; }  // complex entries of one Estimate: G*G + J*Gc*Gc
+  cudaStream_t stream() const { return s_; }
+  int device() const { return dev_; }
+
+  // ---- inputs (host, complex64 interleaved) ----
+  void set_psf(const float* P);    // G*G
+  void set_data(const float* z);   // J*G*G
+  void set_psf_device(const float2* P);
+  void set_data_device(const float2* z);
+  const float* winv_host() const { return winv_host_.data(); }
+
+  // ---- op-level, synchronous, host in / host out (nlinv.hpp:41-98) ----
+  void apply_W_inv(const float* chat, float* out);
+  void apply_W_invH(const float* u, float* out);
+  void toeplitz_apply(float* x);
+  void make_step_cache(const float* x, float* rho_out, float* coils_out);  // sets the linearisation point
+  void apply_normal(const float* dx, float* out);                          // at that point
+  void cg_solve(const float* rhs, float alpha, float tol, int max_iter, float* x_out, int* iters,
+                std::vector<double>* residuals);
+  void newton_step(float* x, const float* reg, float alpha, float tol, int cap, int* iters,
+                   double* residual0);
+  // reg == nullptr: every step regularises towards init (nlinv.cpp:425-429)
+  void reconstruct_frame(const float* init, const float* reg, float* image, float* est_out,
+                         FrameStats* stats);
+
+  // ---- device-resident frame pipeline ----
+  // Enqueue a whole frame on the stream: x_dev holds init on entry and the final
+  // estimate on exit; reg_dev(m) supplies the regularisation target of step m.
+  // Budget mode is enqueued speculatively (every step runs its cap) and verified by
+  // finish_frame(); tolerance mode synchronises per iteration.
+  using RegFn = std::function<const float2*(int m)>;
+  void enqueue_frame(float2* x_dev, const RegFn& reg_dev, float2* image_dev, float image_scale,
+                     bool apply_scale, FrameStats* stats);
+  // Synchronise and validate the enqueued frame; returns false when a step ended
+  // early (zero right-hand side) so the speculative budget split was wrong and the
+  // frame must be re-run with run_frame_sync().
+  bool finish_frame(FrameStats* stats);
+  void run_frame_sync(float2* x_dev, const RegFn& reg_dev, float2* image_dev, float image_scale,
+                      bool apply_scale, FrameStats* stats);
+
+  float2* x_dev() { return x_; }
+  float2* scratch_est(int i) { return est_scratch_[i]; }
+  float2* image_dev() { return img_; }
+  void sync();
+
+ public:
+  struct Ops;  // per-grid-size kernel launchers (engine.cu)
+
+ private:
+  void alloc();
+  void ensure_cr_capacity(int max_iter);
+  void enq_step_begin(int m);
+  void enq_decode(const float2* est);
+  void enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt);
+  void enq_setup(const float2* x, const float2* reg, float alpha);
+  void enq_cr(float alpha, float tol, int cap, bool sync_each);
+  void enq_newton_step(int m, float2* x, const float2* reg, float alpha, float tol, int cap,
+                       bool sync_each);
+  void enq_image(const float2* est, float2* img, float scale, bool apply_scale);
+  void read_state();
+  void raise_status(const char* where);
+
+  Plan plan_;
+  Dims dims_{};
+  int dev_ = 0;
+  int D_ = 0;
+  cudaStream_t s_ = nullptr;
+  const Ops* ops_ = nullptr;
+  int vec_grid_ = 0;
+  int nbr_ = 0;
+
+  std::vector<float> winv_host_;
+  float* winv_ = nullptr;
+  float2* twG_ = nullptr;
+  float2* P_ = nullptr;
+  float2* z_ = nullptr;
+  float2* x_ = nullptr;
+  float2* xcg_ = nullptr;
+  float2* r_ = nullptr;
+  float2* p_ = nullptr;
+  float2* ap_ = nullptr;
+  float2* ar_ = nullptr;
+  float2* est_scratch_[3] = {nullptr, nullptr, nullptr};
+  float2* coils_ = nullptr;
+  float2* rhom_ = nullptr;
+  float2* U_ = nullptr;
+  float2* V_ = nullptr;
+  float2* RC_ = nullptr;
+  float2* Y_ = nullptr;
+  float2* gbuf_ = nullptr;
+  float2* img_ = nullptr;
+  double* partials_ = nullptr;
+  DevState* st_ = nullptr;
+  DevState* st_host_ = nullptr;  // pinned mirror
+  double* cr_buf_ = nullptr;
+  int cr_cap_ = 0;
+  CrScalars cr_{};
+  bool have_cache_ = false;
+  std::vector<int> spec_caps_;
+};
+
+}  // namespace rtnb

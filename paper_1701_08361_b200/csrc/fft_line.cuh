@@ -1,0 +1,209 @@
+// Line transforms for the centered 2D FFT on sm_100a.
+//
+// The reference runs every transform through FFTW in double with two roll passes
+// (fft.cpp:41-77). Here a 2D transform is two passes of 1D line transforms; each
+// pass is a tile of LPB lines staged in shared memory, and each length-G line is a
+// two-step (four-step) Cooley-Tukey transform G = N1 x N2:
+//   step 1: N2 threads per line, each an N1-point DFT in registers over the
+//           stride-N2 subsequence, then the inter-step twiddle W_G^{n2 k1};
+//   step 2: N1 threads per line, each an N2-point DFT in registers over a
+//           contiguous (padded) smem block, results in natural order.
+// The small DFTs are fully unrolled mixed-radix recursions (radix 2/3/4 closed
+// forms, direct sums for other primes) whose twiddles are compile-time constant
+// indices into a __constant__ table, so they become constant-bank FMA operands.
+//
+// Centering (DC at G/2) for even G is folded into sign flips: the centered DFT
+// equals (-1)^{G/2} (-1)^p * DFT[(-1)^t x[t]][p]; the (-1)^{G/2} factors of the
+// two passes of a 2D transform cancel, so each pass only flips input and output
+// signs by parity. The 1/G scale of the unitary 2D transform is applied once, in
+// the pass that finishes it.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rtnb {
+
+// exp(-2 pi i k / N) for N = 1..32, k = 0..N-1, at offset N(N-1)/2. Filled from
+// double-precision values by the host (engine.cu, the one TU that includes this).
+static __constant__ float2 c_small_tw[528];
+
+__host__ __device__ constexpr int small_tw_offset(int n) { return n * (n - 1) / 2; }
+
+__host__ __device__ constexpr bool is_prime_c(int n) {
+  if (n < 2) return false;
+  for (int d = 2; d * d <= n; ++d)
+    if (n % d == 0) return false;
+  return true;
+}
+
+__host__ __device__ constexpr int split_factor(int n) {
+  if (n % 4 == 0 && n > 4) return 4;
+  for (int d = 2; d <= n; ++d)
+    if (n % d == 0) return d;
+  return n;
+}
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cneg(float2 a) { return make_float2(-a.x, -a.y); }
+
+// W_N^k for sign S (S = -1 forward: exp(-2 pi i k/N); S = +1 inverse: conjugate)
+template <int N, int S>
+__device__ __forceinline__ float2 small_w(int k) {
+  float2 w = c_small_tw[small_tw_offset(N) + (k % N)];
+  if (S > 0) w.y = -w.y;
+  return w;
+}
+
+// multiply by -i*S... i.e. by W_4^1 = exp(S * 2 pi i / 4) = S*i
+template <int S>
+__device__ __forceinline__ float2 mul_w4(float2 a) {
+  // S = -1: multiply by -i -> (a.y, -a.x);  S = +1: multiply by i -> (-a.y, a.x)
+  return S < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+}
+
+template <int N, int S>
+__device__ __forceinline__ void dft(float2 (&x)[N]);
+
+template <int N, int S>
+__device__ __forceinline__ void dft_direct(float2 (&x)[N]) {
+  float2 y[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    float2 acc = x[0];
+#pragma unroll
+    for (int t = 1; t < N; ++t) {
+      const float2 w = small_w<N, S>((k * t) % N);
+      acc.x += x[t].x * w.x - x[t].y * w.y;
+      acc.y += x[t].x * w.y + x[t].y * w.x;
+    }
+    y[k] = acc;
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) x[k] = y[k];
+}
+
+template <int N, int S>
+__device__ __forceinline__ void dft(float2 (&x)[N]) {
+  if constexpr (N == 1) {
+    return;
+  } else if constexpr (N == 2) {
+    const float2 a = x[0], b = x[1];
+    x[0] = cadd(a, b);
+    x[1] = csub(a, b);
+  } else if constexpr (N == 3) {
+    // X0 = a+b+c; X1,2 = a - (b+c)/2 -/+ S*i*(sqrt3/2)(b-c)
+    const float2 a = x[0], b = x[1], c = x[2];
+    const float2 s = cadd(b, c);
+    const float2 d = csub(b, c);
+    const float h = 0.86602540378443864676f;  // sqrt(3)/2
+    const float2 m = make_float2(a.x - 0.5f * s.x, a.y - 0.5f * s.y);
+    // S*i*h*d = S*h*(-d.y, d.x)
+    const float2 r = make_float2(-S * h * d.y, S * h * d.x);
+    x[0] = cadd(a, s);
+    x[1] = cadd(m, r);
+    x[2] = csub(m, r);
+  } else if constexpr (N == 4) {
+    const float2 a = x[0], b = x[1], c = x[2], d = x[3];
+    const float2 s0 = cadd(a, c), d0 = csub(a, c);
+    const float2 s1 = cadd(b, d), d1 = mul_w4<S>(csub(b, d));
+    x[0] = cadd(s0, s1);
+    x[2] = csub(s0, s1);
+    x[1] = cadd(d0, d1);
+    x[3] = csub(d0, d1);
+  } else if constexpr (is_prime_c(N)) {
+    dft_direct<N, S>(x);
+  } else {
+    // decimation in time, N = P * Q: sub-DFTs of length Q on the P interleaved
+    // subsequences, then P-point butterflies with twiddles W_N^{p k}
+    constexpr int P = split_factor(N);
+    constexpr int Q = N / P;
+    float2 sub[P][Q];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) sub[p][q] = x[p + P * q];
+      dft<Q, S>(sub[p]);
+    }
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+      float2 t[P];
+      t[0] = sub[0][k];
+#pragma unroll
+      for (int p = 1; p < P; ++p) t[p] = cmul(sub[p][k], small_w<N, S>(p * k));
+      dft<P, S>(t);
+#pragma unroll
+      for (int m = 0; m < P; ++m) x[k + Q * m] = t[m];
+    }
+  }
+}
+
+// Shared-memory geometry of one tile of LPB lines of length G = N1*N2.
+//   A (input, padded): element q of line l at l*LSA + q + q/N2 (one pad slot per
+//     N2 block, so step-2 reads of contiguous blocks by consecutive threads hit
+//     distinct banks); LSA odd so column-tile fills are conflict-free.
+//   B (output): element p of line l at l*LSB + p, LSB = G + 1 (odd).
+template <int N1_, int N2_, int LPB_>
+struct LineGeom {
+  static constexpr int N1 = N1_;
+  static constexpr int N2 = N2_;
+  static constexpr int G = N1 * N2;
+  static constexpr int LPB = LPB_;
+  static constexpr int LSA0 = G + N1;
+  static constexpr int LSA = (LSA0 % 2 == 1) ? LSA0 : LSA0 + 1;
+  static constexpr int LSB = G + 1;
+  static constexpr int SMEM_FLOAT2 = LPB * (LSA + LSB);
+  __device__ __forceinline__ static int a_idx(int l, int q) { return l * LSA + q + q / N2; }
+  __device__ __forceinline__ static int b_idx(int l, int p) { return l * LSB + p; }
+};
+
+// Transforms lines [0, nl) of tile A into tile B (natural order, unnormalised).
+// twG: exp(-2 pi i e / G), e = 0..G-1 (global, read-only). Must be called by all
+// threads of the block; ends with a __syncthreads().
+template <class Geo, int S>
+__device__ __forceinline__ void tile_fft(float2* A, float2* B, int nl, const float2* __restrict__ twG) {
+  constexpr int N1 = Geo::N1, N2 = Geo::N2, G = Geo::G;
+  __syncthreads();
+  // step 1: item (l, n2)
+  for (int it = threadIdx.x; it < nl * N2; it += blockDim.x) {
+    const int l = it / N2;
+    const int n2 = it - l * N2;
+    float2 v[N1];
+    float2* base = A + l * Geo::LSA + n2;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = base[n1 * (N2 + 1)];
+    dft<N1, S>(v);
+#pragma unroll
+    for (int k1 = 1; k1 < N1; ++k1) {
+      float2 w = __ldg(twG + n2 * k1);
+      if (S > 0) w.y = -w.y;
+      v[k1] = cmul(v[k1], w);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) base[k1 * (N2 + 1)] = v[k1];
+  }
+  __syncthreads();
+  // step 2: item (l, k1)
+  for (int it = threadIdx.x; it < nl * N1; it += blockDim.x) {
+    const int l = it / N1;
+    const int k1 = it - l * N1;
+    float2 v[N2];
+    const float2* src = A + l * Geo::LSA + k1 * (N2 + 1);
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) v[n2] = src[n2];
+    dft<N2, S>(v);
+    float2* dst = B + l * Geo::LSB + k1;
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) dst[N1 * k2] = v[k2];
+  }
+  (void)G;
+  __syncthreads();
+}
+
+}  // namespace rtnb

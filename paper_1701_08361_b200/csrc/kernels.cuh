@@ -1,0 +1,51 @@
+// Device-side data structures shared by the kernels and the engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rtnb {
+
+// Geometry of one plan on the device (SURVEY.md §8 "Sizes").
+//   G   oversampled grid side (even), L = G/2 the field-of-view window side,
+//   lo  = (G-L)/2 first window row/col (preproc.cpp:152-156),
+//   Gc  cropped coil k-space side, off = dc(G) - dc(Gc) its offset (planner.cpp:187-207)
+struct Dims {
+  int G, Gc, J, L, lo, off, N;
+  float invG;
+};
+
+enum Status : int { ST_OK = 0, ST_USAGE = 2, ST_DATA = 3, ST_SOLVER = 4 };
+
+// Per-frame device state. Scalars are indexed by Newton step m and CR iteration.
+// All reductions are FP64 (types.hpp:47-59) and deterministic (fixed-order
+// last-block reduction of per-block partials).
+constexpr int kMaxSteps = 64;
+struct StepRec {
+  int iters;          // CR iterations completed (cg_per_step)
+  int zero_rhs;       // rhs was exactly zero: CR returned without iterating
+  double resid_win;   // |z - T(rho c)|^2 on the window (partial of StepStats.residual0^2)
+  double resid_out;   // same outside the window
+  double rhs_nrm2;    // |rhs|^2
+};
+
+struct DevState {
+  int status;     // sticky error for the frame (ST_SOLVER on non-finite values)
+  int cr_halt;    // skip the remaining CR work of the current step
+  int cur_step;
+  int pad_;
+  unsigned int counter;  // last-block reduction ticket
+  unsigned int pad2_;
+  StepRec steps[kMaxSteps];
+  double scal[8];        // scratch scalar outputs (op-level calls)
+};
+
+// CR scalars of the current step: rar[k] = <r, A r> after apply k, ap2[k] = |ap|^2
+// after update k, rn[k] = |r| after iteration k (cg_solve nlinv.cpp:179-234).
+struct CrScalars {
+  double* rar;
+  double* ap2;
+  double* rn;
+};
+
+}  // namespace rtnb
