@@ -136,7 +136,8 @@ def test_cg_solve_matches_reference(gpu, ref, tol, max_iter):
     want, wit, wres = ref.cg_solve(plan, x, rhs, P, 0.5, tol, max_iter)
     assert it == wit
     assert rel_err(got, want) < 1e-4
-    np.testing.assert_allclose(res, wres, rtol=1e-4)
+    # residuals agree to 1e-4 until they reach float round-off of the first one
+    np.testing.assert_allclose(res, wres, rtol=1e-4, atol=1e-6 * wres[0])
     # residual norms never increase (test_nlinv.cpp:279-286)
     assert np.all(res[1:] <= res[:-1] * (1 + 1e-5))
 
