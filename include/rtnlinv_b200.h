@@ -94,6 +94,72 @@ int rtn_newton_step(rtn_ctx* ctx, float* x, const float* reg, float alpha, float
 int rtn_reconstruct_frame(rtn_ctx* ctx, const float* init, const float* reg, float* image,
                           float* est_out, int* cg_per_step, double* seconds);
 
+/* --- nlinv.hpp:136-169: series drivers over device-resident frames ------------- */
+typedef struct rtn_series rtn_series;
+/* SeriesOptions (nlinv.hpp:136-145) + TemporalSchedule (decomp.hpp:70-76).
+ * T = frames in flight (one CUDA stream + workspace each); plain != 0 selects
+ * reconstruct_series_plain. */
+typedef struct rtn_series_opts_t {
+  int T;
+  int A;
+  int sched_l;
+  int sched_o;
+  int chain;
+  int normalize;
+  int plain;
+} rtn_series_opts_t;
+
+int rtn_series_create(rtn_ctx* ctx, int frames, int n_psf, rtn_series** out);
+void rtn_series_destroy(rtn_series* s);
+/* gridded frames z (count*J*G*G, GriddedData::z per frame) into the device store */
+int rtn_series_upload_frames(rtn_series* s, int first, int count, const float* z);
+int rtn_series_upload_psf(rtn_series* s, int k, const float* P);
+int rtn_series_set_psf_index(rtn_series* s, const int* idx /* frames */);
+/* prep_series normalisation: frame 0 scaled to norm 100 (nlinv.cpp:390-400) */
+int rtn_series_normalize(rtn_series* s, double* data_scale);
+/* reconstruct frames [first, first+count). z_host != NULL streams those frames from
+ * host memory inside the call (end-to-end path). Outputs (all nullable):
+ * images count*N*N, audit count*(5+M) ints {frame, thread, workers, init_src,
+ * reg_final_src, reg_src[M]}, seqs count*3 {start, reg_final, finish}, cg_iters
+ * count, gpu_ms count (frame start -> image ready). */
+int rtn_series_run(rtn_series* s, const rtn_series_opts_t* opts, int first, int count, const float* z_host,
+                   float* images, int* audit, uint64_t* seqs, int* cg_iters, float* gpu_ms);
+int rtn_series_images(rtn_series* s, int first, int count, float* images);
+int rtn_series_estimate(rtn_series* s, int n, float* est /* D */);
+
+/* --- decomp.hpp:25-130: decomposition and scheduling (host logic) ----------------- */
+/* cap = largest group (4 = reference kGroupSizeMax, 8 = NVSwitch) */
+int rtn_partition_channels(int J, int A, int cap, int* out_pairs /* 2*A */);
+typedef struct rtn_ledger rtn_ledger;
+int rtn_ledger_create(int frames, rtn_ledger** out);
+void rtn_ledger_destroy(rtn_ledger* l);
+int rtn_ledger_mark_step(rtn_ledger* l, int n, int m);
+int rtn_ledger_mark_complete(rtn_ledger* l, int n);
+int rtn_ledger_completed(rtn_ledger* l, int n);
+int rtn_ledger_last_step(rtn_ledger* l, int n, int* out);
+int rtn_ledger_wait_complete(rtn_ledger* l, int n, int deadline_ms);
+void rtn_ledger_poison(rtn_ledger* l);
+int rtn_ledger_poisoned(rtn_ledger* l);
+uint64_t rtn_ledger_next_seq(rtn_ledger* l);
+int rtn_h_choose(int n, int m, int M, int sched_l, int sched_o, rtn_ledger* l, int* out);
+
+/* --- autotune.hpp:13-77 ----------------------------------------------------------- */
+/* records: n rows of {mode, N, bucket, J, T, A}; a_cap as in rtn_partition_channels;
+ * returns the number of configs (negative status on error) */
+int rtn_legal_configs(int total_workers, int a_cap, int* out_pairs, int max_pairs);
+int rtn_frames_bucket(int frames, int* out);
+int rtn_select_config(const int* key4, const int* rows6, const double* runtime_ms, int n, int* out_ta);
+int rtn_learn_step(const int* key4, const int* rows6, const double* runtime_ms, int n, int total_workers,
+                   int a_cap, int* out_ta);
+int rtn_tunedb_append(const char* path, const int* row6, double runtime_ms, int64_t timestamp);
+int rtn_tunedb_load(const char* path, int* rows6, double* runtime_ms, int64_t* timestamps, int max_rows,
+                    int* n_rows, int* skipped);
+
+/* --- measurement --------------------------------------------------------------------- */
+/* average ms per launch of one kernel class ("colsT", "rows1", "rows2", "colA",
+ * "apply") at the cached linearisation point, and its algorithmic bytes */
+int rtn_time_kernel(rtn_ctx* ctx, const char* which, int reps, double* ms, double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -245,6 +245,17 @@ def reconstruct_frame(plan, z, P, init, reg=None, A=1):
     return img, est, per[:plan.newton_steps].tolist(), secs.value
 
 
+def reconstruct_frame_regs(plan, z, P, init, regs):
+    """frame with a per-step regularisation target regs[m] (audit replay)"""
+    regs = _c64(np.stack([_c64(r) for r in regs]))
+    img = np.zeros((plan.N, plan.N), np.complex64)
+    est = np.zeros_like(_c64(init))
+    per = np.zeros(max(plan.newton_steps, 1), np.int32)
+    _chk(lib().ref_reconstruct_frame_regs(ctypes.byref(plan_c(plan)), _fp(_c64(z)), _fp(_c64(P)), _fp(_c64(init)),
+                                          _fp(regs), _fp(img), _fp(est), _ip(per)))
+    return img, est, per[:plan.newton_steps].tolist()
+
+
 def reconstruct_series(plan, samples, angles, T=1, A=1, sched=(1, 1), chain=True, normalize=True, plain=False):
     samples = _c64(samples)
     angles = np.ascontiguousarray(angles, np.float64)

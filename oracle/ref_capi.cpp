@@ -388,6 +388,27 @@ int ref_reconstruct_frame(const ref_plan_t* p, const float* z, const float* P, c
   });
 }
 
+// per-step regularisation targets regs[m] (M*D): replays a scheduled frame whose
+// sources were recorded in an audit (SURVEY.md §7 "audit replay")
+int ref_reconstruct_frame_regs(const ref_plan_t* p, const float* z, const float* P, const float* init,
+                               const float* regs, float* out_image, float* out_est, int* out_cg_per_step) {
+  return guarded([&] {
+    const ReconPlan plan = to_plan(p);
+    const PsfKernel psf = load_psf(P, plan.G);
+    const CImage winv = make_weights_inv(plan.Gc, plan.G);
+    const size_t D = static_cast<size_t>(plan.G) * plan.G + static_cast<size_t>(plan.J) * plan.Gc * plan.Gc;
+    std::vector<Estimate> r;
+    for (int m = 0; m < plan.newton_steps; ++m) r.push_back(load_est(regs + 2 * D * m, plan));
+    const RegProvider rp = [&r](int m) -> const Estimate& { return r[static_cast<size_t>(m)]; };
+    const FrameResult fr = reconstruct_frame(load_z(z, plan), psf, plan, winv, load_est(init, plan), rp);
+    store_img(fr.image, out_image);
+    if (out_est) store_est(fr.est, out_est);
+    if (out_cg_per_step) {
+      for (size_t m = 0; m < fr.cg_per_step.size(); ++m) out_cg_per_step[m] = fr.cg_per_step[m];
+    }
+  });
+}
+
 int ref_initial_estimate(const ref_plan_t* p, float* out) {
   return guarded([&] { store_est(initial_estimate(to_plan(p)), out); });
 }

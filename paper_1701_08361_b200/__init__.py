@@ -59,6 +59,11 @@ class _Plan(ctypes.Structure):
     ]
 
 
+class _SeriesOpts(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_int), ("A", ctypes.c_int), ("sched_l", ctypes.c_int), ("sched_o", ctypes.c_int),
+                ("chain", ctypes.c_int), ("normalize", ctypes.c_int), ("plain", ctypes.c_int)]
+
+
 @dataclass
 class ReconPlan:
     """rtnlinv::ReconPlan (planner.hpp:21-35) with the reference defaults."""
@@ -142,6 +147,36 @@ def load_library(path: str = LIB_PATH):
         "rtn_cg_solve": ([vp, f, ctypes.c_float, ctypes.c_float, ctypes.c_int, f, i, d], ctypes.c_int),
         "rtn_newton_step": ([vp, f, f, ctypes.c_float, ctypes.c_float, ctypes.c_int, i, d], ctypes.c_int),
         "rtn_reconstruct_frame": ([vp, f, f, f, f, i, d], ctypes.c_int),
+        "rtn_series_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
+        "rtn_series_destroy": ([vp], None),
+        "rtn_series_upload_frames": ([vp, ctypes.c_int, ctypes.c_int, vp], ctypes.c_int),
+        "rtn_series_upload_psf": ([vp, ctypes.c_int, f], ctypes.c_int),
+        "rtn_series_set_psf_index": ([vp, i], ctypes.c_int),
+        "rtn_series_normalize": ([vp, d], ctypes.c_int),
+        "rtn_series_run": ([vp, ctypes.POINTER(_SeriesOpts), ctypes.c_int, ctypes.c_int, vp, vp, i,
+                            ctypes.POINTER(ctypes.c_uint64), i, f], ctypes.c_int),
+        "rtn_series_images": ([vp, ctypes.c_int, ctypes.c_int, f], ctypes.c_int),
+        "rtn_series_estimate": ([vp, ctypes.c_int, f], ctypes.c_int),
+        "rtn_partition_channels": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, i], ctypes.c_int),
+        "rtn_ledger_create": ([ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
+        "rtn_ledger_destroy": ([vp], None),
+        "rtn_ledger_mark_step": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+        "rtn_ledger_mark_complete": ([vp, ctypes.c_int], ctypes.c_int),
+        "rtn_ledger_completed": ([vp, ctypes.c_int], ctypes.c_int),
+        "rtn_ledger_last_step": ([vp, ctypes.c_int, i], ctypes.c_int),
+        "rtn_ledger_wait_complete": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+        "rtn_ledger_poison": ([vp], None),
+        "rtn_ledger_poisoned": ([vp], ctypes.c_int),
+        "rtn_ledger_next_seq": ([vp], ctypes.c_uint64),
+        "rtn_h_choose": ([ctypes.c_int] * 5 + [vp, i], ctypes.c_int),
+        "rtn_legal_configs": ([ctypes.c_int, ctypes.c_int, i, ctypes.c_int], ctypes.c_int),
+        "rtn_frames_bucket": ([ctypes.c_int, i], ctypes.c_int),
+        "rtn_select_config": ([i, i, d, ctypes.c_int, i], ctypes.c_int),
+        "rtn_learn_step": ([i, i, d, ctypes.c_int, ctypes.c_int, ctypes.c_int, i], ctypes.c_int),
+        "rtn_tunedb_append": ([ctypes.c_char_p, i, ctypes.c_double, ctypes.c_int64], ctypes.c_int),
+        "rtn_tunedb_load": ([ctypes.c_char_p, i, d, ctypes.POINTER(ctypes.c_int64), ctypes.c_int, i, i],
+                            ctypes.c_int),
+        "rtn_time_kernel": ([vp, ctypes.c_char_p, ctypes.c_int, d, d], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -366,3 +401,299 @@ class Context:
                                               ctypes.byref(secs)))
         cg = [per[m] for m in range(self.plan.newton_steps)]
         return FrameResult(img, est, cg, sum(cg), secs.value)
+
+    def time_kernel(self, which: str, reps: int = 20):
+        """(average ms per launch, algorithmic bytes per launch) of one kernel class"""
+        ms = ctypes.c_double(0)
+        by = ctypes.c_double(0)
+        _check(self.lib.rtn_time_kernel(self._h, which.encode(), reps, ctypes.byref(ms), ctypes.byref(by)))
+        return ms.value, by.value
+
+
+# ---- decomposition / scheduling (decomp.hpp) ------------------------------------------------
+@dataclass
+class TemporalSchedule:
+    """decomp.hpp:70-76"""
+    l: int = 1
+    o: int = 1
+
+    @staticmethod
+    def for_turns(U: int) -> "TemporalSchedule":
+        return TemporalSchedule(U, (U + 1) // 2)
+
+
+@dataclass
+class SeriesOptions:
+    """nlinv.hpp:136-145 (T = frames in flight on the device)"""
+    sched: TemporalSchedule = field(default_factory=TemporalSchedule)
+    T: int = 1
+    A: int = 1
+    chain: bool = True
+    normalize: bool = True
+    plain: bool = False
+
+    def to_c(self) -> _SeriesOpts:
+        return _SeriesOpts(self.T, self.A, self.sched.l, self.sched.o, int(self.chain), int(self.normalize),
+                           int(self.plain))
+
+
+@dataclass
+class FrameAudit:
+    frame: int
+    thread: int
+    workers: int
+    init_src: int
+    reg_final_src: int
+    reg_src: list
+    start_seq: int = 0
+    reg_final_seq: int = 0
+    finish_seq: int = 0
+
+
+def format_audit(a: FrameAudit) -> str:
+    return (f"frame {a.frame}: init<-{a.init_src}, reg_final<-{a.reg_final_src}, "
+            f"thread {a.thread}, workers {a.workers}")
+
+
+class Series:
+    """Device-resident frame series (reconstruct_series / _plain, nlinv.cpp:412-526)."""
+
+    def __init__(self, ctx: Context, frames: int, n_psf: int):
+        self.ctx = ctx
+        self.lib = ctx.lib
+        self.F = frames
+        self._h = ctypes.c_void_p()
+        _check(self.lib.rtn_series_create(ctx._h, frames, n_psf, ctypes.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            self.lib.rtn_series_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload_frames(self, z, first: int = 0):
+        p = self.ctx.plan
+        z = _c64(z)
+        count = z.size // (p.J * p.G * p.G)
+        _check(self.lib.rtn_series_upload_frames(self._h, first, count, z.ctypes.data))
+
+    def upload_psf(self, k: int, P):
+        P = _c64(P, (self.ctx.plan.G, self.ctx.plan.G))
+        _check(self.lib.rtn_series_upload_psf(self._h, k, _fp(P)))
+
+    def set_psf_index(self, idx):
+        a = np.ascontiguousarray(np.asarray(idx, np.int32))
+        _check(self.lib.rtn_series_set_psf_index(self._h, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int))))
+
+    def normalize(self) -> float:
+        v = ctypes.c_double(0)
+        _check(self.lib.rtn_series_normalize(self._h, ctypes.byref(v)))
+        return v.value
+
+    def run(self, opts: SeriesOptions, first: int = 0, count: Optional[int] = None, z_host=None,
+            want_images: bool = True, z_host_ptr: Optional[int] = None, images_ptr: Optional[int] = None):
+        p = self.ctx.plan
+        count = self.F - first if count is None else count
+        M = p.newton_steps
+        images = np.zeros((count, p.N, p.N), np.complex64) if (want_images and images_ptr is None) else None
+        audit = np.zeros((count, 5 + M), np.int32)
+        seqs = np.zeros((count, 3), np.uint64)
+        cg = np.zeros(count, np.int32)
+        ms = np.zeros(count, np.float32)
+        zp = None
+        if z_host_ptr is not None:
+            zp = z_host_ptr
+        elif z_host is not None:
+            z_host = _c64(z_host)
+            zp = z_host.ctypes.data
+        ip = images_ptr if images_ptr is not None else (None if images is None else images.ctypes.data)
+        o = opts.to_c()
+        _check(self.lib.rtn_series_run(self._h, ctypes.byref(o), first, count, zp, ip,
+                                       audit.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                       seqs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                       cg.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _fp(ms)))
+        audits = [FrameAudit(int(r[0]), int(r[1]), int(r[2]), int(r[3]), int(r[4]), [int(v) for v in r[5:]],
+                             int(q[0]), int(q[1]), int(q[2])) for r, q in zip(audit, seqs)]
+        return dict(images=images, audit=audits, cg_iters=cg, gpu_ms=ms)
+
+    def images(self, first: int = 0, count: Optional[int] = None):
+        p = self.ctx.plan
+        count = self.F - first if count is None else count
+        out = np.zeros((count, p.N, p.N), np.complex64)
+        _check(self.lib.rtn_series_images(self._h, first, count, _fp(out)))
+        return out
+
+    def estimate(self, n: int):
+        out = np.zeros(self.ctx.D, np.complex64)
+        _check(self.lib.rtn_series_estimate(self._h, n, _fp(out)))
+        return out
+
+
+def reconstruct_series(ctx: Context, z, P, opts: SeriesOptions, psf_index=None):
+    """gridded frames z (F, J, G, G) + PSF set P (U, G, G) -> images (F, N, N) and audit"""
+    z = _c64(z)
+    P = _c64(P)
+    if P.ndim == 2:
+        P = P[None]
+    F = z.shape[0]
+    s = Series(ctx, F, P.shape[0])
+    try:
+        s.upload_frames(z)
+        for k in range(P.shape[0]):
+            s.upload_psf(k, P[k])
+        if psf_index is not None:
+            s.set_psf_index(psf_index)
+        out = s.run(opts)
+        return out
+    finally:
+        s.close()
+
+
+def partition_channels(J: int, A: int, cap: int = 4):
+    lib = load_library()
+    out = (ctypes.c_int * (2 * max(A, 1)))()
+    _check(lib.rtn_partition_channels(J, A, cap, out))
+    return [(out[2 * a], out[2 * a + 1]) for a in range(A)]
+
+
+class CompletionLedger:
+    """decomp.hpp:81-109"""
+
+    def __init__(self, frames: int):
+        self.lib = load_library()
+        self._h = ctypes.c_void_p()
+        _check(self.lib.rtn_ledger_create(frames, ctypes.byref(self._h)))
+
+    def __del__(self):
+        try:
+            self.lib.rtn_ledger_destroy(self._h)
+        except Exception:
+            pass
+
+    def mark_step(self, n, m):
+        _check(self.lib.rtn_ledger_mark_step(self._h, n, m))
+
+    def mark_complete(self, n):
+        _check(self.lib.rtn_ledger_mark_complete(self._h, n))
+
+    def completed(self, n) -> bool:
+        return bool(self.lib.rtn_ledger_completed(self._h, n))
+
+    def last_step(self, n) -> int:
+        v = ctypes.c_int(0)
+        _check(self.lib.rtn_ledger_last_step(self._h, n, ctypes.byref(v)))
+        return v.value
+
+    def wait_complete(self, n, deadline_ms=600000):
+        st = self.lib.rtn_ledger_wait_complete(self._h, n, deadline_ms)
+        if st == 4:
+            raise DecompFault(self.lib.rtn_last_error().decode())
+        _check(st)
+
+    def poison(self):
+        self.lib.rtn_ledger_poison(self._h)
+
+    def poisoned(self) -> bool:
+        return bool(self.lib.rtn_ledger_poisoned(self._h))
+
+    def next_seq(self) -> int:
+        return int(self.lib.rtn_ledger_next_seq(self._h))
+
+
+def h_choose(n: int, m: int, M: int, sched: TemporalSchedule, ledger: CompletionLedger) -> int:
+    lib = load_library()
+    v = ctypes.c_int(0)
+    st = lib.rtn_h_choose(n, m, M, sched.l, sched.o, ledger._h, ctypes.byref(v))
+    if st == 4:
+        raise DecompFault(lib.rtn_last_error().decode())
+    _check(st)
+    return v.value
+
+
+# ---- autotune (autotune.hpp) --------------------------------------------------------------------
+class ImagingMode:
+    single_slice, multi_slice, flow = 0, 1, 2
+
+
+def frames_bucket(frames: int) -> int:
+    lib = load_library()
+    v = ctypes.c_int(0)
+    _check(lib.rtn_frames_bucket(frames, ctypes.byref(v)))
+    return v.value
+
+
+def legal_configs(total_workers: int = 8, a_cap: int = 4):
+    lib = load_library()
+    buf = (ctypes.c_int * 512)()
+    n = lib.rtn_legal_configs(total_workers, a_cap, buf, 256)
+    if n < 0:
+        _check(-n)
+    return [(buf[2 * k], buf[2 * k + 1]) for k in range(n)]
+
+
+def _db_arrays(db):
+    rows = np.zeros((max(len(db), 1), 6), np.int32)
+    ms = np.zeros(max(len(db), 1), np.float64)
+    for k, r in enumerate(db):
+        rows[k] = r[:6]
+        ms[k] = r[6]
+    return rows, ms
+
+
+def select_config(key, db):
+    """key = (mode, N, bucket, J); db rows = (mode, N, bucket, J, T, A, runtime_ms)"""
+    lib = load_library()
+    rows, ms = _db_arrays(db)
+    k = np.asarray(key, np.int32)
+    out = np.zeros(2, np.int32)
+    ip = ctypes.POINTER(ctypes.c_int)
+    _check(lib.rtn_select_config(k.ctypes.data_as(ip), rows.ctypes.data_as(ip),
+                                 ms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(db), out.ctypes.data_as(ip)))
+    return int(out[0]), int(out[1])
+
+
+def learn_step(key, db, total_workers: int = 8, a_cap: int = 4):
+    lib = load_library()
+    rows, ms = _db_arrays(db)
+    k = np.asarray(key, np.int32)
+    out = np.zeros(2, np.int32)
+    ip = ctypes.POINTER(ctypes.c_int)
+    _check(lib.rtn_learn_step(k.ctypes.data_as(ip), rows.ctypes.data_as(ip),
+                              ms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(db), total_workers, a_cap,
+                              out.ctypes.data_as(ip)))
+    return int(out[0]), int(out[1])
+
+
+class TuneDb:
+    """append-only TSV store (autotune.hpp:57-75)"""
+
+    def __init__(self, path: str):
+        self.path = path
+        self.skipped = 0
+
+    def append(self, row, runtime_ms: float, timestamp: int):
+        lib = load_library()
+        r = np.asarray(row[:6], np.int32)
+        _check(lib.rtn_tunedb_append(self.path.encode(), r.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                     runtime_ms, timestamp))
+
+    def load(self):
+        lib = load_library()
+        cap = 4096
+        rows = np.zeros((cap, 6), np.int32)
+        ms = np.zeros(cap, np.float64)
+        ts = np.zeros(cap, np.int64)
+        n = ctypes.c_int(0)
+        sk = ctypes.c_int(0)
+        ip = ctypes.POINTER(ctypes.c_int)
+        _check(lib.rtn_tunedb_load(self.path.encode(), rows.ctypes.data_as(ip),
+                                   ms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                   ts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), cap, ctypes.byref(n),
+                                   ctypes.byref(sk)))
+        self.skipped = sk.value
+        return [tuple(int(v) for v in rows[k]) + (float(ms[k]), int(ts[k])) for k in range(n.value)]

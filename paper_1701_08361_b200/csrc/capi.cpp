@@ -8,6 +8,8 @@
 
 #include "../../include/rtnlinv_b200.h"
 #include "engine.hpp"
+#include "sched.hpp"
+#include "series.hpp"
 
 struct rtn_ctx {
   rtnb::Engine* eng = nullptr;
@@ -174,6 +176,254 @@ int rtn_reconstruct_frame(rtn_ctx* ctx, const float* init, const float* reg, flo
       for (size_t m = 0; m < st.cg_per_step.size(); ++m) cg_per_step[m] = st.cg_per_step[m];
     }
     if (seconds) *seconds = st.seconds;
+  });
+}
+
+// ---- series -------------------------------------------------------------------------
+
+struct rtn_series {
+  rtn_ctx* ctx = nullptr;
+  rtnb::Series* s = nullptr;
+};
+
+int rtn_series_create(rtn_ctx* ctx, int frames, int n_psf, rtn_series** out) {
+  return guarded([&] {
+    auto* s = new rtn_series;
+    try {
+      s->ctx = ctx;
+      s->s = new rtnb::Series(eng(ctx), frames, n_psf);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+void rtn_series_destroy(rtn_series* s) {
+  if (!s) return;
+  delete s->s;
+  delete s;
+}
+
+static rtnb::Series& ser(rtn_series* s) {
+  if (!s || !s->s) rtnb::fail(2, "null series");
+  return *s->s;
+}
+
+int rtn_series_upload_frames(rtn_series* s, int first, int count, const float* z) {
+  return guarded([&] { ser(s).upload_frames(first, count, z); });
+}
+int rtn_series_upload_psf(rtn_series* s, int k, const float* P) {
+  return guarded([&] { ser(s).upload_psf(k, P); });
+}
+int rtn_series_set_psf_index(rtn_series* s, const int* idx) {
+  return guarded([&] { ser(s).set_psf_index(idx); });
+}
+int rtn_series_normalize(rtn_series* s, double* scale) {
+  return guarded([&] {
+    const double v = ser(s).normalize();
+    if (scale) *scale = v;
+  });
+}
+
+int rtn_series_run(rtn_series* s, const rtn_series_opts_t* o, int first, int count, const float* z_host,
+                   float* images, int* audit, uint64_t* seqs, int* cg_iters, float* gpu_ms) {
+  return guarded([&] {
+    rtnb::SeriesOptions so;
+    so.T = o->T;
+    so.A = o->A;
+    so.sched = rtnb::TemporalSchedule{o->sched_l, o->sched_o};
+    so.chain = o->chain != 0;
+    so.normalize = o->normalize != 0;
+    so.plain = o->plain != 0;
+    std::vector<rtnb::SeriesFrameOut> out;
+    ser(s).run(so, first, count, z_host, images, &out);
+    const int M = s->ctx->eng->plan().newton_steps;
+    for (int k = 0; k < count; ++k) {
+      const rtnb::SeriesFrameOut& f = out[static_cast<size_t>(k)];
+      if (audit) {
+        int* row = audit + static_cast<size_t>(k) * (5 + M);
+        row[0] = f.audit.frame;
+        row[1] = f.audit.thread;
+        row[2] = f.audit.workers;
+        row[3] = f.audit.init_src;
+        row[4] = f.audit.reg_final_src;
+        for (int m = 0; m < M; ++m) row[5 + m] = f.audit.reg_src[static_cast<size_t>(m)];
+      }
+      if (seqs) {
+        seqs[3 * k] = f.audit.start_seq;
+        seqs[3 * k + 1] = f.audit.reg_final_seq;
+        seqs[3 * k + 2] = f.audit.finish_seq;
+      }
+      if (cg_iters) cg_iters[k] = f.cg_iters;
+      if (gpu_ms) gpu_ms[k] = f.gpu_ms;
+    }
+  });
+}
+
+int rtn_series_images(rtn_series* s, int first, int count, float* images) {
+  return guarded([&] {
+    const rtnb::Plan& p = s->ctx->eng->plan();
+    const size_t isz = static_cast<size_t>(p.N) * p.N;
+    if (first < 0 || first + count > ser(s).frames()) rtnb::fail(2, "series_images: range out of bounds");
+    rtnb::check_cuda(cudaMemcpy(images, ser(s).images_dev() + isz * first, sizeof(float2) * isz * count,
+                                cudaMemcpyDeviceToHost),
+                     "images d2h");
+  });
+}
+
+int rtn_series_estimate(rtn_series* s, int n, float* est) {
+  return guarded([&] {
+    if (n < 0 || n >= ser(s).frames()) rtnb::fail(2, "series_estimate: frame out of range");
+    rtnb::check_cuda(cudaMemcpy(est, ser(s).estimate_dev(n), sizeof(float2) * s->ctx->eng->D(),
+                                cudaMemcpyDeviceToHost),
+                     "estimate d2h");
+  });
+}
+
+// ---- decomposition / scheduling ------------------------------------------------------
+
+int rtn_partition_channels(int J, int A, int cap, int* out_pairs) {
+  return guarded([&] {
+    const auto b = rtnb::partition_channels(J, A, cap);
+    for (size_t a = 0; a < b.size(); ++a) {
+      out_pairs[2 * a] = b[a].first;
+      out_pairs[2 * a + 1] = b[a].second;
+    }
+  });
+}
+
+struct rtn_ledger {
+  rtnb::CompletionLedger* l = nullptr;
+};
+
+int rtn_ledger_create(int frames, rtn_ledger** out) {
+  return guarded([&] {
+    auto* l = new rtn_ledger;
+    l->l = new rtnb::CompletionLedger(frames);
+    *out = l;
+  });
+}
+void rtn_ledger_destroy(rtn_ledger* l) {
+  if (!l) return;
+  delete l->l;
+  delete l;
+}
+int rtn_ledger_mark_step(rtn_ledger* l, int n, int m) {
+  return guarded([&] { l->l->mark_step(n, m); });
+}
+int rtn_ledger_mark_complete(rtn_ledger* l, int n) {
+  return guarded([&] { l->l->mark_complete(n); });
+}
+int rtn_ledger_completed(rtn_ledger* l, int n) { return l->l->completed(n) ? 1 : 0; }
+int rtn_ledger_last_step(rtn_ledger* l, int n, int* out) {
+  return guarded([&] { *out = l->l->last_step(n); });
+}
+int rtn_ledger_wait_complete(rtn_ledger* l, int n, int deadline_ms) {
+  return guarded([&] { l->l->wait_complete(n, std::chrono::milliseconds(deadline_ms)); });
+}
+void rtn_ledger_poison(rtn_ledger* l) { l->l->poison(); }
+int rtn_ledger_poisoned(rtn_ledger* l) { return l->l->poisoned() ? 1 : 0; }
+uint64_t rtn_ledger_next_seq(rtn_ledger* l) { return l->l->next_seq(); }
+int rtn_h_choose(int n, int m, int M, int sched_l, int sched_o, rtn_ledger* l, int* out) {
+  return guarded([&] { *out = rtnb::h_choose(n, m, M, rtnb::TemporalSchedule{sched_l, sched_o}, *l->l); });
+}
+
+// ---- autotune ----------------------------------------------------------------------------
+
+static std::vector<rtnb::TuningRecord> records(const int* rows, const double* ms, int n) {
+  std::vector<rtnb::TuningRecord> db;
+  for (int i = 0; i < n; ++i) {
+    rtnb::TuningRecord r;
+    r.key.mode = static_cast<rtnb::ImagingMode>(rows[6 * i]);
+    r.key.N = rows[6 * i + 1];
+    r.key.bucket = rows[6 * i + 2];
+    r.key.J = rows[6 * i + 3];
+    r.T = rows[6 * i + 4];
+    r.A = rows[6 * i + 5];
+    r.runtime_ms = ms[i];
+    db.push_back(r);
+  }
+  return db;
+}
+
+static rtnb::ProtocolKey key_of(const int* k) {
+  rtnb::ProtocolKey key;
+  key.mode = static_cast<rtnb::ImagingMode>(k[0]);
+  key.N = k[1];
+  key.bucket = k[2];
+  key.J = k[3];
+  return key;
+}
+
+int rtn_legal_configs(int total, int a_cap, int* out_pairs, int max_pairs) {
+  int count = 0;
+  const int st = guarded([&] {
+    const auto v = rtnb::legal_configs(total, a_cap);
+    count = static_cast<int>(v.size());
+    for (int i = 0; i < count && i < max_pairs; ++i) {
+      out_pairs[2 * i] = v[static_cast<size_t>(i)].first;
+      out_pairs[2 * i + 1] = v[static_cast<size_t>(i)].second;
+    }
+  });
+  return st == 0 ? count : -st;
+}
+
+int rtn_frames_bucket(int frames, int* out) {
+  return guarded([&] { *out = rtnb::frames_bucket(frames); });
+}
+
+int rtn_select_config(const int* key4, const int* rows6, const double* ms, int n, int* out_ta) {
+  return guarded([&] {
+    const auto r = rtnb::select_config(key_of(key4), records(rows6, ms, n));
+    out_ta[0] = r.first;
+    out_ta[1] = r.second;
+  });
+}
+
+int rtn_learn_step(const int* key4, const int* rows6, const double* ms, int n, int total, int a_cap,
+                   int* out_ta) {
+  return guarded([&] {
+    const auto r = rtnb::learn_step(key_of(key4), records(rows6, ms, n), total, a_cap);
+    out_ta[0] = r.first;
+    out_ta[1] = r.second;
+  });
+}
+
+int rtn_tunedb_append(const char* path, const int* row6, double runtime_ms, int64_t timestamp) {
+  return guarded([&] {
+    rtnb::TuningRecord r = records(row6, &runtime_ms, 1)[0];
+    r.timestamp = timestamp;
+    rtnb::TuneDb(path).append(r);
+  });
+}
+
+int rtn_tunedb_load(const char* path, int* rows6, double* ms, int64_t* ts, int max_rows, int* n_rows,
+                    int* skipped) {
+  return guarded([&] {
+    rtnb::TuneDb db(path);
+    const auto v = db.load();
+    *n_rows = static_cast<int>(v.size());
+    if (skipped) *skipped = static_cast<int>(db.skipped_lines());
+    for (int i = 0; i < static_cast<int>(v.size()) && i < max_rows; ++i) {
+      const auto& r = v[static_cast<size_t>(i)];
+      rows6[6 * i] = static_cast<int>(r.key.mode);
+      rows6[6 * i + 1] = r.key.N;
+      rows6[6 * i + 2] = r.key.bucket;
+      rows6[6 * i + 3] = r.key.J;
+      rows6[6 * i + 4] = r.T;
+      rows6[6 * i + 5] = r.A;
+      ms[i] = r.runtime_ms;
+      if (ts) ts[i] = r.timestamp;
+    }
+  });
+}
+
+int rtn_time_kernel(rtn_ctx* ctx, const char* which, int reps, double* ms, double* bytes) {
+  return guarded([&] {
+    *ms = eng(ctx).time_kernel(which, reps);
+    if (bytes) *bytes = eng(ctx).kernel_bytes(which);
   });
 }
 

@@ -351,7 +351,11 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), dev_(device) {
 Engine::~Engine() {
   cudaSetDevice(dev_);
   cudaStreamSynchronize(s_);
-  void* bufs[] = {winv_, P_, z_, x_, xcg_, r_, p_, ap_, ar_, est_scratch_[0], est_scratch_[1],
+  for (auto& g : step_graph_) {
+    if (g) cudaGraphExecDestroy(g);
+  }
+  if (frame_graph_) cudaGraphExecDestroy(frame_graph_);
+  void* bufs[] = {winv_, P_, z_, x_, xcg_, r_, p_, ap_, ar_, reg_, est_scratch_[0], est_scratch_[1],
                   est_scratch_[2], coils_, rhom_, U_, V_, RC_, Y_, gbuf_, img_, partials_, st_, cr_buf_};
   for (void* b : bufs) {
     if (b) cudaFree(b);
@@ -385,7 +389,7 @@ void Engine::alloc() {
   twG_ = twiddles_for(plan_.G, dev_);
   c2(&P_, G2, "psf");
   c2(&z_, J * G2, "z");
-  for (float2** b : {&x_, &xcg_, &r_, &p_, &ap_, &ar_, &est_scratch_[0], &est_scratch_[1], &est_scratch_[2]}) {
+  for (float2** b : {&x_, &xcg_, &r_, &p_, &ap_, &ar_, &reg_, &est_scratch_[0], &est_scratch_[1], &est_scratch_[2]}) {
     c2(b, static_cast<size_t>(D_), "estimate");
   }
   c2(&coils_, J * G2, "coils");
@@ -405,6 +409,19 @@ void Engine::alloc() {
   check_cuda(cudaMallocHost(&st_host_, sizeof(DevState)), "state mirror");
   std::memset(st_host_, 0, sizeof(DevState));
   ensure_cr_capacity(std::max({plan_.cg_max_iter, plan_.cg_iter_budget, 1}));
+  // alpha schedule and budget split are data independent (nlinv.cpp:295-313)
+  float alpha = plan_.alpha0;
+  int remaining = plan_.cg_iter_budget;
+  for (int m = 0; m < plan_.newton_steps; ++m) {
+    alphas_.push_back(alpha);
+    if (plan_.cg_iter_budget > 0) {
+      const int left = plan_.newton_steps - m;
+      const int cap = (remaining + left - 1) / left;
+      caps_.push_back(cap);
+      remaining -= cap;
+    }
+    alpha = std::max(alpha * plan_.alpha_q, plan_.alpha_min);
+  }
 }
 
 void Engine::ensure_cr_capacity(int max_iter) {
@@ -522,10 +539,7 @@ void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
 void Engine::enq_newton_step(int m, float2* x, const float2* reg, float alpha, float tol, int cap,
                              bool sync_each) {
   enq_step_begin(m);
-  {
-    fft_book(CTX_SETUP, 4ull * plan_.J);
-    enq_setup(x, reg, alpha);
-  }
+  enq_setup(x, reg, alpha);
   if (cap >= 1) {
     if (sync_each) {
       read_state();
@@ -653,6 +667,7 @@ void Engine::newton_step(float* x, const float* reg, float alpha, float tol, int
   check_cuda(cudaMemcpyAsync(est_scratch_[1], reg, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
   check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
   const int ctx_n = CTX_NORMAL_OP;
+  fft_book(CTX_SETUP, 4ull * plan_.J);
   enq_newton_step(0, x_, est_scratch_[1], alpha, tol, cap, true);
   read_state();
   raise_status("newton_step");
@@ -667,93 +682,131 @@ void Engine::newton_step(float* x, const float* reg, float alpha, float tol, int
 
 // ---- frame pipeline -------------------------------------------------------------
 
-void Engine::enqueue_frame(float2* x_dev, const RegFn& reg_dev, float2* image_dev, float image_scale,
-                           bool apply_scale, FrameStats* stats) {
-  const int M = plan_.newton_steps;
-  check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
-  float alpha = plan_.alpha0;
-  int remaining = plan_.cg_iter_budget;
-  const bool budget = plan_.cg_iter_budget > 0;
-  spec_caps_.assign(static_cast<size_t>(M), 0);
-  for (int m = 0; m < M; ++m) {
-    int cap = plan_.cg_max_iter;
-    float tol = plan_.cg_tol;
-    if (budget) {
-      const int steps_left = M - m;
-      cap = (remaining + steps_left - 1) / steps_left;  // nlinv.cpp:301-306
-      tol = 0.0f;
-    }
-    const float2* reg = reg_dev(m);
-    enq_newton_step(m, x_dev, reg, alpha, tol, cap, !budget);
-    if (!budget) {
-      read_state();
-      raise_status("reconstruct_frame");
-      cap = st_host_->steps[m].iters;
-    }
-    spec_caps_[static_cast<size_t>(m)] = cap;
-    fft_book(CTX_NORMAL_OP, 4ull * plan_.J * static_cast<uint64_t>(cap));
-    if (budget) remaining -= cap;
-    alpha = std::max(alpha * plan_.alpha_q, plan_.alpha_min);
-  }
-  fft_book(CTX_SETUP, static_cast<uint64_t>(plan_.J));
-  enq_image(x_dev, image_dev, image_scale, apply_scale);
-  check_cuda(cudaMemcpyAsync(st_host_, st_, sizeof(DevState), cudaMemcpyDeviceToHost, s_), "state read");
-  check_cuda(cudaGetLastError(), "frame launch");
-  if (stats) {
-    stats->cg_per_step = spec_caps_;
-    stats->cg_iters = 0;
-    for (int c : spec_caps_) stats->cg_iters += c;
-  }
+void Engine::book_frame_ffts(const std::vector<int>& iters) {
+  // per frame: 4J per step (setup), 4J per CR iteration (normal_op), J final decode
+  uint64_t n = 0;
+  for (int c : iters) n += static_cast<uint64_t>(c);
+  fft_book(CTX_SETUP, 4ull * plan_.J * iters.size() + plan_.J);
+  fft_book(CTX_NORMAL_OP, 4ull * plan_.J * n);
 }
 
-bool Engine::finish_frame(FrameStats* stats) {
+void Engine::frame_begin() { check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset"); }
+
+void Engine::frame_step(int m, const float2* reg_src) {
+  if (reg_src && reg_src != reg_) {
+    check_cuda(cudaMemcpyAsync(reg_, reg_src, sizeof(float2) * D_, cudaMemcpyDeviceToDevice, s_), "reg copy");
+  }
+  if (!budget_mode()) {
+    // tolerance mode: data-dependent iteration counts, synchronous CR
+    enq_newton_step(m, x_, reg_, alphas_[static_cast<size_t>(m)], plan_.cg_tol, plan_.cg_max_iter, true);
+    return;
+  }
+  const int cap = caps_[static_cast<size_t>(m)];
+  if (!use_graphs_) {
+    enq_newton_step(m, x_, reg_, alphas_[static_cast<size_t>(m)], 0.0f, cap, false);
+    return;
+  }
+  if (!step_graph_[m]) {
+    cudaGraph_t g = nullptr;
+    check_cuda(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal), "capture begin");
+    enq_newton_step(m, x_, reg_, alphas_[static_cast<size_t>(m)], 0.0f, cap, false);
+    check_cuda(cudaStreamEndCapture(s_, &g), "capture end");
+    check_cuda(cudaGraphInstantiate(&step_graph_[m], g, 0), "graph instantiate");
+    cudaGraphDestroy(g);
+  }
+  check_cuda(cudaGraphLaunch(step_graph_[m], s_), "graph launch");
+}
+
+void Engine::frame_image(float2* img_dst, float image_scale, bool apply_scale) {
+  enq_image(x_, img_dst ? img_dst : img_, image_scale, apply_scale);
+  check_cuda(cudaMemcpyAsync(st_host_, st_, sizeof(DevState), cudaMemcpyDeviceToHost, s_), "state read");
+}
+
+void Engine::frame_all(float2* img_dst, float image_scale, bool apply_scale) {
+  if (!budget_mode()) fail(2, "frame_all: whole-frame graphs need the CG iteration budget mode");
+  float2* img = img_dst ? img_dst : img_;
+  if (!use_graphs_) {
+    frame_begin();
+    for (int m = 0; m < plan_.newton_steps; ++m) frame_step(m, nullptr);
+    frame_image(img, image_scale, apply_scale);
+    return;
+  }
+  if (frame_graph_ && (frame_graph_img_ != img || frame_graph_scale_ != image_scale ||
+                       frame_graph_apply_ != apply_scale)) {
+    cudaGraphExecDestroy(frame_graph_);
+    frame_graph_ = nullptr;
+  }
+  if (!frame_graph_) {
+    cudaGraph_t g = nullptr;
+    check_cuda(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal), "capture begin");
+    frame_begin();
+    for (int m = 0; m < plan_.newton_steps; ++m) {
+      enq_newton_step(m, x_, reg_, alphas_[static_cast<size_t>(m)], 0.0f, caps_[static_cast<size_t>(m)], false);
+    }
+    enq_image(x_, img, image_scale, apply_scale);
+    check_cuda(cudaMemcpyAsync(st_host_, st_, sizeof(DevState), cudaMemcpyDeviceToHost, s_), "state read");
+    check_cuda(cudaStreamEndCapture(s_, &g), "capture end");
+    check_cuda(cudaGraphInstantiate(&frame_graph_, g, 0), "graph instantiate");
+    cudaGraphDestroy(g);
+    frame_graph_img_ = img;
+    frame_graph_scale_ = image_scale;
+    frame_graph_apply_ = apply_scale;
+  }
+  check_cuda(cudaGraphLaunch(frame_graph_, s_), "graph launch");
+}
+
+bool Engine::frame_verify(FrameStats* stats) {
   sync();
   raise_status("reconstruct_frame");
   const int M = plan_.newton_steps;
+  std::vector<int> got(static_cast<size_t>(M));
   bool ok = true;
   for (int m = 0; m < M; ++m) {
-    if (st_host_->steps[m].iters != spec_caps_[static_cast<size_t>(m)] || st_host_->steps[m].zero_rhs) ok = false;
+    got[static_cast<size_t>(m)] = st_host_->steps[m].iters;
+    if (budget_mode() && (st_host_->steps[m].iters != caps_[static_cast<size_t>(m)] || st_host_->steps[m].zero_rhs)) {
+      ok = false;
+    }
   }
-  if (!ok) {
-    // undo the speculative booking; the synchronous re-run books the real counts
-    uint64_t n = 0;
-    for (int c : spec_caps_) n += static_cast<uint64_t>(c);
-    g_counts[CTX_NORMAL_OP].fetch_sub(4ull * plan_.J * n);
-    g_counts[CTX_SETUP].fetch_sub(4ull * plan_.J * M + plan_.J);
+  if (ok) {
+    book_frame_ffts(got);
+    if (stats) {
+      stats->cg_per_step = got;
+      stats->cg_iters = 0;
+      for (int c : got) stats->cg_iters += c;
+    }
   }
-  (void)stats;
   return ok;
 }
 
-void Engine::run_frame_sync(float2* x_dev, const RegFn& reg_dev, float2* image_dev, float image_scale,
-                            bool apply_scale, FrameStats* stats) {
+void Engine::frame_run_sync(const RegFn& reg, float2* img_dst, float image_scale, bool apply_scale,
+                            FrameStats* stats) {
   const int M = plan_.newton_steps;
-  check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
-  float alpha = plan_.alpha0;
+  frame_begin();
   int remaining = plan_.cg_iter_budget;
-  const bool budget = plan_.cg_iter_budget > 0;
   std::vector<int> per;
   for (int m = 0; m < M; ++m) {
     int cap = plan_.cg_max_iter;
     float tol = plan_.cg_tol;
-    if (budget) {
-      const int steps_left = M - m;
-      cap = (remaining + steps_left - 1) / steps_left;
+    if (budget_mode()) {
+      const int left = M - m;
+      cap = (remaining + left - 1) / left;
       tol = 0.0f;
     }
-    enq_newton_step(m, x_dev, reg_dev(m), alpha, tol, cap, true);
+    const float2* src = reg ? reg(m) : nullptr;
+    if (src && src != reg_) {
+      check_cuda(cudaMemcpyAsync(reg_, src, sizeof(float2) * D_, cudaMemcpyDeviceToDevice, s_), "reg copy");
+    }
+    enq_newton_step(m, x_, reg_, alphas_[static_cast<size_t>(m)], tol, cap, true);
     read_state();
     raise_status("reconstruct_frame");
     const int it = st_host_->steps[m].iters;
-    fft_book(CTX_NORMAL_OP, 4ull * plan_.J * static_cast<uint64_t>(it));
     per.push_back(it);
-    if (budget) remaining -= it;
-    alpha = std::max(alpha * plan_.alpha_q, plan_.alpha_min);
+    if (budget_mode()) remaining -= it;
   }
-  fft_book(CTX_SETUP, static_cast<uint64_t>(plan_.J));
-  enq_image(x_dev, image_dev, image_scale, apply_scale);
+  enq_image(x_, img_dst ? img_dst : img_, image_scale, apply_scale);
   read_state();
   raise_status("reconstruct_frame");
+  book_frame_ffts(per);
   if (stats) {
     stats->cg_per_step = per;
     stats->cg_iters = 0;
@@ -765,20 +818,76 @@ void Engine::reconstruct_frame(const float* init, const float* reg, float* image
                                FrameStats* stats) {
   const auto t0 = std::chrono::steady_clock::now();
   check_cuda(cudaMemcpyAsync(x_, init, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
-  check_cuda(cudaMemcpyAsync(est_scratch_[1], reg ? reg : init, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_),
-             "h2d");
-  float2* regp = est_scratch_[1];
-  const RegFn rf = [regp](int) -> const float2* { return regp; };
-  enqueue_frame(x_, rf, img_, 1.0f, false, stats);
-  if (!finish_frame(stats)) {
+  check_cuda(cudaMemcpyAsync(reg_, reg ? reg : init, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
+  bool ok = false;
+  if (budget_mode()) {
+    frame_all(img_, 1.0f, false);
+    ok = frame_verify(stats);
+  }
+  if (!ok) {
     check_cuda(cudaMemcpyAsync(x_, init, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
-    run_frame_sync(x_, rf, img_, 1.0f, false, stats);
+    frame_run_sync(nullptr, img_, 1.0f, false, stats);
   }
   check_cuda(cudaMemcpyAsync(image, img_, sizeof(float2) * plan_.N * plan_.N, cudaMemcpyDeviceToHost, s_), "d2h");
   if (est_out) check_cuda(cudaMemcpyAsync(est_out, x_, sizeof(float2) * D_, cudaMemcpyDeviceToHost, s_), "d2h");
   sync();
   have_cache_ = true;
   if (stats) stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ---- isolated kernel timing (bench roofline) ------------------------------------------
+
+double Engine::kernel_bytes(const char* which) const {
+  // algorithmic bytes: every operand read once, every result written once
+  const double c8 = 8.0;
+  const double J = plan_.J, G = plan_.G, L = dims_.L, Gc = plan_.Gc;
+  const std::string w(which);
+  if (w == "colsT") return c8 * (2.0 * J * L * G + G * G);                   // V in + out, P
+  if (w == "rows1") return c8 * (J * L * Gc + 2.0 * J * L * L + 2.0 * L * L + J * L * G);  // U, c_j, drho, rho, V
+  if (w == "rows2") return c8 * (J * L * G + J * L * L + L * L + J * L * L + J * L * Gc);  // V, c_j, rho, RC, Y
+  if (w == "colA") return c8 * (J * Gc * Gc + J * L * Gc) + 4.0 * Gc * Gc;
+  if (w == "colsW") return c8 * (J * L * Gc + J * L * L + 2.0 * (G * G + J * Gc * Gc)) + 4.0 * Gc * Gc;
+  if (w == "apply") {
+    // one fused normal-operator application (SURVEY.md §8(d) B_op, window pruned)
+    return 8.0 * L * L * (J + 3) + 8.0 * G * G + 16.0 * J * Gc * Gc + 4.0 * Gc * Gc;
+  }
+  return 0.0;
+}
+
+double Engine::time_kernel(const char* which, int reps) {
+  if (!have_cache_) fail(2, "time_kernel: no step cache");
+  const std::string w(which);
+  const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
+  const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
+  check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
+  auto launch = [&] {
+    if (w == "colsT") {
+      ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, 0);
+    } else if (w == "rows1") {
+      ops_->rows1(s_, J * tL, dims_, R1_OP, twG_, U_, coils_, rhom_, r_, V_, nullptr, nullptr, nullptr, st_, 0);
+    } else if (w == "rows2") {
+      ops_->rows2(s_, J * tL, dims_, R2_OP, twG_, V_, coils_, rhom_, z_, RC_, Y_, partials_, st_, 0);
+    } else if (w == "colA") {
+      ops_->colA(s_, J * tGc, dims_, winv_, twG_, r_ + static_cast<size_t>(G) * G, U_, dims_.lo, dims_.L, st_, 0);
+    } else if (w == "apply") {
+      enq_apply(r_, ar_, CW_OP, 0.f, -1, 0);
+    } else {
+      fail(2, "time_kernel: unknown kernel " + w);
+    }
+  };
+  for (int i = 0; i < 3; ++i) launch();
+  cudaEvent_t a, b;
+  check_cuda(cudaEventCreate(&a), "event");
+  check_cuda(cudaEventCreate(&b), "event");
+  check_cuda(cudaEventRecord(a, s_), "event");
+  for (int i = 0; i < reps; ++i) launch();
+  check_cuda(cudaEventRecord(b, s_), "event");
+  check_cuda(cudaEventSynchronize(b), "event sync");
+  float ms = 0;
+  check_cuda(cudaEventElapsedTime(&ms, a, b), "elapsed");
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return ms / reps;
 }
 
 }  // namespace rtnb

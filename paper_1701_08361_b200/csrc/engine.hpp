@@ -97,24 +97,41 @@ class Engine {
                          FrameStats* stats);
 
   // ---- device-resident frame pipeline ----
-  // Enqueue a whole frame on the stream: x_dev holds init on entry and the final
-  // estimate on exit; reg_dev(m) supplies the regularisation target of step m.
-  // Budget mode is enqueued speculatively (every step runs its cap) and verified by
-  // finish_frame(); tolerance mode synchronises per iteration.
-  using RegFn = std::function<const float2*(int m)>;
-  void enqueue_frame(float2* x_dev, const RegFn& reg_dev, float2* image_dev, float image_scale,
-                     bool apply_scale, FrameStats* stats);
-  // Synchronise and validate the enqueued frame; returns false when a step ended
-  // early (zero right-hand side) so the speculative budget split was wrong and the
-  // frame must be re-run with run_frame_sync().
-  bool finish_frame(FrameStats* stats);
-  void run_frame_sync(float2* x_dev, const RegFn& reg_dev, float2* image_dev, float image_scale,
-                      bool apply_scale, FrameStats* stats);
+  // A frame runs on the engine's own buffers: x (estimate; holds init on entry and
+  // the final estimate on exit), reg (regularisation target), z / P (frame data).
+  // Budget mode (plan.cg_iter_budget > 0) is enqueued speculatively from CUDA
+  // graphs captured once per engine: every step runs its budget cap
+  // ceil(remaining / steps_left) (nlinv.cpp:301-306), which is exact unless a step
+  // meets an exactly-zero right-hand side; frame_verify() detects that and the
+  // caller re-runs the frame with frame_run_sync(). Tolerance mode synchronises per
+  // CR iteration and never uses graphs.
+  using RegFn = std::function<const float2*(int m)>;  // device pointer of reg(m), or nullptr = keep reg
+  void frame_begin();
+  void frame_step(int m, const float2* reg_src);        // enqueue Newton step m
+  void frame_image(float2* img_dst, float image_scale, bool apply_scale);
+  void frame_all(float2* img_dst, float image_scale, bool apply_scale);  // budget mode: one graph
+  bool frame_verify(FrameStats* stats);                 // sync + check the speculative split
+  void frame_run_sync(const RegFn& reg, float2* img_dst, float image_scale, bool apply_scale,
+                      FrameStats* stats);
+  bool budget_mode() const { return plan_.cg_iter_budget > 0; }
+  const std::vector<int>& budget_caps() const { return caps_; }
+  void set_use_graphs(bool on) { use_graphs_ = on; }
 
   float2* x_dev() { return x_; }
-  float2* scratch_est(int i) { return est_scratch_[i]; }
+  float2* reg_dev() { return reg_; }
+  float2* z_dev() { return z_; }
+  float2* psf_dev() { return P_; }
   float2* image_dev() { return img_; }
+  DevState* state_dev() { return st_; }
+  const DevState& state_host() const { return *st_host_; }
+  void read_state();
   void sync();
+
+  // isolated timing of one kernel class (bench roofline): average ms per launch of
+  // `reps` back-to-back launches on the engine stream, CUDA events
+  double time_kernel(const char* which, int reps);
+  // algorithmic bytes one launch of that kernel moves
+  double kernel_bytes(const char* which) const;
 
  public:
   struct Ops;  // per-grid-size kernel launchers (engine.cu)
@@ -130,8 +147,8 @@ class Engine {
   void enq_newton_step(int m, float2* x, const float2* reg, float alpha, float tol, int cap,
                        bool sync_each);
   void enq_image(const float2* est, float2* img, float scale, bool apply_scale);
-  void read_state();
   void raise_status(const char* where);
+  void book_frame_ffts(const std::vector<int>& iters);
 
   Plan plan_;
   Dims dims_{};
@@ -154,6 +171,7 @@ class Engine {
   float2* ap_ = nullptr;
   float2* ar_ = nullptr;
   float2* est_scratch_[3] = {nullptr, nullptr, nullptr};
+  float2* reg_ = nullptr;
   float2* coils_ = nullptr;
   float2* rhom_ = nullptr;
   float2* U_ = nullptr;
@@ -169,7 +187,14 @@ class Engine {
   int cr_cap_ = 0;
   CrScalars cr_{};
   bool have_cache_ = false;
-  std::vector<int> spec_caps_;
+  std::vector<int> caps_;       // budget-mode per-step caps
+  std::vector<float> alphas_;   // per-step alpha schedule
+  bool use_graphs_ = true;
+  cudaGraphExec_t step_graph_[kMaxSteps] = {};
+  cudaGraphExec_t frame_graph_ = nullptr;
+  float2* frame_graph_img_ = nullptr;
+  float frame_graph_scale_ = 0.f;
+  bool frame_graph_apply_ = false;
 };
 
 }  // namespace rtnb

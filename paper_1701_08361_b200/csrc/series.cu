@@ -1,0 +1,299 @@
+// Series drivers over device-resident frames (nlinv.cpp:366-526).
+#include "series.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <thread>
+
+namespace rtnb {
+
+namespace {
+
+__global__ void k_nrm2_frame(const float2* __restrict__ z, long long n, double* out) {
+  // single block, fixed order: deterministic FP64 |z|^2 of one frame
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const float2 v = z[i];
+    acc += (double)v.x * v.x + (double)v.y * v.y;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+__global__ void k_scale_frames(float2* __restrict__ z, long long n, float s) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float2 v = z[i];
+    z[i] = make_float2(v.x * s, v.y * s);
+  }
+}
+
+}  // namespace
+
+Series::Series(Engine& primary, int frames, int n_psf) : eng0_(primary), F_(frames), n_psf_(n_psf) {
+  if (frames < 1) fail(2, "reconstruct_series: no frames");
+  if (n_psf < 1) fail(2, "reconstruct_series: need at least one PSF");
+  const Plan& p = eng0_.plan();
+  D_ = eng0_.D();
+  zsz_ = static_cast<size_t>(p.J) * p.G * p.G;
+  psz_ = static_cast<size_t>(p.G) * p.G;
+  isz_ = static_cast<size_t>(p.N) * p.N;
+  check_cuda(cudaSetDevice(eng0_.device()), "set device");
+  check_cuda(cudaMalloc(&z_, sizeof(float2) * zsz_ * F_), "series frames");
+  check_cuda(cudaMalloc(&psf_, sizeof(float2) * psz_ * n_psf_), "series psf");
+  check_cuda(cudaMalloc(&ests_, sizeof(float2) * static_cast<size_t>(D_) * F_), "series estimates");
+  check_cuda(cudaMalloc(&unity_, sizeof(float2) * D_), "unity");
+  check_cuda(cudaMalloc(&images_, sizeof(float2) * isz_ * F_), "series images");
+  check_cuda(cudaMalloc(&nsq_, sizeof(double)), "nsq");
+  check_cuda(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "copy stream");
+  // initial_estimate: rho = 1 on the window, coils 0 (nlinv.cpp:60-70)
+  std::vector<float2> u(static_cast<size_t>(D_), make_float2(0.f, 0.f));
+  const int L = p.G / 2, lo = (p.G - L) / 2;
+  for (int r = lo; r < lo + L; ++r) {
+    for (int c = lo; c < lo + L; ++c) u[static_cast<size_t>(r) * p.G + c] = make_float2(1.f, 0.f);
+  }
+  check_cuda(cudaMemcpy(unity_, u.data(), sizeof(float2) * D_, cudaMemcpyHostToDevice), "unity upload");
+  psf_idx_.resize(static_cast<size_t>(F_));
+  for (int n = 0; n < F_; ++n) psf_idx_[static_cast<size_t>(n)] = n % n_psf_;
+}
+
+Series::~Series() {
+  cudaSetDevice(eng0_.device());
+  for (void* b : {static_cast<void*>(z_), static_cast<void*>(psf_), static_cast<void*>(ests_),
+                  static_cast<void*>(unity_), static_cast<void*>(images_), static_cast<void*>(nsq_)}) {
+    if (b) cudaFree(b);
+  }
+  if (copy_) cudaStreamDestroy(copy_);
+}
+
+Engine& Series::worker(int t) {
+  if (t == 0) return eng0_;
+  while (static_cast<int>(extra_.size()) < t) {
+    extra_.push_back(std::make_unique<Engine>(eng0_.plan(), eng0_.device()));
+  }
+  return *extra_[static_cast<size_t>(t - 1)];
+}
+
+void Series::upload_frames(int first, int count, const float* z_host) {
+  if (first < 0 || count < 0 || first + count > F_) fail(2, "upload_frames: frame range out of bounds");
+  check_cuda(cudaSetDevice(eng0_.device()), "set device");
+  check_cuda(cudaMemcpy(z_ + zsz_ * first, z_host, sizeof(float2) * zsz_ * count, cudaMemcpyHostToDevice),
+             "frame upload");
+  if (first == 0) normalized_ = false;
+}
+
+void Series::upload_psf(int k, const float* P_host) {
+  if (k < 0 || k >= n_psf_) fail(2, "upload_psf: index out of range");
+  check_cuda(cudaMemcpy(psf_ + psz_ * k, P_host, sizeof(float2) * psz_, cudaMemcpyHostToDevice), "psf upload");
+}
+
+void Series::set_psf_index(const int* idx) {
+  for (int n = 0; n < F_; ++n) {
+    if (idx[n] < 0 || idx[n] >= n_psf_) fail(2, "set_psf_index: index out of range");
+    psf_idx_[static_cast<size_t>(n)] = idx[n];
+  }
+}
+
+double Series::normalize() {
+  if (normalized_) return scale_;
+  check_cuda(cudaSetDevice(eng0_.device()), "set device");
+  k_nrm2_frame<<<1, 256>>>(z_, static_cast<long long>(zsz_), nsq_);
+  double nsq = 0;
+  check_cuda(cudaMemcpy(&nsq, nsq_, sizeof(double), cudaMemcpyDeviceToHost), "nsq read");
+  scale_ = 1.0;
+  if (nsq > 0) {
+    scale_ = 100.0 / std::sqrt(nsq);
+    k_scale_frames<<<148 * 8, 256>>>(z_, static_cast<long long>(zsz_) * F_, static_cast<float>(scale_));
+    check_cuda(cudaDeviceSynchronize(), "normalise");
+  }
+  normalized_ = true;
+  return scale_;
+}
+
+void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& ledger, SeriesFrameOut& out,
+                       cudaEvent_t ready) {
+  Engine& e = worker(t);
+  const Plan& p = e.plan();
+  const int M = p.newton_steps;
+  cudaStream_t s = e.stream();
+  const bool chained = o.chain && n > 0;
+  FrameAudit a;
+  a.frame = n;
+  a.thread = t;
+  a.workers = o.A;
+  a.reg_src.assign(static_cast<size_t>(M), -1);
+  if (!o.plain) {
+    // frames in the strict prefix start only after the predecessor finished
+    if (chained && n <= o.sched.l) ledger.wait_complete(n - 1);
+    a.start_seq = ledger.next_seq();
+  }
+  if (chained) a.init_src = o.plain ? n - 1 : h_choose(n, 0, M, o.sched, ledger);
+  const float2* init = chained ? estimate_dev(a.init_src) : unity_;
+
+  if (ready) check_cuda(cudaStreamWaitEvent(s, ready, 0), "wait frame upload");
+  check_cuda(cudaMemcpyAsync(e.z_dev(), z_ + zsz_ * n, sizeof(float2) * zsz_, cudaMemcpyDeviceToDevice, s), "z");
+  check_cuda(cudaMemcpyAsync(e.psf_dev(), psf_ + psz_ * psf_idx_[static_cast<size_t>(n)], sizeof(float2) * psz_,
+                             cudaMemcpyDeviceToDevice, s),
+             "psf");
+  check_cuda(cudaMemcpyAsync(e.x_dev(), init, sizeof(float2) * D_, cudaMemcpyDeviceToDevice, s), "init");
+  cudaEvent_t ev0, ev1;
+  check_cuda(cudaEventCreate(&ev0), "event");
+  check_cuda(cudaEventCreate(&ev1), "event");
+  check_cuda(cudaEventRecord(ev0, s), "event");
+  float2* img = images_ + isz_ * n;
+  const float iscale = static_cast<float>(1.0 / scale_);
+  const bool undo = o.normalize && scale_ != 1.0;
+  const bool fixed_reg = o.plain || !chained;  // every step regularises towards init
+  if (fixed_reg) {
+    for (int m = 0; m < M; ++m) a.reg_src[static_cast<size_t>(m)] = chained ? a.init_src : -1;
+    check_cuda(cudaMemcpyAsync(e.reg_dev(), init, sizeof(float2) * D_, cudaMemcpyDeviceToDevice, s), "reg");
+    if (!o.plain && M > 0) a.reg_final_seq = ledger.next_seq();
+    if (e.budget_mode()) {
+      e.frame_all(img, iscale, undo);
+    } else {
+      e.frame_begin();
+      for (int m = 0; m < M; ++m) e.frame_step(m, nullptr);
+      e.frame_image(img, iscale, undo);
+    }
+  } else {
+    e.frame_begin();
+    for (int m = 0; m < M; ++m) {
+      const int src = h_choose(n, m, M, o.sched, ledger);
+      if (m == M - 1) a.reg_final_seq = ledger.next_seq();
+      a.reg_src[static_cast<size_t>(m)] = src;
+      e.frame_step(m, estimate_dev(src));
+      if (o.T > 1) e.sync();  // the next step's source is chosen when it is about to run
+      ledger.mark_step(n, m);
+    }
+    e.frame_image(img, iscale, undo);
+  }
+  check_cuda(cudaEventRecord(ev1, s), "event");
+  FrameStats fs;
+  if (!e.frame_verify(&fs)) {
+    // a step met an exactly-zero right-hand side: redo with the true budget split,
+    // replaying the recorded regularisation sources
+    check_cuda(cudaMemcpyAsync(e.x_dev(), init, sizeof(float2) * D_, cudaMemcpyDeviceToDevice, s), "init");
+    const std::vector<int> srcs = a.reg_src;
+    const float2* u = unity_;
+    Engine::RegFn rf = [this, srcs, u](int m) -> const float2* {
+      const int sidx = srcs[static_cast<size_t>(m)];
+      return sidx >= 0 ? estimate_dev(sidx) : u;
+    };
+    e.frame_run_sync(rf, img, iscale, undo, &fs);
+    check_cuda(cudaEventRecord(ev1, s), "event");
+  }
+  check_cuda(cudaMemcpyAsync(estimate_dev(n), e.x_dev(), sizeof(float2) * D_, cudaMemcpyDeviceToDevice, s),
+             "estimate");
+  e.sync();
+  float ms = 0;
+  check_cuda(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  a.reg_final_src = chained ? a.reg_src[static_cast<size_t>(M - 1)] : -1;
+  if (!o.plain) a.finish_seq = ledger.next_seq();
+  out.audit = a;
+  out.cg_iters = fs.cg_iters;
+  out.gpu_ms = ms;
+  ledger.mark_complete(n);
+}
+
+void Series::run(const SeriesOptions& o, int first, int count, const float* z_host, float* images_host,
+                 std::vector<SeriesFrameOut>* out) {
+  if (first < 0 || count < 1 || first + count > F_) fail(2, "reconstruct_series: frame range out of bounds");
+  if (o.T < 1) fail(2, "reconstruct_series: thread count out of range");
+  if (o.A < 1 || o.A > kGroupSizeMaxDevice) fail(2, "reconstruct_series: workers per thread out of range");
+  const int dev = eng0_.device();
+  check_cuda(cudaSetDevice(dev), "set device");
+  const Plan& p = eng0_.plan();
+  const int T = o.plain ? 1 : std::min(o.T, count);
+  for (int t = 1; t < T; ++t) worker(t);
+
+  // end-to-end path: stream frames from host on the copy stream, normalise on arrival
+  std::vector<cudaEvent_t> ready;
+  if (z_host) {
+    ready.resize(static_cast<size_t>(count));
+    int k0 = 0;
+    if (first == 0) {
+      check_cuda(cudaMemcpyAsync(z_, z_host, sizeof(float2) * zsz_, cudaMemcpyHostToDevice, copy_), "frame 0");
+      check_cuda(cudaStreamSynchronize(copy_), "frame 0");
+      normalized_ = false;
+      if (o.normalize) {
+        k_nrm2_frame<<<1, 256, 0, copy_>>>(z_, static_cast<long long>(zsz_), nsq_);
+        double nsq = 0;
+        check_cuda(cudaMemcpyAsync(&nsq, nsq_, sizeof(double), cudaMemcpyDeviceToHost, copy_), "nsq");
+        check_cuda(cudaStreamSynchronize(copy_), "nsq");
+        scale_ = nsq > 0 ? 100.0 / std::sqrt(nsq) : 1.0;
+      } else {
+        scale_ = 1.0;
+      }
+    }
+    for (int k = k0; k < count; ++k) {
+      const int n = first + k;
+      if (!(n == 0 && first == 0)) {
+        check_cuda(cudaMemcpyAsync(z_ + zsz_ * n, z_host + 2 * zsz_ * k, sizeof(float2) * zsz_,
+                                   cudaMemcpyHostToDevice, copy_),
+                   "frame upload");
+      }
+      if (o.normalize && scale_ != 1.0) {
+        k_scale_frames<<<148 * 2, 256, 0, copy_>>>(z_ + zsz_ * n, static_cast<long long>(zsz_),
+                                                   static_cast<float>(scale_));
+      }
+      check_cuda(cudaEventCreateWithFlags(&ready[static_cast<size_t>(k)], cudaEventDisableTiming), "event");
+      check_cuda(cudaEventRecord(ready[static_cast<size_t>(k)], copy_), "event");
+    }
+    normalized_ = true;
+  } else if (o.normalize) {
+    normalize();
+  } else if (first == 0) {
+    scale_ = 1.0;
+  }
+
+  CompletionLedger ledger(F_);
+  for (int n = 0; n < first; ++n) ledger.mark_complete(n);
+  out->assign(static_cast<size_t>(count), SeriesFrameOut{});
+  std::mutex err_mu;
+  std::exception_ptr first_err;
+  auto thread_main = [&](int t) {
+    try {
+      check_cuda(cudaSetDevice(dev), "set device");
+      for (int k = t; k < count; k += T) {
+        if (ledger.poisoned()) return;
+        run_frame(t, first + k, o, ledger, (*out)[static_cast<size_t>(k)],
+                  ready.empty() ? nullptr : ready[static_cast<size_t>(k)]);
+        if (images_host) {
+          Engine& e = worker(t);
+          check_cuda(cudaMemcpyAsync(images_host + 2 * isz_ * k, images_ + isz_ * (first + k), sizeof(float2) * isz_,
+                                     cudaMemcpyDeviceToHost, e.stream()),
+                     "image d2h");
+          e.sync();
+        }
+      }
+    } catch (...) {
+      {
+        std::lock_guard<std::mutex> g(err_mu);
+        if (!first_err) first_err = std::current_exception();
+      }
+      ledger.poison();
+    }
+  };
+  if (T == 1) {
+    thread_main(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(thread_main, t);
+    thread_main(0);
+    for (auto& th : pool) th.join();
+  }
+  for (cudaEvent_t ev : ready) cudaEventDestroy(ev);
+  if (first_err) std::rethrow_exception(first_err);
+  (void)p;
+}
+
+}  // namespace rtnb

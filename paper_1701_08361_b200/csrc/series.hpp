@@ -1,0 +1,83 @@
+// Frame-series drivers: reconstruct_series_plain and
+// the temporally decomposed reconstruct_series (nlinv.cpp:412-526) over
+// device-resident frames.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "engine.hpp"
+#include "sched.hpp"
+
+namespace rtnb {
+
+struct SeriesOptions {
+  TemporalSchedule sched{1, 1};
+  int T = 1;            // frames in flight: one worker (stream + workspace) each
+  int A = 1;            // channel-decomposition width (1 on a single device)
+  bool chain = true;
+  bool normalize = true;
+  bool plain = false;   // reconstruct_series_plain semantics (strictly sequential)
+};
+
+struct SeriesFrameOut {
+  FrameAudit audit;
+  int cg_iters = 0;
+  float gpu_ms = 0;     // frame start -> image ready, CUDA events on the worker stream
+};
+
+// Owns the device-resident series store: gridded frames z[F][J][G][G], the PSF set
+// (a K-spoke, U-turn trajectory has at most U distinct kernels), per-frame final
+// estimates and images. Worker 0 is the caller's engine; T-1 more are created on the
+// same device on demand.
+class Series {
+ public:
+  Series(Engine& primary, int frames, int n_psf);
+  ~Series();
+  Series(const Series&) = delete;
+  Series& operator=(const Series&) = delete;
+
+  int frames() const { return F_; }
+  void upload_frames(int first, int count, const float* z_host);  // synchronous H2D
+  void upload_psf(int k, const float* P_host);
+  void set_psf_index(const int* idx);
+  // prep_series normalisation (nlinv.cpp:390-400): scale every frame so frame 0 has
+  // norm 100; returns the scale. Idempotent per upload.
+  double normalize();
+  double data_scale() const { return scale_; }
+
+  // Reconstruct frames [first, first + count). Frames before `first` count as
+  // complete (their estimates from earlier calls are the chain). When z_host is not
+  // null the frames are streamed from host memory inside the call (copy stream,
+  // overlapped with compute) and normalised on arrival: the end-to-end path.
+  // images_host (count*N*N) receives the images; nullable.
+  void run(const SeriesOptions& o, int first, int count, const float* z_host, float* images_host,
+           std::vector<SeriesFrameOut>* out);
+
+  float2* images_dev() { return images_; }
+  float2* estimate_dev(int n) { return ests_ + static_cast<size_t>(n) * D_; }
+
+ private:
+  Engine& worker(int t);
+  void run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& ledger, SeriesFrameOut& out,
+                 cudaEvent_t ready);
+
+  Engine& eng0_;
+  std::vector<std::unique_ptr<Engine>> extra_;
+  int F_ = 0, n_psf_ = 0, D_ = 0;
+  size_t zsz_ = 0, psz_ = 0, isz_ = 0;
+  float2* z_ = nullptr;
+  float2* psf_ = nullptr;
+  float2* ests_ = nullptr;
+  float2* unity_ = nullptr;
+  float2* images_ = nullptr;
+  double* nsq_ = nullptr;
+  std::vector<int> psf_idx_;
+  double scale_ = 1.0;
+  bool normalized_ = false;
+  cudaStream_t copy_ = nullptr;
+};
+
+}  // namespace rtnb

@@ -1,0 +1,170 @@
+"""Series drivers on the device: plain chaining, temporal decomposition (T frames in
+flight on one B200), the end-to-end host-streaming path, and audit-replay parity
+against the compiled reference (SURVEY.md §7 "audit replay")."""
+import numpy as np
+import pytest
+
+from helpers import rel_err
+
+pytestmark = pytest.mark.gpu
+
+FRAME_TOL = 1e-3
+
+
+def _series_inputs(ref, plan, F, K, U, noise=1e-4, seed=11):
+    samples, angles = ref.phantom_series(plan.J, F, K, U, plan.N, noise, seed)
+    z = np.stack([ref.grid_adjoint(plan, samples[n], angles[n]) for n in range(F)])
+    # a K-spoke U-turn trajectory revisits its angle set every U frames
+    P = np.stack([ref.build_psf(plan, angles[n], 2 * plan.N) for n in range(min(U, F))])
+    idx = [n % U for n in range(F)]
+    return samples, angles, z, P, idx
+
+
+def _small_plan(gpu, N, J, M, budget):
+    plan = gpu.make_plan(N, J)
+    plan.newton_steps, plan.cg_iter_budget = M, budget
+    return plan
+
+
+def _run(gpu, plan, z, P, idx, opts, **kw):
+    ctx = gpu.Context(plan)
+    s = gpu.Series(ctx, z.shape[0], P.shape[0])
+    s.upload_frames(z)
+    for k in range(P.shape[0]):
+        s.upload_psf(k, P[k])
+    s.set_psf_index(idx)
+    out = s.run(opts, **kw)
+    out["series"], out["ctx"] = s, ctx
+    return out
+
+
+def test_plain_series_matches_reference(gpu, ref):
+    plan = _small_plan(gpu, 24, 3, 7, 30)
+    samples, angles, z, P, idx = _series_inputs(ref, plan, F=6, K=11, U=5)
+    want = ref.reconstruct_series(plan, samples, angles, plain=True)
+    got = _run(gpu, plan, z, P, idx, gpu.SeriesOptions(plain=True))
+    for n in range(6):
+        assert rel_err(got["images"][n], want["images"][n]) < FRAME_TOL, n
+        a = got["audit"][n]
+        assert a.init_src == want["audit"][n][3] and a.reg_final_src == want["audit"][n][4]
+    assert list(got["cg_iters"]) == list(want["cg_iters"])
+
+
+def test_one_scheduled_thread_reproduces_plain_bit_for_bit(gpu, ref):
+    # test_decomp.cpp:328-343
+    plan = _small_plan(gpu, 16, 3, 3, 6)
+    _, _, z, P, idx = _series_inputs(ref, plan, F=6, K=5, U=3)
+    plain = _run(gpu, plan, z, P, idx, gpu.SeriesOptions(plain=True, sched=gpu.TemporalSchedule.for_turns(3)))
+    sched = _run(gpu, plan, z, P, idx, gpu.SeriesOptions(T=1, sched=gpu.TemporalSchedule.for_turns(3)))
+    assert np.array_equal(plain["images"], sched["images"])
+    for a, b in zip(plain["audit"], sched["audit"]):
+        assert (a.init_src, a.reg_final_src) == (b.init_src, b.reg_final_src)
+
+
+@pytest.mark.parametrize("T", [2, 4])
+def test_scheduled_threads_keep_the_ordering_contract_and_replay_exactly(gpu, ref, T):
+    # test_decomp.cpp:345-387, then every frame replayed through the reference with
+    # the sources its audit recorded
+    plan = _small_plan(gpu, 16, 3, 3, 6)
+    F = 8
+    _, _, z, P, idx = _series_inputs(ref, plan, F=F, K=5, U=3)
+    sched = gpu.TemporalSchedule(2, 2)
+    out = _run(gpu, plan, z, P, idx, gpu.SeriesOptions(T=T, sched=sched))
+    M = plan.newton_steps
+    audit = out["audit"]
+    for n in range(F):
+        a = audit[n]
+        assert a.frame == n
+        assert np.sum(np.abs(out["images"][n]) ** 2) > 0
+        if n == 0:
+            assert a.init_src == -1
+            continue
+        assert 0 <= a.init_src < n
+        for m in range(M):
+            assert 0 <= a.reg_src[m] < n
+            if n > sched.l and m < M - 1:
+                assert a.reg_src[m] >= n - sched.o
+        assert a.reg_final_src == n - 1
+        assert a.reg_final_seq > audit[n - 1].finish_seq
+        if n <= sched.l:
+            assert a.start_seq > audit[n - 1].finish_seq
+    # replay: the data were normalised on the device with the series scale
+    scale = out["series"].normalize()
+    zs = (z * np.float32(scale)).astype(np.complex64)
+    unity = gpu.initial_estimate(plan)
+    ests = {}
+    for n in range(F):
+        a = audit[n]
+        init = unity if a.init_src < 0 else ests[a.init_src]
+        regs = [unity if a.init_src < 0 else ests[a.reg_src[m]] for m in range(M)]
+        img, est, _ = ref.reconstruct_frame_regs(plan, zs[n], P[idx[n]], init, regs)
+        ests[n] = est
+        img = img * np.float32(1.0 / scale)
+        assert rel_err(out["images"][n], img) < FRAME_TOL, n
+        assert rel_err(out["series"].estimate(n), est) < FRAME_TOL, n
+
+
+def test_host_streaming_path_equals_resident_path(gpu, ref):
+    plan = _small_plan(gpu, 24, 3, 7, 30)
+    _, _, z, P, idx = _series_inputs(ref, plan, F=5, K=11, U=5)
+    resident = _run(gpu, plan, z, P, idx, gpu.SeriesOptions(plain=True))
+    ctx = gpu.Context(plan)
+    s = gpu.Series(ctx, 5, P.shape[0])
+    for k in range(P.shape[0]):
+        s.upload_psf(k, P[k])
+    s.set_psf_index(idx)
+    streamed = s.run(gpu.SeriesOptions(plain=True), z_host=z)
+    assert np.array_equal(streamed["images"], resident["images"])
+
+
+def test_fully_sampled_phantoms_are_recovered(gpu, ref):
+    # test_nlinv.cpp:407-429 (default plan: M = 6, cg_tol 1e-3, max 200)
+    N = 32
+    for J in (1, 4):
+        plan = gpu.make_plan(N, J)
+        samples, angles = ref.phantom_series(J, 1, 51, 1, N, 0.0, 5)
+        z = ref.grid_adjoint(plan, samples[0], angles[0])[None]
+        P = ref.build_psf(plan, angles[0], 2 * N)[None]
+        out = _run(gpu, plan, z, P, [0], gpu.SeriesOptions(plain=True))
+        truth = ref.bandlimited_truth_rss(J, 5, 0, N)
+        assert ref.nrmse_scaled(out["images"][0], truth) <= 0.05, J
+
+
+def test_chaining_beats_scratch(gpu, ref):
+    # test_nlinv.cpp:431-458
+    N, F = 24, 12
+    plan = _small_plan(gpu, N, 3, 6, 30)
+    samples, angles = ref.phantom_series(3, F, 11, 5, N, 1e-3, 9)
+    z = np.stack([ref.grid_adjoint(plan, samples[n], angles[n]) for n in range(F)])
+    P = np.stack([ref.build_psf(plan, angles[n], 2 * N) for n in range(5)])
+    idx = [n % 5 for n in range(F)]
+    ch = _run(gpu, plan, z, P, idx, gpu.SeriesOptions(plain=True))
+    sc = _run(gpu, plan, z, P, idx, gpu.SeriesOptions(plain=True, chain=False))
+    wins = 0
+    for n in range(6, F):
+        truth = ref.bandlimited_truth_rss(3, 9, n, N)
+        e_ch = ref.nrmse_scaled(ch["images"][n], truth)
+        e_sc = ref.nrmse_scaled(sc["images"][n], truth)
+        assert e_ch < 0.5
+        wins += e_ch <= e_sc
+    assert wins >= 5
+
+
+def test_failing_frame_poisons_the_series(gpu, ref):
+    # test_decomp.cpp:389-398
+    plan = _small_plan(gpu, 16, 2, 2, 4)
+    _, _, z, P, idx = _series_inputs(ref, plan, F=4, K=5, U=2)
+    z[2, 0, 24, 24] = np.nan
+    with pytest.raises(RuntimeError):
+        _run(gpu, plan, z, P, idx, gpu.SeriesOptions(T=2, sched=gpu.TemporalSchedule(1, 1)))
+
+
+def test_c1_series_against_reference(gpu, ref):
+    # configs[0]: 64x64, G 128, 8 channels, 13 spokes, 5 frames, 7 Newton steps
+    plan = gpu.raw_plan(128, 8)
+    plan.newton_steps, plan.cg_iter_budget = 7, 50
+    samples, angles, z, P, idx = _series_inputs(ref, plan, F=5, K=13, U=5, noise=0.0, seed=1234)
+    want = ref.reconstruct_series(plan, samples, angles, plain=True)
+    got = _run(gpu, plan, z, P, idx, gpu.SeriesOptions(plain=True))
+    for n in range(5):
+        assert rel_err(got["images"][n], want["images"][n]) < FRAME_TOL, n
