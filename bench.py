@@ -1,0 +1,424 @@
+#!/usr/bin/env python3
+"""NLINV real-time reconstruction benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+
+A step is one frame: the full IRGNM reconstruction of one gridded k-space frame
+(7 Newton steps, 50-iteration conjugate-residual budget, final RSS image), chained
+from the previous frame's estimate as in reconstruct_series_plain (nlinv.cpp:412-444).
+At N = 1 the workload is configs[2] of BASELINE.json (C3: 256x256 grid, 32 channels),
+the configuration the north-star 30 frames/s target is quoted on; the other configs
+are parity-test cases. Under torchrun every rank reconstructs its own slice series
+(multi-slice imaging): no data-path collective, weak scaling.
+
+Inputs are synthetic (numpy): an ellipse phantom with one moving feature, smooth
+coil profiles, an exact radial-trajectory Toeplitz kernel (K = 15 spokes, U = 5
+turns) and gridded data z_j = T(rho c_j) + noise. They are staged in HBM before the
+timed region; every frame has its own 16 MB data buffer and the staged series is
+larger than L2, so each frame starts cold. `value` is device time (CUDA events
+spanning the worker streams); `e2e` is the public C-ABI series call with pinned
+host frames streamed in (H2D) and images read back (D2H) inside the timed region.
+"""
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (G, J, K spokes, U turns, description)
+    "c1": (128, 8, 13, 5, "configs[0]: 64x64 image, 128x128 grid, 8 channels, 13 spokes"),
+    "c2": (320, 10, 15, 5, "configs[1]: 160x160 image, 320x320 grid, 10 channels, 15 spokes"),
+    "c3": (256, 32, 15, 5, "configs[2]: 256x256 grid, 32 channels, 15 spokes"),
+    "c4": (256, 16, 15, 5, "configs[3]: 256x256 grid, 16 channels, 15 spokes"),
+    "c5": (384, 64, 15, 5, "configs[4]: 384x384 grid, 64 channels, 15 spokes"),
+}
+METRIC = "frames/sec (NLINV, 7 Newton steps)"
+
+
+# ------------------------------------------------------------------------------------
+# synthetic inputs (numpy only; no oracle code on this path)
+# ------------------------------------------------------------------------------------
+def fftc2(x):
+    """centered unitary forward 2D DFT (DC at n/2), the reference convention (fft.hpp:22-30)"""
+    n = x.shape[-1]
+    return np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(x, axes=(-2, -1))), axes=(-2, -1)) / n
+
+
+def ifftc2(x):
+    n = x.shape[-1]
+    return np.fft.fftshift(np.fft.ifft2(np.fft.ifftshift(x, axes=(-2, -1))), axes=(-2, -1)) * n
+
+
+def radial_psf(G, N, K, U, turn):
+    """Toeplitz kernel of a K-spoke radial frame (turn `turn` of U), built from the exact
+    trajectory response q(d) = sum_s v_s exp(2 pi i k_s . d) with ramp density weights."""
+    S = 2 * N
+    c = G // 2
+    i = np.arange(S)
+    r = (2.0 * i + 1.0 - S) / (2.0 * S)
+    ang = (np.arange(K) * 2 * np.pi / K + turn * 2 * np.pi / (K * U)) % (2 * np.pi)
+    kx = (r[None, :] * np.cos(ang)[:, None]).ravel()
+    ky = (r[None, :] * np.sin(ang)[:, None]).ravel()
+    v = np.maximum(np.hypot(kx, ky), 0.5 / G) * (np.pi / K) / S
+    d = np.arange(G) - c
+    ax = np.exp(2j * np.pi * kx[:, None] * d[None, :])
+    ay = np.exp(2j * np.pi * ky[:, None] * d[None, :])
+    q = (ax.T * v[None, :]) @ ay
+    q[0, :] = 0
+    q[:, 0] = 0
+    return (fftc2(q) * G).astype(np.complex64)
+
+
+def phantom_and_coils(G, N, J, n):
+    L = G // 2
+    lo = (G - L) // 2
+    yy, xx = np.mgrid[0:G, 0:G]
+    x = (xx - G / 2) / N
+    y = (yy - G / 2) / N
+    rho = np.zeros((G, G), np.complex128)
+    shift = 0.05 * math.sin(2 * math.pi * n / 16)
+    for cx, cy, a, b, th, amp in ((0.0, 0.0, 0.44, 0.40, 0.0, 1.0), (0.0, 0.0, 0.38, 0.35, 0.2, -0.5),
+                                  (-0.12, 0.08, 0.12, 0.09, 0.4, 0.4 + 0.1j), (0.1, -0.12, 0.09, 0.07, -0.3, 0.3),
+                                  (0.05 + shift, 0.17, 0.06, 0.06, 0.0, 0.6)):
+        ct, st = math.cos(th), math.sin(th)
+        u = ((x - cx) * ct + (y - cy) * st) / a
+        w = (-(x - cx) * st + (y - cy) * ct) / b
+        rho += amp * (u * u + w * w <= 1.0)
+    win = np.zeros((G, G), bool)
+    win[lo:lo + L, lo:lo + L] = True
+    rho *= win
+    coils = np.empty((J, G, G), np.complex128)
+    for j in range(J):
+        a = 2 * math.pi * j / J + math.pi / 4
+        mx, my = 0.3 * math.cos(a), 0.3 * math.sin(a)
+        env = (1 + 0.3 * np.cos(np.pi * (x - mx))) * (1 + 0.3 * np.cos(np.pi * (y - my)))
+        ph = 2 * np.pi * (0.35 * math.cos(a + 0.7) * x + 0.35 * math.sin(a + 0.7) * y) + a
+        coils[j] = env * np.exp(1j * ph)
+    return rho, coils, win
+
+
+def synth_series(G, J, K, U, n_unique, seed=1234, noise=1e-3):
+    N = G // 2
+    P = np.stack([radial_psf(G, N, K, U, t) for t in range(U)])
+    rng = np.random.default_rng(seed)
+    frames = []
+    for n in range(n_unique):
+        rho, coils, win = phantom_and_coils(G, N, J, n)
+        x = rho[None] * coils
+        t = ifftc2(P[n % U][None].astype(np.complex128) * fftc2(x * win)) * win
+        t += noise * (rng.standard_normal(t.shape) + 1j * rng.standard_normal(t.shape)) * win
+        frames.append(t.astype(np.complex64))
+    return np.stack(frames), P
+
+
+# ------------------------------------------------------------------------------------
+# measurement helpers
+# ------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region"""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def profile_traffic(kernel, cfg):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        e = d.get(cfg, {}).get(kernel)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def launches_per_frame(caps, M):
+    """kernels one frame launches (engine.cu enqueue order): per step 1 step_begin +
+    2 decode + 4 setup passes + 5 priming-apply + 1 prime + cap x_r updates + (cap-1)
+    x (5 apply + 1 p/ap update) + 1 axpy; then 2 decode + 1 image"""
+    n = 0
+    for m in range(M):
+        cap = caps[m]
+        n += 1 + 2 + 4 + (5 + 1 + cap + (cap - 1) * 6 if cap >= 1 else 0) + 1
+    return n + 3
+
+
+def dist_setup(n_gpus):
+    rank, world, local = 0, 1, 0
+    if "RANK" in os.environ and "WORLD_SIZE" in os.environ:
+        rank = int(os.environ["RANK"])
+        world = int(os.environ["WORLD_SIZE"])
+        local = int(os.environ.get("LOCAL_RANK", rank))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def max_over_ranks(v, world, local):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world, local):
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(local)
+
+
+# ------------------------------------------------------------------------------------
+# reference arm: the reference's own CPU path (oracle/_ref) on the same workload
+# ------------------------------------------------------------------------------------
+def reference_arm(args, cfg):
+    G, J, K, U, _ = CONFIGS[cfg]
+    from oracle import ref
+    import paper_1701_08361_b200 as pb
+    plan = pb.raw_plan(G, J)
+    plan.newton_steps, plan.cg_iter_budget = 7, 50
+    nproc = os.cpu_count() or 1
+    A = max(1, min(4, nproc, J))  # the reference's WorkerGroup cap (decomp.hpp:21)
+    z, P = synth_series(G, J, K, U, n_unique=min(4, args.steps + args.warmup))
+    nsq = float(np.sum(np.abs(z[0].astype(np.complex128)) ** 2))
+    z = (z * np.float32(100.0 / math.sqrt(nsq))).astype(np.complex64)
+    est = ref.initial_estimate(plan)
+    budget_s = float(os.environ.get("RTN_REF_BUDGET_S", "150"))
+    times = []
+    t_all = time.time()
+    total = args.warmup + args.steps
+    for n in range(total):
+        t0 = time.perf_counter()
+        _, est, _, _ = ref.reconstruct_frame(plan, z[n % len(z)], P[n % U], est, est, A=A)
+        dt = time.perf_counter() - t0
+        if n >= args.warmup:
+            times.append(dt)
+        if time.time() - t_all > budget_s and len(times) >= 1:
+            break
+    fps = len(times) / sum(times)
+    sample = (f"{len(times)} chained {cfg.upper()} frames (7 Newton steps, 50 CR iterations each) after "
+              f"{min(args.warmup, total)} warm-up; reference reconstruct_frame, A={A} WorkerGroup lanes; "
+              f"FFTW replaced by the oracle shim FFT (oracle/shim, pocketfft-class speed)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": 1000.0 / fps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c64/f64", "data": "synthetic",
+        "config": {"workload": cfg, "description": CONFIGS[cfg][4], "G": G, "J": J, "newton_steps": 7,
+                   "cg_iter_budget": 50},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": A, "kind": "reference", "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, z, P, plan):
+    """bounded sample of the reference CPU path on this host (rank 0, N = 1)"""
+    from oracle import ref
+    nproc = os.cpu_count() or 1
+    A = max(1, min(4, nproc, plan.J))
+    est = ref.initial_estimate(plan)
+    t0 = time.perf_counter()
+    ref.reconstruct_frame(plan, z, P, est, est, A=A)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": "frames/s", "cores": A, "kind": "reference",
+            "sample": f"1 {cfg.upper()} frame (7 Newton steps, 50 CR iterations) through the reference "
+                      f"reconstruct_frame with A={A} WorkerGroup lanes, {dt:.1f} s; FFTW replaced by the "
+                      f"oracle shim FFT"}
+
+
+# ------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--T", type=int, default=1, help="frames in flight (temporal decomposition); 1 = plain chain")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = args.config
+
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank == 0:
+            reference_arm(args, cfg)
+        return
+
+    rank, world, local = dist_setup(args.gpus)
+    import paper_1701_08361_b200 as pb
+    G, J, K, U, desc = CONFIGS[cfg]
+    plan = pb.raw_plan(G, J)
+    plan.newton_steps, plan.cg_iter_budget = 7, 50
+    M = plan.newton_steps
+    W, S = args.warmup, args.steps
+    F = W + S
+
+    z_unique, P = synth_series(G, J, K, U, n_unique=min(F, 10), seed=1234 + rank)
+    ctx = pb.Context(plan, device=local)
+    series = pb.Series(ctx, F, U)
+    frames = np.stack([z_unique[n % len(z_unique)] for n in range(F)])
+    series.upload_frames(frames)
+    for k in range(U):
+        series.upload_psf(k, P[k])
+    series.set_psf_index([n % U for n in range(F)])
+    series.normalize()
+    opts = pb.SeriesOptions(T=args.T, plain=args.T == 1, sched=pb.TemporalSchedule.for_turns(U))
+
+    # warm-up (graph capture happens here)
+    series.run(opts, first=0, count=W, want_images=False)
+    barrier(world, local)
+    with ClockSampler(local) as clk:
+        out = series.run(opts, first=W, count=S, want_images=False)
+        span_ms = series.last_span_ms()
+    barrier(world, local)
+    span_ms = max_over_ranks(span_ms, world, local)
+    value = world * S / (span_ms / 1000.0)
+    lat = [float(v) for v in out["gpu_ms"]]
+    caps = [0] * M
+    rem = plan.cg_iter_budget
+    for m in range(M):
+        caps[m] = (rem + (M - m) - 1) // (M - m)
+        rem -= caps[m]
+    assert list(out["cg_iters"]) == [sum(caps)] * S
+
+    # end to end: pinned host frames streamed through the public series call
+    e2e = None
+    if not args.no_e2e:
+        import torch
+        zt = torch.empty((S, J, G, G), dtype=torch.complex64, pin_memory=True)
+        zt.numpy()[:] = frames[W:W + S]
+        imt = torch.empty((S, plan.N, plan.N), dtype=torch.complex64, pin_memory=True)
+        barrier(world, local)
+        t0 = time.perf_counter()
+        series.run(opts, first=W, count=S, z_host_ptr=zt.data_ptr(), images_ptr=imt.data_ptr())
+        wall = time.perf_counter() - t0
+        barrier(world, local)
+        wall = max_over_ranks(wall, world, local)
+        e2e = {"value": world * S / wall, "unit": "frames/s", "h2d_bytes_per_step": J * G * G * 8,
+               "d2h_bytes_per_step": plan.N * plan.N * 8,
+               "path": "rtn_series_run with pinned host frames (copy stream overlapped) and images to pinned host"}
+
+    # roofline of the dominant kernel (isolated CUDA-event timing on the engine stream)
+    peak, peak_kind = measured_peaks()
+    ctx.make_step_cache(series.estimate(F - 1))
+    per_frame = {"colsT": 57, "rows1": 57, "rows2": 57, "colA": 57}
+    kern = {}
+    for name in per_frame:
+        ms, by = ctx.time_kernel(name, 50)
+        kern[name] = {"ms": ms, "bytes": by, "share_ms_per_frame": ms * per_frame[name]}
+    dom = max(kern, key=lambda k: kern[k]["share_ms_per_frame"])
+    achieved = kern[dom]["bytes"] / (kern[dom]["ms"] / 1000.0) / 1e9
+    app_ms, app_by = ctx.time_kernel("apply", 20)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": profile_traffic(dom, cfg), "peak_source": peak_kind,
+                "kernel_ms": kern[dom]["ms"], "algorithmic_bytes_per_launch": kern[dom]["bytes"],
+                "apply": {"ms": app_ms, "algorithmic_bytes": app_by,
+                          "achieved_gbs": app_by / (app_ms / 1000.0) / 1e9},
+                "kernels": kern}
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": S, "warmup": W,
+        "ms_per_step": span_ms / S, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c64 (fp32 arithmetic, fp64 reductions)",
+        "data": "synthetic (numpy phantom, coils, exact radial Toeplitz kernel; staged in HBM)",
+        "config": {"workload": cfg, "description": desc, "G": G, "N": plan.N, "Gc": plan.Gc, "J": J,
+                   "spokes": K, "turns": U, "newton_steps": M, "cg_iter_budget": plan.cg_iter_budget,
+                   "frames_in_flight": args.T, "per_rank": "independent slice series (multi-slice)",
+                   "l2": "inputs larger than L2: every frame has its own 16 MB buffer, "
+                         f"{F} frames staged ({F * J * G * G * 8 / 2**20:.0f} MiB)"},
+        "p50_latency_ms": statistics.median(lat), "latency_ms_min_max": [min(lat), max(lat)],
+        "e2e": e2e, "gpu_launches": launches_per_frame(caps, M) * S, "roofline": roofline,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg, frames[0] * np.float32(100.0 / math.sqrt(
+                float(np.sum(np.abs(frames[0].astype(np.complex128)) ** 2)))), P[0], plan)
+        except Exception as e:  # the oracle may be absent on a stripped box
+            line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

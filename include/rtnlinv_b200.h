@@ -125,6 +125,8 @@ int rtn_series_normalize(rtn_series* s, double* data_scale);
 int rtn_series_run(rtn_series* s, const rtn_series_opts_t* opts, int first, int count, const float* z_host,
                    float* images, int* audit, uint64_t* seqs, int* cg_iters, float* gpu_ms);
 int rtn_series_images(rtn_series* s, int first, int count, float* images);
+/* device time (ms) of the last rtn_series_run: CUDA events spanning all worker streams */
+float rtn_series_last_span_ms(rtn_series* s);
 int rtn_series_estimate(rtn_series* s, int n, float* est /* D */);
 
 /* --- decomp.hpp:25-130: decomposition and scheduling (host logic) ----------------- */

@@ -157,6 +157,7 @@ def load_library(path: str = LIB_PATH):
                             ctypes.POINTER(ctypes.c_uint64), i, f], ctypes.c_int),
         "rtn_series_images": ([vp, ctypes.c_int, ctypes.c_int, f], ctypes.c_int),
         "rtn_series_estimate": ([vp, ctypes.c_int, f], ctypes.c_int),
+        "rtn_series_last_span_ms": ([vp], ctypes.c_float),
         "rtn_partition_channels": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, i], ctypes.c_int),
         "rtn_ledger_create": ([ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
         "rtn_ledger_destroy": ([vp], None),
@@ -520,6 +521,10 @@ class Series:
         audits = [FrameAudit(int(r[0]), int(r[1]), int(r[2]), int(r[3]), int(r[4]), [int(v) for v in r[5:]],
                              int(q[0]), int(q[1]), int(q[2])) for r, q in zip(audit, seqs)]
         return dict(images=images, audit=audits, cg_iters=cg, gpu_ms=ms)
+
+    def last_span_ms(self) -> float:
+        """device time of the last run (CUDA events across all worker streams)"""
+        return float(self.lib.rtn_series_last_span_ms(self._h))
 
     def images(self, first: int = 0, count: Optional[int] = None):
         p = self.ctx.plan

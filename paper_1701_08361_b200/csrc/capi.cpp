@@ -273,6 +273,8 @@ int rtn_series_images(rtn_series* s, int first, int count, float* images) {
   });
 }
 
+float rtn_series_last_span_ms(rtn_series* s) { return (s && s->s) ? s->s->last_span_ms() : 0.f; }
+
 int rtn_series_estimate(rtn_series* s, int n, float* est) {
   return guarded([&] {
     if (n < 0 || n >= ser(s).frames()) rtnb::fail(2, "series_estimate: frame out of range");

@@ -53,6 +53,8 @@ Series::Series(Engine& primary, int frames, int n_psf) : eng0_(primary), F_(fram
   check_cuda(cudaMalloc(&images_, sizeof(float2) * isz_ * F_), "series images");
   check_cuda(cudaMalloc(&nsq_, sizeof(double)), "nsq");
   check_cuda(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "copy stream");
+  check_cuda(cudaEventCreate(&span0_), "event");
+  check_cuda(cudaEventCreate(&span1_), "event");
   // initial_estimate: rho = 1 on the window, coils 0 (nlinv.cpp:60-70)
   std::vector<float2> u(static_cast<size_t>(D_), make_float2(0.f, 0.f));
   const int L = p.G / 2, lo = (p.G - L) / 2;
@@ -71,6 +73,8 @@ Series::~Series() {
     if (b) cudaFree(b);
   }
   if (copy_) cudaStreamDestroy(copy_);
+  if (span0_) cudaEventDestroy(span0_);
+  if (span1_) cudaEventDestroy(span1_);
 }
 
 Engine& Series::worker(int t) {
@@ -214,6 +218,8 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   const Plan& p = eng0_.plan();
   const int T = o.plain ? 1 : std::min(o.T, count);
   for (int t = 1; t < T; ++t) worker(t);
+  check_cuda(cudaEventRecord(span0_, copy_), "span event");
+  for (int t = 0; t < T; ++t) check_cuda(cudaStreamWaitEvent(worker(t).stream(), span0_, 0), "span wait");
 
   // end-to-end path: stream frames from host on the copy stream, normalise on arrival
   std::vector<cudaEvent_t> ready;
@@ -293,6 +299,18 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   }
   for (cudaEvent_t ev : ready) cudaEventDestroy(ev);
   if (first_err) std::rethrow_exception(first_err);
+  // every worker stream has been synchronised by now; close the span on the copy
+  // stream after all of them
+  for (int t = 0; t < T; ++t) {
+    cudaEvent_t e;
+    check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    check_cuda(cudaEventRecord(e, worker(t).stream()), "event");
+    check_cuda(cudaStreamWaitEvent(copy_, e, 0), "event wait");
+    cudaEventDestroy(e);
+  }
+  check_cuda(cudaEventRecord(span1_, copy_), "span event");
+  check_cuda(cudaEventSynchronize(span1_), "span sync");
+  check_cuda(cudaEventElapsedTime(&span_ms_, span0_, span1_), "span elapsed");
   (void)p;
 }
 

@@ -57,6 +57,9 @@ class Series {
            std::vector<SeriesFrameOut>* out);
 
   float2* images_dev() { return images_; }
+  // device time of the last run(): CUDA events spanning every worker stream, from
+  // before the first frame's first copy to after the last frame's image
+  float last_span_ms() const { return span_ms_; }
   float2* estimate_dev(int n) { return ests_ + static_cast<size_t>(n) * D_; }
 
  private:
@@ -78,6 +81,8 @@ class Series {
   double scale_ = 1.0;
   bool normalized_ = false;
   cudaStream_t copy_ = nullptr;
+  cudaEvent_t span0_ = nullptr, span1_ = nullptr;
+  float span_ms_ = 0.f;
 };
 
 }  // namespace rtnb
