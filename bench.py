@@ -126,7 +126,8 @@ def synth_series(G, J, K, U, n_unique, seed=1234, noise=1e-3):
 # measurement helpers
 # ------------------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region"""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (written to a
+    file by nvidia-smi itself: a pipe would block-buffer the samples)"""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -134,29 +135,32 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.lines = []
+        self.path = os.path.join("/tmp", f"rtn_clocks_{os.getpid()}_{device}.csv")
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                                          "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
         except OSError:
             self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
         if self.proc:
+            time.sleep(0.2)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+            try:
+                with open(self.path) as f:
+                    self.lines = [ln.strip() for ln in f if ln.strip()]
+                os.remove(self.path)
+            except OSError:
+                pass
 
     def summary(self):
         sm, smax, reasons = [], 0.0, set()

@@ -97,7 +97,7 @@ __global__ void k_mul(float2* __restrict__ x, const float2* __restrict__ P, int 
 // ------------------------------------------------------------------------------
 
 struct Engine::Ops {
-  int G = 0, N1 = 0, N2 = 0, LPB = 0;
+  int G = 0, N1 = 0, N2 = 0, LPB = 0, NT = 0;
   size_t smem = 0;
   void (*colA)(cudaStream_t, int, Dims, const float*, const float2*, const float2*, float2*, int, int,
                const DevState*, int) = nullptr;
@@ -116,8 +116,11 @@ namespace {
 
 template <int N1, int N2>
 struct Inst {
-  using Geo = LineGeom<N1, N2, 16>;
+  // 16 lines per block, 32 when that keeps the block a whole number of warps
+  static constexpr int kLpb = ((16 * (N1 > N2 ? N1 : N2)) % 32 == 0) ? 16 : 32;
+  using Geo = LineGeom<N1, N2, kLpb>;
   static constexpr size_t kSmem = sizeof(float2) * Geo::SMEM_FLOAT2;
+  static constexpr int kNT = Geo::NT;
 
   static void set_attrs() {
     const int s = static_cast<int>(kSmem);
@@ -126,8 +129,10 @@ struct Inst {
     check_cuda(cudaFuncSetAttribute(k_colsT<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsT");
     check_cuda(cudaFuncSetAttribute(k_rows2<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr rows2");
     check_cuda(cudaFuncSetAttribute(k_colsW<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsW");
-    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
-    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, +1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr ifft");
+    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
+    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, +1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr ifft");
+    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
+    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, +1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr ifft");
   }
 
   static Engine::Ops make();
@@ -143,36 +148,45 @@ Engine::Ops Inst<N1, N2>::make() {
   o.N2 = N2;
   o.LPB = Geo::LPB;
   o.smem = kSmem;
+  o.NT = kNT;
   o.colA = [](cudaStream_t s, int grid, Dims d, const float* winv, const float2* tw, const float2* chat,
               float2* U, int r0, int nr, const DevState* st, int h) {
-    k_colA<Geo><<<grid, kThreads, kSmem, s>>>(d, winv, tw, chat, U, r0, nr, st, h);
+    k_colA<Geo><<<grid, kNT, kSmem, s>>>(d, winv, tw, chat, U, r0, nr, st, h);
   };
   o.rows1 = [](cudaStream_t s, int grid, Dims d, int mode, const float2* tw, const float2* U,
                const float2* coils, const float2* rhom, const float2* drho, float2* V, float2* coils_out,
                const float2* rho_src, float2* rhom_out, const DevState* st, int h) {
-    k_rows1<Geo><<<grid, kThreads, kSmem, s>>>(d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
+    k_rows1<Geo><<<grid, kNT, kSmem, s>>>(d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
                                                 rhom_out, st, h);
   };
   o.colsT = [](cudaStream_t s, int grid, Dims d, const float2* tw, const float2* P, float2* V,
                const DevState* st, int h) {
-    k_colsT<Geo><<<grid, kThreads, kSmem, s>>>(d, tw, P, V, st, h);
+    k_colsT<Geo><<<grid, kNT, kSmem, s>>>(d, tw, P, V, st, h);
   };
   o.rows2 = [](cudaStream_t s, int grid, Dims d, int mode, const float2* tw, const float2* V,
                const float2* coils, const float2* rhom, const float2* z, float2* RC, float2* Y,
                double* partials, DevState* st, int h) {
-    k_rows2<Geo><<<grid, kThreads, kSmem, s>>>(d, mode, tw, V, coils, rhom, z, RC, Y, partials, st, h);
+    k_rows2<Geo><<<grid, kNT, kSmem, s>>>(d, mode, tw, V, coils, rhom, z, RC, Y, partials, st, h);
   };
   o.colsW = [](cudaStream_t s, int grid, Dims d, ColsWArgs a, const float* winv, const float2* tw,
                const float2* Y, const float2* RC, const float2* coils, const float2* z, int nbw,
                double* partials, DevState* st, CrScalars cr, int h) {
-    k_colsW<Geo><<<grid, kThreads, kSmem, s>>>(d, a, winv, tw, Y, RC, coils, z, nbw, partials, st, cr, h);
+    k_colsW<Geo><<<grid, kNT, kSmem, s>>>(d, a, winv, tw, Y, RC, coils, z, nbw, partials, st, cr, h);
   };
   o.fft = [](cudaStream_t s, int grid, int sign, float2* data, int batch, int axis, const float2* tw,
              float scale) {
     if (sign < 0) {
-      k_fft_pass<Geo, -1><<<grid, kThreads, kSmem, s>>>(data, batch, axis, tw, scale);
+      if (axis == 0) {
+        k_fft_pass<Geo, -1, true><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
+      } else {
+        k_fft_pass<Geo, -1, false><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
+      }
     } else {
-      k_fft_pass<Geo, +1><<<grid, kThreads, kSmem, s>>>(data, batch, axis, tw, scale);
+      if (axis == 0) {
+        k_fft_pass<Geo, +1, true><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
+      } else {
+        k_fft_pass<Geo, +1, false><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
+      }
     }
   };
   return o;
@@ -401,7 +415,7 @@ void Engine::alloc() {
   c2(&gbuf_, G2, "scratch");
   c2(&img_, static_cast<size_t>(plan_.N) * plan_.N, "image");
   vec_grid_ = blocks_for(D_, 148 * 4);
-  nbr_ = blocks_for(static_cast<long long>(G2) / 4, 148);
+  nbr_ = static_cast<int>((G2 + ops_->NT - 1) / ops_->NT);  // one rho element per thread
   const int max_grid = std::max(vec_grid_, plan_.J * ((plan_.G + ops_->LPB - 1) / ops_->LPB) + nbr_ + 8);
   check_cuda(cudaMalloc(&partials_, sizeof(double) * 2 * max_grid), "partials");
   check_cuda(cudaMalloc(&st_, sizeof(DevState)), "state");

@@ -144,66 +144,90 @@ __device__ __forceinline__ void dft(float2 (&x)[N]) {
   }
 }
 
-// Shared-memory geometry of one tile of LPB lines of length G = N1*N2.
-//   A (input, padded): element q of line l at l*LSA + q + q/N2 (one pad slot per
-//     N2 block, so step-2 reads of contiguous blocks by consecutive threads hit
-//     distinct banks); LSA odd so column-tile fills are conflict-free.
-//   B (output): element p of line l at l*LSB + p, LSB = G + 1 (odd).
+// ---------------------------------------------------------------------------------
+// Tile geometry. A block transforms LPB lines of length G = N1*N2 with
+// NT = LPB * max(N1, N2) threads and ONE padded shared tile, reused in place:
+//   step 1 items (l, n2): the thread loads x[N2*n1 + n2], n1 = 0..N1-1, straight
+//     from global memory (fusing the producer's pointwise work), runs an N1-point
+//     DFT in registers, applies W_G^{n2 k1} and parks v[k1] at q = N2*k1 + n2;
+//   step 2 items (l, k1): after one barrier the thread reads the contiguous block
+//     q = N2*k1 + n2, n2 = 0..N2-1, runs an N2-point DFT and holds X[k1 + N1*k2]
+//     in registers for the consumer's pointwise work and global stores.
+// Element q of line l lives at l*LS + q + q/N2: one pad slot per N2 block keeps the
+// step-2 block reads (stride N2+1 across threads) and the natural-order writes
+// (stride 1) conflict-free; LS is odd so column tiles spread over banks.
+// Item maps: ROWS tiles put the in-line index fastest across threads (a line is
+// contiguous in memory), COLS tiles put the line fastest (lines are adjacent
+// columns), so every global access of both passes is coalesced.
+// ---------------------------------------------------------------------------------
 template <int N1_, int N2_, int LPB_>
 struct LineGeom {
   static constexpr int N1 = N1_;
   static constexpr int N2 = N2_;
   static constexpr int G = N1 * N2;
   static constexpr int LPB = LPB_;
-  static constexpr int LSA0 = G + N1;
-  static constexpr int LSA = (LSA0 % 2 == 1) ? LSA0 : LSA0 + 1;
-  static constexpr int LSB = G + 1;
-  static constexpr int SMEM_FLOAT2 = LPB * (LSA + LSB);
-  __device__ __forceinline__ static int a_idx(int l, int q) { return l * LSA + q + q / N2; }
-  __device__ __forceinline__ static int b_idx(int l, int p) { return l * LSB + p; }
+  static constexpr int NMAX = N1 > N2 ? N1 : N2;
+  static constexpr int NT = LPB * NMAX;
+  static constexpr int LS0 = G + G / N2;
+  static constexpr int LS = (LS0 % 2 == 1) ? LS0 : LS0 + 1;
+  static constexpr int SMEM_FLOAT2 = LPB * LS;
+  __device__ __forceinline__ static int a(int l, int q) { return l * LS + q + q / N2; }
 };
 
-// Transforms lines [0, nl) of tile A into tile B (natural order, unnormalised).
-// twG: exp(-2 pi i e / G), e = 0..G-1 (global, read-only). Must be called by all
-// threads of the block; ends with a __syncthreads().
-template <class Geo, int S>
-__device__ __forceinline__ void tile_fft(float2* A, float2* B, int nl, const float2* __restrict__ twG) {
-  constexpr int N1 = Geo::N1, N2 = Geo::N2, G = Geo::G;
-  __syncthreads();
-  // step 1: item (l, n2)
-  for (int it = threadIdx.x; it < nl * N2; it += blockDim.x) {
-    const int l = it / N2;
-    const int n2 = it - l * N2;
-    float2 v[N1];
-    float2* base = A + l * Geo::LSA + n2;
-#pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) v[n1] = base[n1 * (N2 + 1)];
-    dft<N1, S>(v);
-#pragma unroll
-    for (int k1 = 1; k1 < N1; ++k1) {
-      float2 w = __ldg(twG + n2 * k1);
-      if (S > 0) w.y = -w.y;
-      v[k1] = cmul(v[k1], w);
+// item decomposition of threadIdx.x for a step with `n` slots per line
+template <class Geo, bool COLS>
+struct Item {
+  int l, k;
+  bool on;
+  __device__ __forceinline__ Item(int tid, int n) {
+    if (COLS) {
+      l = tid % Geo::LPB;
+      k = tid / Geo::LPB;
+    } else {
+      l = tid / n;
+      k = tid - (tid / n) * n;
     }
-#pragma unroll
-    for (int k1 = 0; k1 < N1; ++k1) base[k1 * (N2 + 1)] = v[k1];
+    on = tid < Geo::LPB * n;
   }
-  __syncthreads();
-  // step 2: item (l, k1)
-  for (int it = threadIdx.x; it < nl * N1; it += blockDim.x) {
-    const int l = it / N1;
-    const int k1 = it - l * N1;
-    float2 v[N2];
-    const float2* src = A + l * Geo::LSA + k1 * (N2 + 1);
+};
+
+// step 1 on registers: v[n1] = x[N2*n1 + n2] -> DFT_N1 -> twiddle W_G^{n2 k1}
+template <class Geo, int S>
+__device__ __forceinline__ void fft_step1(float2 (&v)[Geo::N1], int n2, const float2* __restrict__ twG) {
+  dft<Geo::N1, S>(v);
 #pragma unroll
-    for (int n2 = 0; n2 < N2; ++n2) v[n2] = src[n2];
-    dft<N2, S>(v);
-    float2* dst = B + l * Geo::LSB + k1;
-#pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) dst[N1 * k2] = v[k2];
+  for (int k1 = 1; k1 < Geo::N1; ++k1) {
+    float2 w = __ldg(twG + n2 * k1);
+    if (S > 0) w.y = -w.y;
+    v[k1] = cmul(v[k1], w);
   }
-  (void)G;
-  __syncthreads();
+}
+
+template <class Geo>
+__device__ __forceinline__ void park_step1(float2* A, int l, int n2, const float2 (&v)[Geo::N1]) {
+#pragma unroll
+  for (int k1 = 0; k1 < Geo::N1; ++k1) A[Geo::a(l, Geo::N2 * k1 + n2)] = v[k1];
+}
+
+// step 2: u[n2] = parked block of k1 -> DFT_N2 -> u[k2] = X[k1 + N1*k2]
+template <class Geo, int S>
+__device__ __forceinline__ void fft_step2(const float2* A, int l, int k1, float2 (&u)[Geo::N2]) {
+  const float2* src = A + Geo::a(l, Geo::N2 * k1);
+#pragma unroll
+  for (int n2 = 0; n2 < Geo::N2; ++n2) u[n2] = src[n2];
+  dft<Geo::N2, S>(u);
+}
+
+// natural-order write / step-1-order read, for chaining two transforms in a block
+template <class Geo>
+__device__ __forceinline__ void put_natural(float2* A, int l, int k1, const float2 (&u)[Geo::N2]) {
+#pragma unroll
+  for (int k2 = 0; k2 < Geo::N2; ++k2) A[Geo::a(l, k1 + Geo::N1 * k2)] = u[k2];
+}
+template <class Geo>
+__device__ __forceinline__ void get_step1(const float2* A, int l, int n2, float2 (&v)[Geo::N1]) {
+#pragma unroll
+  for (int n1 = 0; n1 < Geo::N1; ++n1) v[n1] = A[Geo::a(l, Geo::N2 * n1 + n2)];
 }
 
 }  // namespace rtnb

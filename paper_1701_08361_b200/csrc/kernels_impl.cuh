@@ -113,45 +113,61 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
 }  // namespace
 
 // ---------------------------------------------------------------------------------
-// Pass kernels. Lines are batched LPB per block and never straddle channels.
+// Pass kernels. Lines are batched LPB per block (never straddling channels); block
+// size Geo::NT. Loads feed the step-1 registers directly, every transform makes one
+// padded shared-memory exchange, and pointwise work is applied where the data sits
+// in registers (see fft_line.cuh). Threads whose line is past the tile end still
+// take part in every barrier.
 // ---------------------------------------------------------------------------------
+
+#define RTNB_TILE_SETUP(COLS_)                                  \
+  extern __shared__ float2 A[];                                 \
+  const Item<Geo, COLS_> i1(threadIdx.x, Geo::N2);              \
+  const Item<Geo, COLS_> i2(threadIdx.x, Geo::N1);              \
+  constexpr int G = Geo::G, N1 = Geo::N1, N2 = Geo::N2;         \
+  (void)N1;                                                     \
+  (void)N2
 
 // W^-1 column pass. Lines: (channel j, coil k-column q). Input chat_j*winv on the
 // Gc centered k-rows, output rows [r0, r0+nr) of U_j (G x Gc, row-major).
 template <class Geo>
-__global__ void __launch_bounds__(kThreads) k_colA(Dims d, const float* __restrict__ winv,
-                                                   const float2* __restrict__ twG,
-                                                   const float2* __restrict__ chat, float2* __restrict__ U,
-                                                   int r0, int nr, const DevState* st, int use_halt) {
+__global__ void __launch_bounds__(Geo::NT) k_colA(Dims d, const float* __restrict__ winv,
+                                                  const float2* __restrict__ twG,
+                                                  const float2* __restrict__ chat, float2* __restrict__ U,
+                                                  int r0, int nr, const DevState* st, int use_halt) {
   if (st->status || (use_halt && st->cr_halt)) return;
-  constexpr int G = Geo::G, LPB = Geo::LPB;
-  extern __shared__ float2 sm[];
-  float2* A = sm;
-  float2* B = sm + LPB * Geo::LSA;
-  const int tiles = (d.Gc + LPB - 1) / LPB;
+  RTNB_TILE_SETUP(true);
+  const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
   const int j = blockIdx.x / tiles;
-  const int q0 = (blockIdx.x - j * tiles) * LPB;
-  const int nl = min(LPB, d.Gc - q0);
+  const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
+  const int nl = min(Geo::LPB, d.Gc - q0);
   const float2* src = chat + (size_t)j * d.Gc * d.Gc;
-  for (int idx = threadIdx.x; idx < G * LPB; idx += blockDim.x) {
-    const int t = idx / LPB, l = idx - (idx / LPB) * LPB;
-    const int i = t - d.off;
-    float2 v = make_float2(0.f, 0.f);
-    if (l < nl && i >= 0 && i < d.Gc) {
-      const int e = i * d.Gc + q0 + l;
-      const float w = winv[e];
-      const float2 c = src[e];
-      v = flip(make_float2(c.x * w, c.y * w), t);
+  if (i1.on && i1.l < nl) {
+    const int q = q0 + i1.l;
+    float2 v[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const int t = N2 * n1 + i1.k;
+      const int i = t - d.off;
+      v[n1] = make_float2(0.f, 0.f);
+      if (i >= 0 && i < d.Gc) {
+        const float w = winv[i * d.Gc + q];
+        const float2 c = src[i * d.Gc + q];
+        v[n1] = flip(make_float2(c.x * w, c.y * w), t);  // chat * winv.real() (nlinv.cpp:121)
+      }
     }
-    A[Geo::a_idx(l, t)] = v;
+    fft_step1<Geo, +1>(v, i1.k, twG);
+    park_step1<Geo>(A, i1.l, i1.k, v);
   }
-  tile_fft<Geo, +1>(A, B, nl, twG);
-  float2* dst = U + (size_t)j * G * d.Gc;
-  for (int idx = threadIdx.x; idx < nr * LPB; idx += blockDim.x) {
-    const int pr = idx / LPB, l = idx - pr * LPB;
-    if (l < nl) {
-      const int p = r0 + pr;
-      dst[(size_t)p * d.Gc + q0 + l] = flip(B[Geo::b_idx(l, p)], p);
+  __syncthreads();
+  if (i2.on && i2.l < nl) {
+    float2 u[N2];
+    fft_step2<Geo, +1>(A, i2.l, i2.k, u);
+    float2* dst = U + (size_t)j * G * d.Gc + q0 + i2.l;
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) {
+      const int p = i2.k + N1 * k2;
+      if (p >= r0 && p < r0 + nr) dst[(size_t)p * d.Gc] = flip(u[k2], p);
     }
   }
 }
@@ -165,121 +181,158 @@ enum Rows1Mode : int { R1_DECODE = 0, R1_OP = 1, R1_SETUP = 2 };
 //          forward row FFT -> V_j (L x G).
 //  SETUP:  window rows: t = rho*c_j (nlinv.cpp:252) -> forward row FFT -> V_j.
 template <class Geo>
-__global__ void __launch_bounds__(kThreads) k_rows1(Dims d, int mode, const float2* __restrict__ twG,
-                                                    const float2* __restrict__ U,
-                                                    const float2* __restrict__ coils,
-                                                    const float2* __restrict__ rhom,
-                                                    const float2* __restrict__ drho, float2* __restrict__ V,
-                                                    float2* __restrict__ coils_out,
-                                                    const float2* __restrict__ rho_src,
-                                                    float2* __restrict__ rhom_out, const DevState* st,
-                                                    int use_halt) {
+__global__ void __launch_bounds__(Geo::NT) k_rows1(Dims d, int mode, const float2* __restrict__ twG,
+                                                   const float2* __restrict__ U,
+                                                   const float2* __restrict__ coils,
+                                                   const float2* __restrict__ rhom,
+                                                   const float2* __restrict__ drho, float2* __restrict__ V,
+                                                   float2* __restrict__ coils_out,
+                                                   const float2* __restrict__ rho_src,
+                                                   float2* __restrict__ rhom_out, const DevState* st,
+                                                   int use_halt) {
   if (st->status || (use_halt && st->cr_halt)) return;
-  constexpr int G = Geo::G, LPB = Geo::LPB;
-  extern __shared__ float2 sm[];
-  float2* A = sm;
-  float2* B = sm + LPB * Geo::LSA;
+  RTNB_TILE_SETUP(false);
   const int nrows = (mode == R1_DECODE) ? G : d.L;
   const int row0 = (mode == R1_DECODE) ? 0 : d.lo;
-  const int tiles = (nrows + LPB - 1) / LPB;
+  const int tiles = (nrows + Geo::LPB - 1) / Geo::LPB;
   const int j = blockIdx.x / tiles;
-  const int rl0 = (blockIdx.x - j * tiles) * LPB;
-  const int nl = min(LPB, nrows - rl0);
+  const int rl0 = (blockIdx.x - j * tiles) * Geo::LPB;
+  const int nl = min(Geo::LPB, nrows - rl0);
   const float2* Uj = U + (size_t)j * G * d.Gc;
   const float2* cj = coils + (size_t)j * G * G;
-
+  const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
+  const int r1 = row0 + rl0 + i1.l, r2 = row0 + rl0 + i2.l;
+  float2 v[N1];
   if (mode != R1_SETUP) {
-    // load U rows into the coil k-columns, inverse row FFT
-    for (int idx = threadIdx.x; idx < LPB * G; idx += blockDim.x) {
-      const int l = idx / G, t = idx - (idx / G) * G;
-      const int q = t - d.off;
-      float2 v = make_float2(0.f, 0.f);
-      if (l < nl && q >= 0 && q < d.Gc) v = flip(Uj[(size_t)(row0 + rl0 + l) * d.Gc + q], t);
-      A[Geo::a_idx(l, t)] = v;
+    if (a1) {
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        const int t = N2 * n1 + i1.k;
+        const int qk = t - d.off;
+        v[n1] = (qk >= 0 && qk < d.Gc) ? flip(Uj[(size_t)r1 * d.Gc + qk], t) : make_float2(0.f, 0.f);
+      }
+      fft_step1<Geo, +1>(v, i1.k, twG);
+      park_step1<Geo>(A, i1.l, i1.k, v);
     }
-    tile_fft<Geo, +1>(A, B, nl, twG);
-    if (mode == R1_DECODE) {
-      float2* out = coils_out + (size_t)j * G * G;
-      for (int idx = threadIdx.x; idx < LPB * G; idx += blockDim.x) {
-        const int l = idx / G, p = idx - (idx / G) * G;
-        if (l < nl) {
-          const int r = rl0 + l;
-          out[(size_t)r * G + p] = cscale(flip(B[Geo::b_idx(l, p)], p), d.invG);
+    __syncthreads();
+    float2 u[N2];
+    if (a2) {
+      fft_step2<Geo, +1>(A, i2.l, i2.k, u);
+      if (mode == R1_DECODE) {
+        float2* out = coils_out + (size_t)j * G * G + (size_t)r2 * G;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+          const int p = i2.k + N1 * k2;
+          out[p] = cscale(flip(u[k2], p), d.invG);
           if (j == 0) {
-            const float2 x = rho_src[(size_t)r * G + p];
-            rhom_out[(size_t)r * G + p] = in_win(d, r, p) ? x : make_float2(0.f, 0.f);
+            const float2 x = rho_src[(size_t)r2 * G + p];
+            rhom_out[(size_t)r2 * G + p] = in_win(d, r2, p) ? x : make_float2(0.f, 0.f);
           }
         }
-      }
-      return;
-    }
-  }
-  // build t on the window and run the forward Toeplitz row pass
-  for (int idx = threadIdx.x; idx < LPB * G; idx += blockDim.x) {
-    const int l = idx / G, t = idx - (idx / G) * G;
-    float2 v = make_float2(0.f, 0.f);
-    if (l < nl && t >= d.lo && t < d.lo + d.L) {
-      const size_t e = (size_t)(row0 + rl0 + l) * G + t;
-      const float2 rm = rhom[e];
-      const float2 c = cj[e];
-      if (mode == R1_OP) {
-        const float2 a = cscale(flip(B[Geo::b_idx(l, t)], t), d.invG);
-        // t = c_j * drho + rho * (W^-1 dchat_j)   (nlinv.cpp:163)
-        const float2 s1 = cmul_rn(c, drho[e]);
-        const float2 s2 = cmul_rn(rm, a);
-        v = make_float2(__fadd_rn(s1.x, s2.x), __fadd_rn(s1.y, s2.y));
       } else {
-        v = cmul_rn(rm, c);  // e = rho * c_j   (nlinv.cpp:252)
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+          const int p = i2.k + N1 * k2;
+          float2 w = make_float2(0.f, 0.f);
+          if (p >= d.lo && p < d.lo + d.L) {
+            const size_t e = (size_t)r2 * G + p;
+            const float2 aw = cscale(flip(u[k2], p), d.invG);
+            // t = c_j * drho + rho * (W^-1 dchat_j)   (nlinv.cpp:163)
+            const float2 s1 = cmul_rn(cj[e], drho[e]);
+            const float2 s2 = cmul_rn(rhom[e], aw);
+            w = flip(make_float2(__fadd_rn(s1.x, s2.x), __fadd_rn(s1.y, s2.y)), p);
+          }
+          u[k2] = w;
+        }
       }
-      v = flip(v, t);
     }
-    A[Geo::a_idx(l, t)] = v;
+    if (mode == R1_DECODE) return;  // uniform across the block: no barrier follows
+    __syncthreads();
+    if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
+    __syncthreads();
+    if (a1) get_step1<Geo>(A, i1.l, i1.k, v);
+  } else if (a1) {
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const int t = N2 * n1 + i1.k;
+      v[n1] = make_float2(0.f, 0.f);
+      if (t >= d.lo && t < d.lo + d.L) {
+        const size_t e = (size_t)r1 * G + t;
+        v[n1] = flip(cmul_rn(rhom[e], cj[e]), t);  // e = rho * c_j   (nlinv.cpp:252)
+      }
+    }
   }
-  tile_fft<Geo, -1>(A, B, nl, twG);
-  float2* Vj = V + (size_t)j * d.L * G;
-  for (int idx = threadIdx.x; idx < LPB * G; idx += blockDim.x) {
-    const int l = idx / G, p = idx - (idx / G) * G;
-    if (l < nl) Vj[(size_t)(rl0 + l) * G + p] = flip(B[Geo::b_idx(l, p)], p);
+  if (a1) {
+    fft_step1<Geo, -1>(v, i1.k, twG);
+    park_step1<Geo>(A, i1.l, i1.k, v);
+  }
+  __syncthreads();
+  if (a2) {
+    float2 u[N2];
+    fft_step2<Geo, -1>(A, i2.l, i2.k, u);
+    float2* Vr = V + (size_t)j * d.L * G + (size_t)(rl0 + i2.l) * G;
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) {
+      const int p = i2.k + N1 * k2;
+      Vr[p] = flip(u[k2], p);
+    }
   }
 }
 
 // Toeplitz column pass: forward column FFT of the window rows of V_j, * P/G, inverse
 // column FFT, keep the window rows (in place in V_j). Lines: (j, column q).
 template <class Geo>
-__global__ void __launch_bounds__(kThreads) k_colsT(Dims d, const float2* __restrict__ twG,
-                                                    const float2* __restrict__ P, float2* __restrict__ V,
-                                                    const DevState* st, int use_halt) {
+__global__ void __launch_bounds__(Geo::NT) k_colsT(Dims d, const float2* __restrict__ twG,
+                                                   const float2* __restrict__ P, float2* __restrict__ V,
+                                                   const DevState* st, int use_halt) {
   if (st->status || (use_halt && st->cr_halt)) return;
-  constexpr int G = Geo::G, LPB = Geo::LPB;
-  extern __shared__ float2 sm[];
-  float2* A = sm;
-  float2* B = sm + LPB * Geo::LSA;
-  constexpr int tiles = (G + LPB - 1) / LPB;
+  RTNB_TILE_SETUP(true);
+  constexpr int tiles = (G + Geo::LPB - 1) / Geo::LPB;
   const int j = blockIdx.x / tiles;
-  const int q0 = (blockIdx.x - j * tiles) * LPB;
-  const int nl = min(LPB, G - q0);
+  const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
+  const int nl = min(Geo::LPB, G - q0);
+  const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
   float2* Vj = V + (size_t)j * d.L * G;
-  for (int idx = threadIdx.x; idx < G * LPB; idx += blockDim.x) {
-    const int t = idx / LPB, l = idx - (idx / LPB) * LPB;
-    float2 v = make_float2(0.f, 0.f);
-    if (l < nl && t >= d.lo && t < d.lo + d.L) v = flip(Vj[(size_t)(t - d.lo) * G + q0 + l], t);
-    A[Geo::a_idx(l, t)] = v;
+  float2 v[N1];
+  if (a1) {
+    const float2* col = Vj + q0 + i1.l;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const int t = N2 * n1 + i1.k;
+      v[n1] = (t >= d.lo && t < d.lo + d.L) ? flip(col[(size_t)(t - d.lo) * G], t) : make_float2(0.f, 0.f);
+    }
+    fft_step1<Geo, -1>(v, i1.k, twG);
+    park_step1<Geo>(A, i1.l, i1.k, v);
   }
-  tile_fft<Geo, -1>(A, B, nl, twG);
-  // k-space multiply; the output sign flip of the forward pass cancels the input
-  // flip of the inverse pass
-  for (int idx = threadIdx.x; idx < G * LPB; idx += blockDim.x) {
-    const int p = idx / LPB, l = idx - (idx / LPB) * LPB;
-    float2 v = make_float2(0.f, 0.f);
-    if (l < nl) v = cscale(cmul(B[Geo::b_idx(l, p)], P[(size_t)p * G + q0 + l]), d.invG);
-    A[Geo::a_idx(l, p)] = v;
+  __syncthreads();
+  float2 u[N2];
+  if (a2) {
+    fft_step2<Geo, -1>(A, i2.l, i2.k, u);
+    // k-space multiply; the forward pass's output flip cancels the inverse pass's
+    // input flip
+    const float2* Pc = P + q0 + i2.l;
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) {
+      const int p = i2.k + N1 * k2;
+      u[k2] = cscale(cmul(u[k2], Pc[(size_t)p * G]), d.invG);
+    }
   }
-  tile_fft<Geo, +1>(A, B, nl, twG);
-  for (int idx = threadIdx.x; idx < d.L * LPB; idx += blockDim.x) {
-    const int pr = idx / LPB, l = idx - pr * LPB;
-    if (l < nl) {
-      const int p = d.lo + pr;
-      Vj[(size_t)pr * G + q0 + l] = flip(B[Geo::b_idx(l, p)], p);
+  __syncthreads();
+  if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
+  __syncthreads();
+  if (a1) {
+    get_step1<Geo>(A, i1.l, i1.k, v);
+    fft_step1<Geo, +1>(v, i1.k, twG);
+    park_step1<Geo>(A, i1.l, i1.k, v);
+  }
+  __syncthreads();
+  if (a2) {
+    fft_step2<Geo, +1>(A, i2.l, i2.k, u);
+    float2* col = Vj + q0 + i2.l;
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) {
+      const int p = i2.k + N1 * k2;
+      if (p >= d.lo && p < d.lo + d.L) col[(size_t)(p - d.lo) * G] = flip(u[k2], p);
     }
   }
 }
@@ -291,63 +344,81 @@ enum Rows2Mode : int { R2_OP = 0, R2_SETUP = 1 };
 // term of out.rho), rt = conj(rho) T -> forward W^-H row pass keeping the Gc
 // coil k-columns -> Y_j (L x Gc).
 template <class Geo>
-__global__ void __launch_bounds__(kThreads) k_rows2(Dims d, int mode, const float2* __restrict__ twG,
-                                                    const float2* __restrict__ V,
-                                                    const float2* __restrict__ coils,
-                                                    const float2* __restrict__ rhom,
-                                                    const float2* __restrict__ z, float2* __restrict__ RC,
-                                                    float2* __restrict__ Y, double* partials, DevState* st,
-                                                    int use_halt) {
+__global__ void __launch_bounds__(Geo::NT) k_rows2(Dims d, int mode, const float2* __restrict__ twG,
+                                                   const float2* __restrict__ V,
+                                                   const float2* __restrict__ coils,
+                                                   const float2* __restrict__ rhom,
+                                                   const float2* __restrict__ z, float2* __restrict__ RC,
+                                                   float2* __restrict__ Y, double* partials, DevState* st,
+                                                   int use_halt) {
   if (st->status || (use_halt && st->cr_halt)) return;
-  constexpr int G = Geo::G, LPB = Geo::LPB;
-  extern __shared__ float2 sm[];
-  float2* A = sm;
-  float2* B = sm + LPB * Geo::LSA;
-  const int tiles = (d.L + LPB - 1) / LPB;
+  RTNB_TILE_SETUP(false);
+  const int tiles = (d.L + Geo::LPB - 1) / Geo::LPB;
   const int j = blockIdx.x / tiles;
-  const int rl0 = (blockIdx.x - j * tiles) * LPB;
-  const int nl = min(LPB, d.L - rl0);
-  const float2* Vj = V + (size_t)j * d.L * G;
+  const int rl0 = (blockIdx.x - j * tiles) * Geo::LPB;
+  const int nl = min(Geo::LPB, d.L - rl0);
+  const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
   const float2* cj = coils + (size_t)j * G * G;
   const float2* zj = z + (size_t)j * G * G;
-  float2* RCj = RC + (size_t)j * d.L * d.L;
-  for (int idx = threadIdx.x; idx < LPB * G; idx += blockDim.x) {
-    const int l = idx / G, t = idx - (idx / G) * G;
-    float2 v = make_float2(0.f, 0.f);
-    if (l < nl) v = flip(Vj[(size_t)(rl0 + l) * G + t], t);
-    A[Geo::a_idx(l, t)] = v;
-  }
-  tile_fft<Geo, +1>(A, B, nl, twG);
-  double resid = 0.0;
-  for (int idx = threadIdx.x; idx < LPB * G; idx += blockDim.x) {
-    const int l = idx / G, t = idx - (idx / G) * G;
-    float2 v = make_float2(0.f, 0.f);
-    if (l < nl && t >= d.lo && t < d.lo + d.L) {
-      const int r = d.lo + rl0 + l;
-      const size_t e = (size_t)r * G + t;
-      float2 T = cscale(flip(B[Geo::b_idx(l, t)], t), d.invG);
-      if (mode == R2_SETUP) {
-        const float2 zz = zj[e];
-        T = make_float2(__fsub_rn(zz.x, T.x), __fsub_rn(zz.y, T.y));
-        resid += nrm2(T);
-      }
-      RCj[(size_t)(rl0 + l) * d.L + (t - d.lo)] = cjmul_rn(cj[e], T);
-      v = flip(cjmul_rn(rhom[e], T), t);
+  float2 v[N1];
+  if (a1) {
+    const float2* Vr = V + (size_t)j * d.L * G + (size_t)(rl0 + i1.l) * G;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const int t = N2 * n1 + i1.k;
+      v[n1] = flip(Vr[t], t);
     }
-    A[Geo::a_idx(l, t)] = v;
+    fft_step1<Geo, +1>(v, i1.k, twG);
+    park_step1<Geo>(A, i1.l, i1.k, v);
   }
-  tile_fft<Geo, -1>(A, B, nl, twG);
-  float2* Yj = Y + (size_t)j * d.L * d.Gc;
-  for (int idx = threadIdx.x; idx < LPB * d.Gc; idx += blockDim.x) {
-    const int l = idx / d.Gc, q = idx - (idx / d.Gc) * d.Gc;
-    if (l < nl) {
-      const int p = d.off + q;
-      Yj[(size_t)(rl0 + l) * d.Gc + q] = flip(B[Geo::b_idx(l, p)], p);
+  __syncthreads();
+  double resid = 0.0;
+  float2 u[N2];
+  if (a2) {
+    fft_step2<Geo, +1>(A, i2.l, i2.k, u);
+    const int rl = rl0 + i2.l;
+    const int r = d.lo + rl;
+    float2* RCr = RC + (size_t)j * d.L * d.L + (size_t)rl * d.L;
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) {
+      const int p = i2.k + N1 * k2;
+      float2 w = make_float2(0.f, 0.f);
+      if (p >= d.lo && p < d.lo + d.L) {
+        const size_t e = (size_t)r * G + p;
+        float2 T = cscale(flip(u[k2], p), d.invG);
+        if (mode == R2_SETUP) {
+          const float2 zz = zj[e];
+          T = make_float2(__fsub_rn(zz.x, T.x), __fsub_rn(zz.y, T.y));
+          resid += nrm2(T);
+        }
+        RCr[p - d.lo] = cjmul_rn(cj[e], T);
+        w = flip(cjmul_rn(rhom[e], T), p);
+      }
+      u[k2] = w;
+    }
+  }
+  __syncthreads();
+  if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
+  __syncthreads();
+  if (a1) {
+    get_step1<Geo>(A, i1.l, i1.k, v);
+    fft_step1<Geo, -1>(v, i1.k, twG);
+    park_step1<Geo>(A, i1.l, i1.k, v);
+  }
+  __syncthreads();
+  if (a2) {
+    fft_step2<Geo, -1>(A, i2.l, i2.k, u);
+    float2* Yr = Y + (size_t)j * d.L * d.Gc + (size_t)(rl0 + i2.l) * d.Gc;
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) {
+      const int p = i2.k + N1 * k2;
+      const int q = p - d.off;
+      if (q >= 0 && q < d.Gc) Yr[q] = flip(u[k2], p);
     }
   }
   if (mode == R2_SETUP) {
-    double v[1] = {resid}, tot[1];
-    if (grid_reduce<1>(v, partials, &st->counter, tot) && threadIdx.x == 0) {
+    double vv[1] = {resid}, tot[1];
+    if (grid_reduce<1>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
       st->steps[st->cur_step].resid_win = tot[0];
     }
   }
@@ -370,19 +441,18 @@ struct ColsWArgs {
 };
 
 // Last pass of an application: W^-H column pass (blocks [0, nbw)) and the channel
-// sum of out.rho over the full G x G grid (blocks [nbw, grid)).
+// sum of out.rho over the full G x G grid (blocks [nbw, grid), one element per thread).
 template <class Geo>
-__global__ void __launch_bounds__(kThreads) k_colsW(Dims d, ColsWArgs a, const float* __restrict__ winv,
-                                                    const float2* __restrict__ twG,
-                                                    const float2* __restrict__ Y,
-                                                    const float2* __restrict__ RC,
-                                                    const float2* __restrict__ coils,
-                                                    const float2* __restrict__ z, int nbw,
-                                                    double* partials, DevState* st, CrScalars cr,
-                                                    int use_halt) {
+__global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const float* __restrict__ winv,
+                                                   const float2* __restrict__ twG,
+                                                   const float2* __restrict__ Y,
+                                                   const float2* __restrict__ RC,
+                                                   const float2* __restrict__ coils,
+                                                   const float2* __restrict__ z, int nbw,
+                                                   double* partials, DevState* st, CrScalars cr,
+                                                   int use_halt) {
   if (st->status || (use_halt && st->cr_halt)) return;
-  constexpr int G = Geo::G, LPB = Geo::LPB;
-  extern __shared__ float2 sm[];
+  RTNB_TILE_SETUP(true);
   const int D0 = G * G;
   double acc0 = 0.0, acc1 = 0.0;
   // combine the normal-operator value n at flat index e with the CR / rhs terms
@@ -396,51 +466,71 @@ __global__ void __launch_bounds__(kThreads) k_colsW(Dims d, ColsWArgs a, const f
       acc0 += nrm2(v);
     } else {
       float2 v = n;
-      if (a.mode == CW_OPALPHA) v = axpy_rn(v, a.alpha, a.dx[e]);
-      a.out[e] = v;
       const float2 p = a.dx[e];
+      if (a.mode == CW_OPALPHA) v = axpy_rn(v, a.alpha, p);
+      a.out[e] = v;
       acc0 += (double)p.x * v.x + (double)p.y * v.y;  // Re <dx, out>
     }
   };
   if ((int)blockIdx.x < nbw) {
-    float2* A = sm;
-    float2* B = sm + LPB * Geo::LSA;
-    const int tiles = (d.Gc + LPB - 1) / LPB;
+    const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
     const int j = blockIdx.x / tiles;
-    const int q0 = (blockIdx.x - j * tiles) * LPB;
-    const int nl = min(LPB, d.Gc - q0);
-    const float2* Yj = Y + (size_t)j * d.L * d.Gc;
-    for (int idx = threadIdx.x; idx < G * LPB; idx += blockDim.x) {
-      const int t = idx / LPB, l = idx - (idx / LPB) * LPB;
-      float2 v = make_float2(0.f, 0.f);
-      if (l < nl && t >= d.lo && t < d.lo + d.L) v = flip(Yj[(size_t)(t - d.lo) * d.Gc + q0 + l], t);
-      A[Geo::a_idx(l, t)] = v;
+    const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
+    const int nl = min(Geo::LPB, d.Gc - q0);
+    const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
+    if (a1) {
+      const float2* col = Y + (size_t)j * d.L * d.Gc + q0 + i1.l;
+      float2 v[N1];
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) {
+        const int t = N2 * n1 + i1.k;
+        v[n1] = (t >= d.lo && t < d.lo + d.L) ? flip(col[(size_t)(t - d.lo) * d.Gc], t) : make_float2(0.f, 0.f);
+      }
+      fft_step1<Geo, -1>(v, i1.k, twG);
+      park_step1<Geo>(A, i1.l, i1.k, v);
     }
-    tile_fft<Geo, -1>(A, B, nl, twG);
-    for (int idx = threadIdx.x; idx < d.Gc * LPB; idx += blockDim.x) {
-      const int i = idx / LPB, l = idx - (idx / LPB) * LPB;
-      if (l < nl) {
-        const int p = d.off + i;
-        const int e = i * d.Gc + q0 + l;
-        const float w = winv[e];
-        const float2 f = cscale(flip(B[Geo::b_idx(l, p)], p), d.invG);
-        // crop_k(FFT(u)) * winv   (nlinv.cpp:127-133)
-        finish((size_t)D0 + (size_t)j * d.Gc * d.Gc + e, make_float2(f.x * w, f.y * w));
+    __syncthreads();
+    if (a2) {
+      float2 u[N2];
+      fft_step2<Geo, -1>(A, i2.l, i2.k, u);
+      const int q = q0 + i2.l;
+#pragma unroll
+      for (int k2 = 0; k2 < N2; ++k2) {
+        const int p = i2.k + N1 * k2;
+        const int i = p - d.off;
+        if (i >= 0 && i < d.Gc) {
+          const int e = i * d.Gc + q;
+          const float w = winv[e];
+          const float2 f = cscale(flip(u[k2], p), d.invG);
+          // crop_k(FFT(u)) * winv   (nlinv.cpp:127-133)
+          finish((size_t)D0 + (size_t)j * d.Gc * d.Gc + e, make_float2(f.x * w, f.y * w));
+        }
       }
     }
   } else {
     // out.rho: window = fixed-order FP64 sum of rc_j over channels (decomp.cpp:26-39);
     // outside the window T is masked to zero, so only the SETUP data term survives
-    for (int e = (blockIdx.x - nbw) * blockDim.x + threadIdx.x; e < D0;
-         e += (gridDim.x - nbw) * blockDim.x) {
+    for (int e = (blockIdx.x - nbw) * blockDim.x + threadIdx.x; e < D0; e += (gridDim.x - nbw) * blockDim.x) {
       const int r = e / G, c = e - (e / G) * G;
       double sx = 0.0, sy = 0.0;
       if (in_win(d, r, c)) {
-        const size_t w = (size_t)(r - d.lo) * d.L + (c - d.lo);
-        for (int j = 0; j < d.J; ++j) {
-          const float2 v = RC[(size_t)j * d.L * d.L + w];
-          sx += v.x;
-          sy += v.y;
+        const float2* src = RC + (size_t)(r - d.lo) * d.L + (c - d.lo);
+        const size_t stride = (size_t)d.L * d.L;
+        int j = 0;
+        for (; j + 8 <= d.J; j += 8) {
+          float2 t[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) t[k] = src[(j + k) * stride];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            sx += t[k].x;
+            sy += t[k].y;
+          }
+        }
+        for (; j < d.J; ++j) {
+          const float2 t = src[j * stride];
+          sx += t.x;
+          sy += t.y;
         }
       } else if (a.mode == CW_SETUP) {
         for (int j = 0; j < d.J; ++j) {
@@ -454,8 +544,8 @@ __global__ void __launch_bounds__(kThreads) k_colsW(Dims d, ColsWArgs a, const f
       finish((size_t)e, make_float2((float)sx, (float)sy));
     }
   }
-  double v[2] = {acc0, acc1}, tot[2];
-  if (grid_reduce<2>(v, partials, &st->counter, tot) && threadIdx.x == 0) {
+  double vv[2] = {acc0, acc1}, tot[2];
+  if (grid_reduce<2>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
     if (a.mode == CW_SETUP) {
       StepRec& s = st->steps[st->cur_step];
       s.rhs_nrm2 = tot[0];
@@ -620,42 +710,38 @@ __global__ void __launch_bounds__(kThreads) k_image(Dims d, const float2* __rest
 // Stand-alone centered 2D transforms (fft::forward / fft::inverse, fft.hpp:22-30).
 // ---------------------------------------------------------------------------------
 
-// one pass of a batched 2D transform over `batch` images: rows (axis 1) or columns
-// (axis 0); scale applied on output
-template <class Geo, int S>
-__global__ void __launch_bounds__(kThreads) k_fft_pass(float2* __restrict__ data, int batch, int axis,
-                                                       const float2* __restrict__ twG, float scale) {
-  constexpr int G = Geo::G, LPB = Geo::LPB;
-  extern __shared__ float2 sm[];
-  float2* A = sm;
-  float2* B = sm + LPB * Geo::LSA;
-  constexpr int tiles = (G + LPB - 1) / LPB;
+// one pass of a batched 2D transform over `batch` images: rows (COLS = false, axis 1)
+// or columns (COLS = true, axis 0); scale applied on output
+template <class Geo, int S, bool COLS>
+__global__ void __launch_bounds__(Geo::NT) k_fft_pass(float2* __restrict__ data, int batch,
+                                                      const float2* __restrict__ twG, float scale) {
+  RTNB_TILE_SETUP(COLS);
+  constexpr int tiles = (G + Geo::LPB - 1) / Geo::LPB;
   const int img = blockIdx.x / tiles;
-  if (img >= batch) return;
-  const int l0 = (blockIdx.x - img * tiles) * LPB;
-  const int nl = min(LPB, G - l0);
+  if (img >= batch) return;  // uniform per block
+  const int l0 = (blockIdx.x - img * tiles) * Geo::LPB;
+  const int nl = min(Geo::LPB, G - l0);
   float2* base = data + (size_t)img * G * G;
-  if (axis == 1) {
-    for (int idx = threadIdx.x; idx < LPB * G; idx += blockDim.x) {
-      const int l = idx / G, t = idx - (idx / G) * G;
-      A[Geo::a_idx(l, t)] = (l < nl) ? flip(base[(size_t)(l0 + l) * G + t], t) : make_float2(0.f, 0.f);
+  // element t of line l: rows -> base[(l0+l)*G + t], columns -> base[t*G + l0+l]
+  const size_t ls = COLS ? 1 : (size_t)G, es = COLS ? (size_t)G : 1;
+  if (i1.on && i1.l < nl) {
+    float2 v[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const int t = N2 * n1 + i1.k;
+      v[n1] = flip(base[(l0 + i1.l) * ls + t * es], t);
     }
-  } else {
-    for (int idx = threadIdx.x; idx < G * LPB; idx += blockDim.x) {
-      const int t = idx / LPB, l = idx - (idx / LPB) * LPB;
-      A[Geo::a_idx(l, t)] = (l < nl) ? flip(base[(size_t)t * G + l0 + l], t) : make_float2(0.f, 0.f);
-    }
+    fft_step1<Geo, S>(v, i1.k, twG);
+    park_step1<Geo>(A, i1.l, i1.k, v);
   }
-  tile_fft<Geo, S>(A, B, nl, twG);
-  if (axis == 1) {
-    for (int idx = threadIdx.x; idx < LPB * G; idx += blockDim.x) {
-      const int l = idx / G, p = idx - (idx / G) * G;
-      if (l < nl) base[(size_t)(l0 + l) * G + p] = cscale(flip(B[Geo::b_idx(l, p)], p), scale);
-    }
-  } else {
-    for (int idx = threadIdx.x; idx < G * LPB; idx += blockDim.x) {
-      const int p = idx / LPB, l = idx - (idx / LPB) * LPB;
-      if (l < nl) base[(size_t)p * G + l0 + l] = cscale(flip(B[Geo::b_idx(l, p)], p), scale);
+  __syncthreads();
+  if (i2.on && i2.l < nl) {
+    float2 u[N2];
+    fft_step2<Geo, S>(A, i2.l, i2.k, u);
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) {
+      const int p = i2.k + N1 * k2;
+      base[(l0 + i2.l) * ls + p * es] = cscale(flip(u[k2], p), scale);
     }
   }
 }
