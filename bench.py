@@ -384,7 +384,9 @@ def main():
     # roofline of the dominant kernel (isolated CUDA-event timing on the engine stream)
     peak, peak_kind = measured_peaks()
     ctx.make_step_cache(series.estimate(F - 1))
-    per_frame = {"colsT": 57, "rows1": 57, "rows2": 57, "colA": 57}
+    napply = sum(caps) + M  # CR applications + Newton-step setups per frame
+    per_frame = {"colsT": napply, "rows1": napply, "rows2": napply, "colA": napply, "colsW": napply,
+                 "cr_xr": sum(caps), "cr_pap": sum(caps) - M}
     kern = {}
     for name in per_frame:
         ms, by = ctx.time_kernel(name, 50)

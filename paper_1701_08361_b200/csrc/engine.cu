@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstddef>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -104,15 +105,38 @@ struct Engine::Ops {
   void (*rows1)(cudaStream_t, int, Dims, int, const float2*, const float2*, const float2*, const float2*,
                 const float2*, float2*, float2*, const float2*, float2*, const DevState*, int) = nullptr;
   void (*colsT)(cudaStream_t, int, Dims, const float2*, const float2*, float2*, const DevState*, int) = nullptr;
-  void (*rows2)(cudaStream_t, int, Dims, int, const float2*, const float2*, const float2*, const float2*,
-                const float2*, float2*, float2*, double*, DevState*, int) = nullptr;
+  void (*rows2)(cudaStream_t, int, Dims, int, const float2*, const float2*, const float2*,
+                const float2*, const float2*, float2*, double2*, double*, DevState*, int) = nullptr;
   void (*colsW)(cudaStream_t, int, Dims, ColsWArgs, const float*, const float2*, const float2*,
-                const float2*, const float2*, const float2*, int, double*, DevState*, CrScalars,
-                int) = nullptr;
+                const double2*, const float2*, const float2*, int, double*, DevState*, CrScalars, int) = nullptr;
   void (*fft)(cudaStream_t, int, int, float2*, int, int, const float2*, float) = nullptr;
 };
 
 namespace {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RTN_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// launch with programmatic stream serialisation (see pdl_enter, kernels_impl.cuh)
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  check_cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "launch");
+}
 
 template <int N1, int N2>
 struct Inst {
@@ -121,13 +145,17 @@ struct Inst {
   using Geo = LineGeom<N1, N2, kLpb>;
   static constexpr size_t kSmem = sizeof(float2) * Geo::SMEM_FLOAT2;
   static constexpr int kNT = Geo::NT;
+  // row pass 2: one window row x one group of kLpb channels (+ the channel terms)
+  static constexpr size_t kSmem2 = sizeof(float2) * (Geo::SMEM_FLOAT2 + kLpb * (N1 * N2 / 2));
 
   static void set_attrs() {
     const int s = static_cast<int>(kSmem);
     check_cuda(cudaFuncSetAttribute(k_colA<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colA");
     check_cuda(cudaFuncSetAttribute(k_rows1<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr rows1");
     check_cuda(cudaFuncSetAttribute(k_colsT<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsT");
-    check_cuda(cudaFuncSetAttribute(k_rows2<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr rows2");
+    check_cuda(cudaFuncSetAttribute(k_rows2<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmem2)),
+               "attr rows2");
     check_cuda(cudaFuncSetAttribute(k_colsW<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsW");
     check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
     check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, +1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr ifft");
@@ -151,27 +179,27 @@ Engine::Ops Inst<N1, N2>::make() {
   o.NT = kNT;
   o.colA = [](cudaStream_t s, int grid, Dims d, const float* winv, const float2* tw, const float2* chat,
               float2* U, int r0, int nr, const DevState* st, int h) {
-    k_colA<Geo><<<grid, kNT, kSmem, s>>>(d, winv, tw, chat, U, r0, nr, st, h);
+    launch_k(k_colA<Geo>, grid, kNT, kSmem, s, d, winv, tw, chat, U, r0, nr, st, h);
   };
   o.rows1 = [](cudaStream_t s, int grid, Dims d, int mode, const float2* tw, const float2* U,
                const float2* coils, const float2* rhom, const float2* drho, float2* V, float2* coils_out,
                const float2* rho_src, float2* rhom_out, const DevState* st, int h) {
-    k_rows1<Geo><<<grid, kNT, kSmem, s>>>(d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
-                                                rhom_out, st, h);
+    launch_k(k_rows1<Geo>, grid, kNT, kSmem, s, d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
+             rhom_out, st, h);
   };
   o.colsT = [](cudaStream_t s, int grid, Dims d, const float2* tw, const float2* P, float2* V,
                const DevState* st, int h) {
-    k_colsT<Geo><<<grid, kNT, kSmem, s>>>(d, tw, P, V, st, h);
+    launch_k(k_colsT<Geo>, grid, kNT, kSmem, s, d, tw, P, V, st, h);
   };
-  o.rows2 = [](cudaStream_t s, int grid, Dims d, int mode, const float2* tw, const float2* V,
-               const float2* coils, const float2* rhom, const float2* z, float2* RC, float2* Y,
+  o.rows2 = [](cudaStream_t s, int grid, Dims d, int setup, const float2* tw, const float2* V,
+               const float2* coils, const float2* rhom, const float2* z, float2* Y, double2* RP,
                double* partials, DevState* st, int h) {
-    k_rows2<Geo><<<grid, kNT, kSmem, s>>>(d, mode, tw, V, coils, rhom, z, RC, Y, partials, st, h);
+    launch_k(k_rows2<Geo>, grid, kNT, kSmem2, s, d, setup, tw, V, coils, rhom, z, Y, RP, partials, st, h);
   };
   o.colsW = [](cudaStream_t s, int grid, Dims d, ColsWArgs a, const float* winv, const float2* tw,
-               const float2* Y, const float2* RC, const float2* coils, const float2* z, int nbw,
+               const float2* Y, const double2* RP, const float2* coils, const float2* z, int nbw,
                double* partials, DevState* st, CrScalars cr, int h) {
-    k_colsW<Geo><<<grid, kNT, kSmem, s>>>(d, a, winv, tw, Y, RC, coils, z, nbw, partials, st, cr, h);
+    launch_k(k_colsW<Geo>, grid, kNT, kSmem, s, d, a, winv, tw, Y, RP, coils, z, nbw, partials, st, cr, h);
   };
   o.fft = [](cudaStream_t s, int grid, int sign, float2* data, int batch, int axis, const float2* tw,
              float scale) {
@@ -357,6 +385,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), dev_(device) {
   dims_.off = plan.G / 2 - plan.Gc / 2;
   dims_.N = plan.N;
   dims_.invG = 1.0f / static_cast<float>(plan.G);
+  dims_.H = (plan.J + ops_->LPB - 1) / ops_->LPB;
   D_ = plan.G * plan.G + plan.J * plan.Gc * plan.Gc;
   check_cuda(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
   alloc();
@@ -370,7 +399,7 @@ Engine::~Engine() {
   }
   if (frame_graph_) cudaGraphExecDestroy(frame_graph_);
   void* bufs[] = {winv_, P_, z_, x_, xcg_, r_, p_, ap_, ar_, reg_, est_scratch_[0], est_scratch_[1],
-                  est_scratch_[2], coils_, rhom_, U_, V_, RC_, Y_, gbuf_, img_, partials_, st_, cr_buf_};
+                  est_scratch_[2], coils_, rhom_, U_, V_, Y_, RP_, gbuf_, img_, partials_, st_, cr_buf_};
   for (void* b : bufs) {
     if (b) cudaFree(b);
   }
@@ -410,8 +439,8 @@ void Engine::alloc() {
   c2(&rhom_, G2, "rho");
   c2(&U_, J * plan_.G * plan_.Gc, "U");
   c2(&V_, J * L * plan_.G, "V");
-  c2(&RC_, J * L * L, "RC");
   c2(&Y_, J * L * plan_.Gc, "Y");
+  check_cuda(cudaMalloc(&RP_, sizeof(double2) * dims_.H * L * L), "RP");
   c2(&gbuf_, G2, "scratch");
   c2(&img_, static_cast<size_t>(plan_.N) * plan_.N, "image");
   vec_grid_ = blocks_for(D_, 148 * 4);
@@ -484,7 +513,7 @@ void Engine::set_data_device(const float2* z) {
 // ---- enqueue helpers ---------------------------------------------------------
 
 void Engine::enq_step_begin(int m) {
-  k_step_begin<<<1, 32, 0, s_>>>(st_, m);
+  launch_k(k_step_begin, 1, 32, 0, s_, st_, m);
 }
 
 void Engine::enq_decode(const float2* est) {
@@ -502,15 +531,15 @@ void Engine::enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, 
              use_halt);
   ops_->rows1(s_, J * tL, dims_, R1_OP, twG_, U_, coils_, rhom_, dx, V_, nullptr, nullptr, nullptr, st_, use_halt);
   ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, use_halt);
-  ops_->rows2(s_, J * tL, dims_, R2_OP, twG_, V_, coils_, rhom_, z_, RC_, Y_, partials_, st_, use_halt);
   ColsWArgs a{};
   a.mode = cw_mode;
   a.alpha = alpha;
   a.dot_slot = dot_slot;
   a.dx = dx;
   a.out = out;
+  ops_->rows2(s_, dims_.L * dims_.H, dims_, 0, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, use_halt);
   const int nbw = J * tGc;
-  ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RC_, coils_, z_, nbw, partials_, st_, cr_, use_halt);
+  ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, use_halt);
 }
 
 void Engine::enq_setup(const float2* x, const float2* reg, float alpha) {
@@ -519,7 +548,6 @@ void Engine::enq_setup(const float2* x, const float2* reg, float alpha) {
   enq_decode(x);
   ops_->rows1(s_, J * tL, dims_, R1_SETUP, twG_, U_, coils_, rhom_, nullptr, V_, nullptr, nullptr, nullptr, st_, 0);
   ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, 0);
-  ops_->rows2(s_, J * tL, dims_, R2_SETUP, twG_, V_, coils_, rhom_, z_, RC_, Y_, partials_, st_, 0);
   ColsWArgs a{};
   a.mode = CW_SETUP;
   a.a_x = static_cast<float>(-static_cast<double>(alpha));
@@ -530,23 +558,24 @@ void Engine::enq_setup(const float2* x, const float2* reg, float alpha) {
   a.out = r_;
   a.out2 = p_;
   a.out3 = xcg_;
+  ops_->rows2(s_, dims_.L * dims_.H, dims_, 1, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, 0);
   const int nbw = J * tGc;
-  ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RC_, coils_, z_, nbw, partials_, st_, cr_, 0);
+  ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, 0);
 }
 
 void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
   ensure_cr_capacity(cap);
   enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1);
-  k_cr_prime<<<vec_grid_, kThreads, 0, s_>>>(D_, ap_, ar_, partials_, st_, cr_);
+  launch_k(k_cr_prime, vec_grid_, kThreads, 0, s_, D_, ap_, ar_, partials_, st_, cr_);
   for (int it = 1; it <= cap; ++it) {
-    k_cr_xr<<<vec_grid_, kThreads, 0, s_>>>(D_, xcg_, r_, p_, ap_, partials_, st_, cr_, it, tol);
+    launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, partials_, st_, cr_, it, tol);
     if (it == cap) break;
     if (sync_each) {
       read_state();
       if (st_host_->status || st_host_->cr_halt) break;
     }
     enq_apply(r_, ar_, CW_OPALPHA, alpha, it, 1);
-    k_cr_pap<<<vec_grid_, kThreads, 0, s_>>>(D_, p_, ap_, r_, ar_, partials_, st_, cr_, it);
+    launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, p_, ap_, r_, ar_, partials_, st_, cr_, it);
   }
 }
 
@@ -561,13 +590,13 @@ void Engine::enq_newton_step(int m, float2* x, const float2* reg, float alpha, f
     }
     if (!sync_each || !st_host_->cr_halt) enq_cr(alpha, tol, cap, sync_each);
   }
-  k_axpy1<<<vec_grid_, kThreads, 0, s_>>>(D_, x, xcg_, st_);
+  launch_k(k_axpy1, vec_grid_, kThreads, 0, s_, D_, x, xcg_, st_);
 }
 
 void Engine::enq_image(const float2* est, float2* img, float scale, bool apply_scale) {
   enq_decode(est);
-  k_image<<<blocks_for(static_cast<long long>(plan_.N) * plan_.N, 148 * 4), kThreads, 0, s_>>>(
-      dims_, est, coils_, scale, apply_scale ? 1 : 0, img, st_);
+  launch_k(k_image, blocks_for(static_cast<long long>(plan_.N) * plan_.N, 148 * 4), kThreads, 0, s_, dims_,
+           est, coils_, scale, apply_scale ? 1 : 0, img, st_);
 }
 
 // ---- op-level API -------------------------------------------------------------
@@ -858,8 +887,10 @@ double Engine::kernel_bytes(const char* which) const {
   const std::string w(which);
   if (w == "colsT") return c8 * (2.0 * J * L * G + G * G);                   // V in + out, P
   if (w == "rows1") return c8 * (J * L * Gc + 2.0 * J * L * L + 2.0 * L * L + J * L * G);  // U, c_j, drho, rho, V
-  if (w == "rows2") return c8 * (J * L * G + J * L * L + L * L + J * L * L + J * L * Gc);  // V, c_j, rho, RC, Y
+  if (w == "rows2") return c8 * (J * L * G + J * L * L + L * L + J * L * Gc) + 16.0 * dims_.H * L * L;  // V, c_j, rho, Y, RP
   if (w == "colA") return c8 * (J * Gc * Gc + J * L * Gc) + 4.0 * Gc * Gc;
+  if (w == "colsW") return c8 * (J * L * Gc + 3.0 * (G * G + J * Gc * Gc)) + 16.0 * dims_.H * L * L + 4.0 * Gc * Gc;
+  if (w == "cr_xr" || w == "cr_pap") return c8 * 6.0 * (G * G + J * Gc * Gc);
   if (w == "colsW") return c8 * (J * L * Gc + J * L * L + 2.0 * (G * G + J * Gc * Gc)) + 4.0 * Gc * Gc;
   if (w == "apply") {
     // one fused normal-operator application (SURVEY.md §8(d) B_op, window pruned)
@@ -880,7 +911,20 @@ double Engine::time_kernel(const char* which, int reps) {
     } else if (w == "rows1") {
       ops_->rows1(s_, J * tL, dims_, R1_OP, twG_, U_, coils_, rhom_, r_, V_, nullptr, nullptr, nullptr, st_, 0);
     } else if (w == "rows2") {
-      ops_->rows2(s_, J * tL, dims_, R2_OP, twG_, V_, coils_, rhom_, z_, RC_, Y_, partials_, st_, 0);
+      ops_->rows2(s_, dims_.L * dims_.H, dims_, 0, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, 0);
+    } else if (w == "colsW") {
+      ColsWArgs a{};
+      a.mode = CW_OPALPHA;
+      a.alpha = 0.5f;
+      a.dot_slot = -1;
+      a.dx = r_;
+      a.out = ar_;
+      const int nbw = J * tGc;
+      ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, 0);
+    } else if (w == "cr_xr") {
+      launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], p_, ap_, partials_, st_, cr_, 1, 0.f);
+    } else if (w == "cr_pap") {
+      launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], r_, ar_, partials_, st_, cr_, 1);
     } else if (w == "colA") {
       ops_->colA(s_, J * tGc, dims_, winv_, twG_, r_ + static_cast<size_t>(G) * G, U_, dims_.lo, dims_.L, st_, 0);
     } else if (w == "apply") {
@@ -889,6 +933,12 @@ double Engine::time_kernel(const char* which, int reps) {
       fail(2, "time_kernel: unknown kernel " + w);
     }
   };
+  if (w.rfind("cr_", 0) == 0) {
+    // finite scalars so the recurrences run their full vector passes
+    const double one[2] = {1.0, 1.0};
+    check_cuda(cudaMemcpyAsync(cr_.rar, one, sizeof(one), cudaMemcpyHostToDevice, s_), "scalars");
+    check_cuda(cudaMemcpyAsync(cr_.ap2, one, sizeof(one), cudaMemcpyHostToDevice, s_), "scalars");
+  }
   for (int i = 0; i < 3; ++i) launch();
   cudaEvent_t a, b;
   check_cuda(cudaEventCreate(&a), "event");

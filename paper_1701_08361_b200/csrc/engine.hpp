@@ -176,8 +176,8 @@ class Engine {
   float2* rhom_ = nullptr;
   float2* U_ = nullptr;
   float2* V_ = nullptr;
-  float2* RC_ = nullptr;
   float2* Y_ = nullptr;
+  double2* RP_ = nullptr;
   float2* gbuf_ = nullptr;
   float2* img_ = nullptr;
   double* partials_ = nullptr;

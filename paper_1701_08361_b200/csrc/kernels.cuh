@@ -12,6 +12,7 @@ namespace rtnb {
 //   Gc  cropped coil k-space side, off = dc(G) - dc(Gc) its offset (planner.cpp:187-207)
 struct Dims {
   int G, Gc, J, L, lo, off, N;
+  int H;  // channel groups of k_rows2 (ceil(J / lines per block))
   float invG;
 };
 

@@ -56,6 +56,16 @@ __device__ __forceinline__ float2 cjmul_rn(float2 a, float2 b) {  // conj(a) * b
 }
 __device__ __forceinline__ double nrm2(float2 v) { return (double)v.x * v.x + (double)v.y * v.y; }
 
+// Programmatic dependent launch: every hot-path kernel is launched with programmatic
+// stream serialisation (engine.cu). It first waits for the previous kernel's grid to
+// complete and flush (griddepcontrol.wait; a no-op without the attribute), then lets
+// the next kernel start launching, so launch latency and block rasterisation of
+// kernel k+1 overlap the tail of kernel k inside the CUDA graph.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -135,6 +145,7 @@ __global__ void __launch_bounds__(Geo::NT) k_colA(Dims d, const float* __restric
                                                   const float2* __restrict__ twG,
                                                   const float2* __restrict__ chat, float2* __restrict__ U,
                                                   int r0, int nr, const DevState* st, int use_halt) {
+  pdl_enter();
   if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(true);
   const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
@@ -190,6 +201,7 @@ __global__ void __launch_bounds__(Geo::NT) k_rows1(Dims d, int mode, const float
                                                    const float2* __restrict__ rho_src,
                                                    float2* __restrict__ rhom_out, const DevState* st,
                                                    int use_halt) {
+  pdl_enter();
   if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(false);
   const int nrows = (mode == R1_DECODE) ? G : d.L;
@@ -285,6 +297,7 @@ template <class Geo>
 __global__ void __launch_bounds__(Geo::NT) k_colsT(Dims d, const float2* __restrict__ twG,
                                                    const float2* __restrict__ P, float2* __restrict__ V,
                                                    const DevState* st, int use_halt) {
+  pdl_enter();
   if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(true);
   constexpr int tiles = (G + Geo::LPB - 1) / Geo::LPB;
@@ -337,93 +350,6 @@ __global__ void __launch_bounds__(Geo::NT) k_colsT(Dims d, const float2* __restr
   }
 }
 
-enum Rows2Mode : int { R2_OP = 0, R2_SETUP = 1 };
-
-// Row pass 2: inverse Toeplitz row pass -> T (window, scaled 1/G). SETUP: e = z - T and
-// the data-residual partial (nlinv.cpp:254-256). rc = conj(c) T -> RC_j (the channel
-// term of out.rho), rt = conj(rho) T -> forward W^-H row pass keeping the Gc
-// coil k-columns -> Y_j (L x Gc).
-template <class Geo>
-__global__ void __launch_bounds__(Geo::NT) k_rows2(Dims d, int mode, const float2* __restrict__ twG,
-                                                   const float2* __restrict__ V,
-                                                   const float2* __restrict__ coils,
-                                                   const float2* __restrict__ rhom,
-                                                   const float2* __restrict__ z, float2* __restrict__ RC,
-                                                   float2* __restrict__ Y, double* partials, DevState* st,
-                                                   int use_halt) {
-  if (st->status || (use_halt && st->cr_halt)) return;
-  RTNB_TILE_SETUP(false);
-  const int tiles = (d.L + Geo::LPB - 1) / Geo::LPB;
-  const int j = blockIdx.x / tiles;
-  const int rl0 = (blockIdx.x - j * tiles) * Geo::LPB;
-  const int nl = min(Geo::LPB, d.L - rl0);
-  const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
-  const float2* cj = coils + (size_t)j * G * G;
-  const float2* zj = z + (size_t)j * G * G;
-  float2 v[N1];
-  if (a1) {
-    const float2* Vr = V + (size_t)j * d.L * G + (size_t)(rl0 + i1.l) * G;
-#pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) {
-      const int t = N2 * n1 + i1.k;
-      v[n1] = flip(Vr[t], t);
-    }
-    fft_step1<Geo, +1>(v, i1.k, twG);
-    park_step1<Geo>(A, i1.l, i1.k, v);
-  }
-  __syncthreads();
-  double resid = 0.0;
-  float2 u[N2];
-  if (a2) {
-    fft_step2<Geo, +1>(A, i2.l, i2.k, u);
-    const int rl = rl0 + i2.l;
-    const int r = d.lo + rl;
-    float2* RCr = RC + (size_t)j * d.L * d.L + (size_t)rl * d.L;
-#pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) {
-      const int p = i2.k + N1 * k2;
-      float2 w = make_float2(0.f, 0.f);
-      if (p >= d.lo && p < d.lo + d.L) {
-        const size_t e = (size_t)r * G + p;
-        float2 T = cscale(flip(u[k2], p), d.invG);
-        if (mode == R2_SETUP) {
-          const float2 zz = zj[e];
-          T = make_float2(__fsub_rn(zz.x, T.x), __fsub_rn(zz.y, T.y));
-          resid += nrm2(T);
-        }
-        RCr[p - d.lo] = cjmul_rn(cj[e], T);
-        w = flip(cjmul_rn(rhom[e], T), p);
-      }
-      u[k2] = w;
-    }
-  }
-  __syncthreads();
-  if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
-  __syncthreads();
-  if (a1) {
-    get_step1<Geo>(A, i1.l, i1.k, v);
-    fft_step1<Geo, -1>(v, i1.k, twG);
-    park_step1<Geo>(A, i1.l, i1.k, v);
-  }
-  __syncthreads();
-  if (a2) {
-    fft_step2<Geo, -1>(A, i2.l, i2.k, u);
-    float2* Yr = Y + (size_t)j * d.L * d.Gc + (size_t)(rl0 + i2.l) * d.Gc;
-#pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) {
-      const int p = i2.k + N1 * k2;
-      const int q = p - d.off;
-      if (q >= 0 && q < d.Gc) Yr[q] = flip(u[k2], p);
-    }
-  }
-  if (mode == R2_SETUP) {
-    double vv[1] = {resid}, tot[1];
-    if (grid_reduce<1>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
-      st->steps[st->cur_step].resid_win = tot[0];
-    }
-  }
-}
-
 enum ColsWMode : int { CW_OP = 0, CW_OPALPHA = 1, CW_SETUP = 2 };
 
 struct ColsWArgs {
@@ -440,38 +366,140 @@ struct ColsWArgs {
   float2* out3;       // SETUP: x_cg (zeroed)
 };
 
-// Last pass of an application: W^-H column pass (blocks [0, nbw)) and the channel
-// sum of out.rho over the full G x G grid (blocks [nbw, grid), one element per thread).
+// combine the normal-operator value n at flat index e with the CR / rhs terms and
+// accumulate the reduction the caller needs (Re<dx,out> or |rhs|^2)
+__device__ __forceinline__ void finish_elem(const ColsWArgs& a, size_t e, float2 n, double& acc) {
+  if (a.mode == CW_SETUP) {
+    float2 v = axpy_rn(n, a.a_x, a.x[e]);
+    v = axpy_rn(v, a.a_reg, a.reg[e]);
+    a.out[e] = v;
+    a.out2[e] = v;
+    a.out3[e] = make_float2(0.f, 0.f);
+    acc += nrm2(v);
+  } else {
+    float2 v = n;
+    const float2 p = a.dx[e];
+    if (a.mode == CW_OPALPHA) v = axpy_rn(v, a.alpha, p);
+    a.out[e] = v;
+    acc += (double)p.x * v.x + (double)p.y * v.y;  // Re <dx, out>
+  }
+}
+
+// Row pass 2. Block (window row r, channel group h of Geo::LPB channels): inverse
+// Toeplitz row pass -> T (window, 1/G); SETUP: e = z - T and the data residual
+// (nlinv.cpp:254-256); rc = conj(c_j) T summed over the group's channels in channel
+// order in FP64 in shared memory -> RP[h][r] (double2 partial of all_reduce_sum,
+// decomp.cpp:26-39; k_colsW adds the groups in order); rt = conj(rho) T -> forward
+// W^-H row pass keeping the Gc coil k-columns -> Y_j (L x Gc).
+template <class Geo>
+__global__ void __launch_bounds__(Geo::NT) k_rows2(Dims d, int setup, const float2* __restrict__ twG,
+                                                   const float2* __restrict__ V,
+                                                   const float2* __restrict__ coils,
+                                                   const float2* __restrict__ rhom,
+                                                   const float2* __restrict__ z, float2* __restrict__ Y,
+                                                   double2* __restrict__ RP, double* partials, DevState* st,
+                                                   int use_halt) {
+  pdl_enter();
+  if (st->status || (use_halt && st->cr_halt)) return;
+  RTNB_TILE_SETUP(false);
+  constexpr int L = G / 2;
+  float2* RCs = A + Geo::SMEM_FLOAT2;  // LPB x L channel terms of this row
+  const int rl = blockIdx.x % d.L;
+  const int h = blockIdx.x / d.L;
+  const int r = d.lo + rl;
+  const int j0 = h * Geo::LPB;
+  const int nl = min(Geo::LPB, d.J - j0);
+  const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
+  double resid = 0.0;
+  float2 v[N1];
+  if (a1) {
+    const float2* Vr = V + (size_t)(j0 + i1.l) * d.L * G + (size_t)rl * G;
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const int t = N2 * n1 + i1.k;
+      v[n1] = flip(Vr[t], t);
+    }
+    fft_step1<Geo, +1>(v, i1.k, twG);
+    park_step1<Geo>(A, i1.l, i1.k, v);
+  }
+  __syncthreads();
+  float2 u[N2];
+  if (a2) {
+    fft_step2<Geo, +1>(A, i2.l, i2.k, u);
+    const int j = j0 + i2.l;
+    const float2* cj = coils + (size_t)j * G * G + (size_t)r * G;
+    const float2* zj = z + (size_t)j * G * G + (size_t)r * G;
+    const float2* rr = rhom + (size_t)r * G;
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) {
+      const int p = i2.k + N1 * k2;
+      float2 w = make_float2(0.f, 0.f);
+      if (p >= d.lo && p < d.lo + d.L) {
+        float2 T = cscale(flip(u[k2], p), d.invG);
+        if (setup) {
+          const float2 zz = zj[p];
+          T = make_float2(__fsub_rn(zz.x, T.x), __fsub_rn(zz.y, T.y));
+          resid += nrm2(T);
+        }
+        RCs[i2.l * L + (p - d.lo)] = cjmul_rn(cj[p], T);
+        w = flip(cjmul_rn(rr[p], T), p);
+      }
+      u[k2] = w;
+    }
+  }
+  __syncthreads();
+  if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
+  if ((int)threadIdx.x < d.L) {
+    double sx = 0.0, sy = 0.0;
+    for (int l = 0; l < nl; ++l) {
+      const float2 t = RCs[l * L + threadIdx.x];
+      sx += t.x;
+      sy += t.y;
+    }
+    RP[((size_t)h * d.L + rl) * d.L + threadIdx.x] = make_double2(sx, sy);
+  }
+  __syncthreads();
+  if (a1) {
+    get_step1<Geo>(A, i1.l, i1.k, v);
+    fft_step1<Geo, -1>(v, i1.k, twG);
+    park_step1<Geo>(A, i1.l, i1.k, v);
+  }
+  __syncthreads();
+  if (a2) {
+    fft_step2<Geo, -1>(A, i2.l, i2.k, u);
+    float2* Yr = Y + (size_t)(j0 + i2.l) * d.L * d.Gc + (size_t)rl * d.Gc;
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) {
+      const int p = i2.k + N1 * k2;
+      const int q = p - d.off;
+      if (q >= 0 && q < d.Gc) Yr[q] = flip(u[k2], p);
+    }
+  }
+  if (setup) {
+    double vv[1] = {resid}, tot[1];
+    if (grid_reduce<1>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
+      st->steps[st->cur_step].resid_win = tot[0];
+    }
+  }
+}
+
+// Last pass of an application: W^-H column pass (blocks [0, nbw)) and out.rho
+// outside the window (blocks [nbw, grid)); the window part of out.rho came from
+// k_rows2, whose reduction partial (st->scal[1]) is folded into the totals here.
 template <class Geo>
 __global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const float* __restrict__ winv,
                                                    const float2* __restrict__ twG,
                                                    const float2* __restrict__ Y,
-                                                   const float2* __restrict__ RC,
+                                                   const double2* __restrict__ RP,
                                                    const float2* __restrict__ coils,
                                                    const float2* __restrict__ z, int nbw,
                                                    double* partials, DevState* st, CrScalars cr,
                                                    int use_halt) {
+  pdl_enter();
   if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(true);
   const int D0 = G * G;
   double acc0 = 0.0, acc1 = 0.0;
-  // combine the normal-operator value n at flat index e with the CR / rhs terms
-  auto finish = [&](size_t e, float2 n) {
-    if (a.mode == CW_SETUP) {
-      float2 v = axpy_rn(n, a.a_x, a.x[e]);
-      v = axpy_rn(v, a.a_reg, a.reg[e]);
-      a.out[e] = v;
-      a.out2[e] = v;
-      a.out3[e] = make_float2(0.f, 0.f);
-      acc0 += nrm2(v);
-    } else {
-      float2 v = n;
-      const float2 p = a.dx[e];
-      if (a.mode == CW_OPALPHA) v = axpy_rn(v, a.alpha, p);
-      a.out[e] = v;
-      acc0 += (double)p.x * v.x + (double)p.y * v.y;  // Re <dx, out>
-    }
-  };
   if ((int)blockIdx.x < nbw) {
     const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
     const int j = blockIdx.x / tiles;
@@ -503,32 +531,22 @@ __global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const fl
           const float w = winv[e];
           const float2 f = cscale(flip(u[k2], p), d.invG);
           // crop_k(FFT(u)) * winv   (nlinv.cpp:127-133)
-          finish((size_t)D0 + (size_t)j * d.Gc * d.Gc + e, make_float2(f.x * w, f.y * w));
+          finish_elem(a, (size_t)D0 + (size_t)j * d.Gc * d.Gc + e, make_float2(f.x * w, f.y * w), acc0);
         }
       }
     }
   } else {
-    // out.rho: window = fixed-order FP64 sum of rc_j over channels (decomp.cpp:26-39);
-    // outside the window T is masked to zero, so only the SETUP data term survives
+    // window: the channel-group partials of k_rows2 added in group order. Outside the
+    // window T is masked to zero (preproc.cpp:442), so out.rho there is only the SETUP
+    // data term sum_j conj(c_j) z_j, in channel order in FP64
+    const int H = d.H;
     for (int e = (blockIdx.x - nbw) * blockDim.x + threadIdx.x; e < D0; e += (gridDim.x - nbw) * blockDim.x) {
       const int r = e / G, c = e - (e / G) * G;
       double sx = 0.0, sy = 0.0;
       if (in_win(d, r, c)) {
-        const float2* src = RC + (size_t)(r - d.lo) * d.L + (c - d.lo);
-        const size_t stride = (size_t)d.L * d.L;
-        int j = 0;
-        for (; j + 8 <= d.J; j += 8) {
-          float2 t[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) t[k] = src[(j + k) * stride];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            sx += t[k].x;
-            sy += t[k].y;
-          }
-        }
-        for (; j < d.J; ++j) {
-          const float2 t = src[j * stride];
+        const double2* src = RP + (size_t)(r - d.lo) * d.L + (c - d.lo);
+        for (int h = 0; h < H; ++h) {
+          const double2 t = src[(size_t)h * d.L * d.L];
           sx += t.x;
           sy += t.y;
         }
@@ -541,16 +559,17 @@ __global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const fl
           acc1 += nrm2(zz);
         }
       }
-      finish((size_t)e, make_float2((float)sx, (float)sy));
+      finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), acc0);
     }
   }
   double vv[2] = {acc0, acc1}, tot[2];
   if (grid_reduce<2>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
+    const double total = tot[0];
     if (a.mode == CW_SETUP) {
       StepRec& s = st->steps[st->cur_step];
-      s.rhs_nrm2 = tot[0];
+      s.rhs_nrm2 = total;
       s.resid_out = tot[1];
-      const double rn = sqrt(tot[0]);
+      const double rn = sqrt(total);
       // cg_solve entry checks (nlinv.cpp:184-186)
       if (!isfinite(rn)) {
         st->status = ST_SOLVER;
@@ -560,9 +579,9 @@ __global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const fl
         st->cr_halt = 1;
       }
     } else if (a.dot_slot >= 0) {
-      cr.rar[a.dot_slot] = tot[0];
+      cr.rar[a.dot_slot] = total;
     } else {
-      st->scal[0] = tot[0];
+      st->scal[0] = total;
     }
   }
 }
@@ -573,6 +592,7 @@ __global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const fl
 
 // first kernel of every Newton step: reset the step record and the CR halt flag
 __global__ void k_step_begin(DevState* st, int m) {
+  pdl_enter();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     st->cur_step = m;
     st->cr_halt = 0;
@@ -589,6 +609,7 @@ __global__ void k_step_begin(DevState* st, int m) {
 __global__ void __launch_bounds__(kThreads) k_cr_prime(int D, float2* __restrict__ ap,
                                                        const float2* __restrict__ ar, double* partials,
                                                        DevState* st, CrScalars cr) {
+  pdl_enter();
   if (st->status || st->cr_halt) return;
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
@@ -605,6 +626,7 @@ __global__ void __launch_bounds__(kThreads) k_cr_xr(int D, float2* __restrict__ 
                                                     const float2* __restrict__ p,
                                                     const float2* __restrict__ ap, double* partials,
                                                     DevState* st, CrScalars cr, int it, float tol) {
+  pdl_enter();
   if (st->status || st->cr_halt) return;
   const double denom = cr.ap2[it - 1];
   const double rar = cr.rar[it - 1];
@@ -654,6 +676,7 @@ __global__ void __launch_bounds__(kThreads) k_cr_pap(int D, float2* __restrict__
                                                      const float2* __restrict__ r,
                                                      const float2* __restrict__ ar, double* partials,
                                                      DevState* st, CrScalars cr, int it) {
+  pdl_enter();
   if (st->status || st->cr_halt) return;
   const double rar_new = cr.rar[it], rar_old = cr.rar[it - 1];
   const double b = (rar_old != 0.0) ? rar_new / rar_old : 0.0;
@@ -677,6 +700,7 @@ __global__ void __launch_bounds__(kThreads) k_cr_pap(int D, float2* __restrict__
 // x += 1.0 * x_cg  (newton_step, nlinv.cpp:281)
 __global__ void __launch_bounds__(kThreads) k_axpy1(int D, float2* __restrict__ x, const float2* __restrict__ d,
                                                     const DevState* st) {
+  pdl_enter();
   if (st->status) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
     const float2 a = x[i], b = d[i];
@@ -690,6 +714,7 @@ __global__ void __launch_bounds__(kThreads) k_image(Dims d, const float2* __rest
                                                     const float2* __restrict__ coils, float scale,
                                                     int apply_scale, float2* __restrict__ img,
                                                     const DevState* st) {
+  pdl_enter();
   if (st->status) return;
   const int G = d.G, N = d.N;
   const int o = G / 2 - N / 2;
