@@ -314,7 +314,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
-    ap.add_argument("--T", type=int, default=1, help="frames in flight (temporal decomposition); 1 = plain chain")
+    ap.add_argument("--T", default="auto",
+                    help="frames in flight (temporal decomposition): 1 = plain chain, N, or auto = autotuner")
+    ap.add_argument("--tune-db", default=os.path.join(ROOT, "profiles", "tune_db.tsv"),
+                    help="autotuner store (autotune.hpp TuneDb format)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -334,7 +337,8 @@ def main():
     plan.newton_steps, plan.cg_iter_budget = 7, 50
     M = plan.newton_steps
     W, S = args.warmup, args.steps
-    F = W + S
+    NTUNE = 8 if args.T == "auto" else 0  # frames per autotune candidate, past the strict prefix
+    F = W + NTUNE + S
 
     z_unique, P = synth_series(G, J, K, U, n_unique=min(F, 10), seed=1234 + rank)
     ctx = pb.Context(plan, device=local)
@@ -345,13 +349,45 @@ def main():
         series.upload_psf(k, P[k])
     series.set_psf_index([n % U for n in range(F)])
     series.normalize()
-    opts = pb.SeriesOptions(T=args.T, plain=args.T == 1, sched=pb.TemporalSchedule.for_turns(U))
+    sched = pb.TemporalSchedule.for_turns(U)
+
+    def opts_for(T):
+        return pb.SeriesOptions(T=T, plain=T == 1, sched=sched)
 
     # warm-up (graph capture happens here)
-    series.run(opts, first=0, count=W, want_images=False)
+    series.run(opts_for(1), first=0, count=W, want_images=False)
+    tuning = None
+    if args.T == "auto":
+        # the paper's (T, A) autotuner (autotune.cpp:49-88): learn_step walks the legal
+        # space (one device: A = 1, T = frames in flight on separate streams), each
+        # candidate measured on W frames (device time), then select_config picks the
+        # best recorded configuration for this protocol key
+        key = (pb.ImagingMode.single_slice, plan.N, pb.frames_bucket(S), J)
+        db = []
+        space = [c for c in pb.legal_configs(6, a_cap=1)]
+        for _ in space:
+            T_try, A_try = pb.learn_step(key, db, 6, 1)
+            series.run(opts_for(T_try), first=W, count=NTUNE, want_images=False)
+            ms = series.last_span_ms() / NTUNE
+            db.append(key + (T_try, A_try, ms))
+        T_sel, _ = pb.select_config(key, db)
+        tuning = {"key": {"mode": "single_slice", "N": plan.N, "bucket": pb.frames_bucket(S), "J": J},
+                  "measured_ms_per_frame": {f"T{r[4]}": round(r[6], 3) for r in db}, "selected_T": T_sel}
+        if rank == 0 and args.tune_db:
+            try:
+                tdb = pb.TuneDb(args.tune_db)
+                for r in db:
+                    tdb.append(r[:6], r[6], int(time.time()))
+            except Exception:
+                pass
+        T = T_sel
+        series.run(opts_for(T), first=W, count=NTUNE, want_images=False)  # warm the selected config
+    else:
+        T = int(args.T)
+    opts = opts_for(T)
     barrier(world, local)
     with ClockSampler(local) as clk:
-        out = series.run(opts, first=W, count=S, want_images=False)
+        out = series.run(opts, first=W + NTUNE, count=S, want_images=False)
         span_ms = series.last_span_ms()
     barrier(world, local)
     span_ms = max_over_ranks(span_ms, world, local)
@@ -369,11 +405,11 @@ def main():
     if not args.no_e2e:
         import torch
         zt = torch.empty((S, J, G, G), dtype=torch.complex64, pin_memory=True)
-        zt.numpy()[:] = frames[W:W + S]
+        zt.numpy()[:] = frames[W + NTUNE:W + NTUNE + S]
         imt = torch.empty((S, plan.N, plan.N), dtype=torch.complex64, pin_memory=True)
         barrier(world, local)
         t0 = time.perf_counter()
-        series.run(opts, first=W, count=S, z_host_ptr=zt.data_ptr(), images_ptr=imt.data_ptr())
+        series.run(opts, first=W + NTUNE, count=S, z_host_ptr=zt.data_ptr(), images_ptr=imt.data_ptr())
         wall = time.perf_counter() - t0
         barrier(world, local)
         wall = max_over_ranks(wall, world, local)
@@ -410,11 +446,12 @@ def main():
         "data": "synthetic (numpy phantom, coils, exact radial Toeplitz kernel; staged in HBM)",
         "config": {"workload": cfg, "description": desc, "G": G, "N": plan.N, "Gc": plan.Gc, "J": J,
                    "spokes": K, "turns": U, "newton_steps": M, "cg_iter_budget": plan.cg_iter_budget,
-                   "frames_in_flight": args.T, "per_rank": "independent slice series (multi-slice)",
+                   "frames_in_flight": T, "temporal_schedule": {"l": sched.l, "o": sched.o},
+                   "per_rank": "independent slice series (multi-slice)",
                    "l2": "inputs larger than L2: every frame has its own 16 MB buffer, "
                          f"{F} frames staged ({F * J * G * G * 8 / 2**20:.0f} MiB)"},
         "p50_latency_ms": statistics.median(lat), "latency_ms_min_max": [min(lat), max(lat)],
-        "e2e": e2e, "gpu_launches": launches_per_frame(caps, M) * S, "roofline": roofline,
+        "e2e": e2e, "gpu_launches": launches_per_frame(caps, M) * S, "roofline": roofline, "autotune": tuning,
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:

@@ -20,7 +20,7 @@ from typing import Callable, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librtnlinv_b200.so")
+LIB_PATH = os.environ.get("RTN_LIB", os.path.join(_HERE, "librtnlinv_b200.so"))
 
 __all__ = [
     "ReconPlan", "Context", "UsageError", "DataError", "SolverError", "DecompFault",

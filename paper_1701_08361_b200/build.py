@@ -34,10 +34,14 @@ def needs_build():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, out=None):
+    global OUT
+    if out:
+        OUT = out
     if not force and not needs_build():
         return OUT
-    cmd = [NVCC] + FLAGS + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", OUT + ".tmp", "-lcudart"]
+    extra = os.environ.get("RTN_NVCC_EXTRA", "").split()
+    cmd = [NVCC] + FLAGS + extra + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", OUT + ".tmp", "-lcudart"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)

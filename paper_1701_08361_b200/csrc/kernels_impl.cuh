@@ -61,9 +61,14 @@ __device__ __forceinline__ double nrm2(float2 v) { return (double)v.x * v.x + (d
 // complete and flush (griddepcontrol.wait; a no-op without the attribute), then lets
 // the next kernel start launching, so launch latency and block rasterisation of
 // kernel k+1 overlap the tail of kernel k inside the CUDA graph.
+#ifndef RTNB_PDL_EARLY
+#define RTNB_PDL_EARLY 0
+#endif
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#if RTNB_PDL_EARLY
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
