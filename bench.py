@@ -422,7 +422,7 @@ def main():
     ctx.make_step_cache(series.estimate(F - 1))
     napply = sum(caps) + M  # CR applications + Newton-step setups per frame
     per_frame = {"colsT": napply, "rows1": napply, "rows2": napply, "colA": napply, "colsW": napply,
-                 "cr_xr": sum(caps), "cr_pap": sum(caps) - M}
+                 "cr_fused": sum(caps)}
     kern = {}
     for name in per_frame:
         ms, by = ctx.time_kernel(name, 50)

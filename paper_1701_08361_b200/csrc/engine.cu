@@ -388,6 +388,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), dev_(device) {
   dims_.H = (plan.J + ops_->LPB - 1) / ops_->LPB;
   D_ = plan.G * plan.G + plan.J * plan.Gc * plan.Gc;
   check_cuda(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
+  if (const char* e = std::getenv("RTN_FUSED_CR")) fused_cr_ = e[0] != '0';
   alloc();
 }
 
@@ -474,11 +475,13 @@ void Engine::ensure_cr_capacity(int max_iter) {
     cudaFree(cr_buf_);
   }
   cr_cap_ = max_iter + 2;
-  check_cuda(cudaMalloc(&cr_buf_, sizeof(double) * 3 * cr_cap_), "cr scalars");
-  check_cuda(cudaMemset(cr_buf_, 0, sizeof(double) * 3 * cr_cap_), "cr scalars");
+  check_cuda(cudaMalloc(&cr_buf_, sizeof(double) * 5 * cr_cap_), "cr scalars");
+  check_cuda(cudaMemset(cr_buf_, 0, sizeof(double) * 5 * cr_cap_), "cr scalars");
   cr_.rar = cr_buf_;
   cr_.ap2 = cr_buf_ + cr_cap_;
   cr_.rn = cr_buf_ + 2 * cr_cap_;
+  cr_.saa = cr_buf_ + 3 * cr_cap_;
+  cr_.spa = cr_buf_ + 4 * cr_cap_;
 }
 
 void Engine::sync() { check_cuda(cudaStreamSynchronize(s_), "stream sync"); }
@@ -524,7 +527,8 @@ void Engine::enq_decode(const float2* est) {
               st_, 0);
 }
 
-void Engine::enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt) {
+void Engine::enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
+                       const float2* ap_prev) {
   const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
   const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
   ops_->colA(s_, J * tGc, dims_, winv_, twG_, dx + static_cast<size_t>(G) * G, U_, dims_.lo, dims_.L, st_,
@@ -537,6 +541,7 @@ void Engine::enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, 
   a.dot_slot = dot_slot;
   a.dx = dx;
   a.out = out;
+  a.ap_prev = ap_prev;
   ops_->rows2(s_, dims_.L * dims_.H, dims_, 0, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, use_halt);
   const int nbw = J * tGc;
   ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, use_halt);
@@ -565,6 +570,18 @@ void Engine::enq_setup(const float2* x, const float2* reg, float alpha) {
 
 void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
   ensure_cr_capacity(cap);
+  if (!sync_each && fused_cr_) {
+    // budget-mode graphs: one fused recurrence kernel per iteration (k_cr_fused)
+    enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1, nullptr);
+    launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, static_cast<const float2*>(ar_),
+             partials_, st_, cr_, 0, tol);
+    for (int it = 1; it < cap; ++it) {
+      enq_apply(r_, ar_, CW_OPALPHA, alpha, it, 1, ap_);
+      launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, static_cast<const float2*>(ar_),
+               partials_, st_, cr_, it, tol);
+    }
+    return;
+  }
   enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1);
   launch_k(k_cr_prime, vec_grid_, kThreads, 0, s_, D_, ap_, ar_, partials_, st_, cr_);
   for (int it = 1; it <= cap; ++it) {
@@ -689,7 +706,11 @@ void Engine::cg_solve(const float* rhs, float alpha, float tol, int max_iter, fl
     sync();
   }
   const int ctx = fft_current_ctx();
+  // the op-level solve keeps the reference's two-pass recurrence exactly
+  const bool fused = fused_cr_;
+  fused_cr_ = false;
   enq_cr(alpha, tol, max_iter, tol > 0.0f);
+  fused_cr_ = fused;
   read_state();
   raise_status("cg_solve");
   const int n = st_host_->steps[0].iters;
@@ -891,6 +912,7 @@ double Engine::kernel_bytes(const char* which) const {
   if (w == "colA") return c8 * (J * Gc * Gc + J * L * Gc) + 4.0 * Gc * Gc;
   if (w == "colsW") return c8 * (J * L * Gc + 3.0 * (G * G + J * Gc * Gc)) + 16.0 * dims_.H * L * L + 4.0 * Gc * Gc;
   if (w == "cr_xr" || w == "cr_pap") return c8 * 6.0 * (G * G + J * Gc * Gc);
+  if (w == "cr_fused") return c8 * 9.0 * (G * G + J * Gc * Gc);  // x,r,p,ap,ar in; x,r,p,ap out
   if (w == "colsW") return c8 * (J * L * Gc + J * L * L + 2.0 * (G * G + J * Gc * Gc)) + 4.0 * Gc * Gc;
   if (w == "apply") {
     // one fused normal-operator application (SURVEY.md §8(d) B_op, window pruned)
@@ -923,6 +945,9 @@ double Engine::time_kernel(const char* which, int reps) {
       ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, 0);
     } else if (w == "cr_xr") {
       launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], p_, ap_, partials_, st_, cr_, 1, 0.f);
+    } else if (w == "cr_fused") {
+      launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], p_, ap_,
+               static_cast<const float2*>(ar_), partials_, st_, cr_, 1, 0.f);
     } else if (w == "cr_pap") {
       launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], r_, ar_, partials_, st_, cr_, 1);
     } else if (w == "colA") {
@@ -936,8 +961,9 @@ double Engine::time_kernel(const char* which, int reps) {
   if (w.rfind("cr_", 0) == 0) {
     // finite scalars so the recurrences run their full vector passes
     const double one[2] = {1.0, 1.0};
-    check_cuda(cudaMemcpyAsync(cr_.rar, one, sizeof(one), cudaMemcpyHostToDevice, s_), "scalars");
-    check_cuda(cudaMemcpyAsync(cr_.ap2, one, sizeof(one), cudaMemcpyHostToDevice, s_), "scalars");
+    for (double* q : {cr_.rar, cr_.ap2, cr_.saa, cr_.spa}) {
+      check_cuda(cudaMemcpyAsync(q, one, sizeof(one), cudaMemcpyHostToDevice, s_), "scalars");
+    }
   }
   for (int i = 0; i < 3; ++i) launch();
   cudaEvent_t a, b;

@@ -141,7 +141,8 @@ class Engine {
   void ensure_cr_capacity(int max_iter);
   void enq_step_begin(int m);
   void enq_decode(const float2* est);
-  void enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt);
+  void enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
+                 const float2* ap_prev = nullptr);
   void enq_setup(const float2* x, const float2* reg, float alpha);
   void enq_cr(float alpha, float tol, int cap, bool sync_each);
   void enq_newton_step(int m, float2* x, const float2* reg, float alpha, float tol, int cap,
@@ -190,6 +191,7 @@ class Engine {
   std::vector<int> caps_;       // budget-mode per-step caps
   std::vector<float> alphas_;   // per-step alpha schedule
   bool use_graphs_ = true;
+  bool fused_cr_ = true;   // RTN_FUSED_CR=0 selects the two-kernel recurrence in graphs too
   cudaGraphExec_t step_graph_[kMaxSteps] = {};
   cudaGraphExec_t frame_graph_ = nullptr;
   float2* frame_graph_img_ = nullptr;

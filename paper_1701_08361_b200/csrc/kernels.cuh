@@ -47,6 +47,8 @@ struct CrScalars {
   double* rar;
   double* ap2;
   double* rn;
+  double* saa;   // fused path: |A r_k|^2 from the application
+  double* spa;   // fused path: Re <ap_{k-1}, A r_k>
 };
 
 }  // namespace rtnb

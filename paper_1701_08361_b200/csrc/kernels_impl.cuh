@@ -369,11 +369,13 @@ struct ColsWArgs {
   float2* out;        // OP: result vector; SETUP: r
   float2* out2;       // SETUP: p (= r)
   float2* out3;       // SETUP: x_cg (zeroed)
+  const float2* ap_prev;  // fused CR: also reduce |out|^2 and Re<ap_prev, out> (nullable)
 };
 
 // combine the normal-operator value n at flat index e with the CR / rhs terms and
 // accumulate the reduction the caller needs (Re<dx,out> or |rhs|^2)
-__device__ __forceinline__ void finish_elem(const ColsWArgs& a, size_t e, float2 n, double& acc) {
+__device__ __forceinline__ void finish_elem(const ColsWArgs& a, size_t e, float2 n, double& acc, double& aa,
+                                            double& pa) {
   if (a.mode == CW_SETUP) {
     float2 v = axpy_rn(n, a.a_x, a.x[e]);
     v = axpy_rn(v, a.a_reg, a.reg[e]);
@@ -387,6 +389,11 @@ __device__ __forceinline__ void finish_elem(const ColsWArgs& a, size_t e, float2
     if (a.mode == CW_OPALPHA) v = axpy_rn(v, a.alpha, p);
     a.out[e] = v;
     acc += (double)p.x * v.x + (double)p.y * v.y;  // Re <dx, out>
+    aa += nrm2(v);
+    if (a.ap_prev) {
+      const float2 q = a.ap_prev[e];
+      pa += (double)q.x * v.x + (double)q.y * v.y;
+    }
   }
 }
 
@@ -504,7 +511,7 @@ __global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const fl
   if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(true);
   const int D0 = G * G;
-  double acc0 = 0.0, acc1 = 0.0;
+  double acc0 = 0.0, acc1 = 0.0, aa = 0.0, pa = 0.0;
   if ((int)blockIdx.x < nbw) {
     const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
     const int j = blockIdx.x / tiles;
@@ -536,7 +543,7 @@ __global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const fl
           const float w = winv[e];
           const float2 f = cscale(flip(u[k2], p), d.invG);
           // crop_k(FFT(u)) * winv   (nlinv.cpp:127-133)
-          finish_elem(a, (size_t)D0 + (size_t)j * d.Gc * d.Gc + e, make_float2(f.x * w, f.y * w), acc0);
+          finish_elem(a, (size_t)D0 + (size_t)j * d.Gc * d.Gc + e, make_float2(f.x * w, f.y * w), acc0, aa, pa);
         }
       }
     }
@@ -564,11 +571,11 @@ __global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const fl
           acc1 += nrm2(zz);
         }
       }
-      finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), acc0);
+      finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), acc0, aa, pa);
     }
   }
-  double vv[2] = {acc0, acc1}, tot[2];
-  if (grid_reduce<2>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
+  double vv[4] = {acc0, acc1, aa, pa}, tot[4];
+  if (grid_reduce<4>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
     const double total = tot[0];
     if (a.mode == CW_SETUP) {
       StepRec& s = st->steps[st->cur_step];
@@ -585,6 +592,8 @@ __global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const fl
       }
     } else if (a.dot_slot >= 0) {
       cr.rar[a.dot_slot] = total;
+      cr.saa[a.dot_slot] = tot[2];
+      cr.spa[a.dot_slot] = tot[3];
     } else {
       st->scal[0] = total;
     }
@@ -700,6 +709,75 @@ __global__ void __launch_bounds__(kThreads) k_cr_pap(int D, float2* __restrict__
   }
   double v[1] = {acc}, tot[1];
   if (grid_reduce<1>(v, partials, &st->counter, tot) && threadIdx.x == 0) cr.ap2[it] = tot[0];
+}
+
+// Fused CR recurrence for the budget-mode frame graphs: iteration `it` second half
+// and iteration it+1 first half in one pass (one kernel and one grid reduction fewer
+// per iteration than k_cr_pap + k_cr_xr):
+//   b = rar[it]/rar[it-1] (b = 0 for it = 0, the priming step);
+//   p = b p + r; ap = b ap + ar;                          (nlinv.cpp:225-230)
+//   |ap|^2 = b^2 |ap_prev|^2 + 2b Re<ap_prev, ar> + |ar|^2  from the exact norm of the
+//     previous ap and the application's dots (exact for it = 0);
+//   a = rar[it]/|ap|^2; x += a p; r -= a ap; rn[it+1] = |r|  (nlinv.cpp:205-220)
+// The exact |ap|^2 of this pass is reduced for the next iteration.
+__global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict__ x, float2* __restrict__ r,
+                                                       float2* __restrict__ p, float2* __restrict__ ap,
+                                                       const float2* __restrict__ ar, double* partials,
+                                                       DevState* st, CrScalars cr, int it, float tol) {
+  pdl_enter();
+  if (st->status || st->cr_halt) return;
+  const double rar_new = cr.rar[it];
+  double b = 0.0, denom = cr.saa[0];
+  if (it > 0) {
+    const double rar_old = cr.rar[it - 1];
+    b = (rar_old != 0.0) ? rar_new / rar_old : 0.0;
+    denom = b * b * cr.ap2[it - 1] + 2.0 * b * cr.spa[it] + cr.saa[it];
+  }
+  if (!isfinite(denom) || !isfinite(rar_new)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->status = ST_SOLVER;
+      st->cr_halt = 1;
+    }
+    return;
+  }
+  if (denom <= 0.0 && tol > 0.0f) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->cr_halt = 1;
+    return;
+  }
+  const bool upd = denom > 0.0;
+  const double a = upd ? rar_new / denom : 0.0;
+  const float bf = (float)b, af = (float)a, naf = (float)(-a);
+  double acc_ap = 0.0, acc_r = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
+    const float2 pv = p[i], apv = ap[i], rv = r[i], arv = ar[i];
+    const float2 np = make_float2(__fadd_rn(__fmul_rn(pv.x, bf), rv.x), __fadd_rn(__fmul_rn(pv.y, bf), rv.y));
+    const float2 nap = make_float2(__fadd_rn(__fmul_rn(apv.x, bf), arv.x), __fadd_rn(__fmul_rn(apv.y, bf), arv.y));
+    p[i] = np;
+    ap[i] = nap;
+    acc_ap += nrm2(nap);
+    float2 nr = rv;
+    if (upd) {
+      x[i] = axpy_rn(x[i], af, np);
+      nr = axpy_rn(rv, naf, nap);
+      r[i] = nr;
+    }
+    acc_r += nrm2(nr);
+  }
+  double v[2] = {acc_ap, acc_r}, tot[2];
+  if (grid_reduce<2>(v, partials, &st->counter, tot) && threadIdx.x == 0) {
+    cr.ap2[it] = tot[0];
+    const double rn = sqrt(tot[1]);
+    cr.rn[it + 1] = rn;
+    StepRec& s = st->steps[st->cur_step];
+    if (!isfinite(rn)) {
+      st->status = ST_SOLVER;
+      st->cr_halt = 1;
+      return;
+    }
+    s.iters = it + 1;
+    const double target = (double)tol * sqrt(s.rhs_nrm2);
+    if (tol > 0.0f && (rn == 0.0 || rn <= target)) st->cr_halt = 1;
+  }
 }
 
 // x += 1.0 * x_cg  (newton_step, nlinv.cpp:281)
