@@ -447,7 +447,8 @@ void Engine::alloc() {
   vec_grid_ = blocks_for(D_, 148 * 4);
   nbr_ = static_cast<int>((G2 + ops_->NT - 1) / ops_->NT);  // one rho element per thread
   const int max_grid = std::max(vec_grid_, plan_.J * ((plan_.G + ops_->LPB - 1) / ops_->LPB) + nbr_ + 8);
-  check_cuda(cudaMalloc(&partials_, sizeof(double) * 2 * max_grid), "partials");
+  // grid_reduce<K> writes K doubles per block; K <= kMaxReduce
+  check_cuda(cudaMalloc(&partials_, sizeof(double) * kMaxReduce * max_grid), "partials");
   check_cuda(cudaMalloc(&st_, sizeof(DevState)), "state");
   check_cuda(cudaMemset(st_, 0, sizeof(DevState)), "state");
   check_cuda(cudaMallocHost(&st_host_, sizeof(DevState)), "state mirror");

@@ -16,6 +16,9 @@ struct Dims {
   float invG;
 };
 
+// largest K of any grid_reduce<K> (sizes the per-block partials buffer)
+constexpr int kMaxReduce = 4;
+
 enum Status : int { ST_OK = 0, ST_USAGE = 2, ST_DATA = 3, ST_SOLVER = 4 };
 
 // Per-frame device state. Scalars are indexed by Newton step m and CR iteration.

@@ -82,6 +82,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // with the totals in tot[] (all threads).
 template <int K>
 __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* counter, double (&tot)[K]) {
+  static_assert(K <= kMaxReduce, "partials buffer holds kMaxReduce doubles per block");
   __shared__ double red[K][32];
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
