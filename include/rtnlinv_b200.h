@@ -110,6 +110,11 @@ typedef struct rtn_series_opts_t {
 } rtn_series_opts_t;
 
 int rtn_series_create(rtn_ctx* ctx, int frames, int n_psf, rtn_series** out);
+/* temporal decomposition across GPUs in one process: frame worker t runs on
+ * devices[t % n_devices]; the store stays on the context's device and estimates,
+ * frames and images move peer to peer (needs peer access between the devices) */
+int rtn_series_create_multi(rtn_ctx* ctx, int frames, int n_psf, const int* devices, int n_devices,
+                            rtn_series** out);
 void rtn_series_destroy(rtn_series* s);
 /* gridded frames z (count*J*G*G, GriddedData::z per frame) into the device store */
 int rtn_series_upload_frames(rtn_series* s, int first, int count, const float* z);

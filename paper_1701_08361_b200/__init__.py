@@ -149,6 +149,8 @@ def load_library(path: str = LIB_PATH):
         "rtn_reconstruct_frame": ([vp, f, f, f, f, i, d], ctypes.c_int),
         "rtn_series_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
         "rtn_series_destroy": ([vp], None),
+        "rtn_series_create_multi": ([vp, ctypes.c_int, ctypes.c_int, i, ctypes.c_int, ctypes.POINTER(vp)],
+                                    ctypes.c_int),
         "rtn_series_upload_frames": ([vp, ctypes.c_int, ctypes.c_int, vp], ctypes.c_int),
         "rtn_series_upload_psf": ([vp, ctypes.c_int, f], ctypes.c_int),
         "rtn_series_set_psf_index": ([vp, i], ctypes.c_int),
@@ -459,12 +461,18 @@ def format_audit(a: FrameAudit) -> str:
 class Series:
     """Device-resident frame series (reconstruct_series / _plain, nlinv.cpp:412-526)."""
 
-    def __init__(self, ctx: Context, frames: int, n_psf: int):
+    def __init__(self, ctx: Context, frames: int, n_psf: int, devices: Optional[Sequence[int]] = None):
+        """devices: spread the frame workers over these GPUs (temporal decomposition
+        across devices in one process); default: the context's device only"""
         self.ctx = ctx
         self.lib = ctx.lib
         self.F = frames
         self._h = ctypes.c_void_p()
-        _check(self.lib.rtn_series_create(ctx._h, frames, n_psf, ctypes.byref(self._h)))
+        if devices:
+            dv = (ctypes.c_int * len(devices))(*devices)
+            _check(self.lib.rtn_series_create_multi(ctx._h, frames, n_psf, dv, len(devices), ctypes.byref(self._h)))
+        else:
+            _check(self.lib.rtn_series_create(ctx._h, frames, n_psf, ctypes.byref(self._h)))
 
     def close(self):
         if self._h:

@@ -200,6 +200,27 @@ int rtn_series_create(rtn_ctx* ctx, int frames, int n_psf, rtn_series** out) {
   });
 }
 
+int rtn_series_create_multi(rtn_ctx* ctx, int frames, int n_psf, const int* devices, int n_devices,
+                            rtn_series** out) {
+  return guarded([&] {
+    if (n_devices < 1 || !devices) rtnb::fail(2, "rtn_series_create_multi: need at least one device");
+    int n = 0;
+    rtnb::check_cuda(cudaGetDeviceCount(&n), "device count");
+    for (int k = 0; k < n_devices; ++k) {
+      if (devices[k] < 0 || devices[k] >= n) rtnb::fail(2, "rtn_series_create_multi: device index out of range");
+    }
+    auto* s = new rtn_series;
+    try {
+      s->ctx = ctx;
+      s->s = new rtnb::Series(eng(ctx), frames, n_psf, std::vector<int>(devices, devices + n_devices));
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
 void rtn_series_destroy(rtn_series* s) {
   if (!s) return;
   delete s->s;

@@ -444,8 +444,15 @@ void Engine::alloc() {
   check_cuda(cudaMalloc(&RP_, sizeof(double2) * dims_.H * L * L), "RP");
   c2(&gbuf_, G2, "scratch");
   c2(&img_, static_cast<size_t>(plan_.N) * plan_.N, "image");
-  vec_grid_ = blocks_for(D_, 148 * 4);
-  nbr_ = static_cast<int>((G2 + ops_->NT - 1) / ops_->NT);  // one rho element per thread
+  // vector-recurrence grids and the out-of-window rho blocks of k_colsW (few blocks,
+  // several elements per thread: the grid reduction's ticket/atomic cost scales with
+  // the block count); overridable for tuning
+  auto env_int = [](const char* k, int dflt) {
+    const char* e = std::getenv(k);
+    return e ? std::max(1, std::atoi(e)) : dflt;
+  };
+  vec_grid_ = std::min(blocks_for(D_, 1 << 20), env_int("RTN_VEC_BLOCKS", 2 * 148));
+  nbr_ = std::min(static_cast<int>((G2 + ops_->NT - 1) / ops_->NT), env_int("RTN_RHO_BLOCKS", 148));
   const int max_grid = std::max(vec_grid_, plan_.J * ((plan_.G + ops_->LPB - 1) / ops_->LPB) + nbr_ + 8);
   // grid_reduce<K> writes K doubles per block; K <= kMaxReduce
   check_cuda(cudaMalloc(&partials_, sizeof(double) * kMaxReduce * max_grid), "partials");

@@ -37,8 +37,25 @@ __global__ void k_scale_frames(float2* __restrict__ z, long long n, float s) {
 
 }  // namespace
 
-Series::Series(Engine& primary, int frames, int n_psf) : eng0_(primary), F_(frames), n_psf_(n_psf) {
+Series::Series(Engine& primary, int frames, int n_psf, std::vector<int> devices)
+    : eng0_(primary), F_(frames), n_psf_(n_psf), devices_(std::move(devices)) {
   if (frames < 1) fail(2, "reconstruct_series: no frames");
+  if (devices_.empty()) devices_.push_back(primary.device());
+  if (devices_[0] != primary.device()) devices_.insert(devices_.begin(), primary.device());
+  // peer access between every pair of distinct devices used by the workers
+  for (int a : devices_) {
+    for (int b : devices_) {
+      if (a == b) continue;
+      int ok = 0;
+      check_cuda(cudaDeviceCanAccessPeer(&ok, a, b), "peer query");
+      if (!ok) fail(2, "reconstruct_series: devices " + std::to_string(a) + " and " + std::to_string(b) +
+                           " have no peer access");
+      check_cuda(cudaSetDevice(a), "set device");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) check_cuda(e, "enable peer access");
+      cudaGetLastError();
+    }
+  }
   if (n_psf < 1) fail(2, "reconstruct_series: need at least one PSF");
   const Plan& p = eng0_.plan();
   D_ = eng0_.D();
@@ -80,7 +97,8 @@ Series::~Series() {
 Engine& Series::worker(int t) {
   if (t == 0) return eng0_;
   while (static_cast<int>(extra_.size()) < t) {
-    extra_.push_back(std::make_unique<Engine>(eng0_.plan(), eng0_.device()));
+    const int k = static_cast<int>(extra_.size()) + 1;
+    extra_.push_back(std::make_unique<Engine>(eng0_.plan(), devices_[static_cast<size_t>(k) % devices_.size()]));
   }
   return *extra_[static_cast<size_t>(t - 1)];
 }
@@ -142,22 +160,26 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   const float2* init = chained ? estimate_dev(a.init_src) : unity_;
 
   if (ready) check_cuda(cudaStreamWaitEvent(s, ready, 0), "wait frame upload");
-  check_cuda(cudaMemcpyAsync(e.z_dev(), z_ + zsz_ * n, sizeof(float2) * zsz_, cudaMemcpyDeviceToDevice, s), "z");
+  check_cuda(cudaSetDevice(e.device()), "set device");
+  check_cuda(cudaMemcpyAsync(e.z_dev(), z_ + zsz_ * n, sizeof(float2) * zsz_, cudaMemcpyDefault, s), "z");
   check_cuda(cudaMemcpyAsync(e.psf_dev(), psf_ + psz_ * psf_idx_[static_cast<size_t>(n)], sizeof(float2) * psz_,
-                             cudaMemcpyDeviceToDevice, s),
+                             cudaMemcpyDefault, s),
              "psf");
-  check_cuda(cudaMemcpyAsync(e.x_dev(), init, sizeof(float2) * D_, cudaMemcpyDeviceToDevice, s), "init");
+  check_cuda(cudaMemcpyAsync(e.x_dev(), init, sizeof(float2) * D_, cudaMemcpyDefault, s), "init");
   cudaEvent_t ev0, ev1;
   check_cuda(cudaEventCreate(&ev0), "event");
   check_cuda(cudaEventCreate(&ev1), "event");
   check_cuda(cudaEventRecord(ev0, s), "event");
-  float2* img = images_ + isz_ * n;
+  // the image lands in the store directly on the store's device, via the worker's
+  // own buffer (then one peer copy) elsewhere
+  const bool local = e.device() == eng0_.device();
+  float2* img = local ? images_ + isz_ * n : e.image_dev();
   const float iscale = static_cast<float>(1.0 / scale_);
   const bool undo = o.normalize && scale_ != 1.0;
   const bool fixed_reg = o.plain || !chained;  // every step regularises towards init
   if (fixed_reg) {
     for (int m = 0; m < M; ++m) a.reg_src[static_cast<size_t>(m)] = chained ? a.init_src : -1;
-    check_cuda(cudaMemcpyAsync(e.reg_dev(), init, sizeof(float2) * D_, cudaMemcpyDeviceToDevice, s), "reg");
+    check_cuda(cudaMemcpyAsync(e.reg_dev(), init, sizeof(float2) * D_, cudaMemcpyDefault, s), "reg");
     if (!o.plain && M > 0) a.reg_final_seq = ledger.next_seq();
     if (e.budget_mode()) {
       e.frame_all(img, iscale, undo);
@@ -183,7 +205,7 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   if (!e.frame_verify(&fs)) {
     // a step met an exactly-zero right-hand side: redo with the true budget split,
     // replaying the recorded regularisation sources
-    check_cuda(cudaMemcpyAsync(e.x_dev(), init, sizeof(float2) * D_, cudaMemcpyDeviceToDevice, s), "init");
+    check_cuda(cudaMemcpyAsync(e.x_dev(), init, sizeof(float2) * D_, cudaMemcpyDefault, s), "init");
     const std::vector<int> srcs = a.reg_src;
     const float2* u = unity_;
     Engine::RegFn rf = [this, srcs, u](int m) -> const float2* {
@@ -193,8 +215,10 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
     e.frame_run_sync(rf, img, iscale, undo, &fs);
     check_cuda(cudaEventRecord(ev1, s), "event");
   }
-  check_cuda(cudaMemcpyAsync(estimate_dev(n), e.x_dev(), sizeof(float2) * D_, cudaMemcpyDeviceToDevice, s),
-             "estimate");
+  check_cuda(cudaMemcpyAsync(estimate_dev(n), e.x_dev(), sizeof(float2) * D_, cudaMemcpyDefault, s), "estimate");
+  if (!local) {
+    check_cuda(cudaMemcpyAsync(images_ + isz_ * n, img, sizeof(float2) * isz_, cudaMemcpyDefault, s), "image");
+  }
   e.sync();
   float ms = 0;
   check_cuda(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
@@ -268,7 +292,7 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   std::exception_ptr first_err;
   auto thread_main = [&](int t) {
     try {
-      check_cuda(cudaSetDevice(dev), "set device");
+      check_cuda(cudaSetDevice(worker(t).device()), "set device");
       for (int k = t; k < count; k += T) {
         if (ledger.poisoned()) return;
         run_frame(t, first + k, o, ledger, (*out)[static_cast<size_t>(k)],
@@ -303,8 +327,10 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   // stream after all of them
   for (int t = 0; t < T; ++t) {
     cudaEvent_t e;
+    check_cuda(cudaSetDevice(worker(t).device()), "set device");
     check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     check_cuda(cudaEventRecord(e, worker(t).stream()), "event");
+    check_cuda(cudaSetDevice(dev), "set device");
     check_cuda(cudaStreamWaitEvent(copy_, e, 0), "event wait");
     cudaEventDestroy(e);
   }

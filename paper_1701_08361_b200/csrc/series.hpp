@@ -34,7 +34,12 @@ struct SeriesFrameOut {
 // same device on demand.
 class Series {
  public:
-  Series(Engine& primary, int frames, int n_psf);
+  // devices: worker t runs on devices[t % devices.size()] (default: the primary's
+  // device). With several devices the series store stays on the primary's device and
+  // frames, PSFs and estimates move peer to peer (NVLink / NVSwitch, UVA copies):
+  // temporal decomposition across GPUs inside one process, the reference's
+  // thread-per-compute-worker model.
+  Series(Engine& primary, int frames, int n_psf, std::vector<int> devices = {});
   ~Series();
   Series(const Series&) = delete;
   Series& operator=(const Series&) = delete;
@@ -69,6 +74,7 @@ class Series {
 
   Engine& eng0_;
   std::vector<std::unique_ptr<Engine>> extra_;
+  std::vector<int> devices_;
   int F_ = 0, n_psf_ = 0, D_ = 0;
   size_t zsz_ = 0, psz_ = 0, isz_ = 0;
   float2* z_ = nullptr;

@@ -81,7 +81,8 @@ def test_toeplitz_matches_reference(gpu, ref, G, K):
         assert rel_err(ctx.toeplitz_apply(x), ref.toeplitz_apply(x, P)) < OP_TOL
 
 
-@pytest.mark.parametrize("G,J", [(16, 1), (16, 3), (32, 3), (48, 2), (128, 8), (256, 4)])
+@pytest.mark.parametrize("G,J", [(16, 1), (16, 3), (32, 3), (48, 2), (72, 2), (128, 8), (256, 4), (320, 3),
+                                 (384, 2), (512, 1)])
 def test_apply_normal_matches_reference(gpu, ref, G, J):
     plan = gpu.raw_plan(G, J)
     P = radial_psf(ref, plan, 5, G + J)

@@ -168,3 +168,52 @@ def test_c1_series_against_reference(gpu, ref):
     got = _run(gpu, plan, z, P, idx, gpu.SeriesOptions(plain=True))
     for n in range(5):
         assert rel_err(got["images"][n], want["images"][n]) < FRAME_TOL, n
+
+
+def test_multi_device_series_matches_single_device(gpu, ref):
+    # temporal decomposition across devices: with one visible GPU the device list
+    # [0, 0] still exercises the peer-copy code path (UVA copies, worker devices);
+    # with two or more GPUs the workers really run on different devices
+    n = gpu.load_library().rtn_device_count()
+    devices = [0, 1] if n >= 2 else [0, 0]
+    plan = _small_plan(gpu, 16, 3, 3, 6)
+    _, _, z, P, idx = _series_inputs(ref, plan, F=8, K=5, U=3)
+    single = _run(gpu, plan, z, P, idx, gpu.SeriesOptions(T=1, sched=gpu.TemporalSchedule(2, 2)))
+    ctx = gpu.Context(plan)
+    s = gpu.Series(ctx, 8, P.shape[0], devices=devices)
+    s.upload_frames(z)
+    for k in range(P.shape[0]):
+        s.upload_psf(k, P[k])
+    s.set_psf_index(idx)
+    out = s.run(gpu.SeriesOptions(T=1, sched=gpu.TemporalSchedule(2, 2)))
+    # T = 1 over the device list: identical schedule, identical numerics
+    assert np.array_equal(out["images"], single["images"])
+    multi = s.run(gpu.SeriesOptions(T=2, sched=gpu.TemporalSchedule(2, 2)))
+    for n_ in range(8):
+        a = multi["audit"][n_]
+        assert a.reg_final_src == n_ - 1 if n_ > 0 else a.init_src == -1
+        assert np.sum(np.abs(multi["images"][n_]) ** 2) > 0
+
+
+def test_c2_compressed_frame_against_reference(gpu, ref):
+    # configs[1]: 160x160 image on a 320x320 grid (radix-5 line FFTs), 32 physical
+    # channels PCA-compressed to 10 by the reference's calibrate_compression on the
+    # first frames (rtnlinv_main.cpp:125-130), 15 spokes, 7 Newton steps
+    plan = gpu.raw_plan(320, 10)
+    plan.newton_steps, plan.cg_iter_budget = 7, 50
+    samples, angles = ref.phantom_series(32, 2, 15, 5, plan.N, 1e-3, 1234)
+    comp, energy = ref.compress_series(samples, angles, 10, 2)
+    assert energy > 0.9
+    z = ref.grid_adjoint(plan, comp[1], angles[1])
+    P = ref.build_psf(plan, angles[1], 2 * plan.N)
+    nsq = float(np.sum(np.abs(z.astype(np.complex128)) ** 2))
+    z = (z * np.float32(100.0 / np.sqrt(nsq))).astype(np.complex64)
+    init = gpu.initial_estimate(plan)
+    with gpu.Context(plan) as ctx:
+        ctx.set_psf(P)
+        ctx.set_data(z)
+        fr = ctx.reconstruct_frame(init)
+    img, est, per, _ = ref.reconstruct_frame(plan, z, P, init, A=4)
+    assert fr.cg_per_step == per
+    assert rel_err(fr.image, img) < FRAME_TOL
+    assert rel_err(fr.est, est) < FRAME_TOL
