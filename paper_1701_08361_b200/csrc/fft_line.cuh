@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace rtnb {
 
 // exp(-2 pi i k / N) for N = 1..32, k = 0..N-1, at offset N(N-1)/2. Filled from
@@ -145,6 +147,142 @@ __device__ __forceinline__ void dft(float2 (&x)[N]) {
 }
 
 // ---------------------------------------------------------------------------------
+// Pruned small DFTs: dft_m<N, S, IN, OUT> computes only the outputs in the bit mask
+// OUT from inputs that may be nonzero only in the bit mask IN. The masks are template
+// constants, so the recursion drops every zero term and every unneeded butterfly at
+// compile time (the window-supported inputs and window-only outputs of the Toeplitz
+// and W passes are half of each line; preproc.cpp:438-442). Outputs outside OUT are
+// left undefined.
+// ---------------------------------------------------------------------------------
+__host__ __device__ constexpr uint32_t full_mask(int n) { return n >= 32 ? 0xffffffffu : ((1u << n) - 1u); }
+
+__host__ __device__ constexpr uint32_t range_mask(int lo, int hi) {  // bits [lo, hi)
+  uint32_t m = 0;
+  for (int i = lo; i < hi; ++i) m |= 1u << i;
+  return m;
+}
+
+__host__ __device__ constexpr uint32_t dm_sub_in(int N, int P, uint32_t IN, int p) {
+  uint32_t m = 0;
+  for (int q = 0; q < N / P; ++q)
+    if ((IN >> (p + P * q)) & 1u) m |= 1u << q;
+  return m;
+}
+__host__ __device__ constexpr uint32_t dm_sub_out(int N, int P, uint32_t OUT) {
+  const int Q = N / P;
+  uint32_t m = 0;
+  for (int k = 0; k < Q; ++k)
+    for (int mm = 0; mm < P; ++mm)
+      if ((OUT >> (k + Q * mm)) & 1u) m |= 1u << k;
+  return m;
+}
+__host__ __device__ constexpr uint32_t dm_comb_out(int N, int P, uint32_t OUT, int k) {
+  const int Q = N / P;
+  uint32_t m = 0;
+  for (int mm = 0; mm < P; ++mm)
+    if ((OUT >> (k + Q * mm)) & 1u) m |= 1u << mm;
+  return m;
+}
+__host__ __device__ constexpr uint32_t dm_comb_in(int N, int P, uint32_t IN) {
+  uint32_t m = 0;
+  for (int p = 0; p < P; ++p)
+    if (dm_sub_in(N, P, IN, p)) m |= 1u << p;
+  return m;
+}
+
+template <int I, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < E) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, E>(f);
+  }
+}
+
+// v * W_N^e (S sign); quarter-turn exponents are sign flips / swaps, no multiply
+template <int N, int S, int E>
+__device__ __forceinline__ float2 mul_wn(float2 v) {
+  constexpr int e = E % N;
+  if constexpr (e == 0) {
+    return v;
+  } else if constexpr ((4 * e) % N == 0) {
+    constexpr int qd = (4 * e) / N;  // quarter turns: W^e = (S i)^qd
+    if constexpr (qd == 2) {
+      return make_float2(-v.x, -v.y);
+    } else if constexpr ((qd == 1) == (S > 0)) {
+      return make_float2(-v.y, v.x);  // * i
+    } else {
+      return make_float2(v.y, -v.x);  // * -i
+    }
+  } else {
+    return cmul(v, small_w<N, S>(e));
+  }
+}
+
+template <int N, int S, uint32_t IN, uint32_t OUT>
+__device__ __forceinline__ void dft_m(float2 (&x)[N]) {
+  if constexpr (IN == full_mask(N) && OUT == full_mask(N)) {
+    dft<N, S>(x);
+  } else if constexpr (OUT == 0) {
+    return;
+  } else if constexpr (IN == 0) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) x[k] = make_float2(0.f, 0.f);
+  } else if constexpr (N <= 4 || is_prime_c(N)) {
+    float2 y[N];
+    static_for<0, N>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      if constexpr ((OUT >> k) & 1u) {
+        float2 acc = make_float2(0.f, 0.f);
+        static_for<0, N>([&](auto tc) {
+          constexpr int t = decltype(tc)::value;
+          if constexpr ((IN >> t) & 1u) acc = cadd(acc, mul_wn<N, S, k * t>(x[t]));
+        });
+        y[k] = acc;
+      }
+    });
+    static_for<0, N>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      if constexpr ((OUT >> k) & 1u) x[k] = y[k];
+    });
+  } else {
+    constexpr int P = split_factor(N);
+    constexpr int Q = N / P;
+    constexpr uint32_t SO = dm_sub_out(N, P, OUT);
+    constexpr uint32_t CI = dm_comb_in(N, P, IN);
+    float2 sub[P][Q];
+    static_for<0, P>([&](auto pc) {
+      constexpr int p = decltype(pc)::value;
+      constexpr uint32_t SI = dm_sub_in(N, P, IN, p);
+      if constexpr (SI != 0) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) sub[p][q] = x[p + P * q];
+        dft_m<Q, S, SI, SO>(sub[p]);
+      }
+    });
+    static_for<0, Q>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr uint32_t CO = dm_comb_out(N, P, OUT, k);
+      if constexpr (CO != 0) {
+        float2 t[P];
+        static_for<0, P>([&](auto pc) {
+          constexpr int p = decltype(pc)::value;
+          if constexpr ((CI >> p) & 1u) {
+            t[p] = mul_wn<N, S, p * k>(sub[p][k]);
+          } else {
+            t[p] = make_float2(0.f, 0.f);
+          }
+        });
+        dft_m<P, S, CI, CO>(t);
+        static_for<0, P>([&](auto mc) {
+          constexpr int m = decltype(mc)::value;
+          if constexpr ((CO >> m) & 1u) x[k + Q * m] = t[m];
+        });
+      }
+    });
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // Tile geometry. A block transforms LPB lines of length G = N1*N2 with
 // NT = LPB * max(N1, N2) threads and ONE padded shared tile, reused in place:
 //   step 1 items (l, n2): the thread loads x[N2*n1 + n2], n1 = 0..N1-1, straight
@@ -171,6 +309,13 @@ struct LineGeom {
   static constexpr int LS0 = G + G / N2;
   static constexpr int LS = (LS0 % 2 == 1) ? LS0 : LS0 + 1;
   static constexpr int SMEM_FLOAT2 = LPB * LS;
+  // The field-of-view window [G/4, 3G/4) in the two-step index space: step-1 inputs
+  // x[N2 n1 + n2] lie in it for n1 in WIN_N1 when G/4 is a multiple of N2, step-2
+  // outputs X[k1 + N1 k2] for k2 in WIN_K2 when G/4 is a multiple of N1 (else: all).
+  static constexpr uint32_t ALL_N1 = full_mask(N1);
+  static constexpr uint32_t ALL_N2 = full_mask(N2);
+  static constexpr uint32_t WIN_N1 = ((G / 4) % N2 == 0) ? range_mask((G / 4) / N2, (3 * G / 4) / N2) : ALL_N1;
+  static constexpr uint32_t WIN_K2 = ((G / 4) % N1 == 0) ? range_mask((G / 4) / N1, (3 * G / 4) / N1) : ALL_N2;
   __device__ __forceinline__ static int a(int l, int q) { return l * LS + q + q / N2; }
 };
 
@@ -191,10 +336,11 @@ struct Item {
   }
 };
 
-// step 1 on registers: v[n1] = x[N2*n1 + n2] -> DFT_N1 -> twiddle W_G^{n2 k1}
-template <class Geo, int S>
+// step 1 on registers: v[n1] = x[N2*n1 + n2] -> DFT_N1 -> twiddle W_G^{n2 k1};
+// IN: which n1 may be nonzero
+template <class Geo, int S, uint32_t IN = Geo::ALL_N1>
 __device__ __forceinline__ void fft_step1(float2 (&v)[Geo::N1], int n2, const float2* __restrict__ twG) {
-  dft<Geo::N1, S>(v);
+  dft_m<Geo::N1, S, IN, Geo::ALL_N1>(v);
 #pragma unroll
   for (int k1 = 1; k1 < Geo::N1; ++k1) {
     float2 w = __ldg(twG + n2 * k1);
@@ -209,13 +355,14 @@ __device__ __forceinline__ void park_step1(float2* A, int l, int n2, const float
   for (int k1 = 0; k1 < Geo::N1; ++k1) A[Geo::a(l, Geo::N2 * k1 + n2)] = v[k1];
 }
 
-// step 2: u[n2] = parked block of k1 -> DFT_N2 -> u[k2] = X[k1 + N1*k2]
-template <class Geo, int S>
+// step 2: u[n2] = parked block of k1 -> DFT_N2 -> u[k2] = X[k1 + N1*k2];
+// OUT: which k2 the caller consumes (the others are left undefined)
+template <class Geo, int S, uint32_t OUT = Geo::ALL_N2>
 __device__ __forceinline__ void fft_step2(const float2* A, int l, int k1, float2 (&u)[Geo::N2]) {
   const float2* src = A + Geo::a(l, Geo::N2 * k1);
 #pragma unroll
   for (int n2 = 0; n2 < Geo::N2; ++n2) u[n2] = src[n2];
-  dft<Geo::N2, S>(u);
+  dft_m<Geo::N2, S, Geo::ALL_N2, OUT>(u);
 }
 
 // natural-order write / step-1-order read, for chaining two transforms in a block

@@ -136,6 +136,12 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
 // take part in every barrier.
 // ---------------------------------------------------------------------------------
 
+// resident blocks per SM the pass kernels ask the register allocator for
+#ifndef RTNB_MINB
+#define RTNB_MINB 3
+#endif
+#define RTNB_PASS_BOUNDS __launch_bounds__(Geo::NT, (RTNB_MINB * 256 + Geo::NT - 1) / Geo::NT)
+
 #define RTNB_TILE_SETUP(COLS_)                                  \
   extern __shared__ float2 A[];                                 \
   const Item<Geo, COLS_> i1(threadIdx.x, Geo::N2);              \
@@ -147,7 +153,7 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
 // W^-1 column pass. Lines: (channel j, coil k-column q). Input chat_j*winv on the
 // Gc centered k-rows, output rows [r0, r0+nr) of U_j (G x Gc, row-major).
 template <class Geo>
-__global__ void __launch_bounds__(Geo::NT) k_colA(Dims d, const float* __restrict__ winv,
+__global__ void RTNB_PASS_BOUNDS k_colA(Dims d, const float* __restrict__ winv,
                                                   const float2* __restrict__ twG,
                                                   const float2* __restrict__ chat, float2* __restrict__ U,
                                                   int r0, int nr, const DevState* st, int use_halt) {
@@ -179,7 +185,11 @@ __global__ void __launch_bounds__(Geo::NT) k_colA(Dims d, const float* __restric
   __syncthreads();
   if (i2.on && i2.l < nl) {
     float2 u[N2];
-    fft_step2<Geo, +1>(A, i2.l, i2.k, u);
+    if (nr == G) {
+      fft_step2<Geo, +1>(A, i2.l, i2.k, u);
+    } else {
+      fft_step2<Geo, +1, Geo::WIN_K2>(A, i2.l, i2.k, u);  // window rows (r0 = lo, nr = L)
+    }
     float2* dst = U + (size_t)j * G * d.Gc + q0 + i2.l;
 #pragma unroll
     for (int k2 = 0; k2 < N2; ++k2) {
@@ -198,7 +208,7 @@ enum Rows1Mode : int { R1_DECODE = 0, R1_OP = 1, R1_SETUP = 2 };
 //          forward row FFT -> V_j (L x G).
 //  SETUP:  window rows: t = rho*c_j (nlinv.cpp:252) -> forward row FFT -> V_j.
 template <class Geo>
-__global__ void __launch_bounds__(Geo::NT) k_rows1(Dims d, int mode, const float2* __restrict__ twG,
+__global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float2* __restrict__ twG,
                                                    const float2* __restrict__ U,
                                                    const float2* __restrict__ coils,
                                                    const float2* __restrict__ rhom,
@@ -235,7 +245,11 @@ __global__ void __launch_bounds__(Geo::NT) k_rows1(Dims d, int mode, const float
     __syncthreads();
     float2 u[N2];
     if (a2) {
-      fft_step2<Geo, +1>(A, i2.l, i2.k, u);
+      if (mode == R1_DECODE) {
+        fft_step2<Geo, +1>(A, i2.l, i2.k, u);
+      } else {
+        fft_step2<Geo, +1, Geo::WIN_K2>(A, i2.l, i2.k, u);
+      }
       if (mode == R1_DECODE) {
         float2* out = coils_out + (size_t)j * G * G + (size_t)r2 * G;
 #pragma unroll
@@ -281,7 +295,7 @@ __global__ void __launch_bounds__(Geo::NT) k_rows1(Dims d, int mode, const float
     }
   }
   if (a1) {
-    fft_step1<Geo, -1>(v, i1.k, twG);
+    fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
   }
   __syncthreads();
@@ -300,7 +314,7 @@ __global__ void __launch_bounds__(Geo::NT) k_rows1(Dims d, int mode, const float
 // Toeplitz column pass: forward column FFT of the window rows of V_j, * P/G, inverse
 // column FFT, keep the window rows (in place in V_j). Lines: (j, column q).
 template <class Geo>
-__global__ void __launch_bounds__(Geo::NT) k_colsT(Dims d, const float2* __restrict__ twG,
+__global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float2* __restrict__ twG,
                                                    const float2* __restrict__ P, float2* __restrict__ V,
                                                    const DevState* st, int use_halt) {
   pdl_enter();
@@ -320,7 +334,7 @@ __global__ void __launch_bounds__(Geo::NT) k_colsT(Dims d, const float2* __restr
       const int t = N2 * n1 + i1.k;
       v[n1] = (t >= d.lo && t < d.lo + d.L) ? flip(col[(size_t)(t - d.lo) * G], t) : make_float2(0.f, 0.f);
     }
-    fft_step1<Geo, -1>(v, i1.k, twG);
+    fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
   }
   __syncthreads();
@@ -346,7 +360,7 @@ __global__ void __launch_bounds__(Geo::NT) k_colsT(Dims d, const float2* __restr
   }
   __syncthreads();
   if (a2) {
-    fft_step2<Geo, +1>(A, i2.l, i2.k, u);
+    fft_step2<Geo, +1, Geo::WIN_K2>(A, i2.l, i2.k, u);
     float2* col = Vj + q0 + i2.l;
 #pragma unroll
     for (int k2 = 0; k2 < N2; ++k2) {
@@ -405,7 +419,7 @@ __device__ __forceinline__ void finish_elem(const ColsWArgs& a, size_t e, float2
 // decomp.cpp:26-39; k_colsW adds the groups in order); rt = conj(rho) T -> forward
 // W^-H row pass keeping the Gc coil k-columns -> Y_j (L x Gc).
 template <class Geo>
-__global__ void __launch_bounds__(Geo::NT) k_rows2(Dims d, int setup, const float2* __restrict__ twG,
+__global__ void RTNB_PASS_BOUNDS k_rows2(Dims d, int setup, const float2* __restrict__ twG,
                                                    const float2* __restrict__ V,
                                                    const float2* __restrict__ coils,
                                                    const float2* __restrict__ rhom,
@@ -438,7 +452,7 @@ __global__ void __launch_bounds__(Geo::NT) k_rows2(Dims d, int setup, const floa
   __syncthreads();
   float2 u[N2];
   if (a2) {
-    fft_step2<Geo, +1>(A, i2.l, i2.k, u);
+    fft_step2<Geo, +1, Geo::WIN_K2>(A, i2.l, i2.k, u);
     const int j = j0 + i2.l;
     const float2* cj = coils + (size_t)j * G * G + (size_t)r * G;
     const float2* zj = z + (size_t)j * G * G + (size_t)r * G;
@@ -474,7 +488,7 @@ __global__ void __launch_bounds__(Geo::NT) k_rows2(Dims d, int setup, const floa
   __syncthreads();
   if (a1) {
     get_step1<Geo>(A, i1.l, i1.k, v);
-    fft_step1<Geo, -1>(v, i1.k, twG);
+    fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
   }
   __syncthreads();
@@ -500,7 +514,7 @@ __global__ void __launch_bounds__(Geo::NT) k_rows2(Dims d, int setup, const floa
 // outside the window (blocks [nbw, grid)); the window part of out.rho came from
 // k_rows2, whose reduction partial (st->scal[1]) is folded into the totals here.
 template <class Geo>
-__global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const float* __restrict__ winv,
+__global__ void RTNB_PASS_BOUNDS k_colsW(Dims d, ColsWArgs a, const float* __restrict__ winv,
                                                    const float2* __restrict__ twG,
                                                    const float2* __restrict__ Y,
                                                    const double2* __restrict__ RP,
@@ -527,7 +541,7 @@ __global__ void __launch_bounds__(Geo::NT) k_colsW(Dims d, ColsWArgs a, const fl
         const int t = N2 * n1 + i1.k;
         v[n1] = (t >= d.lo && t < d.lo + d.L) ? flip(col[(size_t)(t - d.lo) * d.Gc], t) : make_float2(0.f, 0.f);
       }
-      fft_step1<Geo, -1>(v, i1.k, twG);
+      fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
       park_step1<Geo>(A, i1.l, i1.k, v);
     }
     __syncthreads();
