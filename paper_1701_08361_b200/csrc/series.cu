@@ -2,7 +2,9 @@
 #include "series.hpp"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <exception>
 #include <mutex>
 #include <thread>
@@ -10,6 +12,8 @@
 namespace rtnb {
 
 namespace {
+
+struct RedoSeries {};
 
 __global__ void k_nrm2_frame(const float2* __restrict__ z, long long n, double* out) {
   // single block, fixed order: deterministic FP64 |z|^2 of one frame
@@ -79,6 +83,7 @@ Series::Series(Engine& primary, int frames, int n_psf, std::vector<int> devices)
     for (int c = lo; c < lo + L; ++c) u[static_cast<size_t>(r) * p.G + c] = make_float2(1.f, 0.f);
   }
   check_cuda(cudaMemcpy(unity_, u.data(), sizeof(float2) * D_, cudaMemcpyHostToDevice), "unity upload");
+  if (const char* e = std::getenv("RTN_STEP_SYNC")) step_sync_ = e[0] == '1';
   psf_idx_.resize(static_cast<size_t>(F_));
   for (int n = 0; n < F_; ++n) psf_idx_[static_cast<size_t>(n)] = n % n_psf_;
 }
@@ -177,6 +182,7 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   const float iscale = static_cast<float>(1.0 / scale_);
   const bool undo = o.normalize && scale_ != 1.0;
   const bool fixed_reg = o.plain || !chained;  // every step regularises towards init
+  const bool chain_events = !safe_mode_ && !o.plain && o.T > 1;
   if (fixed_reg) {
     for (int m = 0; m < M; ++m) a.reg_src[static_cast<size_t>(m)] = chained ? a.init_src : -1;
     check_cuda(cudaMemcpyAsync(e.reg_dev(), init, sizeof(float2) * D_, cudaMemcpyDefault, s), "reg");
@@ -191,18 +197,43 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   } else {
     e.frame_begin();
     for (int m = 0; m < M; ++m) {
-      const int src = h_choose(n, m, M, o.sched, ledger);
-      if (m == M - 1) a.reg_final_seq = ledger.next_seq();
+      int src;
+      if (m == M - 1 && chain_events) {
+        // closing step: pinned to n-1 (decomp.cpp:197-201). The host waits only until
+        // n-1's final work is enqueued; the stream waits on n-1's completion event, so
+        // the serial chain of closing steps runs device-side with no host round trip.
+        src = n - 1;
+        if (n - 1 >= run_first_) enq_->wait_complete(n - 1);
+        a.reg_final_seq = ledger.next_seq();
+        if (n - 1 >= run_first_) {
+          check_cuda(cudaStreamWaitEvent(s, done_[static_cast<size_t>(n - 1 - run_first_)], 0), "chain wait");
+        }
+      } else {
+        src = h_choose(n, m, M, o.sched, ledger);
+        if (m == M - 1) a.reg_final_seq = ledger.next_seq();
+      }
       a.reg_src[static_cast<size_t>(m)] = src;
       e.frame_step(m, estimate_dev(src));
-      if (o.T > 1) e.sync();  // the next step's source is chosen when it is about to run
+      // Sources are chosen when a step is enqueued; h_choose blocks the host thread
+      // only when Eq. 10 requires it (empty window, closing step), while this frame's
+      // queued steps keep the device busy. step_sync_ re-creates the reference's
+      // "choose when the step starts" timing at the cost of one host round trip per step.
+      if (step_sync_ && o.T > 1) e.sync();
       ledger.mark_step(n, m);
     }
     e.frame_image(img, iscale, undo);
   }
   check_cuda(cudaEventRecord(ev1, s), "event");
   FrameStats fs;
-  if (!e.frame_verify(&fs)) {
+  if (chain_events) {
+    // publish the estimate and its completion event before this thread blocks, so the
+    // next frame's closing step can be queued behind it on the device
+    check_cuda(cudaMemcpyAsync(estimate_dev(n), e.x_dev(), sizeof(float2) * D_, cudaMemcpyDefault, s), "estimate");
+    check_cuda(cudaEventRecord(done_[static_cast<size_t>(n - run_first_)], s), "done event");
+    a.finish_seq = ledger.next_seq();
+    enq_->mark_complete(n);
+    if (!e.frame_verify(&fs)) throw RedoSeries{};  // consumers may hold the speculative estimate
+  } else if (!e.frame_verify(&fs)) {
     // a step met an exactly-zero right-hand side: redo with the true budget split,
     // replaying the recorded regularisation sources
     check_cuda(cudaMemcpyAsync(e.x_dev(), init, sizeof(float2) * D_, cudaMemcpyDefault, s), "init");
@@ -215,7 +246,9 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
     e.frame_run_sync(rf, img, iscale, undo, &fs);
     check_cuda(cudaEventRecord(ev1, s), "event");
   }
-  check_cuda(cudaMemcpyAsync(estimate_dev(n), e.x_dev(), sizeof(float2) * D_, cudaMemcpyDefault, s), "estimate");
+  if (!chain_events) {
+    check_cuda(cudaMemcpyAsync(estimate_dev(n), e.x_dev(), sizeof(float2) * D_, cudaMemcpyDefault, s), "estimate");
+  }
   if (!local) {
     check_cuda(cudaMemcpyAsync(images_ + isz_ * n, img, sizeof(float2) * isz_, cudaMemcpyDefault, s), "image");
   }
@@ -225,7 +258,7 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   a.reg_final_src = chained ? a.reg_src[static_cast<size_t>(M - 1)] : -1;
-  if (!o.plain) a.finish_seq = ledger.next_seq();
+  if (!o.plain && !chain_events) a.finish_seq = ledger.next_seq();
   out.audit = a;
   out.cg_iters = fs.cg_iters;
   out.gpu_ms = ms;
@@ -286,10 +319,23 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   }
 
   CompletionLedger ledger(F_);
-  for (int n = 0; n < first; ++n) ledger.mark_complete(n);
+  CompletionLedger enq(F_);
+  for (int n = 0; n < first; ++n) {
+    ledger.mark_complete(n);
+    enq.mark_complete(n);
+  }
+  enq_ = &enq;
+  run_first_ = first;
+  done_.assign(static_cast<size_t>(count), nullptr);
+  for (int k = 0; k < count; ++k) {
+    check_cuda(cudaSetDevice(worker(k % T).device()), "set device");
+    check_cuda(cudaEventCreateWithFlags(&done_[static_cast<size_t>(k)], cudaEventDisableTiming), "event");
+  }
+  check_cuda(cudaSetDevice(dev), "set device");
   out->assign(static_cast<size_t>(count), SeriesFrameOut{});
   std::mutex err_mu;
   std::exception_ptr first_err;
+  std::atomic<bool> redo{false};
   auto thread_main = [&](int t) {
     try {
       check_cuda(cudaSetDevice(worker(t).device()), "set device");
@@ -305,12 +351,17 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
           e.sync();
         }
       }
+    } catch (const RedoSeries&) {
+      redo = true;
+      ledger.poison();
+      enq.poison();
     } catch (...) {
       {
         std::lock_guard<std::mutex> g(err_mu);
         if (!first_err) first_err = std::current_exception();
       }
       ledger.poison();
+      enq.poison();
     }
   };
   if (T == 1) {
@@ -322,6 +373,24 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
     for (auto& th : pool) th.join();
   }
   for (cudaEvent_t ev : ready) cudaEventDestroy(ev);
+  for (int t = 0; t < T; ++t) worker(t).sync();
+  for (cudaEvent_t ev : done_) cudaEventDestroy(ev);
+  done_.clear();
+  enq_ = nullptr;
+  if (redo && !first_err) {
+    // a speculative budget split was wrong (exactly-zero right-hand side) while later
+    // frames already consumed the estimate: re-run the range with per-frame
+    // verification before publication
+    safe_mode_ = true;
+    try {
+      run(o, first, count, z_host, images_host, out);
+    } catch (...) {
+      safe_mode_ = false;
+      throw;
+    }
+    safe_mode_ = false;
+    return;
+  }
   if (first_err) std::rethrow_exception(first_err);
   // every worker stream has been synchronised by now; close the span on the copy
   // stream after all of them

@@ -89,6 +89,11 @@ class Series {
   cudaStream_t copy_ = nullptr;
   cudaEvent_t span0_ = nullptr, span1_ = nullptr;
   float span_ms_ = 0.f;
+  bool step_sync_ = false;
+  bool safe_mode_ = false;                 // no device-side chaining of closing steps
+  CompletionLedger* enq_ = nullptr;        // frames whose final work is enqueued
+  int run_first_ = 0;
+  std::vector<cudaEvent_t> done_;          // per frame of the current run: estimate published
 };
 
 }  // namespace rtnb
