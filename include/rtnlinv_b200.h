@@ -58,6 +58,18 @@ int rtn_device_count(void);
 /* context = device buffers + stream for one plan on one GPU */
 int rtn_ctx_create(const rtn_plan_t* plan, int device, rtn_ctx** out);
 void rtn_ctx_destroy(rtn_ctx* ctx);
+/* Channel decomposition (decomp.hpp:25-66 WorkerGroup + partition_channels +
+ * all_reduce_sum, passed as `WorkerGroup* wg` to apply_normal / cg_solve /
+ * newton_step / reconstruct_frame, nlinv.hpp:73-112): one context over n_devices
+ * members (entries may repeat a device), member d owning the channel block
+ * partition_channels(J, n_devices, a_cap)[d]. The channel sum is read from peer
+ * memory inside the last pass kernel and the CR scalars are summed in member
+ * order, so results do not depend on timing. Supports rtn_set_psf, rtn_set_data,
+ * rtn_make_step_cache (rho_out = coils_out = NULL), rtn_apply_normal and
+ * rtn_reconstruct_frame; the other per-context entry points return 2. */
+int rtn_ctx_create_group(const rtn_plan_t* plan, const int* devices, int n_devices, int a_cap, rtn_ctx** out);
+/* the members' channel blocks, 2*n_devices ints {j0, j1} */
+int rtn_ctx_group_blocks(rtn_ctx* ctx, int* out_pairs);
 
 /* --- fft.hpp:10-38 ------------------------------------------------------------ */
 /* centered unitary 2D transform in place; sign -1 = fft::forward, +1 = fft::inverse */

@@ -131,6 +131,9 @@ def load_library(path: str = LIB_PATH):
         "rtn_device_count": ([], ctypes.c_int),
         "rtn_ctx_create": ([ctypes.POINTER(_Plan), ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
         "rtn_ctx_destroy": ([vp], None),
+        "rtn_ctx_create_group": ([ctypes.POINTER(_Plan), i, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
+                                 ctypes.c_int),
+        "rtn_ctx_group_blocks": ([vp, i], ctypes.c_int),
         "rtn_fft2": ([f, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "rtn_fft_set_ctx": ([ctypes.c_int], None),
         "rtn_fft_get_ctx": ([], ctypes.c_int),
@@ -304,14 +307,35 @@ class FrameResult:
 
 
 class Context:
-    """One plan on one GPU: owns the device buffers and the CUDA stream."""
+    """One plan on one GPU: owns the device buffers and the CUDA stream.
 
-    def __init__(self, plan: ReconPlan, device: int = 0):
+    devices=[d0, d1, ...] builds a channel-decomposed context instead (the
+    reference's WorkerGroup passed to apply_normal / reconstruct_frame,
+    decomp.hpp:25-66): member k owns partition_channels(J, len(devices), a_cap)[k]
+    on device devices[k]; a device may repeat (members then share that GPU)."""
+
+    def __init__(self, plan: ReconPlan, device: int = 0, devices: Optional[Sequence[int]] = None,
+                 a_cap: int = 8):
         self.lib = load_library()
         self.plan = plan
         self._h = ctypes.c_void_p()
+        self.devices = None if devices is None else [int(d) for d in devices]
         c = plan.to_c()
-        _check(self.lib.rtn_ctx_create(ctypes.byref(c), device, ctypes.byref(self._h)))
+        if self.devices is None:
+            _check(self.lib.rtn_ctx_create(ctypes.byref(c), device, ctypes.byref(self._h)))
+        else:
+            arr = (ctypes.c_int * len(self.devices))(*self.devices)
+            _check(self.lib.rtn_ctx_create_group(ctypes.byref(c), arr, len(self.devices), a_cap,
+                                                 ctypes.byref(self._h)))
+
+    @property
+    def group_blocks(self):
+        """channel blocks [(j0, j1), ...] of a channel-decomposed context"""
+        if self.devices is None:
+            return [(0, self.plan.J)]
+        out = (ctypes.c_int * (2 * len(self.devices)))()
+        _check(self.lib.rtn_ctx_group_blocks(self._h, out))
+        return [(out[2 * k], out[2 * k + 1]) for k in range(len(self.devices))]
 
     def close(self):
         if self._h:
@@ -361,6 +385,9 @@ class Context:
 
     def make_step_cache(self, x):
         x = _c64(x, (self.D,))
+        if self.devices is not None:
+            _check(self.lib.rtn_make_step_cache(self._h, _fp(x), None, None))
+            return None, None
         G, J = self.plan.G, self.plan.J
         rho = np.zeros((G, G), np.complex64)
         coils = np.zeros((J, G, G), np.complex64)

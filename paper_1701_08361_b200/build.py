@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "librtnlinv_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["engine.cu", "series.cu", "sched.cpp", "capi.cpp"]
+SOURCES = ["engine.cu", "inst0.cu", "inst1.cu", "inst2.cu", "inst3.cu", "group.cu", "series.cu", "sched.cpp", "capi.cpp"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++20",
@@ -40,12 +40,27 @@ def build(force=False, verbose=False, out=None):
         OUT = out
     if not force and not needs_build():
         return OUT
+    from concurrent.futures import ThreadPoolExecutor
+
     extra = os.environ.get("RTN_NVCC_EXTRA", "").split()
-    cmd = [NVCC] + FLAGS + extra + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", OUT + ".tmp", "-lcudart"]
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f not in ("-shared",)] + ["-Xcompiler", "-fPIC"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
+        cflags = ["-Xptxas=-v"] + cflags
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src + ".o")
+        cmd = [NVCC] + cflags + extra + ["-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xlinker", "-Bsymbolic"]
+    subprocess.run(link + objs + ["-o", OUT + ".tmp", "-lcudart"], check=True)
     os.replace(OUT + ".tmp", OUT)
     return OUT
 

@@ -8,11 +8,13 @@
 
 #include "../../include/rtnlinv_b200.h"
 #include "engine.hpp"
+#include "group.hpp"
 #include "sched.hpp"
 #include "series.hpp"
 
 struct rtn_ctx {
   rtnb::Engine* eng = nullptr;
+  rtnb::Group* grp = nullptr;  // channel-decomposed context (rtn_ctx_create_group)
 };
 
 namespace {
@@ -55,6 +57,7 @@ rtnb::Plan to_plan(const rtn_plan_t* p) {
 }
 
 rtnb::Engine& eng(rtn_ctx* c) {
+  if (c && c->grp) rtnb::fail(2, "this entry point is not available on a channel-group context");
   if (!c || !c->eng) rtnb::fail(2, "null context");
   return *c->eng;
 }
@@ -89,8 +92,39 @@ int rtn_ctx_create(const rtn_plan_t* plan, int device, rtn_ctx** out) {
   });
 }
 
+int rtn_ctx_create_group(const rtn_plan_t* plan, const int* devices, int n_devices, int a_cap, rtn_ctx** out) {
+  return guarded([&] {
+    if (!plan || !out || !devices) rtnb::fail(2, "rtn_ctx_create_group: null argument");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) rtnb::fail(5, "no CUDA device available");
+    for (int k = 0; k < n_devices; ++k) {
+      if (devices[k] < 0 || devices[k] >= n) rtnb::fail(2, "rtn_ctx_create_group: device index out of range");
+    }
+    auto* c = new rtn_ctx;
+    try {
+      c->grp = new rtnb::Group(to_plan(plan), std::vector<int>(devices, devices + n_devices), a_cap);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int rtn_ctx_group_blocks(rtn_ctx* ctx, int* out_pairs) {
+  return guarded([&] {
+    if (!ctx || !ctx->grp) rtnb::fail(2, "rtn_ctx_group_blocks: not a channel-group context");
+    const auto& b = ctx->grp->blocks();
+    for (size_t k = 0; k < b.size(); ++k) {
+      out_pairs[2 * k] = b[k].first;
+      out_pairs[2 * k + 1] = b[k].second;
+    }
+  });
+}
+
 void rtn_ctx_destroy(rtn_ctx* ctx) {
   if (!ctx) return;
+  delete ctx->grp;
   delete ctx->eng;
   delete ctx;
 }
@@ -135,10 +169,22 @@ int rtn_make_weights_inv(int Gc, int G, float* out) {
 }
 
 int rtn_set_psf(rtn_ctx* ctx, const float* P) {
-  return guarded([&] { eng(ctx).set_psf(P); });
+  return guarded([&] {
+    if (ctx && ctx->grp) {
+      ctx->grp->set_psf(P);
+    } else {
+      eng(ctx).set_psf(P);
+    }
+  });
 }
 int rtn_set_data(rtn_ctx* ctx, const float* z) {
-  return guarded([&] { eng(ctx).set_data(z); });
+  return guarded([&] {
+    if (ctx && ctx->grp) {
+      ctx->grp->set_data(z);
+    } else {
+      eng(ctx).set_data(z);
+    }
+  });
 }
 int rtn_apply_W_inv(rtn_ctx* ctx, const float* chat, float* out) {
   return guarded([&] { eng(ctx).apply_W_inv(chat, out); });
@@ -150,10 +196,23 @@ int rtn_toeplitz_apply(rtn_ctx* ctx, float* x) {
   return guarded([&] { eng(ctx).toeplitz_apply(x); });
 }
 int rtn_make_step_cache(rtn_ctx* ctx, const float* x, float* rho_out, float* coils_out) {
-  return guarded([&] { eng(ctx).make_step_cache(x, rho_out, coils_out); });
+  return guarded([&] {
+    if (ctx && ctx->grp) {
+      if (rho_out || coils_out) rtnb::fail(2, "make_step_cache: a channel group keeps its cache distributed");
+      ctx->grp->make_step_cache(x);
+    } else {
+      eng(ctx).make_step_cache(x, rho_out, coils_out);
+    }
+  });
 }
 int rtn_apply_normal(rtn_ctx* ctx, const float* dx, float* out) {
-  return guarded([&] { eng(ctx).apply_normal(dx, out); });
+  return guarded([&] {
+    if (ctx && ctx->grp) {
+      ctx->grp->apply_normal(dx, out);
+    } else {
+      eng(ctx).apply_normal(dx, out);
+    }
+  });
 }
 int rtn_cg_solve(rtn_ctx* ctx, const float* rhs, float alpha, float tol, int max_iter, float* x_out,
                  int* iters, double* residuals) {
@@ -171,7 +230,11 @@ int rtn_reconstruct_frame(rtn_ctx* ctx, const float* init, const float* reg, flo
                           int* cg_per_step, double* seconds) {
   return guarded([&] {
     rtnb::FrameStats st;
-    eng(ctx).reconstruct_frame(init, reg, image, est_out, &st);
+    if (ctx && ctx->grp) {
+      ctx->grp->reconstruct_frame(init, reg, image, est_out, &st);
+    } else {
+      eng(ctx).reconstruct_frame(init, reg, image, est_out, &st);
+    }
     if (cg_per_step) {
       for (size_t m = 0; m < st.cg_per_step.size(); ++m) cg_per_step[m] = st.cg_per_step[m];
     }

@@ -11,7 +11,7 @@
 #include <numbers>
 #include <string>
 
-#include "kernels_impl.cuh"
+#include "ops.cuh"
 
 namespace rtnb {
 
@@ -97,129 +97,6 @@ __global__ void k_mul(float2* __restrict__ x, const float2* __restrict__ P, int 
 // size dispatch
 // ------------------------------------------------------------------------------
 
-struct Engine::Ops {
-  int G = 0, N1 = 0, N2 = 0, LPB = 0, NT = 0;
-  size_t smem = 0;
-  void (*colA)(cudaStream_t, int, Dims, const float*, const float2*, const float2*, float2*, int, int,
-               const DevState*, int) = nullptr;
-  void (*rows1)(cudaStream_t, int, Dims, int, const float2*, const float2*, const float2*, const float2*,
-                const float2*, float2*, float2*, const float2*, float2*, const DevState*, int) = nullptr;
-  void (*colsT)(cudaStream_t, int, Dims, const float2*, const float2*, float2*, const DevState*, int) = nullptr;
-  void (*rows2)(cudaStream_t, int, Dims, int, const float2*, const float2*, const float2*,
-                const float2*, const float2*, float2*, double2*, double*, DevState*, int) = nullptr;
-  void (*colsW)(cudaStream_t, int, Dims, ColsWArgs, const float*, const float2*, const float2*,
-                const double2*, const float2*, const float2*, int, double*, DevState*, CrScalars, int) = nullptr;
-  void (*fft)(cudaStream_t, int, int, float2*, int, int, const float2*, float) = nullptr;
-};
-
-namespace {
-
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("RTN_PDL");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-// launch with programmatic stream serialisation (see pdl_enter, kernels_impl.cuh)
-template <typename... KArgs, typename... Args>
-void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(static_cast<unsigned>(block));
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  check_cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "launch");
-}
-
-template <int N1, int N2>
-struct Inst {
-  // 16 lines per block, 32 when that keeps the block a whole number of warps
-  static constexpr int kLpb = ((16 * (N1 > N2 ? N1 : N2)) % 32 == 0) ? 16 : 32;
-  using Geo = LineGeom<N1, N2, kLpb>;
-  static constexpr size_t kSmem = sizeof(float2) * Geo::SMEM_FLOAT2;
-  static constexpr int kNT = Geo::NT;
-  // row pass 2: one window row x one group of kLpb channels (+ the channel terms)
-  static constexpr size_t kSmem2 = sizeof(float2) * (Geo::SMEM_FLOAT2 + kLpb * (N1 * N2 / 2));
-
-  static void set_attrs() {
-    const int s = static_cast<int>(kSmem);
-    check_cuda(cudaFuncSetAttribute(k_colA<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colA");
-    check_cuda(cudaFuncSetAttribute(k_rows1<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr rows1");
-    check_cuda(cudaFuncSetAttribute(k_colsT<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsT");
-    check_cuda(cudaFuncSetAttribute(k_rows2<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kSmem2)),
-               "attr rows2");
-    check_cuda(cudaFuncSetAttribute(k_colsW<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsW");
-    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
-    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, +1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr ifft");
-    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
-    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, +1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr ifft");
-  }
-
-  static Engine::Ops make();
-};
-
-}  // namespace
-
-template <int N1, int N2>
-Engine::Ops Inst<N1, N2>::make() {
-  Engine::Ops o;
-  o.G = N1 * N2;
-  o.N1 = N1;
-  o.N2 = N2;
-  o.LPB = Geo::LPB;
-  o.smem = kSmem;
-  o.NT = kNT;
-  o.colA = [](cudaStream_t s, int grid, Dims d, const float* winv, const float2* tw, const float2* chat,
-              float2* U, int r0, int nr, const DevState* st, int h) {
-    launch_k(k_colA<Geo>, grid, kNT, kSmem, s, d, winv, tw, chat, U, r0, nr, st, h);
-  };
-  o.rows1 = [](cudaStream_t s, int grid, Dims d, int mode, const float2* tw, const float2* U,
-               const float2* coils, const float2* rhom, const float2* drho, float2* V, float2* coils_out,
-               const float2* rho_src, float2* rhom_out, const DevState* st, int h) {
-    launch_k(k_rows1<Geo>, grid, kNT, kSmem, s, d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
-             rhom_out, st, h);
-  };
-  o.colsT = [](cudaStream_t s, int grid, Dims d, const float2* tw, const float2* P, float2* V,
-               const DevState* st, int h) {
-    launch_k(k_colsT<Geo>, grid, kNT, kSmem, s, d, tw, P, V, st, h);
-  };
-  o.rows2 = [](cudaStream_t s, int grid, Dims d, int setup, const float2* tw, const float2* V,
-               const float2* coils, const float2* rhom, const float2* z, float2* Y, double2* RP,
-               double* partials, DevState* st, int h) {
-    launch_k(k_rows2<Geo>, grid, kNT, kSmem2, s, d, setup, tw, V, coils, rhom, z, Y, RP, partials, st, h);
-  };
-  o.colsW = [](cudaStream_t s, int grid, Dims d, ColsWArgs a, const float* winv, const float2* tw,
-               const float2* Y, const double2* RP, const float2* coils, const float2* z, int nbw,
-               double* partials, DevState* st, CrScalars cr, int h) {
-    launch_k(k_colsW<Geo>, grid, kNT, kSmem, s, d, a, winv, tw, Y, RP, coils, z, nbw, partials, st, cr, h);
-  };
-  o.fft = [](cudaStream_t s, int grid, int sign, float2* data, int batch, int axis, const float2* tw,
-             float scale) {
-    if (sign < 0) {
-      if (axis == 0) {
-        k_fft_pass<Geo, -1, true><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
-      } else {
-        k_fft_pass<Geo, -1, false><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
-      }
-    } else {
-      if (axis == 0) {
-        k_fft_pass<Geo, +1, true><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
-      } else {
-        k_fft_pass<Geo, +1, false><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
-      }
-    }
-  };
-  return o;
-}
-
 namespace {
 
 struct Registry {
@@ -235,24 +112,10 @@ struct Registry {
 Registry& registry() {
   static Registry* r = [] {
     auto* reg = new Registry;
-#define RTNB_INST(a, b)                                 \
-  reg->ops.push_back(Inst<a, b>::make());               \
-  reg->attrs.push_back({a * b, &Inst<a, b>::set_attrs});
-    RTNB_INST(4, 4)
-    RTNB_INST(4, 6)
-    RTNB_INST(4, 8)
-    RTNB_INST(6, 8)
-    RTNB_INST(8, 8)
-    RTNB_INST(8, 9)
-    RTNB_INST(8, 12)
-    RTNB_INST(8, 16)
-    RTNB_INST(10, 16)
-    RTNB_INST(12, 16)
-    RTNB_INST(16, 16)
-    RTNB_INST(16, 20)
-    RTNB_INST(16, 24)
-    RTNB_INST(16, 32)
-#undef RTNB_INST
+add_ops_0(reg->ops, reg->attrs);
+    add_ops_1(reg->ops, reg->attrs);
+    add_ops_2(reg->ops, reg->attrs);
+    add_ops_3(reg->ops, reg->attrs);
     return reg;
   }();
   return *r;
@@ -386,6 +249,8 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), dev_(device) {
   dims_.N = plan.N;
   dims_.invG = 1.0f / static_cast<float>(plan.G);
   dims_.H = (plan.J + ops_->LPB - 1) / ops_->LPB;
+  dims_.grp = 0;
+  dims_.count_rho = 1;
   D_ = plan.G * plan.G + plan.J * plan.Gc * plan.Gc;
   check_cuda(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
   if (const char* e = std::getenv("RTN_FUSED_CR")) fused_cr_ = e[0] != '0';
@@ -400,7 +265,8 @@ Engine::~Engine() {
   }
   if (frame_graph_) cudaGraphExecDestroy(frame_graph_);
   void* bufs[] = {winv_, P_, z_, x_, xcg_, r_, p_, ap_, ar_, reg_, est_scratch_[0], est_scratch_[1],
-                  est_scratch_[2], coils_, rhom_, U_, V_, Y_, RP_, gbuf_, img_, partials_, st_, cr_buf_};
+                  est_scratch_[2], coils_, rhom_, U_, V_, Y_, RP_, gbuf_, img_, partials_, st_, cr_buf_,
+                  RPO_, SS_};
   for (void* b : bufs) {
     if (b) cudaFree(b);
   }
@@ -482,14 +348,17 @@ void Engine::ensure_cr_capacity(int max_iter) {
     check_cuda(cudaStreamSynchronize(s_), "sync");
     cudaFree(cr_buf_);
   }
+  if (grp_rank_ >= 0) fail(2, "cg capacity of a channel-group member is fixed when the group is built");
   cr_cap_ = max_iter + 2;
-  check_cuda(cudaMalloc(&cr_buf_, sizeof(double) * 5 * cr_cap_), "cr scalars");
-  check_cuda(cudaMemset(cr_buf_, 0, sizeof(double) * 5 * cr_cap_), "cr scalars");
+  check_cuda(cudaMalloc(&cr_buf_, sizeof(double) * 10 * cr_cap_), "cr scalars");
+  check_cuda(cudaMemset(cr_buf_, 0, sizeof(double) * 10 * cr_cap_), "cr scalars");
   cr_.rar = cr_buf_;
   cr_.ap2 = cr_buf_ + cr_cap_;
   cr_.rn = cr_buf_ + 2 * cr_cap_;
   cr_.saa = cr_buf_ + 3 * cr_cap_;
   cr_.spa = cr_buf_ + 4 * cr_cap_;
+  cr_.pcw = cr_buf_ + 5 * cr_cap_;
+  cr_.pcr = cr_buf_ + 8 * cr_cap_;
 }
 
 void Engine::sync() { check_cuda(cudaStreamSynchronize(s_), "stream sync"); }
@@ -537,12 +406,24 @@ void Engine::enq_decode(const float2* est) {
 
 void Engine::enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
                        const float2* ap_prev) {
+  enq_apply_front(dx, use_halt);
+  enq_apply_back(dx, out, cw_mode, alpha, dot_slot, use_halt, ap_prev);
+}
+
+void Engine::enq_apply_front(const float2* dx, int use_halt) {
   const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
   const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
   ops_->colA(s_, J * tGc, dims_, winv_, twG_, dx + static_cast<size_t>(G) * G, U_, dims_.lo, dims_.L, st_,
              use_halt);
   ops_->rows1(s_, J * tL, dims_, R1_OP, twG_, U_, coils_, rhom_, dx, V_, nullptr, nullptr, nullptr, st_, use_halt);
   ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, use_halt);
+  ops_->rows2(s_, dims_.L * dims_.H, dims_, 0, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, use_halt);
+}
+
+void Engine::enq_apply_back(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
+                            const float2* ap_prev) {
+  const int J = plan_.J, LPB = ops_->LPB;
+  const int tGc = (plan_.Gc + LPB - 1) / LPB;
   ColsWArgs a{};
   a.mode = cw_mode;
   a.alpha = alpha;
@@ -550,17 +431,28 @@ void Engine::enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, 
   a.dx = dx;
   a.out = out;
   a.ap_prev = ap_prev;
-  ops_->rows2(s_, dims_.L * dims_.H, dims_, 0, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, use_halt);
   const int nbw = J * tGc;
-  ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, use_halt);
+  ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, use_halt, gv_);
 }
 
 void Engine::enq_setup(const float2* x, const float2* reg, float alpha) {
+  enq_setup_front(x);
+  enq_setup_back(x, reg, alpha);
+}
+
+void Engine::enq_setup_front(const float2* x) {
   const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
-  const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
+  const int tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
   enq_decode(x);
   ops_->rows1(s_, J * tL, dims_, R1_SETUP, twG_, U_, coils_, rhom_, nullptr, V_, nullptr, nullptr, nullptr, st_, 0);
   ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, 0);
+  ops_->rows2(s_, dims_.L * dims_.H, dims_, 1, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, 0);
+  if (dims_.grp) launch_k(k_rho_out, nbr_, kThreads, 0, s_, dims_, coils_, z_, RPO_, partials_, st_);
+}
+
+void Engine::enq_setup_back(const float2* x, const float2* reg, float alpha) {
+  const int J = plan_.J, LPB = ops_->LPB;
+  const int tGc = (plan_.Gc + LPB - 1) / LPB;
   ColsWArgs a{};
   a.mode = CW_SETUP;
   a.a_x = static_cast<float>(-static_cast<double>(alpha));
@@ -571,9 +463,8 @@ void Engine::enq_setup(const float2* x, const float2* reg, float alpha) {
   a.out = r_;
   a.out2 = p_;
   a.out3 = xcg_;
-  ops_->rows2(s_, dims_.L * dims_.H, dims_, 1, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, 0);
   const int nbw = J * tGc;
-  ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, 0);
+  ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, 0, gv_);
 }
 
 void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
@@ -581,12 +472,10 @@ void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
   if (!sync_each && fused_cr_) {
     // budget-mode graphs: one fused recurrence kernel per iteration (k_cr_fused)
     enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1, nullptr);
-    launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, static_cast<const float2*>(ar_),
-             partials_, st_, cr_, 0, tol);
+    enq_cr_fused(0, tol);
     for (int it = 1; it < cap; ++it) {
       enq_apply(r_, ar_, CW_OPALPHA, alpha, it, 1, ap_);
-      launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, static_cast<const float2*>(ar_),
-               partials_, st_, cr_, it, tol);
+      enq_cr_fused(it, tol);
     }
     return;
   }
@@ -622,6 +511,55 @@ void Engine::enq_image(const float2* est, float2* img, float scale, bool apply_s
   enq_decode(est);
   launch_k(k_image, blocks_for(static_cast<long long>(plan_.N) * plan_.N, 148 * 4), kThreads, 0, s_, dims_,
            est, coils_, scale, apply_scale ? 1 : 0, img, st_);
+}
+
+void Engine::enq_cr_fused(int it, float tol) {
+  const int rho_skip = (dims_.grp && !dims_.count_rho) ? plan_.G * plan_.G : 0;
+  launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, static_cast<const float2*>(ar_),
+           partials_, st_, cr_, it, tol, rho_skip, dims_.grp);
+}
+
+void Engine::join_group(int rank, const GroupView& gv, const GroupScal& gs) {
+  check_cuda(cudaSetDevice(dev_), "set device");
+  grp_rank_ = rank;
+  dims_.grp = 1;
+  dims_.count_rho = rank == 0 ? 1 : 0;
+  gv_ = gv;
+  gs_ = gs;
+}
+
+void Engine::enq_grp_fin(int setup, int op_slot, int cr_slot, float tol) {
+  launch_k(k_grp_fin, 1, 32, 0, s_, gs_, st_, cr_, setup, op_slot, cr_slot, tol);
+}
+
+void Engine::enq_axpy1() { launch_k(k_axpy1, vec_grid_, kThreads, 0, s_, D_, x_, static_cast<const float2*>(xcg_), static_cast<const DevState*>(st_)); }
+
+void Engine::enq_state_reset() { check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset"); }
+
+void Engine::enq_coil_ss() {
+  launch_k(k_coil_ss, blocks_for(static_cast<long long>(plan_.N) * plan_.N, 148 * 4), kThreads, 0, s_, dims_,
+           static_cast<const float2*>(coils_), SS_, static_cast<const DevState*>(st_));
+}
+
+void Engine::enq_image_grp(float2* img, float scale, bool apply_scale) {
+  launch_k(k_image_grp, blocks_for(static_cast<long long>(plan_.N) * plan_.N, 148 * 4), kThreads, 0, s_, dims_,
+           static_cast<const float2*>(x_), gs_, scale, apply_scale ? 1 : 0, img, static_cast<const DevState*>(st_));
+}
+
+// ---- FrameWorker: full-layout device buffers in, stream ordered -----------------
+
+void Engine::load_frame(const float2* z, const float2* P) {
+  check_cuda(cudaMemcpyAsync(z_, z, sizeof(float2) * plan_.J * plan_.G * plan_.G, cudaMemcpyDefault, s_), "z");
+  check_cuda(cudaMemcpyAsync(P_, P, sizeof(float2) * plan_.G * plan_.G, cudaMemcpyDefault, s_), "psf");
+}
+void Engine::load_x(const float2* src) {
+  check_cuda(cudaMemcpyAsync(x_, src, sizeof(float2) * D_, cudaMemcpyDefault, s_), "x");
+}
+void Engine::load_reg(const float2* src) {
+  check_cuda(cudaMemcpyAsync(reg_, src, sizeof(float2) * D_, cudaMemcpyDefault, s_), "reg");
+}
+void Engine::store_x(float2* dst) {
+  check_cuda(cudaMemcpyAsync(dst, x_, sizeof(float2) * D_, cudaMemcpyDefault, s_), "estimate");
 }
 
 // ---- op-level API -------------------------------------------------------------
@@ -950,12 +888,12 @@ double Engine::time_kernel(const char* which, int reps) {
       a.dx = r_;
       a.out = ar_;
       const int nbw = J * tGc;
-      ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, 0);
+      ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, 0, gv_);
     } else if (w == "cr_xr") {
       launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], p_, ap_, partials_, st_, cr_, 1, 0.f);
     } else if (w == "cr_fused") {
       launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], p_, ap_,
-               static_cast<const float2*>(ar_), partials_, st_, cr_, 1, 0.f);
+               static_cast<const float2*>(ar_), partials_, st_, cr_, 1, 0.f, 0, 0);
     } else if (w == "cr_pap") {
       launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], r_, ar_, partials_, st_, cr_, 1);
     } else if (w == "colA") {

@@ -63,17 +63,49 @@ struct FrameStats {
   double seconds = 0;
 };
 
-class Engine {
+using RegFn = std::function<const float2*(int m)>;  // device pointer of reg(m), or nullptr = keep reg
+
+// What a series driver needs from one frame worker: a single-device Engine, or a
+// channel-decomposed device Group (group.hpp). Estimates, frames and PSFs are in
+// the full layout (rho then chat_0..chat_{J-1}) wherever they come from; a group
+// splits them across its members. Every enqueue is ordered on stream().
+class FrameWorker {
+ public:
+  virtual ~FrameWorker() = default;
+  virtual const Plan& plan() const = 0;
+  virtual int D() const = 0;
+  virtual int device() const = 0;
+  virtual cudaStream_t stream() const = 0;
+  virtual int width() const { return 1; }  // channel-decomposition width A
+  virtual bool budget_mode() const = 0;
+  virtual void load_frame(const float2* z, const float2* P) = 0;
+  virtual void load_x(const float2* src) = 0;
+  virtual void load_reg(const float2* src) = 0;
+  virtual void store_x(float2* dst) = 0;
+  virtual float2* image_dev() = 0;
+  virtual void frame_begin() = 0;
+  virtual void frame_step(int m, const float2* reg_src) = 0;
+  virtual void frame_image(float2* img_dst, float image_scale, bool apply_scale) = 0;
+  virtual void frame_all(float2* img_dst, float image_scale, bool apply_scale) = 0;
+  virtual bool frame_verify(FrameStats* stats) = 0;
+  virtual void frame_run_sync(const RegFn& reg, float2* img_dst, float image_scale, bool apply_scale,
+                              FrameStats* stats) = 0;
+  virtual void sync() = 0;
+};
+
+class Group;
+
+class Engine : public FrameWorker {
  public:
   Engine(const Plan& plan, int device = 0);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
 
-  const Plan& plan() const { return plan_; }
-  int D() const { return D_; }  // complex entries of one Estimate: G*G + J*Gc*Gc
-  cudaStream_t stream() const { return s_; }
-  int device() const { return dev_; }
+  const Plan& plan() const override { return plan_; }
+  int D() const override { return D_; }  // complex entries of one Estimate: G*G + J*Gc*Gc
+  cudaStream_t stream() const override { return s_; }
+  int device() const override { return dev_; }
 
   // ---- inputs (host, complex64 interleaved) ----
   void set_psf(const float* P);    // G*G
@@ -105,15 +137,20 @@ class Engine {
   // meets an exactly-zero right-hand side; frame_verify() detects that and the
   // caller re-runs the frame with frame_run_sync(). Tolerance mode synchronises per
   // CR iteration and never uses graphs.
-  using RegFn = std::function<const float2*(int m)>;  // device pointer of reg(m), or nullptr = keep reg
-  void frame_begin();
-  void frame_step(int m, const float2* reg_src);        // enqueue Newton step m
-  void frame_image(float2* img_dst, float image_scale, bool apply_scale);
-  void frame_all(float2* img_dst, float image_scale, bool apply_scale);  // budget mode: one graph
-  bool frame_verify(FrameStats* stats);                 // sync + check the speculative split
+  using RegFn = rtnb::RegFn;
+  void frame_begin() override;
+  void frame_step(int m, const float2* reg_src) override;  // enqueue Newton step m
+  void frame_image(float2* img_dst, float image_scale, bool apply_scale) override;
+  void frame_all(float2* img_dst, float image_scale, bool apply_scale) override;  // budget mode: one graph
+  bool frame_verify(FrameStats* stats) override;           // sync + check the speculative split
   void frame_run_sync(const RegFn& reg, float2* img_dst, float image_scale, bool apply_scale,
-                      FrameStats* stats);
-  bool budget_mode() const { return plan_.cg_iter_budget > 0; }
+                      FrameStats* stats) override;
+  bool budget_mode() const override { return plan_.cg_iter_budget > 0; }
+  void load_frame(const float2* z, const float2* P) override;
+  void load_x(const float2* src) override;
+  void load_reg(const float2* src) override;
+  void store_x(float2* dst) override;
+  float2* image_dev() override { return img_; }
   const std::vector<int>& budget_caps() const { return caps_; }
   void set_use_graphs(bool on) { use_graphs_ = on; }
 
@@ -121,11 +158,10 @@ class Engine {
   float2* reg_dev() { return reg_; }
   float2* z_dev() { return z_; }
   float2* psf_dev() { return P_; }
-  float2* image_dev() { return img_; }
   DevState* state_dev() { return st_; }
   const DevState& state_host() const { return *st_host_; }
   void read_state();
-  void sync();
+  void sync() override;
 
   // isolated timing of one kernel class (bench roofline): average ms per launch of
   // `reps` back-to-back launches on the engine stream, CUDA events
@@ -137,13 +173,30 @@ class Engine {
   struct Ops;  // per-grid-size kernel launchers (engine.cu)
 
  private:
+  friend class Group;
   void alloc();
   void ensure_cr_capacity(int max_iter);
   void enq_step_begin(int m);
   void enq_decode(const float2* est);
   void enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
                  const float2* ap_prev = nullptr);
+  // the two halves of an application / a Newton-step setup: everything up to the
+  // channel-sum partials (front), and the W^-H column pass + rho sum (back). A
+  // channel group puts its all-member barrier between them.
+  void enq_apply_front(const float2* dx, int use_halt);
+  void enq_apply_back(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
+                      const float2* ap_prev);
+  void enq_setup_front(const float2* x);
+  void enq_setup_back(const float2* x, const float2* reg, float alpha);
   void enq_setup(const float2* x, const float2* reg, float alpha);
+  // group-member kernels (group.cu)
+  void join_group(int rank, const GroupView& gv, const GroupScal& gs);
+  void enq_grp_fin(int setup, int op_slot, int cr_slot, float tol);
+  void enq_cr_fused(int it, float tol);
+  void enq_axpy1();
+  void enq_state_reset();
+  void enq_coil_ss();
+  void enq_image_grp(float2* img, float scale, bool apply_scale);
   void enq_cr(float alpha, float tol, int cap, bool sync_each);
   void enq_newton_step(int m, float2* x, const float2* reg, float alpha, float tol, int cap,
                        bool sync_each);
@@ -187,6 +240,12 @@ class Engine {
   double* cr_buf_ = nullptr;
   int cr_cap_ = 0;
   CrScalars cr_{};
+  // group membership (channel decomposition); grp_rank_ < 0: stand-alone
+  int grp_rank_ = -1;
+  GroupView gv_{};
+  GroupScal gs_{};
+  double2* RPO_ = nullptr;
+  double* SS_ = nullptr;
   bool have_cache_ = false;
   std::vector<int> caps_;       // budget-mode per-step caps
   std::vector<float> alphas_;   // per-step alpha schedule

@@ -14,7 +14,28 @@ struct Dims {
   int G, Gc, J, L, lo, off, N;
   int H;  // channel groups of k_rows2 (ceil(J / lines per block))
   float invG;
+  // channel decomposition (group.cu): grp != 0 when this context is one member of a
+  // device group owning a contiguous channel block; count_rho != 0 on the member whose
+  // reductions include the (replicated) rho part of every Estimate dot product
+  int grp;
+  int count_rho;
 };
+
+// Channel decomposition across a device group (decomp.cpp:10-39).
+// Every member owns channels [j0, j1) and replicates rho. The cross-channel sums
+// are read straight from the peers' memory (NVLink / NVSwitch loads; members share
+// one process, peer access enabled) in member order, so every member computes
+// bit-identical totals.
+constexpr int kMaxGroup = 8;
+struct GroupView {
+  int A;
+  int h[kMaxGroup];                 // k_rows2 channel groups of each member
+  const double2* rp[kMaxGroup];     // window channel-sum partials (H_d x L x L)
+  const double2* rpo[kMaxGroup];    // SETUP: out-of-window partials sum_j conj(c_j) z_j (G x G)
+};
+
+// k_colsW epilogue modes: plain application, application + alpha*dx (CR), Newton setup
+enum ColsWMode : int { CW_OP = 0, CW_OPALPHA = 1, CW_SETUP = 2 };
 
 // largest K of any grid_reduce<K> (sizes the per-block partials buffer)
 constexpr int kMaxReduce = 4;
@@ -42,6 +63,15 @@ struct DevState {
   unsigned int pad2_;
   StepRec steps[kMaxSteps];
   double scal[8];        // scratch scalar outputs (op-level calls)
+  double gp[4];          // group mode: this member's SETUP partials {|rhs|^2, resid_out, resid_win, -}
+};
+
+struct GroupScal {
+  int A;
+  const DevState* st[kMaxGroup];
+  const double* pcw[kMaxGroup];     // per-slot colsW partials {<dx,out>, |out|^2, <ap_prev,out>}
+  const double* pcr[kMaxGroup];     // per-iteration CR partials {|ap|^2, |r|^2}
+  const double* ss[kMaxGroup];      // final image: per-member sum_j |c_j|^2 (N x N)
 };
 
 // CR scalars of the current step: rar[k] = <r, A r> after apply k, ap2[k] = |ap|^2
@@ -52,6 +82,8 @@ struct CrScalars {
   double* rn;
   double* saa;   // fused path: |A r_k|^2 from the application
   double* spa;   // fused path: Re <ap_{k-1}, A r_k>
+  double* pcw;   // group mode: this member's colsW partials, 3 per slot
+  double* pcr;   // group mode: this member's k_cr_fused partials, 2 per iteration
 };
 
 }  // namespace rtnb

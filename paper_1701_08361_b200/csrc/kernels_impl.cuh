@@ -370,7 +370,6 @@ __global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float2* __restrict__ twG,
   }
 }
 
-enum ColsWMode : int { CW_OP = 0, CW_OPALPHA = 1, CW_SETUP = 2 };
 
 struct ColsWArgs {
   int mode;
@@ -505,7 +504,11 @@ __global__ void RTNB_PASS_BOUNDS k_rows2(Dims d, int setup, const float2* __rest
   if (setup) {
     double vv[1] = {resid}, tot[1];
     if (grid_reduce<1>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
-      st->steps[st->cur_step].resid_win = tot[0];
+      if (d.grp) {
+        st->gp[2] = tot[0];  // member partial, summed by k_grp_fin
+      } else {
+        st->steps[st->cur_step].resid_win = tot[0];
+      }
     }
   }
 }
@@ -521,7 +524,7 @@ __global__ void RTNB_PASS_BOUNDS k_colsW(Dims d, ColsWArgs a, const float* __res
                                                    const float2* __restrict__ coils,
                                                    const float2* __restrict__ z, int nbw,
                                                    double* partials, DevState* st, CrScalars cr,
-                                                   int use_halt) {
+                                                   int use_halt, GroupView gv) {
   pdl_enter();
   if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(true);
@@ -567,9 +570,37 @@ __global__ void RTNB_PASS_BOUNDS k_colsW(Dims d, ColsWArgs a, const float* __res
     // window T is masked to zero (preproc.cpp:442), so out.rho there is only the SETUP
     // data term sum_j conj(c_j) z_j, in channel order in FP64
     const int H = d.H;
+    double dummy0 = 0.0, dummy1 = 0.0, dummy2 = 0.0;
     for (int e = (blockIdx.x - nbw) * blockDim.x + threadIdx.x; e < D0; e += (gridDim.x - nbw) * blockDim.x) {
       const int r = e / G, c = e - (e / G) * G;
       double sx = 0.0, sy = 0.0;
+      if (d.grp) {
+        // channel decomposition: every member's partials, in member order, loaded
+        // from the peers' memory (the all_reduce_sum of decomp.cpp:26-39)
+        if (in_win(d, r, c)) {
+          const size_t w = (size_t)(r - d.lo) * d.L + (c - d.lo);
+          for (int m = 0; m < gv.A; ++m) {
+            for (int h = 0; h < gv.h[m]; ++h) {
+              const double2 t = __ldcg(gv.rp[m] + (size_t)h * d.L * d.L + w);
+              sx += t.x;
+              sy += t.y;
+            }
+          }
+        } else if (a.mode == CW_SETUP) {
+          for (int m = 0; m < gv.A; ++m) {
+            const double2 t = __ldcg(gv.rpo[m] + e);
+            sx += t.x;
+            sy += t.y;
+          }
+        }
+        // the rho part of every dot product is replicated: counted on one member
+        if (d.count_rho) {
+          finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), acc0, aa, pa);
+        } else {
+          finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), dummy0, dummy1, dummy2);
+        }
+        continue;
+      }
       if (in_win(d, r, c)) {
         const double2* src = RP + (size_t)(r - d.lo) * d.L + (c - d.lo);
         for (int h = 0; h < H; ++h) {
@@ -592,7 +623,18 @@ __global__ void RTNB_PASS_BOUNDS k_colsW(Dims d, ColsWArgs a, const float* __res
   double vv[4] = {acc0, acc1, aa, pa}, tot[4];
   if (grid_reduce<4>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
     const double total = tot[0];
-    if (a.mode == CW_SETUP) {
+    if (d.grp) {
+      // member partials; k_grp_fin forms the totals once every member has them
+      if (a.mode == CW_SETUP) {
+        st->gp[0] = total;
+      } else if (a.dot_slot >= 0) {
+        cr.pcw[3 * a.dot_slot + 0] = total;
+        cr.pcw[3 * a.dot_slot + 1] = tot[2];
+        cr.pcw[3 * a.dot_slot + 2] = tot[3];
+      } else {
+        st->scal[0] = total;
+      }
+    } else if (a.mode == CW_SETUP) {
       StepRec& s = st->steps[st->cur_step];
       s.rhs_nrm2 = total;
       s.resid_out = tot[1];
@@ -615,6 +657,7 @@ __global__ void RTNB_PASS_BOUNDS k_colsW(Dims d, ColsWArgs a, const float* __res
   }
 }
 
+#ifndef RTNB_PASS_ONLY  // non-template kernels: compiled once (engine.cu)
 // ---------------------------------------------------------------------------------
 // CR recurrences (nlinv.cpp:197-232). D = G*G + J*Gc*Gc complex entries.
 // ---------------------------------------------------------------------------------
@@ -738,7 +781,8 @@ __global__ void __launch_bounds__(kThreads) k_cr_pap(int D, float2* __restrict__
 __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict__ x, float2* __restrict__ r,
                                                        float2* __restrict__ p, float2* __restrict__ ap,
                                                        const float2* __restrict__ ar, double* partials,
-                                                       DevState* st, CrScalars cr, int it, float tol) {
+                                                       DevState* st, CrScalars cr, int it, float tol,
+                                                       int rho_skip, int grp) {
   pdl_enter();
   if (st->status || st->cr_halt) return;
   const double rar_new = cr.rar[it];
@@ -769,17 +813,24 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
     const float2 nap = make_float2(__fadd_rn(__fmul_rn(apv.x, bf), arv.x), __fadd_rn(__fmul_rn(apv.y, bf), arv.y));
     p[i] = np;
     ap[i] = nap;
-    acc_ap += nrm2(nap);
     float2 nr = rv;
     if (upd) {
       x[i] = axpy_rn(x[i], af, np);
       nr = axpy_rn(rv, naf, nap);
       r[i] = nr;
     }
-    acc_r += nrm2(nr);
+    if (i >= rho_skip) {  // group members other than the first skip the replicated rho
+      acc_ap += nrm2(nap);
+      acc_r += nrm2(nr);
+    }
   }
   double v[2] = {acc_ap, acc_r}, tot[2];
   if (grid_reduce<2>(v, partials, &st->counter, tot) && threadIdx.x == 0) {
+    if (grp) {
+      cr.pcr[2 * it + 0] = tot[0];
+      cr.pcr[2 * it + 1] = tot[1];
+      return;
+    }
     cr.ap2[it] = tot[0];
     const double rn = sqrt(tot[1]);
     cr.rn[it + 1] = rn;
@@ -792,6 +843,138 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
     s.iters = it + 1;
     const double target = (double)tol * sqrt(s.rhs_nrm2);
     if (tol > 0.0f && (rn == 0.0 || rn <= target)) st->cr_halt = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Channel decomposition (group mode). Members run the pass kernels on their own
+// channel block; the cross-member sums happen at two kinds of points:
+//   - vectors: k_colsW reads every member's k_rows2 window partials (and, in SETUP,
+//     k_rho_out's out-of-window partials) from peer memory;
+//   - scalars: every reduction writes the member's partial, and k_grp_fin (one
+//     thread) forms the totals in member order after an all-member event barrier,
+//     then runs exactly the decisions the single-device kernels take in their last
+//     block (nlinv.cpp:184-186, 205-220). Every member computes identical totals, so
+//     every member takes identical decisions.
+// ---------------------------------------------------------------------------------
+
+// SETUP, outside the window: partial sum over this member's channels of
+// conj(c_j) z_j (the T term is masked to zero there, preproc.cpp:442) and |z_j|^2
+__global__ void __launch_bounds__(kThreads) k_rho_out(Dims d, const float2* __restrict__ coils,
+                                                      const float2* __restrict__ z, double2* __restrict__ RPO,
+                                                      double* partials, DevState* st) {
+  pdl_enter();
+  if (st->status) return;
+  const int G = d.G, D0 = G * G;
+  double acc = 0.0;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < D0; e += gridDim.x * blockDim.x) {
+    const int r = e / G, c = e - (e / G) * G;
+    if (in_win(d, r, c)) continue;
+    double sx = 0.0, sy = 0.0;
+    for (int j = 0; j < d.J; ++j) {
+      const float2 zz = z[(size_t)j * D0 + e];
+      const float2 v = cjmul_rn(coils[(size_t)j * D0 + e], zz);
+      sx += v.x;
+      sy += v.y;
+      acc += nrm2(zz);
+    }
+    RPO[e] = make_double2(sx, sy);
+  }
+  double vv[1] = {acc}, tot[1];
+  if (grid_reduce<1>(vv, partials, &st->counter, tot) && threadIdx.x == 0) st->gp[1] = tot[0];
+}
+
+__device__ __forceinline__ double grp_sum(const GroupScal& g, const double* const* base, int idx) {
+  double t = 0.0;
+  for (int m = 0; m < g.A; ++m) t += __ldcg(base[m] + idx);
+  return t;
+}
+
+// Group totals and the decisions that depend on them.
+//  setup:       |rhs|^2, resid_out, resid_win of the step; cg_solve entry checks
+//  cr_slot >= 0: k_cr_fused(cr_slot): ap2[cr_slot], rn[cr_slot+1], iters, tolerance stop
+//  op_slot >= 0: colsW of application op_slot: rar, saa, spa
+__global__ void k_grp_fin(GroupScal g, DevState* st, CrScalars cr, int setup, int op_slot, int cr_slot,
+                          float tol) {
+  pdl_enter();
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (st->status) return;
+  StepRec& s = st->steps[st->cur_step];
+  if (setup) {
+    double rhs = 0.0, ro = 0.0, rw = 0.0;
+    for (int m = 0; m < g.A; ++m) {
+      rhs += __ldcg(&g.st[m]->gp[0]);
+      ro += __ldcg(&g.st[m]->gp[1]);
+      rw += __ldcg(&g.st[m]->gp[2]);
+    }
+    s.rhs_nrm2 = rhs;
+    s.resid_out = ro;
+    s.resid_win = rw;
+    const double rn = sqrt(rhs);
+    if (!isfinite(rn)) {
+      st->status = ST_SOLVER;
+      st->cr_halt = 1;
+    } else if (rn == 0.0) {
+      s.zero_rhs = 1;
+      st->cr_halt = 1;
+    }
+    return;
+  }
+  if (st->cr_halt) return;
+  if (cr_slot >= 0) {
+    cr.ap2[cr_slot] = grp_sum(g, g.pcr, 2 * cr_slot);
+    const double rn = sqrt(grp_sum(g, g.pcr, 2 * cr_slot + 1));
+    cr.rn[cr_slot + 1] = rn;
+    if (!isfinite(rn)) {
+      st->status = ST_SOLVER;
+      st->cr_halt = 1;
+      return;
+    }
+    s.iters = cr_slot + 1;
+    const double target = (double)tol * sqrt(s.rhs_nrm2);
+    if (tol > 0.0f && (rn == 0.0 || rn <= target)) {
+      st->cr_halt = 1;
+      return;
+    }
+  }
+  if (op_slot >= 0) {
+    cr.rar[op_slot] = grp_sum(g, g.pcw, 3 * op_slot + 0);
+    cr.saa[op_slot] = grp_sum(g, g.pcw, 3 * op_slot + 1);
+    cr.spa[op_slot] = grp_sum(g, g.pcw, 3 * op_slot + 2);
+  }
+}
+
+// final image, group mode: this member's sum_j |c_j|^2 over the N x N crop
+__global__ void __launch_bounds__(kThreads) k_coil_ss(Dims d, const float2* __restrict__ coils,
+                                                      double* __restrict__ ss, const DevState* st) {
+  pdl_enter();
+  if (st->status) return;
+  const int G = d.G, N = d.N;
+  const int o = G / 2 - N / 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N * N; e += gridDim.x * blockDim.x) {
+    const size_t g = (size_t)(e / N + o) * G + (e % N + o);
+    double acc = 0.0;
+    for (int j = 0; j < d.J; ++j) acc += nrm2(coils[(size_t)j * G * G + g]);
+    ss[e] = acc;
+  }
+}
+
+// final image, group mode (first member): rho * sqrt(sum over members of k_coil_ss)
+__global__ void __launch_bounds__(kThreads) k_image_grp(Dims d, const float2* __restrict__ rho, GroupScal g,
+                                                        float scale, int apply_scale, float2* __restrict__ img,
+                                                        const DevState* st) {
+  pdl_enter();
+  if (st->status) return;
+  const int G = d.G, N = d.N;
+  const int o = G / 2 - N / 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N * N; e += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int m = 0; m < g.A; ++m) acc += __ldcg(g.ss[m] + e);
+    const float s = (float)sqrt(acc);
+    const float2 rv = rho[(size_t)(e / N + o) * G + (e % N + o)];
+    float2 v = make_float2(rv.x * s, rv.y * s);
+    if (apply_scale) v = make_float2(v.x * scale, v.y * scale);
+    img[e] = v;
   }
 }
 
@@ -828,6 +1011,8 @@ __global__ void __launch_bounds__(kThreads) k_image(Dims d, const float2* __rest
     img[e] = v;
   }
 }
+
+#endif  // RTNB_PASS_ONLY
 
 // ---------------------------------------------------------------------------------
 // Stand-alone centered 2D transforms (fft::forward / fft::inverse, fft.hpp:22-30).
@@ -869,6 +1054,7 @@ __global__ void __launch_bounds__(Geo::NT) k_fft_pass(float2* __restrict__ data,
   }
 }
 
+#ifndef RTNB_PASS_ONLY
 // Direct centered DFT along one axis for sizes the line engine does not cover
 // (odd sides, large prime factors): X[p] = sum_t x[t] W^{(p-c)(t-c)}, one block per
 // line, FP64 accumulation. tw: exp(sign 2 pi i e / n), e = 0..n-1.
@@ -898,5 +1084,7 @@ __global__ void k_dft_direct(const float2* __restrict__ in, float2* __restrict__
     dst[base + p * stride] = make_float2((float)(ax * scale), (float)(ay * scale));
   }
 }
+
+#endif  // RTNB_PASS_ONLY
 
 }  // namespace rtnb

@@ -1,0 +1,150 @@
+// Per-grid-size kernel launchers (Engine::Ops) and the launch helper shared by the
+// engine and the instantiation units inst*.cu (the 14 line-FFT geometries are
+// compiled in parallel translation units).
+#pragma once
+
+#include <cstdlib>
+#include <utility>
+#include <vector>
+
+#include "engine.hpp"
+#include "kernels_impl.cuh"
+
+namespace rtnb {
+
+struct Engine::Ops {
+  int G = 0, N1 = 0, N2 = 0, LPB = 0, NT = 0;
+  size_t smem = 0;
+  void (*colA)(cudaStream_t, int, Dims, const float*, const float2*, const float2*, float2*, int, int,
+               const DevState*, int) = nullptr;
+  void (*rows1)(cudaStream_t, int, Dims, int, const float2*, const float2*, const float2*, const float2*,
+                const float2*, float2*, float2*, const float2*, float2*, const DevState*, int) = nullptr;
+  void (*colsT)(cudaStream_t, int, Dims, const float2*, const float2*, float2*, const DevState*, int) = nullptr;
+  void (*rows2)(cudaStream_t, int, Dims, int, const float2*, const float2*, const float2*,
+                const float2*, const float2*, float2*, double2*, double*, DevState*, int) = nullptr;
+  void (*colsW)(cudaStream_t, int, Dims, ColsWArgs, const float*, const float2*, const float2*,
+                const double2*, const float2*, const float2*, int, double*, DevState*, CrScalars, int,
+                const GroupView&) = nullptr;
+  void (*fft)(cudaStream_t, int, int, float2*, int, int, const float2*, float) = nullptr;
+};
+
+namespace {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RTN_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// launch with programmatic stream serialisation (see pdl_enter, kernels_impl.cuh)
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  check_cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "launch");
+}
+
+template <int N1, int N2>
+struct Inst {
+  // 16 lines per block, 32 when that keeps the block a whole number of warps
+  static constexpr int kLpb = ((16 * (N1 > N2 ? N1 : N2)) % 32 == 0) ? 16 : 32;
+  using Geo = LineGeom<N1, N2, kLpb>;
+  static constexpr size_t kSmem = sizeof(float2) * Geo::SMEM_FLOAT2;
+  static constexpr int kNT = Geo::NT;
+  // row pass 2: one window row x one group of kLpb channels (+ the channel terms)
+  static constexpr size_t kSmem2 = sizeof(float2) * (Geo::SMEM_FLOAT2 + kLpb * (N1 * N2 / 2));
+
+  static void set_attrs() {
+    const int s = static_cast<int>(kSmem);
+    check_cuda(cudaFuncSetAttribute(k_colA<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colA");
+    check_cuda(cudaFuncSetAttribute(k_rows1<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr rows1");
+    check_cuda(cudaFuncSetAttribute(k_colsT<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsT");
+    check_cuda(cudaFuncSetAttribute(k_rows2<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmem2)),
+               "attr rows2");
+    check_cuda(cudaFuncSetAttribute(k_colsW<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsW");
+    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
+    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, +1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr ifft");
+    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
+    check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, +1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr ifft");
+  }
+
+  static Engine::Ops make();
+};
+
+}  // namespace
+
+template <int N1, int N2>
+Engine::Ops Inst<N1, N2>::make() {
+  Engine::Ops o;
+  o.G = N1 * N2;
+  o.N1 = N1;
+  o.N2 = N2;
+  o.LPB = Geo::LPB;
+  o.smem = kSmem;
+  o.NT = kNT;
+  o.colA = [](cudaStream_t s, int grid, Dims d, const float* winv, const float2* tw, const float2* chat,
+              float2* U, int r0, int nr, const DevState* st, int h) {
+    launch_k(k_colA<Geo>, grid, kNT, kSmem, s, d, winv, tw, chat, U, r0, nr, st, h);
+  };
+  o.rows1 = [](cudaStream_t s, int grid, Dims d, int mode, const float2* tw, const float2* U,
+               const float2* coils, const float2* rhom, const float2* drho, float2* V, float2* coils_out,
+               const float2* rho_src, float2* rhom_out, const DevState* st, int h) {
+    launch_k(k_rows1<Geo>, grid, kNT, kSmem, s, d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
+             rhom_out, st, h);
+  };
+  o.colsT = [](cudaStream_t s, int grid, Dims d, const float2* tw, const float2* P, float2* V,
+               const DevState* st, int h) {
+    launch_k(k_colsT<Geo>, grid, kNT, kSmem, s, d, tw, P, V, st, h);
+  };
+  o.rows2 = [](cudaStream_t s, int grid, Dims d, int setup, const float2* tw, const float2* V,
+               const float2* coils, const float2* rhom, const float2* z, float2* Y, double2* RP,
+               double* partials, DevState* st, int h) {
+    launch_k(k_rows2<Geo>, grid, kNT, kSmem2, s, d, setup, tw, V, coils, rhom, z, Y, RP, partials, st, h);
+  };
+  o.colsW = [](cudaStream_t s, int grid, Dims d, ColsWArgs a, const float* winv, const float2* tw,
+               const float2* Y, const double2* RP, const float2* coils, const float2* z, int nbw,
+               double* partials, DevState* st, CrScalars cr, int h, const GroupView& gv) {
+    launch_k(k_colsW<Geo>, grid, kNT, kSmem, s, d, a, winv, tw, Y, RP, coils, z, nbw, partials, st, cr, h, gv);
+  };
+  o.fft = [](cudaStream_t s, int grid, int sign, float2* data, int batch, int axis, const float2* tw,
+             float scale) {
+    if (sign < 0) {
+      if (axis == 0) {
+        k_fft_pass<Geo, -1, true><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
+      } else {
+        k_fft_pass<Geo, -1, false><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
+      }
+    } else {
+      if (axis == 0) {
+        k_fft_pass<Geo, +1, true><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
+      } else {
+        k_fft_pass<Geo, +1, false><<<grid, kNT, kSmem, s>>>(data, batch, tw, scale);
+      }
+    }
+  };
+  return o;
+}
+
+
+using OpsAttrList = std::vector<std::pair<int, void (*)()>>;
+void add_ops_0(std::vector<Engine::Ops>& ops, OpsAttrList& attrs);
+void add_ops_1(std::vector<Engine::Ops>& ops, OpsAttrList& attrs);
+void add_ops_2(std::vector<Engine::Ops>& ops, OpsAttrList& attrs);
+void add_ops_3(std::vector<Engine::Ops>& ops, OpsAttrList& attrs);
+
+#define RTNB_INST(a, b)                  \
+  ops.push_back(Inst<a, b>::make());     \
+  attrs.push_back({a * b, &Inst<a, b>::set_attrs});
+
+}  // namespace rtnb

@@ -99,7 +99,16 @@ Series::~Series() {
   if (span1_) cudaEventDestroy(span1_);
 }
 
-Engine& Series::worker(int t) {
+FrameWorker& Series::worker(int t) {
+  if (A_ > 1) {
+    while (static_cast<int>(groups_.size()) <= t) {
+      const int k = static_cast<int>(groups_.size());
+      std::vector<int> devs;
+      for (int a = 0; a < A_; ++a) devs.push_back(devices_[static_cast<size_t>(k * A_ + a) % devices_.size()]);
+      groups_.push_back(std::make_unique<Group>(eng0_.plan(), devs));
+    }
+    return *groups_[static_cast<size_t>(t)];
+  }
   if (t == 0) return eng0_;
   while (static_cast<int>(extra_.size()) < t) {
     const int k = static_cast<int>(extra_.size()) + 1;
@@ -146,7 +155,7 @@ double Series::normalize() {
 
 void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& ledger, SeriesFrameOut& out,
                        cudaEvent_t ready) {
-  Engine& e = worker(t);
+  FrameWorker& e = worker(t);
   const Plan& p = e.plan();
   const int M = p.newton_steps;
   cudaStream_t s = e.stream();
@@ -166,11 +175,8 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
 
   if (ready) check_cuda(cudaStreamWaitEvent(s, ready, 0), "wait frame upload");
   check_cuda(cudaSetDevice(e.device()), "set device");
-  check_cuda(cudaMemcpyAsync(e.z_dev(), z_ + zsz_ * n, sizeof(float2) * zsz_, cudaMemcpyDefault, s), "z");
-  check_cuda(cudaMemcpyAsync(e.psf_dev(), psf_ + psz_ * psf_idx_[static_cast<size_t>(n)], sizeof(float2) * psz_,
-                             cudaMemcpyDefault, s),
-             "psf");
-  check_cuda(cudaMemcpyAsync(e.x_dev(), init, sizeof(float2) * D_, cudaMemcpyDefault, s), "init");
+  e.load_frame(z_ + zsz_ * n, psf_ + psz_ * psf_idx_[static_cast<size_t>(n)]);
+  e.load_x(init);
   cudaEvent_t ev0, ev1;
   check_cuda(cudaEventCreate(&ev0), "event");
   check_cuda(cudaEventCreate(&ev1), "event");
@@ -185,7 +191,7 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   const bool chain_events = !safe_mode_ && !o.plain && o.T > 1;
   if (fixed_reg) {
     for (int m = 0; m < M; ++m) a.reg_src[static_cast<size_t>(m)] = chained ? a.init_src : -1;
-    check_cuda(cudaMemcpyAsync(e.reg_dev(), init, sizeof(float2) * D_, cudaMemcpyDefault, s), "reg");
+    e.load_reg(init);
     if (!o.plain && M > 0) a.reg_final_seq = ledger.next_seq();
     if (e.budget_mode()) {
       e.frame_all(img, iscale, undo);
@@ -228,7 +234,7 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   if (chain_events) {
     // publish the estimate and its completion event before this thread blocks, so the
     // next frame's closing step can be queued behind it on the device
-    check_cuda(cudaMemcpyAsync(estimate_dev(n), e.x_dev(), sizeof(float2) * D_, cudaMemcpyDefault, s), "estimate");
+    e.store_x(estimate_dev(n));
     check_cuda(cudaEventRecord(done_[static_cast<size_t>(n - run_first_)], s), "done event");
     a.finish_seq = ledger.next_seq();
     enq_->mark_complete(n);
@@ -236,19 +242,17 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   } else if (!e.frame_verify(&fs)) {
     // a step met an exactly-zero right-hand side: redo with the true budget split,
     // replaying the recorded regularisation sources
-    check_cuda(cudaMemcpyAsync(e.x_dev(), init, sizeof(float2) * D_, cudaMemcpyDefault, s), "init");
+    e.load_x(init);
     const std::vector<int> srcs = a.reg_src;
     const float2* u = unity_;
-    Engine::RegFn rf = [this, srcs, u](int m) -> const float2* {
+    RegFn rf = [this, srcs, u](int m) -> const float2* {
       const int sidx = srcs[static_cast<size_t>(m)];
       return sidx >= 0 ? estimate_dev(sidx) : u;
     };
     e.frame_run_sync(rf, img, iscale, undo, &fs);
     check_cuda(cudaEventRecord(ev1, s), "event");
   }
-  if (!chain_events) {
-    check_cuda(cudaMemcpyAsync(estimate_dev(n), e.x_dev(), sizeof(float2) * D_, cudaMemcpyDefault, s), "estimate");
-  }
+  if (!chain_events) e.store_x(estimate_dev(n));
   if (!local) {
     check_cuda(cudaMemcpyAsync(images_ + isz_ * n, img, sizeof(float2) * isz_, cudaMemcpyDefault, s), "image");
   }
@@ -273,6 +277,11 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   const int dev = eng0_.device();
   check_cuda(cudaSetDevice(dev), "set device");
   const Plan& p = eng0_.plan();
+  if (o.A > p.J) fail(2, "reconstruct_series: more channel-group members than channels");
+  if (o.A != A_) {
+    groups_.clear();
+    A_ = o.A;
+  }
   const int T = o.plain ? 1 : std::min(o.T, count);
   for (int t = 1; t < T; ++t) worker(t);
   check_cuda(cudaEventRecord(span0_, copy_), "span event");
@@ -344,7 +353,7 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
         run_frame(t, first + k, o, ledger, (*out)[static_cast<size_t>(k)],
                   ready.empty() ? nullptr : ready[static_cast<size_t>(k)]);
         if (images_host) {
-          Engine& e = worker(t);
+          FrameWorker& e = worker(t);
           check_cuda(cudaMemcpyAsync(images_host + 2 * isz_ * k, images_ + isz_ * (first + k), sizeof(float2) * isz_,
                                      cudaMemcpyDeviceToHost, e.stream()),
                      "image d2h");

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "engine.hpp"
+#include "group.hpp"
 #include "sched.hpp"
 
 namespace rtnb {
@@ -16,7 +17,7 @@ namespace rtnb {
 struct SeriesOptions {
   TemporalSchedule sched{1, 1};
   int T = 1;            // frames in flight: one worker (stream + workspace) each
-  int A = 1;            // channel-decomposition width (1 on a single device)
+  int A = 1;            // channel-decomposition width: each worker is a Group of A devices
   bool chain = true;
   bool normalize = true;
   bool plain = false;   // reconstruct_series_plain semantics (strictly sequential)
@@ -35,7 +36,8 @@ struct SeriesFrameOut {
 class Series {
  public:
   // devices: worker t runs on devices[t % devices.size()] (default: the primary's
-  // device). With several devices the series store stays on the primary's device and
+  // device); with channel decomposition (SeriesOptions::A > 1) worker t is a Group
+  // over devices[(t*A + k) % devices.size()], k < A (hybrid T x A split). With several devices the series store stays on the primary's device and
   // frames, PSFs and estimates move peer to peer (NVLink / NVSwitch, UVA copies):
   // temporal decomposition across GPUs inside one process, the reference's
   // thread-per-compute-worker model.
@@ -68,12 +70,14 @@ class Series {
   float2* estimate_dev(int n) { return ests_ + static_cast<size_t>(n) * D_; }
 
  private:
-  Engine& worker(int t);
+  FrameWorker& worker(int t);
   void run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& ledger, SeriesFrameOut& out,
                  cudaEvent_t ready);
 
   Engine& eng0_;
   std::vector<std::unique_ptr<Engine>> extra_;
+  std::vector<std::unique_ptr<Group>> groups_;
+  int A_ = 1;  // width of the current run's workers
   std::vector<int> devices_;
   int F_ = 0, n_psf_ = 0, D_ = 0;
   size_t zsz_ = 0, psz_ = 0, isz_ = 0;
