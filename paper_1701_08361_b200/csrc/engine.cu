@@ -104,7 +104,6 @@ struct Registry {
   std::vector<Engine::Ops> ops;
   std::vector<std::pair<int, void (*)()>> attrs;  // per G, run once per device
   std::vector<std::vector<int>> attrs_done;       // [device] -> list of G
-  bool tw_done[64] = {};
   std::vector<std::pair<std::pair<int, int>, float2*>> twG;  // (device, G) -> table
   std::vector<std::pair<std::pair<int, int>, double2*>> twD;  // (device, n*sign) -> direct table
 };
@@ -131,17 +130,6 @@ const Engine::Ops* ops_for(int G, int dev) {
   }
   if (!found) return nullptr;
   if (dev < 0 || dev >= 64) fail(2, "device index out of range");
-  if (!r.tw_done[dev]) {
-    float2 tw[528];
-    for (int n = 1; n <= 32; ++n) {
-      for (int k = 0; k < n; ++k) {
-        const double a = -2.0 * std::numbers::pi * k / n;
-        tw[small_tw_offset(n) + k] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
-      }
-    }
-    check_cuda(cudaMemcpyToSymbol(c_small_tw, tw, sizeof(tw)), "upload small twiddles");
-    r.tw_done[dev] = true;
-  }
   if (r.attrs_done.size() <= static_cast<size_t>(dev)) r.attrs_done.resize(dev + 1);
   bool done = false;
   for (int g : r.attrs_done[dev]) done = done || g == G;

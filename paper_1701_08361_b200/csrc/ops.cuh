@@ -3,6 +3,7 @@
 // compiled in parallel translation units).
 #pragma once
 
+#include <cmath>
 #include <cstdlib>
 #include <utility>
 #include <vector>
@@ -54,6 +55,17 @@ void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStre
   check_cuda(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "launch");
 }
 
+inline void upload_small_twiddles() {
+  float2 tw[528];
+  for (int n = 1; n <= 32; ++n) {
+    for (int k = 0; k < n; ++k) {
+      const double a = -2.0 * 3.14159265358979323846 * k / n;
+      tw[small_tw_offset(n) + k] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+    }
+  }
+  check_cuda(cudaMemcpyToSymbol(c_small_tw, tw, sizeof(tw)), "upload small twiddles");
+}
+
 template <int N1, int N2>
 struct Inst {
   // 16 lines per block, 32 when that keeps the block a whole number of warps
@@ -65,6 +77,9 @@ struct Inst {
   static constexpr size_t kSmem2 = sizeof(float2) * (Geo::SMEM_FLOAT2 + kLpb * (N1 * N2 / 2));
 
   static void set_attrs() {
+    // c_small_tw is a per-translation-unit __constant__ (no relocatable device code):
+    // every instantiation unit uploads its own copy on the current device
+    upload_small_twiddles();
     const int s = static_cast<int>(kSmem);
     check_cuda(cudaFuncSetAttribute(k_colA<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colA");
     check_cuda(cudaFuncSetAttribute(k_rows1<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr rows1");
