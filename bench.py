@@ -203,13 +203,12 @@ def profile_traffic(kernel, cfg):
 
 
 def launches_per_frame(caps, M):
-    """kernels one frame launches (engine.cu enqueue order): per step 1 step_begin +
-    2 decode + 4 setup passes + 5 priming-apply + 1 prime + cap x_r updates + (cap-1)
-    x (5 apply + 1 p/ap update) + 1 axpy; then 2 decode + 1 image"""
+    """kernels one frame launches (engine.cu enqueue order, fused CR): per step 1
+    step_begin + 2 decode + 4 setup passes + cap x (5 apply passes + 1 fused CR
+    recurrence) + 1 axpy; then 2 decode + 1 image"""
     n = 0
     for m in range(M):
-        cap = caps[m]
-        n += 1 + 2 + 4 + (5 + 1 + cap + (cap - 1) * 6 if cap >= 1 else 0) + 1
+        n += 1 + 2 + 4 + 6 * caps[m] + 1
     return n + 3
 
 

@@ -722,11 +722,13 @@ void Engine::frame_image(float2* img_dst, float image_scale, bool apply_scale) {
 
 void Engine::frame_all(float2* img_dst, float image_scale, bool apply_scale) {
   if (!budget_mode()) fail(2, "frame_all: whole-frame graphs need the CG iteration budget mode");
-  float2* img = img_dst ? img_dst : img_;
+  // the graph always writes the engine's own image buffer (a per-frame destination
+  // would force a re-capture per frame); a D2D copy delivers it
+  float2* img = img_;
   if (!use_graphs_) {
     frame_begin();
     for (int m = 0; m < plan_.newton_steps; ++m) frame_step(m, nullptr);
-    frame_image(img, image_scale, apply_scale);
+    frame_image(img_dst ? img_dst : img_, image_scale, apply_scale);
     return;
   }
   if (frame_graph_ && (frame_graph_img_ != img || frame_graph_scale_ != image_scale ||
@@ -751,6 +753,9 @@ void Engine::frame_all(float2* img_dst, float image_scale, bool apply_scale) {
     frame_graph_apply_ = apply_scale;
   }
   check_cuda(cudaGraphLaunch(frame_graph_, s_), "graph launch");
+  if (img_dst && img_dst != img_) {
+    check_cuda(cudaMemcpyAsync(img_dst, img_, sizeof(float2) * plan_.N * plan_.N, cudaMemcpyDefault, s_), "image");
+  }
 }
 
 bool Engine::frame_verify(FrameStats* stats) {

@@ -298,7 +298,7 @@ void Group::frame_image(float2* img_dst, float image_scale, bool apply_scale) {
 void Group::frame_all(float2* img_dst, float image_scale, bool apply_scale) {
   if (!budget_mode()) fail(2, "frame_all: whole-frame graphs need the CG iteration budget mode");
   Engine& e0 = *mem_[0];
-  float2* img = img_dst ? img_dst : e0.img_;
+  float2* img = e0.img_;  // fixed graph destination, copied out below
   auto enqueue = [&] {
     fork();
     each([&](int, Engine& e) { e.enq_state_reset(); });
@@ -307,8 +307,15 @@ void Group::frame_all(float2* img_dst, float image_scale, bool apply_scale) {
     join();
     check_cuda(cudaMemcpyAsync(e0.st_host_, e0.st_, sizeof(DevState), cudaMemcpyDeviceToHost, e0.s_), "state read");
   };
+  auto deliver = [&] {
+    if (img_dst && img_dst != e0.img_) {
+      check_cuda(cudaMemcpyAsync(img_dst, e0.img_, sizeof(float2) * plan_.N * plan_.N, cudaMemcpyDefault, e0.s_),
+                 "image");
+    }
+  };
   if (!use_graphs_) {
     enqueue();
+    deliver();
     return;
   }
   if (frame_graph_ && (frame_graph_img_ != img || frame_graph_scale_ != image_scale ||
@@ -328,6 +335,7 @@ void Group::frame_all(float2* img_dst, float image_scale, bool apply_scale) {
     frame_graph_apply_ = apply_scale;
   }
   check_cuda(cudaGraphLaunch(frame_graph_, e0.s_), "graph launch");
+  deliver();
 }
 
 bool Group::frame_verify(FrameStats* stats) {
