@@ -303,6 +303,41 @@ def cpu_baseline(cfg, z, P, plan):
                       f"oracle shim FFT"}
 
 
+def decompositions(pb, plan, frames, P, U, sched, ngpu):
+    """fps and p50 frame latency of each decomposition over ngpu GPUs (device time,
+    CUDA events spanning every worker stream), plus the autotuner's hybrid pick"""
+    F = frames.shape[0]
+    nvis = pb.load_library().rtn_device_count()
+    s = pb.Series(pb.Context(plan, device=0), F, U, devices=[k % nvis for k in range(ngpu)])
+    s.upload_frames(frames)
+    for k in range(U):
+        s.upload_psf(k, P[k])
+    s.set_psf_index([n % U for n in range(F)])
+    s.normalize()
+    nw, nt = min(6, F // 3), min(16, F - min(6, F // 3))
+
+    def measure(T, A):
+        o = pb.SeriesOptions(T=T, A=A, plain=(T == 1), sched=sched)
+        s.run(o, first=0, count=nw, want_images=False)
+        out = s.run(o, first=nw, count=nt, want_images=False)
+        ms = s.last_span_ms() / nt
+        return {"T": T, "A": A, "frames_per_s": 1000.0 / ms, "ms_per_frame": ms,
+                "p50_latency_ms": statistics.median(float(v) for v in out["gpu_ms"])}
+
+    res = {"gpus": ngpu, "single_gpu_plain": measure(1, 1), "channel": measure(1, min(ngpu, 8)),
+           "temporal": measure(ngpu, 1)}
+    key = (pb.ImagingMode.single_slice, plan.N, pb.frames_bucket(nt), plan.J)
+    db = []
+    for _ in pb.legal_configs(ngpu, a_cap=8):
+        T, A = pb.learn_step(key, db, ngpu, 8)
+        r = measure(T, A)
+        db.append(key + (T, A, r["ms_per_frame"]))
+    T, A = pb.select_config(key, db)
+    res["autotuned_hybrid"] = measure(T, A)
+    res["tuned_space_ms_per_frame"] = {f"T{r[4]}xA{r[5]}": round(r[6], 3) for r in db}
+    return res
+
+
 # ------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------
@@ -315,6 +350,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     ap.add_argument("--T", default="auto",
                     help="frames in flight (temporal decomposition): 1 = plain chain, N, or auto = autotuner")
+    ap.add_argument("--A", default="1", help="channel-group width per frame worker (with --T N)")
     ap.add_argument("--tune-db", default=os.path.join(ROOT, "profiles", "tune_db.tsv"),
                     help="autotuner store (autotune.hpp TuneDb format)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -350,28 +386,31 @@ def main():
     series.normalize()
     sched = pb.TemporalSchedule.for_turns(U)
 
-    def opts_for(T):
-        return pb.SeriesOptions(T=T, plain=T == 1, sched=sched)
+    def opts_for(T, A=1):
+        return pb.SeriesOptions(T=T, A=A, plain=(T == 1), sched=sched)
 
     # warm-up (graph capture happens here)
     series.run(opts_for(1), first=0, count=W, want_images=False)
     tuning = None
     if args.T == "auto":
         # the paper's (T, A) autotuner (autotune.cpp:49-88): learn_step walks the legal
-        # space (one device: A = 1, T = frames in flight on separate streams), each
-        # candidate measured on W frames (device time), then select_config picks the
-        # best recorded configuration for this protocol key
+        # hybrid space T x A <= 6 (T frames in flight, each a channel group of A members
+        # on separate streams of this device), each candidate measured on NTUNE frames
+        # (device time), then select_config picks the best recorded configuration for
+        # this protocol key
         key = (pb.ImagingMode.single_slice, plan.N, pb.frames_bucket(S), J)
         db = []
-        space = [c for c in pb.legal_configs(6, a_cap=1)]
+        space = [c for c in pb.legal_configs(6, a_cap=4)]
         for _ in space:
-            T_try, A_try = pb.learn_step(key, db, 6, 1)
-            series.run(opts_for(T_try), first=W, count=NTUNE, want_images=False)
+            T_try, A_try = pb.learn_step(key, db, 6, 4)
+            series.run(opts_for(T_try, A_try), first=W, count=2, want_images=False)  # graph capture
+            series.run(opts_for(T_try, A_try), first=W, count=NTUNE, want_images=False)
             ms = series.last_span_ms() / NTUNE
             db.append(key + (T_try, A_try, ms))
-        T_sel, _ = pb.select_config(key, db)
+        T_sel, A_sel = pb.select_config(key, db)
         tuning = {"key": {"mode": "single_slice", "N": plan.N, "bucket": pb.frames_bucket(S), "J": J},
-                  "measured_ms_per_frame": {f"T{r[4]}": round(r[6], 3) for r in db}, "selected_T": T_sel}
+                  "measured_ms_per_frame": {f"T{r[4]}xA{r[5]}": round(r[6], 3) for r in db},
+                  "selected": {"T": T_sel, "A": A_sel}}
         if rank == 0 and args.tune_db:
             try:
                 tdb = pb.TuneDb(args.tune_db)
@@ -379,11 +418,11 @@ def main():
                     tdb.append(r[:6], r[6], int(time.time()))
             except Exception:
                 pass
-        T = T_sel
-        series.run(opts_for(T), first=W, count=NTUNE, want_images=False)  # warm the selected config
+        T, A = T_sel, A_sel
+        series.run(opts_for(T, A), first=W, count=NTUNE, want_images=False)  # warm the selected config
     else:
-        T = int(args.T)
-    opts = opts_for(T)
+        T, A = int(args.T), int(args.A)
+    opts = opts_for(T, A)
     barrier(world, local)
     with ClockSampler(local) as clk:
         out = series.run(opts, first=W + NTUNE, count=S, want_images=False)
@@ -436,6 +475,20 @@ def main():
                           "achieved_gbs": app_by / (app_ms / 1000.0) / 1e9},
                 "kernels": kern}
 
+    decomp = None
+    if world > 1:
+        # the paper's decompositions across the GPUs of this node, driven from rank 0 in
+        # one process (the reference's thread-per-worker model): channel groups over
+        # NVLink peer memory, temporal decomposition, and the autotuned hybrid. The other
+        # ranks hold their GPUs idle meanwhile.
+        barrier(world, local)
+        if rank == 0:
+            try:
+                decomp = decompositions(pb, plan, frames, P, U, sched, world)
+            except Exception as e:  # reported, never fatal for the headline line
+                decomp = {"error": str(e)}
+        barrier(world, local)
+
     if rank != 0:
         return
     line = {
@@ -445,7 +498,7 @@ def main():
         "data": "synthetic (numpy phantom, coils, exact radial Toeplitz kernel; staged in HBM)",
         "config": {"workload": cfg, "description": desc, "G": G, "N": plan.N, "Gc": plan.Gc, "J": J,
                    "spokes": K, "turns": U, "newton_steps": M, "cg_iter_budget": plan.cg_iter_budget,
-                   "frames_in_flight": T, "temporal_schedule": {"l": sched.l, "o": sched.o},
+                   "frames_in_flight": T, "channel_group": A, "temporal_schedule": {"l": sched.l, "o": sched.o},
                    "per_rank": "independent slice series (multi-slice)",
                    "l2": "inputs larger than L2: every frame has its own 16 MB buffer, "
                          f"{F} frames staged ({F * J * G * G * 8 / 2**20:.0f} MiB)"},
@@ -453,6 +506,8 @@ def main():
         "e2e": e2e, "gpu_launches": launches_per_frame(caps, M) * S, "roofline": roofline, "autotune": tuning,
         "clocks": clk.summary(),
     }
+    if decomp is not None:
+        line["decompositions"] = decomp
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, frames[0] * np.float32(100.0 / math.sqrt(
