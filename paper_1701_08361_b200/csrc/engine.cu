@@ -368,6 +368,7 @@ void Engine::set_psf(const float* P) {
 void Engine::set_data(const float* z) {
   check_cuda(cudaMemcpyAsync(z_, z, sizeof(float2) * plan_.J * plan_.G * plan_.G, cudaMemcpyHostToDevice, s_),
              "data upload");
+  enq_z_scan();
   sync();
 }
 void Engine::set_psf_device(const float2* P) {
@@ -376,6 +377,7 @@ void Engine::set_psf_device(const float2* P) {
 void Engine::set_data_device(const float2* z) {
   check_cuda(cudaMemcpyAsync(z_, z, sizeof(float2) * plan_.J * plan_.G * plan_.G, cudaMemcpyDeviceToDevice, s_),
              "data copy");
+  enq_z_scan();
 }
 
 // ---- enqueue helpers ---------------------------------------------------------
@@ -522,6 +524,12 @@ void Engine::enq_grp_fin(int setup, int op_slot, int cr_slot, float tol) {
 
 void Engine::enq_axpy1() { launch_k(k_axpy1, vec_grid_, kThreads, 0, s_, D_, x_, static_cast<const float2*>(xcg_), static_cast<const DevState*>(st_)); }
 
+void Engine::enq_z_scan() {
+  check_cuda(cudaMemsetAsync(&st_->z_out, 0, sizeof(int), s_), "z scan reset");
+  launch_k(k_z_outside, blocks_for(static_cast<long long>(plan_.J) * plan_.G * plan_.G, 148 * 4), kThreads, 0, s_,
+           dims_, static_cast<const float2*>(z_), st_);
+}
+
 void Engine::enq_state_reset() { check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset"); }
 
 void Engine::enq_coil_ss() {
@@ -539,6 +547,7 @@ void Engine::enq_image_grp(float2* img, float scale, bool apply_scale) {
 void Engine::load_frame(const float2* z, const float2* P) {
   check_cuda(cudaMemcpyAsync(z_, z, sizeof(float2) * plan_.J * plan_.G * plan_.G, cudaMemcpyDefault, s_), "z");
   check_cuda(cudaMemcpyAsync(P_, P, sizeof(float2) * plan_.G * plan_.G, cudaMemcpyDefault, s_), "psf");
+  enq_z_scan();
 }
 void Engine::load_x(const float2* src) {
   check_cuda(cudaMemcpyAsync(x_, src, sizeof(float2) * D_, cudaMemcpyDefault, s_), "x");

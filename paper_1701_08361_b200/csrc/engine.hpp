@@ -195,6 +195,7 @@ class Engine : public FrameWorker {
   void enq_cr_fused(int it, float tol);
   void enq_axpy1();
   void enq_state_reset();
+  void enq_z_scan();  // st->z_out for the data now in z_ (stream ordered)
   void enq_coil_ss();
   void enq_image_grp(float2* img, float scale, bool apply_scale);
   void enq_cr(float alpha, float tol, int cap, bool sync_each);

@@ -170,6 +170,10 @@ void Group::load_frame(const float2* z, const float2* P) {
     check_cuda(cudaMemcpyAsync(e.z_, z + j0 * G2, sizeof(float2) * G2 * e.plan_.J, cudaMemcpyDefault, s), "z split");
     check_cuda(cudaMemcpyAsync(e.P_, P, sizeof(float2) * G2, cudaMemcpyDefault, s), "psf");
   }
+  // each member scans its own block on its stream, ordered after the copies
+  fork();
+  each([&](int, Engine& e) { e.enq_z_scan(); });
+  join();
 }
 
 void Group::load_x(const float2* src) { split_copy(src, false); }
@@ -416,6 +420,8 @@ void Group::set_data(const float* z) {
     check_cuda(cudaSetDevice(e.dev_), "set device");
     check_cuda(cudaMemcpy(e.z_, z + 2 * j0 * G2, sizeof(float2) * G2 * e.plan_.J, cudaMemcpyHostToDevice),
                "data upload");
+    e.enq_z_scan();
+    e.sync();
   }
 }
 

@@ -61,6 +61,8 @@ struct DevState {
   int pad_;
   unsigned int counter;  // last-block reduction ticket
   unsigned int pad2_;
+  int z_out;      // the loaded data has a nonzero sample outside the window (k_z_outside)
+  int pad3_;
   StepRec steps[kMaxSteps];
   double scal[8];        // scratch scalar outputs (op-level calls)
   double gp[4];          // group mode: this member's SETUP partials {|rhs|^2, resid_out, resid_win, -}

@@ -608,7 +608,7 @@ __global__ void RTNB_PASS_BOUNDS k_colsW(Dims d, ColsWArgs a, const float* __res
           sx += t.x;
           sy += t.y;
         }
-      } else if (a.mode == CW_SETUP) {
+      } else if (a.mode == CW_SETUP && st->z_out) {
         for (int j = 0; j < d.J; ++j) {
           const float2 zz = z[(size_t)j * D0 + e];
           const float2 v = cjmul_rn(coils[(size_t)j * D0 + e], zz);
@@ -866,12 +866,13 @@ __global__ void __launch_bounds__(kThreads) k_rho_out(Dims d, const float2* __re
   pdl_enter();
   if (st->status) return;
   const int G = d.G, D0 = G * G;
+  const int zo = st->z_out;
   double acc = 0.0;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < D0; e += gridDim.x * blockDim.x) {
     const int r = e / G, c = e - (e / G) * G;
     if (in_win(d, r, c)) continue;
     double sx = 0.0, sy = 0.0;
-    for (int j = 0; j < d.J; ++j) {
+    for (int j = 0; zo && j < d.J; ++j) {
       const float2 zz = z[(size_t)j * D0 + e];
       const float2 v = cjmul_rn(coils[(size_t)j * D0 + e], zz);
       sx += v.x;
@@ -976,6 +977,26 @@ __global__ void __launch_bounds__(kThreads) k_image_grp(Dims d, const float2* __
     if (apply_scale) v = make_float2(v.x * scale, v.y * scale);
     img[e] = v;
   }
+}
+
+// Does the frame's gridded data have a nonzero sample outside the field-of-view
+// window? grid_adjoint masks it (preproc.cpp:195), so normally not, and then the
+// out-of-window part of rhs.rho (sum_j conj(c_j) z_j, zero there) and of the data
+// residual need not be read in every Newton-step setup. st->z_out is cleared by the
+// caller before the launch.
+__global__ void __launch_bounds__(kThreads) k_z_outside(Dims d, const float2* __restrict__ z, DevState* st) {
+  pdl_enter();
+  const int G = d.G;
+  const long long n = (long long)d.J * G * G;
+  int any = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(i % ((long long)G * G));
+    const int r = e / G, c = e - (e / G) * G;
+    if (in_win(d, r, c)) continue;
+    const float2 v = z[i];
+    any |= (v.x != 0.f || v.y != 0.f);
+  }
+  if (__syncthreads_or(any) && threadIdx.x == 0) st->z_out = 1;
 }
 
 // x += 1.0 * x_cg  (newton_step, nlinv.cpp:281)

@@ -186,6 +186,27 @@ def test_newton_step_matches_reference(gpu, ref, cg_tol, cap):
     assert rel_err(got, want) < 1e-4
 
 
+@pytest.mark.parametrize("group", [False, True])
+def test_newton_step_with_data_outside_the_window(gpu, ref, group):
+    # gridded data that is not window-masked (grid_adjoint masks, the API does not
+    # require it): the out-of-window rhs.rho term sum_j conj(c_j) z_j is live
+    plan = gpu.make_plan(16, 3)
+    plan.newton_steps, plan.cg_iter_budget = 3, 9
+    inp = phantom_frame_inputs(ref, plan, K=7, U=1)
+    z = inp["z"][0] + 0.05 * random_image(plan.G, 5, (plan.J, plan.G, plan.G))
+    P = inp["P"][0]
+    init = gpu.initial_estimate(plan)
+    kw = {"devices": [0, 0]} if group else {}
+    with gpu.Context(plan, **kw) as ctx:
+        ctx.set_psf(P)
+        ctx.set_data(z)
+        fr = ctx.reconstruct_frame(init)
+    img, est, per, _ = ref.reconstruct_frame(plan, z, P, init)
+    assert fr.cg_per_step == per
+    assert rel_err(fr.image, img) < FRAME_TOL
+    assert rel_err(fr.est, est) < FRAME_TOL
+
+
 def test_fixed_point_needs_no_iterations(gpu, ref):
     # test_nlinv.cpp:314-349: data manufactured from x itself leaves x unchanged
     plan = gpu.make_plan(16, 2)
