@@ -88,6 +88,27 @@ int rtn_apply_W_inv(rtn_ctx* ctx, const float* chat /* Gc*Gc */, float* out /* G
 int rtn_apply_W_invH(rtn_ctx* ctx, const float* u /* G*G */, float* out /* Gc*Gc */);
 int rtn_toeplitz_apply(rtn_ctx* ctx, float* x /* G*G, in place, uses the context PSF */);
 
+/* --- preproc.hpp:81-133: the pre stage on the device ----
+ * samples: J*K*S complex64 in KSpaceFrame::samples order [j][k][s]; angles: K
+ * spoke angles (rad); S samples per spoke; delay in samples (frame_coords).
+ * Out-of-range coordinates return 3 (DataError) like check_coord. */
+/* grid_adjoint(frame, plan, delay): density-compensated Kaiser-Bessel gather
+ * (bit-identical float accumulation to spread_sample), centered inverse FFT,
+ * G / deapodization, window mask. z_out: J*G*G. */
+int rtn_grid_adjoint(rtn_ctx* ctx, const float* samples, int J, const double* angles, int K, int S, double delay,
+                     float* z_out);
+/* the gridded k-space of grid_adjoint before its inverse FFT (J*G*G) */
+int rtn_grid_spread(rtn_ctx* ctx, const float* samples, int J, const double* angles, int K, int S, double delay,
+                    float* grid_out);
+/* build_psf(angles, S, plan) and build_psf_coords(coords, weights, plan): P is G*G */
+int rtn_build_psf(rtn_ctx* ctx, const double* angles, int K, int S, float* P_out);
+int rtn_build_psf_coords(rtn_ctx* ctx, const double* coords /* 2n: kx, ky */, const double* weights, int n,
+                         float* P_out);
+/* apply_compression: out (Jv*n) = m (Jv*Jp) x in (Jp*n), FP64 accumulation */
+int rtn_apply_compression(rtn_ctx* ctx, const float* m, int Jv, int Jp, const float* in, int n, float* out);
+/* PsfCache::angle_key (preproc.cpp:301-313) */
+uint64_t rtn_psf_angle_key(const double* angles, int K, int S, int G);
+
 /* --- nlinv.hpp:61-98 ----------------------------------------------------------- */
 /* make_step_cache: linearise at estimate x; optional outputs masked rho (G*G), coils (J*G*G) */
 int rtn_make_step_cache(rtn_ctx* ctx, const float* x, float* rho_out, float* coils_out);

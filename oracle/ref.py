@@ -128,6 +128,35 @@ def build_psf(plan, angles, S):
     return P
 
 
+def grid_spread(plan, samples, angles, delay=0.0):
+    """the density-compensated KB spread of grid_adjoint before its inverse FFT"""
+    samples = _c64(samples)
+    angles = np.ascontiguousarray(angles, np.float64)
+    J, K, S = samples.shape
+    g = np.zeros((J, plan.G, plan.G), np.complex64)
+    _chk(lib().ref_grid_spread(ctypes.byref(plan_c(plan)), _fp(samples), _dp(angles), J, K, S,
+                               ctypes.c_double(delay), _fp(g)))
+    return g
+
+
+def build_psf_coords(plan, coords, weights):
+    coords = np.ascontiguousarray(coords, np.float64)
+    weights = np.ascontiguousarray(weights, np.float64)
+    P = np.zeros((plan.G, plan.G), np.complex64)
+    _chk(lib().ref_build_psf_coords(ctypes.byref(plan_c(plan)), _dp(coords), _dp(weights), len(weights), _fp(P)))
+    return P
+
+
+def calibrate_compression(samples, angles, Jv):
+    samples = _c64(samples)
+    angles = np.ascontiguousarray(angles, np.float64)
+    F, Jp, K, S = samples.shape
+    m = np.zeros((Jv, Jp), np.complex64)
+    energy = ctypes.c_double(0)
+    _chk(lib().ref_calibrate_compression(_fp(samples), _dp(angles), F, Jp, K, S, Jv, _fp(m), ctypes.byref(energy)))
+    return m, energy.value
+
+
 def compress_series(samples, angles, Jv, ncal):
     samples = _c64(samples)
     angles = np.ascontiguousarray(angles, np.float64)

@@ -17,6 +17,7 @@
 // chat[j] (Gc*Gc each), the order of test_nlinv.cpp:70-79 (est_flatten).
 // Status codes follow the CLI mapping (rtnlinv_main.cpp:381-391): 0 ok, 2 UsageError,
 // 3 DataError, 4 SolverError / DecompFault, 5 other.
+#include <array>
 #include <complex>
 #include <cstdint>
 #include <cstring>
@@ -235,6 +236,54 @@ int ref_build_psf(const ref_plan_t* p, const double* angles, int K, int S, float
     const ReconPlan plan = to_plan(p);
     std::vector<double> a(angles, angles + K);
     store_img(build_psf(a, S, plan).P, P_out);
+  });
+}
+
+// the density-compensated Kaiser-Bessel spread of grid_adjoint before its inverse
+// FFT (preproc.cpp:180-192, spread_sample preproc.cpp:120-133), per channel
+int ref_grid_spread(const ref_plan_t* p, const float* samples, const double* angles, int J, int K, int S,
+                    double delay, float* grid_out) {
+  return guarded([&] {
+    const ReconPlan plan = to_plan(p);
+    const KSpaceFrame fr = load_frame(samples, angles, J, K, S, 0);
+    const auto coords = frame_coords(fr, delay);
+    const int G = plan.G;
+    for (int j = 0; j < J; ++j) {
+      CImage g(G);
+      size_t s = 0;
+      for (int k = 0; k < K; ++k) {
+        for (int i = 0; i < S; ++i, ++s) {
+          const double v = dcf_ramp(coords[s][0], coords[s][1], K, S, G);
+          spread_sample(g, coords[s][0], coords[s][1], fr.at(j, k, i) * static_cast<float>(v));
+        }
+      }
+      store_img(g, grid_out + static_cast<size_t>(j) * G * G * 2);
+    }
+  });
+}
+
+int ref_build_psf_coords(const ref_plan_t* p, const double* coords, const double* weights, int n, float* P_out) {
+  return guarded([&] {
+    const ReconPlan plan = to_plan(p);
+    std::vector<std::array<double, 2>> c(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) c[static_cast<size_t>(i)] = {coords[2 * i], coords[2 * i + 1]};
+    std::vector<double> w(weights, weights + n);
+    store_img(build_psf_coords(c, w, plan).P, P_out);
+  });
+}
+
+// calibrate_compression (preproc.cpp:390-444) on F frames: the Jv x Jp matrix
+int ref_calibrate_compression(const float* samples_in, const double* angles, int F, int Jp, int K, int S, int Jv,
+                              float* m_out, double* energy) {
+  return guarded([&] {
+    std::vector<KSpaceFrame> frames;
+    const size_t per_in = static_cast<size_t>(Jp) * K * S * 2;
+    for (int n = 0; n < F; ++n) {
+      frames.push_back(load_frame(samples_in + n * per_in, angles + static_cast<size_t>(n) * K, Jp, K, S, n));
+    }
+    const CompressionMatrix cm = calibrate_compression(frames, Jv);
+    if (energy) *energy = cm.energy_fraction;
+    std::memcpy(m_out, cm.m.data(), sizeof(cfloat) * cm.m.size());
   });
 }
 

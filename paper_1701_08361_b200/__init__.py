@@ -134,6 +134,12 @@ def load_library(path: str = LIB_PATH):
         "rtn_ctx_create_group": ([ctypes.POINTER(_Plan), i, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
                                  ctypes.c_int),
         "rtn_ctx_group_blocks": ([vp, i], ctypes.c_int),
+        "rtn_grid_adjoint": ([vp, f, ctypes.c_int, d, ctypes.c_int, ctypes.c_int, ctypes.c_double, f], ctypes.c_int),
+        "rtn_grid_spread": ([vp, f, ctypes.c_int, d, ctypes.c_int, ctypes.c_int, ctypes.c_double, f], ctypes.c_int),
+        "rtn_build_psf": ([vp, d, ctypes.c_int, ctypes.c_int, f], ctypes.c_int),
+        "rtn_build_psf_coords": ([vp, d, d, ctypes.c_int, f], ctypes.c_int),
+        "rtn_apply_compression": ([vp, f, ctypes.c_int, ctypes.c_int, f, ctypes.c_int, f], ctypes.c_int),
+        "rtn_psf_angle_key": ([d, ctypes.c_int, ctypes.c_int, ctypes.c_int], ctypes.c_uint64),
         "rtn_fft2": ([f, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "rtn_fft_set_ctx": ([ctypes.c_int], None),
         "rtn_fft_get_ctx": ([], ctypes.c_int),
@@ -432,6 +438,64 @@ class Context:
         cg = [per[m] for m in range(self.plan.newton_steps)]
         return FrameResult(img, est, cg, sum(cg), secs.value)
 
+    # ---- pre stage (preproc.hpp:81-133), on the device ---------------------------------
+    def _frame(self, samples, angles):
+        samples = np.ascontiguousarray(samples, np.complex64)
+        if samples.ndim != 3:
+            raise UsageError("samples must be J x K x S")
+        angles = np.ascontiguousarray(angles, np.float64)
+        if angles.shape != (samples.shape[1],):
+            raise UsageError("one angle per spoke")
+        return samples, angles
+
+    def grid_adjoint(self, samples, angles, delay: float = 0.0):
+        """grid_adjoint(frame, plan, delay): J x G x G gridded, window-masked data"""
+        samples, angles = self._frame(samples, angles)
+        J, K, S = samples.shape
+        z = np.zeros((J, self.plan.G, self.plan.G), np.complex64)
+        _check(self.lib.rtn_grid_adjoint(self._h, _fp(samples), J, angles.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                         K, S, delay, _fp(z)))
+        return z
+
+    def grid_spread(self, samples, angles, delay: float = 0.0):
+        """the density-compensated KB spread of grid_adjoint, before its inverse FFT"""
+        samples, angles = self._frame(samples, angles)
+        J, K, S = samples.shape
+        g = np.zeros((J, self.plan.G, self.plan.G), np.complex64)
+        _check(self.lib.rtn_grid_spread(self._h, _fp(samples), J, angles.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                        K, S, delay, _fp(g)))
+        return g
+
+    def build_psf(self, angles, S: int):
+        angles = np.ascontiguousarray(angles, np.float64)
+        P = np.zeros((self.plan.G, self.plan.G), np.complex64)
+        _check(self.lib.rtn_build_psf(self._h, angles.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(angles),
+                                      S, _fp(P)))
+        return P
+
+    def build_psf_coords(self, coords, weights):
+        coords = np.ascontiguousarray(coords, np.float64).reshape(-1, 2)
+        weights = np.ascontiguousarray(weights, np.float64)
+        if len(weights) != len(coords):
+            raise UsageError("build_psf_coords: coordinate/weight count mismatch")
+        P = np.zeros((self.plan.G, self.plan.G), np.complex64)
+        dp = ctypes.POINTER(ctypes.c_double)
+        _check(self.lib.rtn_build_psf_coords(self._h, coords.ctypes.data_as(dp), weights.ctypes.data_as(dp),
+                                             len(weights), _fp(P)))
+        return P
+
+    def apply_compression(self, m, samples):
+        """samples (Jp, ...) -> (Jv, ...) with the Jv x Jp matrix m"""
+        m = np.ascontiguousarray(m, np.complex64)
+        samples = np.ascontiguousarray(samples, np.complex64)
+        Jv, Jp = m.shape
+        if samples.shape[0] != Jp:
+            raise DataError("apply_compression: channel count does not match matrix")
+        n = samples[0].size
+        out = np.zeros((Jv,) + samples.shape[1:], np.complex64)
+        _check(self.lib.rtn_apply_compression(self._h, _fp(m), Jv, Jp, _fp(samples), n, _fp(out)))
+        return out
+
     def time_kernel(self, which: str, reps: int = 20):
         """(average ms per launch, algorithmic bytes per launch) of one kernel class"""
         ms = ctypes.c_double(0)
@@ -592,6 +656,12 @@ def reconstruct_series(ctx: Context, z, P, opts: SeriesOptions, psf_index=None):
         return out
     finally:
         s.close()
+
+
+def psf_angle_key(angles, S: int, G: int) -> int:
+    """PsfCache::angle_key (preproc.cpp:301-313)"""
+    a = np.ascontiguousarray(angles, np.float64)
+    return int(load_library().rtn_psf_angle_key(a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(a), S, G))
 
 
 def partition_channels(J: int, A: int, cap: int = 4):

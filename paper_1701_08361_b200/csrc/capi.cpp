@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <memory>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -9,12 +10,14 @@
 #include "../../include/rtnlinv_b200.h"
 #include "engine.hpp"
 #include "group.hpp"
+#include "preproc.hpp"
 #include "sched.hpp"
 #include "series.hpp"
 
 struct rtn_ctx {
   rtnb::Engine* eng = nullptr;
   rtnb::Group* grp = nullptr;  // channel-decomposed context (rtn_ctx_create_group)
+  std::unique_ptr<rtnb::Preproc> pre;  // pre stage, created on first use
 };
 
 namespace {
@@ -122,8 +125,57 @@ int rtn_ctx_group_blocks(rtn_ctx* ctx, int* out_pairs) {
   });
 }
 
+static rtnb::Preproc& pre(rtn_ctx* c) {
+  if (!c || (!c->eng && !c->grp)) rtnb::fail(2, "null context");
+  if (!c->pre) {
+    if (c->grp) {
+      c->pre = std::make_unique<rtnb::Preproc>(c->grp->plan(), c->grp->device());
+    } else {
+      c->pre = std::make_unique<rtnb::Preproc>(c->eng->plan(), c->eng->device());
+    }
+  }
+  return *c->pre;
+}
+
+int rtn_grid_adjoint(rtn_ctx* ctx, const float* samples, int J, const double* angles, int K, int S, double delay,
+                     float* z_out) {
+  return guarded([&] {
+    if (!samples || !angles || !z_out) rtnb::fail(2, "grid_adjoint: null buffer");
+    pre(ctx).grid_adjoint_host(samples, J, angles, K, S, delay, z_out, false);
+  });
+}
+int rtn_grid_spread(rtn_ctx* ctx, const float* samples, int J, const double* angles, int K, int S, double delay,
+                    float* grid_out) {
+  return guarded([&] {
+    if (!samples || !angles || !grid_out) rtnb::fail(2, "grid_spread: null buffer");
+    pre(ctx).grid_adjoint_host(samples, J, angles, K, S, delay, grid_out, true);
+  });
+}
+int rtn_build_psf(rtn_ctx* ctx, const double* angles, int K, int S, float* P_out) {
+  return guarded([&] {
+    if (!angles || !P_out || K < 1 || S < 1) rtnb::fail(2, "build_psf: bad arguments");
+    pre(ctx).build_psf_host(angles, K, S, P_out);
+  });
+}
+int rtn_build_psf_coords(rtn_ctx* ctx, const double* coords, const double* weights, int n, float* P_out) {
+  return guarded([&] {
+    if (!coords || !weights || !P_out || n < 1) rtnb::fail(2, "build_psf_coords: bad arguments");
+    pre(ctx).build_psf_coords_host(coords, weights, n, P_out);
+  });
+}
+int rtn_apply_compression(rtn_ctx* ctx, const float* m, int Jv, int Jp, const float* in, int n, float* out) {
+  return guarded([&] {
+    if (!m || !in || !out || n < 0) rtnb::fail(2, "apply_compression: bad arguments");
+    pre(ctx).apply_compression_host(m, Jv, Jp, in, n, out);
+  });
+}
+uint64_t rtn_psf_angle_key(const double* angles, int K, int S, int G) {
+  return rtnb::psf_angle_key(angles, K, S, G);
+}
+
 void rtn_ctx_destroy(rtn_ctx* ctx) {
   if (!ctx) return;
+  ctx->pre.reset();
   delete ctx->grp;
   delete ctx->eng;
   delete ctx;
