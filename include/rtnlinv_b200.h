@@ -162,6 +162,17 @@ int rtn_series_normalize(rtn_series* s, double* data_scale);
  * count, gpu_ms count (frame start -> image ready). */
 int rtn_series_run(rtn_series* s, const rtn_series_opts_t* opts, int first, int count, const float* z_host,
                    float* images, int* audit, uint64_t* seqs, int* cg_iters, float* gpu_ms);
+/* the same series run fed with raw acquisitions (KSpaceFrame per frame,
+ * seqsim.hpp:52-65): samples count*Jp*K*S complex64, angles count*K. The pre stage
+ * runs on the device on the copy stream: optional coil compression (cmat: J*Jp
+ * complex64 apply_compression matrix, NULL when Jp == J), grid_adjoint into the
+ * series store, PSFs built once per distinct angle set (PsfCache semantics, at
+ * most n_psf of them), prep_series normalisation. */
+int rtn_series_run_raw(rtn_series* s, const rtn_series_opts_t* opts, int first, int count, const float* samples,
+                       const double* angles, int K, int S, double delay, const float* cmat, int Jp, float* images,
+                       int* audit, uint64_t* seqs, int* cg_iters, float* gpu_ms);
+/* distinct PSFs built by rtn_series_run_raw so far */
+int rtn_series_psf_cache_size(rtn_series* s);
 int rtn_series_images(rtn_series* s, int first, int count, float* images);
 /* device time (ms) of the last rtn_series_run: CUDA events spanning all worker streams */
 float rtn_series_last_span_ms(rtn_series* s);

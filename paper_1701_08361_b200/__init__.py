@@ -167,6 +167,10 @@ def load_library(path: str = LIB_PATH):
         "rtn_series_run": ([vp, ctypes.POINTER(_SeriesOpts), ctypes.c_int, ctypes.c_int, vp, vp, i,
                             ctypes.POINTER(ctypes.c_uint64), i, f], ctypes.c_int),
         "rtn_series_images": ([vp, ctypes.c_int, ctypes.c_int, f], ctypes.c_int),
+        "rtn_series_run_raw": ([vp, ctypes.POINTER(_SeriesOpts), ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int,
+                                ctypes.c_int, ctypes.c_double, vp, ctypes.c_int, vp, i,
+                                ctypes.POINTER(ctypes.c_uint64), i, f], ctypes.c_int),
+        "rtn_series_psf_cache_size": ([vp], ctypes.c_int),
         "rtn_series_estimate": ([vp, ctypes.c_int, f], ctypes.c_int),
         "rtn_series_last_span_ms": ([vp], ctypes.c_float),
         "rtn_partition_channels": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, i], ctypes.c_int),
@@ -596,7 +600,10 @@ class Series:
         return v.value
 
     def run(self, opts: SeriesOptions, first: int = 0, count: Optional[int] = None, z_host=None,
-            want_images: bool = True, z_host_ptr: Optional[int] = None, images_ptr: Optional[int] = None):
+            want_images: bool = True, z_host_ptr: Optional[int] = None, images_ptr: Optional[int] = None,
+            raw: Optional[dict] = None):
+        """raw = dict(samples=(count, Jp, K, S) complex64 or samples_ptr=int, angles=(count, K),
+        delay=0.0, cmat=(J, Jp) or None): raw acquisitions through the device pre stage"""
         p = self.ctx.plan
         count = self.F - first if count is None else count
         M = p.newton_steps
@@ -613,13 +620,38 @@ class Series:
             zp = z_host.ctypes.data
         ip = images_ptr if images_ptr is not None else (None if images is None else images.ctypes.data)
         o = opts.to_c()
-        _check(self.lib.rtn_series_run(self._h, ctypes.byref(o), first, count, zp, ip,
-                                       audit.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
-                                       seqs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
-                                       cg.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _fp(ms)))
+        outs = (audit.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), seqs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                cg.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _fp(ms))
+        if raw is not None:
+            ang = np.ascontiguousarray(raw["angles"], np.float64)
+            K = ang.shape[-1]
+            cm = raw.get("cmat")
+            keep = [ang]
+            if "samples_ptr" in raw:
+                sp, S, Jp = raw["samples_ptr"], raw["S"], raw.get("Jp", p.J)
+            else:
+                smp = _c64(raw["samples"])
+                keep.append(smp)
+                sp, Jp, S = smp.ctypes.data, smp.shape[1], smp.shape[-1]
+                if smp.shape[0] != count or smp.shape[2] != K:
+                    raise UsageError("raw samples must be (count, Jp, K, S) with K = angles per frame")
+            cmp = None
+            if cm is not None:
+                cm = np.ascontiguousarray(cm, np.complex64)
+                keep.append(cm)
+                cmp = cm.ctypes.data
+            elif Jp != p.J:
+                raise UsageError("raw samples have Jp != J channels and no compression matrix")
+            _check(self.lib.rtn_series_run_raw(self._h, ctypes.byref(o), first, count, sp, ang.ctypes.data, K, S,
+                                               float(raw.get("delay", 0.0)), cmp, Jp, ip, *outs))
+        else:
+            _check(self.lib.rtn_series_run(self._h, ctypes.byref(o), first, count, zp, ip, *outs))
         audits = [FrameAudit(int(r[0]), int(r[1]), int(r[2]), int(r[3]), int(r[4]), [int(v) for v in r[5:]],
                              int(q[0]), int(q[1]), int(q[2])) for r, q in zip(audit, seqs)]
         return dict(images=images, audit=audits, cg_iters=cg, gpu_ms=ms)
+
+    def psf_cache_size(self) -> int:
+        return int(self.lib.rtn_series_psf_cache_size(self._h))
 
     def last_span_ms(self) -> float:
         """device time of the last run (CUDA events across all worker streams)"""

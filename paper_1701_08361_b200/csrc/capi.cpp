@@ -363,9 +363,11 @@ int rtn_series_normalize(rtn_series* s, double* scale) {
   });
 }
 
-int rtn_series_run(rtn_series* s, const rtn_series_opts_t* o, int first, int count, const float* z_host,
-                   float* images, int* audit, uint64_t* seqs, int* cg_iters, float* gpu_ms) {
+static int series_run_impl(rtn_series* s, const rtn_series_opts_t* o, int first, int count, const float* z_host,
+                           const rtnb::RawInput* raw, float* images, int* audit, uint64_t* seqs, int* cg_iters,
+                           float* gpu_ms) {
   return guarded([&] {
+    if (!o) rtnb::fail(2, "reconstruct_series: null options");
     rtnb::SeriesOptions so;
     so.T = o->T;
     so.A = o->A;
@@ -374,7 +376,7 @@ int rtn_series_run(rtn_series* s, const rtn_series_opts_t* o, int first, int cou
     so.normalize = o->normalize != 0;
     so.plain = o->plain != 0;
     std::vector<rtnb::SeriesFrameOut> out;
-    ser(s).run(so, first, count, z_host, images, &out);
+    ser(s).run(so, first, count, z_host, images, &out, raw);
     const int M = s->ctx->eng->plan().newton_steps;
     for (int k = 0; k < count; ++k) {
       const rtnb::SeriesFrameOut& f = out[static_cast<size_t>(k)];
@@ -397,6 +399,27 @@ int rtn_series_run(rtn_series* s, const rtn_series_opts_t* o, int first, int cou
     }
   });
 }
+
+int rtn_series_run(rtn_series* s, const rtn_series_opts_t* o, int first, int count, const float* z_host,
+                   float* images, int* audit, uint64_t* seqs, int* cg_iters, float* gpu_ms) {
+  return series_run_impl(s, o, first, count, z_host, nullptr, images, audit, seqs, cg_iters, gpu_ms);
+}
+
+int rtn_series_run_raw(rtn_series* s, const rtn_series_opts_t* o, int first, int count, const float* samples,
+                       const double* angles, int K, int S, double delay, const float* cmat, int Jp, float* images,
+                       int* audit, uint64_t* seqs, int* cg_iters, float* gpu_ms) {
+  rtnb::RawInput raw;
+  raw.samples = samples;
+  raw.angles = angles;
+  raw.K = K;
+  raw.S = S;
+  raw.Jp = Jp;
+  raw.delay = delay;
+  raw.cmat = cmat;
+  return series_run_impl(s, o, first, count, nullptr, &raw, images, audit, seqs, cg_iters, gpu_ms);
+}
+
+int rtn_series_psf_cache_size(rtn_series* s) { return (s && s->s) ? s->s->psf_cache_size() : 0; }
 
 int rtn_series_images(rtn_series* s, int first, int count, float* images) {
   return guarded([&] {

@@ -90,6 +90,10 @@ Series::Series(Engine& primary, int frames, int n_psf, std::vector<int> devices)
 
 Series::~Series() {
   cudaSetDevice(eng0_.device());
+  if (copy_) cudaStreamSynchronize(copy_);
+  pre_.reset();
+  if (raw_) cudaFree(raw_);
+  if (raw_c_) cudaFree(raw_c_);
   for (void* b : {static_cast<void*>(z_), static_cast<void*>(psf_), static_cast<void*>(ests_),
                   static_cast<void*>(unity_), static_cast<void*>(images_), static_cast<void*>(nsq_)}) {
     if (b) cudaFree(b);
@@ -269,8 +273,100 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   ledger.mark_complete(n);
 }
 
+void Series::produce_frames(const SeriesOptions& o, int first, int count, const float* z_host,
+                            const RawInput* raw, std::vector<cudaEvent_t>& ready) {
+  const Plan& p = eng0_.plan();
+  const size_t nsamp = raw ? static_cast<size_t>(raw->K) * raw->S : 0;
+  if (raw) {
+    if (!raw->samples || !raw->angles || raw->K < 1 || raw->S < 1) fail(2, "reconstruct_series: empty raw input");
+    const int Jp = raw->cmat ? raw->Jp : p.J;
+    if (raw->cmat && Jp < p.J) fail(2, "reconstruct_series: fewer physical than virtual channels");
+    if (!pre_) pre_ = std::make_unique<Preproc>(p, eng0_.device());
+    const size_t need = static_cast<size_t>(count) * Jp * nsamp;
+    if (need > raw_cap_) {
+      if (raw_) cudaFree(raw_);
+      check_cuda(cudaMalloc(&raw_, sizeof(float2) * need), "raw staging");
+      raw_cap_ = need;
+    }
+    if (raw->cmat) {
+      const size_t needc = static_cast<size_t>(p.J) * nsamp * count + static_cast<size_t>(p.J) * Jp;
+      if (needc > raw_c_cap_) {
+        if (raw_c_) cudaFree(raw_c_);
+        check_cuda(cudaMalloc(&raw_c_, sizeof(float2) * needc), "compression staging");
+        raw_c_cap_ = needc;
+      }
+      check_cuda(cudaMemcpyAsync(raw_c_, raw->cmat, sizeof(float2) * p.J * Jp, cudaMemcpyHostToDevice, copy_),
+                 "compression matrix");
+    }
+  }
+  // frame k of the call into store slot first + k, on the copy stream
+  auto produce = [&](int k) {
+    const int n = first + k;
+    float2* zn = z_ + zsz_ * n;
+    if (!raw) {
+      check_cuda(cudaMemcpyAsync(zn, z_host + 2 * zsz_ * k, sizeof(float2) * zsz_, cudaMemcpyHostToDevice, copy_),
+                 "frame upload");
+      return;
+    }
+    const int Jp = raw->cmat ? raw->Jp : p.J;
+    float2* smp = raw_ + static_cast<size_t>(k) * Jp * nsamp;
+    check_cuda(cudaMemcpyAsync(smp, raw->samples + 2 * static_cast<size_t>(k) * Jp * nsamp,
+                               sizeof(float2) * Jp * nsamp, cudaMemcpyHostToDevice, copy_),
+               "raw upload");
+    if (raw->cmat) {
+      float2* cs = raw_c_ + static_cast<size_t>(p.J) * Jp + static_cast<size_t>(k) * p.J * nsamp;
+      pre_->apply_compression(raw_c_, p.J, Jp, smp, static_cast<int>(nsamp), cs, copy_);
+      smp = cs;
+    }
+    const double* ang = raw->angles + static_cast<size_t>(k) * raw->K;
+    pre_->grid_adjoint(smp, p.J, ang, raw->K, raw->S, raw->delay, zn, copy_);
+    // PsfCache::get (preproc.cpp:315-332): one PSF per distinct angle set
+    const uint64_t key = psf_angle_key(ang, raw->K, raw->S, p.G);
+    int slot = -1;
+    for (size_t i = 0; i < psf_keys_.size(); ++i) {
+      if (psf_keys_[i] == key) slot = static_cast<int>(i);
+    }
+    if (slot < 0) {
+      if (static_cast<int>(psf_keys_.size()) >= n_psf_) {
+        fail(2, "reconstruct_series: more distinct spoke-angle sets than PSF slots");
+      }
+      slot = static_cast<int>(psf_keys_.size());
+      pre_->build_psf(ang, raw->K, raw->S, psf_ + psz_ * slot, copy_);
+      psf_keys_.push_back(key);
+    }
+    psf_idx_[static_cast<size_t>(n)] = slot;
+  };
+  ready.resize(static_cast<size_t>(count));
+  check_cuda(cudaSetDevice(eng0_.device()), "set device");
+  if (first == 0) {
+    produce(0);
+    normalized_ = false;
+    if (o.normalize) {
+      k_nrm2_frame<<<1, 256, 0, copy_>>>(z_, static_cast<long long>(zsz_), nsq_);
+      double nsq = 0;
+      check_cuda(cudaMemcpyAsync(&nsq, nsq_, sizeof(double), cudaMemcpyDeviceToHost, copy_), "nsq");
+      check_cuda(cudaStreamSynchronize(copy_), "nsq");
+      scale_ = nsq > 0 ? 100.0 / std::sqrt(nsq) : 1.0;
+    } else {
+      scale_ = 1.0;
+    }
+  }
+  for (int k = 0; k < count; ++k) {
+    const int n = first + k;
+    if (!(n == 0 && first == 0)) produce(k);
+    if (o.normalize && scale_ != 1.0) {
+      k_scale_frames<<<148 * 2, 256, 0, copy_>>>(z_ + zsz_ * n, static_cast<long long>(zsz_),
+                                                 static_cast<float>(scale_));
+    }
+    check_cuda(cudaEventCreateWithFlags(&ready[static_cast<size_t>(k)], cudaEventDisableTiming), "event");
+    check_cuda(cudaEventRecord(ready[static_cast<size_t>(k)], copy_), "event");
+  }
+  normalized_ = true;
+}
+
 void Series::run(const SeriesOptions& o, int first, int count, const float* z_host, float* images_host,
-                 std::vector<SeriesFrameOut>* out) {
+                 std::vector<SeriesFrameOut>* out, const RawInput* raw) {
+  if (z_host && raw) fail(2, "reconstruct_series: gridded and raw input are exclusive");
   if (first < 0 || count < 1 || first + count > F_) fail(2, "reconstruct_series: frame range out of bounds");
   if (o.T < 1) fail(2, "reconstruct_series: thread count out of range");
   if (o.A < 1 || o.A > kGroupSizeMaxDevice) fail(2, "reconstruct_series: workers per thread out of range");
@@ -287,40 +383,11 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   check_cuda(cudaEventRecord(span0_, copy_), "span event");
   for (int t = 0; t < T; ++t) check_cuda(cudaStreamWaitEvent(worker(t).stream(), span0_, 0), "span wait");
 
-  // end-to-end path: stream frames from host on the copy stream, normalise on arrival
+  // end-to-end path: frames produced on the copy stream (H2D, or raw samples through
+  // the device pre stage), normalised on arrival
   std::vector<cudaEvent_t> ready;
-  if (z_host) {
-    ready.resize(static_cast<size_t>(count));
-    int k0 = 0;
-    if (first == 0) {
-      check_cuda(cudaMemcpyAsync(z_, z_host, sizeof(float2) * zsz_, cudaMemcpyHostToDevice, copy_), "frame 0");
-      check_cuda(cudaStreamSynchronize(copy_), "frame 0");
-      normalized_ = false;
-      if (o.normalize) {
-        k_nrm2_frame<<<1, 256, 0, copy_>>>(z_, static_cast<long long>(zsz_), nsq_);
-        double nsq = 0;
-        check_cuda(cudaMemcpyAsync(&nsq, nsq_, sizeof(double), cudaMemcpyDeviceToHost, copy_), "nsq");
-        check_cuda(cudaStreamSynchronize(copy_), "nsq");
-        scale_ = nsq > 0 ? 100.0 / std::sqrt(nsq) : 1.0;
-      } else {
-        scale_ = 1.0;
-      }
-    }
-    for (int k = k0; k < count; ++k) {
-      const int n = first + k;
-      if (!(n == 0 && first == 0)) {
-        check_cuda(cudaMemcpyAsync(z_ + zsz_ * n, z_host + 2 * zsz_ * k, sizeof(float2) * zsz_,
-                                   cudaMemcpyHostToDevice, copy_),
-                   "frame upload");
-      }
-      if (o.normalize && scale_ != 1.0) {
-        k_scale_frames<<<148 * 2, 256, 0, copy_>>>(z_ + zsz_ * n, static_cast<long long>(zsz_),
-                                                   static_cast<float>(scale_));
-      }
-      check_cuda(cudaEventCreateWithFlags(&ready[static_cast<size_t>(k)], cudaEventDisableTiming), "event");
-      check_cuda(cudaEventRecord(ready[static_cast<size_t>(k)], copy_), "event");
-    }
-    normalized_ = true;
+  if (z_host || raw) {
+    produce_frames(o, first, count, z_host, raw, ready);
   } else if (o.normalize) {
     normalize();
   } else if (first == 0) {
@@ -392,7 +459,7 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
     // verification before publication
     safe_mode_ = true;
     try {
-      run(o, first, count, z_host, images_host, out);
+      run(o, first, count, z_host, images_host, out, raw);
     } catch (...) {
       safe_mode_ = false;
       throw;

@@ -10,6 +10,7 @@
 
 #include "engine.hpp"
 #include "group.hpp"
+#include "preproc.hpp"
 #include "sched.hpp"
 
 namespace rtnb {
@@ -21,6 +22,20 @@ struct SeriesOptions {
   bool chain = true;
   bool normalize = true;
   bool plain = false;   // reconstruct_series_plain semantics (strictly sequential)
+};
+
+// Raw acquisition input of the end-to-end path (KSpaceFrame per frame, seqsim.hpp:52-65):
+// samples count x Jp x K x S complex64 (host), angles count x K; with a compression
+// matrix (Jv x Jp, Jv = plan.J) the physical channels are compressed on the device
+// first (apply_compression), else Jp = plan.J.
+struct RawInput {
+  const float* samples = nullptr;
+  const double* angles = nullptr;
+  int K = 0;
+  int S = 0;
+  int Jp = 0;
+  double delay = 0.0;
+  const float* cmat = nullptr;
 };
 
 struct SeriesFrameOut {
@@ -60,8 +75,13 @@ class Series {
   // null the frames are streamed from host memory inside the call (copy stream,
   // overlapped with compute) and normalised on arrival: the end-to-end path.
   // images_host (count*N*N) receives the images; nullable.
+  // raw: the frames arrive as raw radial samples instead (z_host must be null); they
+  // are compressed, gridded (grid_adjoint) and their PSFs built or taken from the
+  // series' PSF cache on the device, all on the copy stream (rtnlinv's pre stage,
+  // pipeline.cpp:420-498)
   void run(const SeriesOptions& o, int first, int count, const float* z_host, float* images_host,
-           std::vector<SeriesFrameOut>* out);
+           std::vector<SeriesFrameOut>* out, const RawInput* raw = nullptr);
+  int psf_cache_size() const { return static_cast<int>(psf_keys_.size()); }
 
   float2* images_dev() { return images_; }
   // device time of the last run(): CUDA events spanning every worker stream, from
@@ -78,6 +98,14 @@ class Series {
   std::vector<std::unique_ptr<Engine>> extra_;
   std::vector<std::unique_ptr<Group>> groups_;
   int A_ = 1;  // width of the current run's workers
+  std::unique_ptr<Preproc> pre_;           // raw-input path (created on first use)
+  std::vector<uint64_t> psf_keys_;         // PsfCache: angle key of each built PSF slot
+  float2* raw_ = nullptr;                  // raw-sample staging (frames x Jp x K x S)
+  size_t raw_cap_ = 0;
+  float2* raw_c_ = nullptr;                // compressed staging (one frame) + matrix
+  size_t raw_c_cap_ = 0;
+  void produce_frames(const SeriesOptions& o, int first, int count, const float* z_host, const RawInput* raw,
+                      std::vector<cudaEvent_t>& ready);
   std::vector<int> devices_;
   int F_ = 0, n_psf_ = 0, D_ = 0;
   size_t zsz_ = 0, psz_ = 0, isz_ = 0;

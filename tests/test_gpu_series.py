@@ -217,3 +217,45 @@ def test_c2_compressed_frame_against_reference(gpu, ref):
     assert fr.cg_per_step == per
     assert rel_err(fr.image, img) < FRAME_TOL
     assert rel_err(fr.est, est) < FRAME_TOL
+
+
+def _raw_series(gpu, plan, F, U, samples, angles, opts, cmat=None):
+    ctx = gpu.Context(plan)
+    s = gpu.Series(ctx, F, U)
+    out = s.run(opts, raw=dict(samples=samples, angles=angles, cmat=cmat))
+    out["series"], out["ctx"] = s, ctx
+    return out
+
+
+def test_raw_acquisitions_through_the_device_pre_stage(gpu, ref):
+    # the reference's series driver grids and builds PSFs on the CPU (prep_series,
+    # nlinv.cpp:366-402); here raw samples go H2D and the pre stage runs on the device
+    plan = gpu.make_plan(24, 3)
+    plan.newton_steps, plan.cg_iter_budget = 7, 30
+    F, U = 7, 5
+    samples, angles = ref.phantom_series(3, F, 11, U, plan.N, 1e-3, 23)
+    want = ref.reconstruct_series(plan, samples, angles, plain=True)
+    got = _raw_series(gpu, plan, F, U, samples, angles, gpu.SeriesOptions(plain=True))
+    for n in range(F):
+        assert rel_err(got["images"][n], want["images"][n]) < FRAME_TOL, n
+    assert list(got["cg_iters"]) == list(want["cg_iters"])
+    assert got["series"].psf_cache_size() == U  # PsfCache: one kernel per angle set
+    # scheduled threads over the same raw input replay exactly like the gridded path
+    sched = got["series"].run(gpu.SeriesOptions(T=2, sched=gpu.TemporalSchedule(2, 2)),
+                              raw=dict(samples=samples, angles=angles))
+    assert sched["audit"][F - 1].reg_final_src == F - 2
+
+
+def test_raw_acquisitions_with_device_coil_compression(gpu, ref):
+    # configs[1] style: physical channels PCA-compressed (calibrate_compression on the
+    # first frames, rtnlinv_main.cpp:125-130), compression applied on the device
+    plan = gpu.make_plan(24, 4)
+    plan.newton_steps, plan.cg_iter_budget = 7, 30
+    F, U, Jp = 5, 5, 12
+    samples, angles = ref.phantom_series(Jp, F, 11, U, plan.N, 1e-3, 29)
+    m, energy = ref.calibrate_compression(samples[:2], angles[:2], plan.J)
+    comp, _ = ref.compress_series(samples, angles, plan.J, 2)
+    want = ref.reconstruct_series(plan, comp, angles, plain=True)
+    got = _raw_series(gpu, plan, F, U, samples, angles, gpu.SeriesOptions(plain=True), cmat=m)
+    for n in range(F):
+        assert rel_err(got["images"][n], want["images"][n]) < FRAME_TOL, n
