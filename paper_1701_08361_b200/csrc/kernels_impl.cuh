@@ -141,6 +141,12 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
 #define RTNB_MINB 3
 #endif
 #define RTNB_PASS_BOUNDS __launch_bounds__(Geo::NT, (RTNB_MINB * 256 + Geo::NT - 1) / Geo::NT)
+// per-kernel overrides: the column passes at the coil resolution and k_rows2 fit 64
+// registers without spills (ptxas -v), k_rows1 / k_colsT need the 80 of MINB 3
+#ifndef RTNB_MINB_LIGHT
+#define RTNB_MINB_LIGHT 4
+#endif
+#define RTNB_PASS_BOUNDS_LIGHT __launch_bounds__(Geo::NT, (RTNB_MINB_LIGHT * 256 + Geo::NT - 1) / Geo::NT)
 
 #define RTNB_TILE_SETUP(COLS_)                                  \
   extern __shared__ float2 A[];                                 \
@@ -153,7 +159,7 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
 // W^-1 column pass. Lines: (channel j, coil k-column q). Input chat_j*winv on the
 // Gc centered k-rows, output rows [r0, r0+nr) of U_j (G x Gc, row-major).
 template <class Geo>
-__global__ void RTNB_PASS_BOUNDS k_colA(Dims d, const float* __restrict__ winv,
+__global__ void RTNB_PASS_BOUNDS_LIGHT k_colA(Dims d, const float* __restrict__ winv,
                                                   const float2* __restrict__ twG,
                                                   const float2* __restrict__ chat, float2* __restrict__ U,
                                                   int r0, int nr, const DevState* st, int use_halt) {
@@ -418,7 +424,7 @@ __device__ __forceinline__ void finish_elem(const ColsWArgs& a, size_t e, float2
 // decomp.cpp:26-39; k_colsW adds the groups in order); rt = conj(rho) T -> forward
 // W^-H row pass keeping the Gc coil k-columns -> Y_j (L x Gc).
 template <class Geo>
-__global__ void RTNB_PASS_BOUNDS k_rows2(Dims d, int setup, const float2* __restrict__ twG,
+__global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float2* __restrict__ twG,
                                                    const float2* __restrict__ V,
                                                    const float2* __restrict__ coils,
                                                    const float2* __restrict__ rhom,
@@ -517,7 +523,7 @@ __global__ void RTNB_PASS_BOUNDS k_rows2(Dims d, int setup, const float2* __rest
 // outside the window (blocks [nbw, grid)); the window part of out.rho came from
 // k_rows2, whose reduction partial (st->scal[1]) is folded into the totals here.
 template <class Geo>
-__global__ void RTNB_PASS_BOUNDS k_colsW(Dims d, ColsWArgs a, const float* __restrict__ winv,
+__global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float* __restrict__ winv,
                                                    const float2* __restrict__ twG,
                                                    const float2* __restrict__ Y,
                                                    const double2* __restrict__ RP,
