@@ -227,7 +227,7 @@ def profile_traffic(kernel, cfg):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        e = d.get(cfg, {}).get(kernel)
+        e = d.get(cfg, {}).get(kernel) or d.get(cfg, {}).get("k_" + kernel)
         return None if e is None else float(e["dram_bytes_per_launch"])
     except (OSError, ValueError, KeyError):
         return None
