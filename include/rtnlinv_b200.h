@@ -106,6 +106,27 @@ int rtn_build_psf_coords(rtn_ctx* ctx, const double* coords /* 2n: kx, ky */, co
                          float* P_out);
 /* apply_compression: out (Jv*n) = m (Jv*Jp) x in (Jp*n), FP64 accumulation */
 int rtn_apply_compression(rtn_ctx* ctx, const float* m, int Jv, int Jp, const float* in, int n, float* out);
+/* --- planner.hpp:37-64 over the device transforms ---------------------------------
+ * benchmark_fft: device time (us, CUDA events, min over trials) of one centered 2D
+ * forward transform of `batch` images per listed size (the sm_100a line engine;
+ * sizes it does not cover run the direct DFT and lose the argmin). select_grid /
+ * the table file format are the reference's (planner.cpp:112-183). */
+int rtn_benchmark_fft(const int* sizes, int n, int trials, int batch, int device, double* out_us);
+int rtn_select_grid(int N, const int* sizes, const double* us, int n, double gamma_min, double gamma_max, int* G,
+                    double* gamma);
+int rtn_fft_table_save(const char* path, const int* sizes, const double* us, int n, const char* machine,
+                       const char* library);
+int rtn_fft_table_load(const char* path, int* sizes, double* us, int max_n, int* n, char* machine, char* library,
+                       int key_cap);
+
+/* --- pipeline.cpp:60-137 postprocessing on the device (host buffers) ---------------- */
+/* magnitude_image: n complex64 -> n float */
+int rtn_post_magnitude(const float* images, long long n, float* out);
+/* phase_difference_image: arg(even * conj(odd)) */
+int rtn_post_phase_difference(const float* even, const float* odd, long long n, float* out);
+/* MedianFilter3 over one slice's `frames` magnitude images of npix pixels */
+int rtn_post_median3(const float* mags, int frames, long long npix, float* out);
+
 /* PsfCache::angle_key (preproc.cpp:301-313) */
 uint64_t rtn_psf_angle_key(const double* angles, int K, int S, int G);
 
@@ -173,6 +194,10 @@ int rtn_series_run_raw(rtn_series* s, const rtn_series_opts_t* opts, int first, 
                        int* audit, uint64_t* seqs, int* cg_iters, float* gpu_ms);
 /* distinct PSFs built by rtn_series_run_raw so far */
 int rtn_series_psf_cache_size(rtn_series* s);
+/* postprocessing of the device-resident images [first, first+count) to host floats:
+ * mode 0 magnitude (count*N*N), 1 magnitude + temporal median-of-3 (count*N*N),
+ * 2 phase difference of frame pairs (count/2 * N*N) */
+int rtn_series_post(rtn_series* s, int first, int count, int mode, float* out);
 int rtn_series_images(rtn_series* s, int first, int count, float* images);
 /* device time (ms) of the last rtn_series_run: CUDA events spanning all worker streams */
 float rtn_series_last_span_ms(rtn_series* s);

@@ -304,6 +304,49 @@ def reconstruct_series(plan, samples, angles, T=1, A=1, sched=(1, 1), chain=True
     return dict(images=images, audit=audit, seqs=seqs, cg_iters=cg, seconds=secs, data_scale=scale.value)
 
 
+# ---- planner / postprocessing -------------------------------------------------------------------
+def select_grid(N, table, gamma_min=1.4, gamma_max=2.0):
+    sizes = np.array(sorted(table), np.int32)
+    us = np.array([table[k] for k in sorted(table)], np.float64)
+    G = ctypes.c_int(0)
+    gamma = ctypes.c_double(0)
+    _chk(lib().ref_select_grid(N, _ip(sizes), _dp(us), len(sizes), ctypes.c_double(gamma_min),
+                               ctypes.c_double(gamma_max), ctypes.byref(G), ctypes.byref(gamma)))
+    return G.value, gamma.value
+
+
+def table_roundtrip(path, table):
+    sizes = np.array(sorted(table), np.int32)
+    us = np.array([table[k] for k in sorted(table)], np.float64)
+    so = np.zeros(len(sizes) + 1, np.int32)
+    uo = np.zeros(len(sizes) + 1, np.float64)
+    n = ctypes.c_int(0)
+    _chk(lib().ref_table_roundtrip(str(path).encode(), _ip(sizes), _dp(us), len(sizes), _ip(so), _dp(uo),
+                                   ctypes.byref(n)))
+    return {int(so[i]): float(uo[i]) for i in range(n.value)}
+
+
+def magnitude_image(img):
+    img = _c64(img)
+    out = np.zeros(img.shape, np.float32)
+    _chk(lib().ref_magnitude_image(_fp(img), img.shape[0], _fp(out)))
+    return out
+
+
+def phase_difference_image(even, odd):
+    even, odd = _c64(even), _c64(odd)
+    out = np.zeros(even.shape, np.float32)
+    _chk(lib().ref_phase_difference_image(_fp(even), _fp(odd), even.shape[0], _fp(out)))
+    return out
+
+
+def median_filter(mags):
+    mags = np.ascontiguousarray(mags, np.float32)
+    out = np.zeros_like(mags)
+    _chk(lib().ref_median_filter(_fp(mags), mags.shape[0], mags.shape[1], _fp(out)))
+    return out
+
+
 # ---- decomposition / autotune --------------------------------------------------------------
 def partition_channels(J, A):
     out = np.zeros(2 * max(A, 1), np.int32)

@@ -31,6 +31,7 @@
 #include "rtnlinv/decomp.hpp"
 #include "rtnlinv/fft.hpp"
 #include "rtnlinv/nlinv.hpp"
+#include "rtnlinv/pipeline.hpp"
 #include "rtnlinv/planner.hpp"
 #include "rtnlinv/preproc.hpp"
 #include "rtnlinv/seqsim.hpp"
@@ -305,6 +306,73 @@ int ref_compress_series(const float* samples_in, const double* angles, int F, in
       const KSpaceFrame c = apply_compression(frames[static_cast<size_t>(n)], cm);
       std::memcpy(samples_out + static_cast<size_t>(n) * per_out * 2, c.samples.data(),
                   sizeof(cfloat) * per_out);
+    }
+  });
+}
+
+// ---- planner (planner.cpp:112-183) and postprocessing (pipeline.cpp:60-137) -----------------
+
+int ref_select_grid(int N, const int* sizes, const double* us, int n, double gmin, double gmax, int* G,
+                    double* gamma) {
+  return guarded([&] {
+    FftLookupTable t;
+    for (int i = 0; i < n; ++i) t.entries_us[sizes[i]] = us[i];
+    const auto g = select_grid(N, t, gmin, gmax);
+    *G = g.first;
+    *gamma = g.second;
+  });
+}
+
+int ref_table_roundtrip(const char* path, const int* sizes, const double* us, int n, int* sizes_out,
+                        double* us_out, int* n_out) {
+  return guarded([&] {
+    FftLookupTable t;
+    t.machine_key = "m";
+    t.library_key = "l";
+    for (int i = 0; i < n; ++i) t.entries_us[sizes[i]] = us[i];
+    save_table(t, path);
+    const FftLookupTable r = load_table(path);
+    int k = 0;
+    for (const auto& [s, v] : r.entries_us) {
+      sizes_out[k] = s;
+      us_out[k] = v;
+      ++k;
+    }
+    *n_out = k;
+  });
+}
+
+int ref_magnitude_image(const float* img, int N, float* out) {
+  return guarded([&] {
+    const ImageOut o = magnitude_image(load_img(img, N), 0, 0);
+    std::memcpy(out, o.pixels.data(), sizeof(float) * o.pixels.size());
+  });
+}
+
+int ref_phase_difference_image(const float* even, const float* odd, int N, float* out) {
+  return guarded([&] {
+    const ImageOut o = phase_difference_image(load_img(even, N), load_img(odd, N), 0, 0);
+    std::memcpy(out, o.pixels.data(), sizeof(float) * o.pixels.size());
+  });
+}
+
+// MedianFilter3 push/drain over F magnitude frames of one slice, outputs in order
+int ref_median_filter(const float* mags, int F, int N, float* out) {
+  return guarded([&] {
+    MedianFilter3 f;
+    std::vector<ImageOut> got;
+    for (int n = 0; n < F; ++n) {
+      ImageOut im;
+      im.frame_index = n;
+      im.n = N;
+      im.kind = ImageKind::magnitude;
+      im.pixels.assign(mags + static_cast<size_t>(n) * N * N, mags + static_cast<size_t>(n + 1) * N * N);
+      for (auto& o : f.push(std::move(im))) got.push_back(std::move(o));
+    }
+    for (auto& o : f.drain()) got.push_back(std::move(o));
+    if (static_cast<int>(got.size()) != F) throw UsageError("median filter: frame count changed");
+    for (const ImageOut& o : got) {
+      std::memcpy(out + static_cast<size_t>(o.frame_index) * N * N, o.pixels.data(), sizeof(float) * N * N);
     }
   });
 }

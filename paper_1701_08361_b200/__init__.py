@@ -140,6 +140,15 @@ def load_library(path: str = LIB_PATH):
         "rtn_build_psf_coords": ([vp, d, d, ctypes.c_int, f], ctypes.c_int),
         "rtn_apply_compression": ([vp, f, ctypes.c_int, ctypes.c_int, f, ctypes.c_int, f], ctypes.c_int),
         "rtn_psf_angle_key": ([d, ctypes.c_int, ctypes.c_int, ctypes.c_int], ctypes.c_uint64),
+        "rtn_benchmark_fft": ([i, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, d], ctypes.c_int),
+        "rtn_select_grid": ([ctypes.c_int, i, d, ctypes.c_int, ctypes.c_double, ctypes.c_double, i, d], ctypes.c_int),
+        "rtn_fft_table_save": ([ctypes.c_char_p, i, d, ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
+        "rtn_fft_table_load": ([ctypes.c_char_p, i, d, ctypes.c_int, i, ctypes.c_char_p, ctypes.c_char_p,
+                                ctypes.c_int], ctypes.c_int),
+        "rtn_post_magnitude": ([f, ctypes.c_longlong, f], ctypes.c_int),
+        "rtn_post_phase_difference": ([f, f, ctypes.c_longlong, f], ctypes.c_int),
+        "rtn_post_median3": ([f, ctypes.c_int, ctypes.c_longlong, f], ctypes.c_int),
+        "rtn_series_post": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, f], ctypes.c_int),
         "rtn_fft2": ([f, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "rtn_fft_set_ctx": ([ctypes.c_int], None),
         "rtn_fft_get_ctx": ([], ctypes.c_int),
@@ -650,6 +659,17 @@ class Series:
                              int(q[0]), int(q[1]), int(q[2])) for r, q in zip(audit, seqs)]
         return dict(images=images, audit=audits, cg_iters=cg, gpu_ms=ms)
 
+    def post(self, first: int = 0, count: Optional[int] = None, mode: str = "magnitude"):
+        """device postprocessing of the stored images: magnitude, median3 (magnitude +
+        MedianFilter3) or phase_difference (frame pairs)"""
+        p = self.ctx.plan
+        count = self.F - first if count is None else count
+        m = {"magnitude": 0, "median3": 1, "phase_difference": 2}[mode]
+        n = count // 2 if m == 2 else count
+        out = np.zeros((n, p.N, p.N), np.float32)
+        _check(self.lib.rtn_series_post(self._h, first, count, m, _fp(out)))
+        return out
+
     def psf_cache_size(self) -> int:
         return int(self.lib.rtn_series_psf_cache_size(self._h))
 
@@ -688,6 +708,98 @@ def reconstruct_series(ctx: Context, z, P, opts: SeriesOptions, psf_index=None):
         return out
     finally:
         s.close()
+
+
+# ---- planner.hpp:12-64 over the device transforms --------------------------------------------
+@dataclass
+class FftLookupTable:
+    """planner.hpp:12-18: size -> device time (us) of one 2D transform"""
+    entries_us: dict = field(default_factory=dict)
+    machine_key: str = ""
+    library_key: str = "rtnlinv_b200-line-fft-sm100a"
+
+    def _arrays(self):
+        sizes = np.array(sorted(self.entries_us), np.int32)
+        us = np.array([self.entries_us[k] for k in sorted(self.entries_us)], np.float64)
+        return sizes, us
+
+
+def benchmark_fft(sizes, trials: int = 5, batch: int = 1, device: int = 0) -> FftLookupTable:
+    lib = load_library()
+    sz = np.ascontiguousarray(list(sizes), np.int32)
+    us = np.zeros(len(sz), np.float64)
+    _check(lib.rtn_benchmark_fft(sz.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), len(sz), trials, batch, device,
+                                 us.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    return FftLookupTable({int(a): float(b) for a, b in zip(sz, us)})
+
+
+def select_grid(N: int, table: FftLookupTable, gamma_min: float = 1.4, gamma_max: float = 2.0):
+    """planner.cpp:112-131: (G, gamma) of the fastest even grid in [2 gamma_min N, 2 gamma_max N]"""
+    lib = load_library()
+    sizes, us = table._arrays()
+    G, gamma = ctypes.c_int(0), ctypes.c_double(0)
+    _check(lib.rtn_select_grid(N, sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                               us.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(sizes), gamma_min, gamma_max,
+                               ctypes.byref(G), ctypes.byref(gamma)))
+    return G.value, gamma.value
+
+
+def save_table(table: FftLookupTable, path: str):
+    lib = load_library()
+    sizes, us = table._arrays()
+    _check(lib.rtn_fft_table_save(str(path).encode(), sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                  us.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(sizes),
+                                  table.machine_key.encode(), table.library_key.encode()))
+
+
+def load_table(path: str) -> FftLookupTable:
+    lib = load_library()
+    cap = 8192
+    sizes = np.zeros(cap, np.int32)
+    us = np.zeros(cap, np.float64)
+    n = ctypes.c_int(0)
+    mk, lk = ctypes.create_string_buffer(512), ctypes.create_string_buffer(512)
+    _check(lib.rtn_fft_table_load(str(path).encode(), sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                  us.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap, ctypes.byref(n), mk, lk,
+                                  512))
+    k = min(n.value, cap)
+    return FftLookupTable({int(sizes[i]): float(us[i]) for i in range(k)}, mk.value.decode(), lk.value.decode())
+
+
+def plan_from_table(N: int, J: int, table: FftLookupTable, gamma_min: float = 1.4, gamma_max: float = 2.0):
+    """make_plan(N, J, &table) (planner.cpp:133-149)"""
+    G, gamma = select_grid(N, table, gamma_min, gamma_max)
+    p = raw_plan(G, J)
+    p.N, p.gamma = N, gamma
+    return p
+
+
+# ---- pipeline.cpp:60-137 postprocessing on the device ------------------------------------------
+def magnitude_image(img) -> np.ndarray:
+    lib = load_library()
+    img = _c64(img)
+    out = np.zeros(img.shape, np.float32)
+    _check(lib.rtn_post_magnitude(_fp(img), img.size, _fp(out)))
+    return out
+
+
+def phase_difference_image(even, odd) -> np.ndarray:
+    lib = load_library()
+    even, odd = _c64(even), _c64(odd)
+    if even.shape != odd.shape:
+        raise UsageError("phase_difference_image: size mismatch")
+    out = np.zeros(even.shape, np.float32)
+    _check(lib.rtn_post_phase_difference(_fp(even), _fp(odd), even.size, _fp(out)))
+    return out
+
+
+def median3_sequence(mags) -> np.ndarray:
+    """MedianFilter3 over one slice's magnitude frames (F, N, N)"""
+    lib = load_library()
+    mags = np.ascontiguousarray(mags, np.float32)
+    out = np.zeros_like(mags)
+    _check(lib.rtn_post_median3(_fp(mags), mags.shape[0], mags[0].size, _fp(out)))
+    return out
 
 
 def psf_angle_key(angles, S: int, G: int) -> int:

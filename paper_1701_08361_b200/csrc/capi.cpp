@@ -1,7 +1,9 @@
 // extern "C" boundary (include/rtnlinv_b200.h) over the engine.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <memory>
 #include <cstring>
 #include <string>
@@ -11,6 +13,7 @@
 #include "engine.hpp"
 #include "group.hpp"
 #include "preproc.hpp"
+#include "post.hpp"
 #include "sched.hpp"
 #include "series.hpp"
 
@@ -65,6 +68,29 @@ rtnb::Engine& eng(rtn_ctx* c) {
   return *c->eng;
 }
 
+}  // namespace
+
+namespace {
+template <typename F>
+void with_device_buffers(size_t in_bytes, size_t out_bytes, F&& f) {
+  void* a = nullptr;
+  void* b = nullptr;
+  rtnb::check_cuda(cudaMalloc(&a, std::max<size_t>(in_bytes, 1)), "post buffer");
+  const cudaError_t e = cudaMalloc(&b, std::max<size_t>(out_bytes, 1));
+  if (e != cudaSuccess) {
+    cudaFree(a);
+    rtnb::check_cuda(e, "post buffer");
+  }
+  try {
+    f(a, b);
+  } catch (...) {
+    cudaFree(a);
+    cudaFree(b);
+    throw;
+  }
+  cudaFree(a);
+  cudaFree(b);
+}
 }  // namespace
 
 extern "C" {
@@ -169,6 +195,99 @@ int rtn_apply_compression(rtn_ctx* ctx, const float* m, int Jv, int Jp, const fl
     pre(ctx).apply_compression_host(m, Jv, Jp, in, n, out);
   });
 }
+// ---- planner.hpp:37-64 over the device transforms ------------------------------------------
+
+int rtn_benchmark_fft(const int* sizes, int n, int trials, int batch, int device, double* out_us) {
+  return guarded([&] {
+    if (!sizes || !out_us || n < 1) rtnb::fail(2, "benchmark_fft: bad size range");
+    const rtnb::FftTable t = rtnb::benchmark_fft_device(std::vector<int>(sizes, sizes + n), trials, batch, device);
+    for (int i = 0; i < n; ++i) out_us[i] = t.entries_us.at(sizes[i]);
+  });
+}
+
+static rtnb::FftTable table_of(const int* sizes, const double* us, int n) {
+  rtnb::FftTable t;
+  for (int i = 0; i < n; ++i) t.entries_us[sizes[i]] = us[i];
+  return t;
+}
+
+int rtn_select_grid(int N, const int* sizes, const double* us, int n, double gamma_min, double gamma_max, int* G,
+                    double* gamma) {
+  return guarded([&] {
+    if (n < 0 || (n > 0 && (!sizes || !us))) rtnb::fail(2, "select_grid: bad table");
+    const auto g = rtnb::select_grid(N, table_of(sizes, us, n), gamma_min, gamma_max);
+    *G = g.first;
+    *gamma = g.second;
+  });
+}
+
+int rtn_fft_table_save(const char* path, const int* sizes, const double* us, int n, const char* machine,
+                       const char* library) {
+  return guarded([&] {
+    rtnb::FftTable t = table_of(sizes, us, n);
+    t.machine_key = machine ? machine : "";
+    t.library_key = library ? library : "";
+    rtnb::save_fft_table(t, path);
+  });
+}
+
+int rtn_fft_table_load(const char* path, int* sizes, double* us, int max_n, int* n, char* machine, char* library,
+                       int key_cap) {
+  return guarded([&] {
+    const rtnb::FftTable t = rtnb::load_fft_table(path);
+    int k = 0;
+    for (const auto& [s, v] : t.entries_us) {
+      if (k < max_n) {
+        sizes[k] = s;
+        us[k] = v;
+      }
+      ++k;
+    }
+    *n = k;
+    if (machine && key_cap > 0) std::snprintf(machine, static_cast<size_t>(key_cap), "%s", t.machine_key.c_str());
+    if (library && key_cap > 0) std::snprintf(library, static_cast<size_t>(key_cap), "%s", t.library_key.c_str());
+  });
+}
+
+// ---- pipeline.cpp:60-137 postprocessing on the device -----------------------------------------
+
+
+int rtn_post_magnitude(const float* images, long long n, float* out) {
+  return guarded([&] {
+    if (!images || !out || n < 0) rtnb::fail(2, "magnitude_image: bad arguments");
+    with_device_buffers(sizeof(float2) * n, sizeof(float) * n, [&](void* a, void* b) {
+      rtnb::check_cuda(cudaMemcpy(a, images, sizeof(float2) * n, cudaMemcpyHostToDevice), "h2d");
+      rtnb::post_magnitude(static_cast<float2*>(a), n, static_cast<float*>(b), nullptr);
+      rtnb::check_cuda(cudaMemcpy(out, b, sizeof(float) * n, cudaMemcpyDeviceToHost), "d2h");
+    });
+  });
+}
+
+int rtn_post_phase_difference(const float* even, const float* odd, long long n, float* out) {
+  return guarded([&] {
+    if (!even || !odd || !out || n < 0) rtnb::fail(2, "phase_difference_image: bad arguments");
+    with_device_buffers(2 * sizeof(float2) * n, sizeof(float) * n, [&](void* a, void* b) {
+      float2* e2 = static_cast<float2*>(a);
+      rtnb::check_cuda(cudaMemcpy(e2, even, sizeof(float2) * n, cudaMemcpyHostToDevice), "h2d");
+      rtnb::check_cuda(cudaMemcpy(e2 + n, odd, sizeof(float2) * n, cudaMemcpyHostToDevice), "h2d");
+      rtnb::post_phase_difference(e2, e2 + n, n, static_cast<float*>(b), nullptr);
+      rtnb::check_cuda(cudaMemcpy(out, b, sizeof(float) * n, cudaMemcpyDeviceToHost), "d2h");
+    });
+  });
+}
+
+int rtn_post_median3(const float* mags, int frames, long long npix, float* out) {
+  return guarded([&] {
+    if (!mags || !out || frames < 1 || npix < 0) rtnb::fail(2, "median filter: bad arguments");
+    const size_t n = static_cast<size_t>(frames) * static_cast<size_t>(npix);
+    with_device_buffers(sizeof(float) * n, sizeof(float) * n, [&](void* a, void* b) {
+      rtnb::check_cuda(cudaMemcpy(a, mags, sizeof(float) * n, cudaMemcpyHostToDevice), "h2d");
+      rtnb::post_median3(static_cast<float*>(a), frames, npix, static_cast<float*>(b), nullptr);
+      rtnb::check_cuda(cudaMemcpy(out, b, sizeof(float) * n, cudaMemcpyDeviceToHost), "d2h");
+    });
+  });
+}
+
 uint64_t rtn_psf_angle_key(const double* angles, int K, int S, int G) {
   return rtnb::psf_angle_key(angles, K, S, G);
 }
@@ -420,6 +539,10 @@ int rtn_series_run_raw(rtn_series* s, const rtn_series_opts_t* o, int first, int
 }
 
 int rtn_series_psf_cache_size(rtn_series* s) { return (s && s->s) ? s->s->psf_cache_size() : 0; }
+
+int rtn_series_post(rtn_series* s, int first, int count, int mode, float* out) {
+  return guarded([&] { ser(s).post(first, count, mode, out); });
+}
 
 int rtn_series_images(rtn_series* s, int first, int count, float* images) {
   return guarded([&] {

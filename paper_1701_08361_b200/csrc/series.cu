@@ -1,6 +1,8 @@
 // Series drivers over device-resident frames (nlinv.cpp:366-526).
 #include "series.hpp"
 
+#include "post.hpp"
+
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -271,6 +273,36 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   out.cg_iters = fs.cg_iters;
   out.gpu_ms = ms;
   ledger.mark_complete(n);
+}
+
+void Series::post(int first, int count, int mode, float* out) {
+  if (first < 0 || count < 1 || first + count > F_) fail(2, "series post: frame range out of bounds");
+  if (mode < 0 || mode > 2) fail(2, "series post: unknown mode");
+  check_cuda(cudaSetDevice(eng0_.device()), "set device");
+  const long long npix = static_cast<long long>(isz_);
+  float* buf = nullptr;
+  check_cuda(cudaMalloc(&buf, sizeof(float) * npix * count * 2), "post buffer");
+  const float2* img = images_ + isz_ * first;
+  long long n_out = npix * count;
+  float* res = buf;
+  if (mode == 2) {
+    const int pairs = count / 2;
+    for (int k = 0; k < pairs; ++k) {
+      post_phase_difference(img + 2 * k * isz_, img + (2 * k + 1) * isz_, npix, buf + k * npix, copy_);
+    }
+    n_out = npix * pairs;
+  } else {
+    post_magnitude(img, npix * count, buf, copy_);
+    if (mode == 1) {
+      post_median3(buf, count, npix, buf + npix * count, copy_);
+      res = buf + npix * count;
+    }
+  }
+  const cudaError_t e = cudaMemcpyAsync(out, res, sizeof(float) * n_out, cudaMemcpyDeviceToHost, copy_);
+  const cudaError_t e2 = cudaStreamSynchronize(copy_);
+  cudaFree(buf);
+  check_cuda(e, "post d2h");
+  check_cuda(e2, "post sync");
 }
 
 void Series::produce_frames(const SeriesOptions& o, int first, int count, const float* z_host,

@@ -82,6 +82,10 @@ class Series {
   void run(const SeriesOptions& o, int first, int count, const float* z_host, float* images_host,
            std::vector<SeriesFrameOut>* out, const RawInput* raw = nullptr);
   int psf_cache_size() const { return static_cast<int>(psf_keys_.size()); }
+  // postprocessing of the device-resident images [first, first + count) into host floats:
+  // mode 0 magnitude, 1 magnitude + temporal median-of-3 (MedianFilter3 over the range),
+  // 2 phase difference of consecutive frame pairs (count/2 images); pipeline.cpp:60-137
+  void post(int first, int count, int mode, float* out);
 
   float2* images_dev() { return images_; }
   // device time of the last run(): CUDA events spanning every worker stream, from

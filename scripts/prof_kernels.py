@@ -22,5 +22,5 @@ with pb.Context(plan) as ctx:
     fr = ctx.reconstruct_frame(pb.initial_estimate(plan))
     ctx.make_step_cache(fr.est)
     for n in names:
-        ms, by = ctx.time_kernel(n, 2)
+        ms, by = ctx.time_kernel(n, int(os.environ.get("REPS", "50")))
         print(f"{n}: {ms * 1000:.1f} us, {by / 1e6:.2f} MB algorithmic, {by / ms / 1e6:.0f} GB/s", flush=True)
