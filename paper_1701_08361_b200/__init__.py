@@ -802,6 +802,11 @@ def median3_sequence(mags) -> np.ndarray:
     return out
 
 
+def grid_supported(G: int) -> bool:
+    """the fused line engine covers grid side G (else transforms fall back to the direct DFT kernel)"""
+    return bool(load_library().rtn_grid_supported(G))
+
+
 def psf_angle_key(angles, S: int, G: int) -> int:
     """PsfCache::angle_key (preproc.cpp:301-313)"""
     a = np.ascontiguousarray(angles, np.float64)

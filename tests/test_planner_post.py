@@ -41,13 +41,16 @@ def test_table_files_interchange_with_the_reference(ref, tmp_path):
 
 @pytest.mark.gpu
 def test_device_fft_table_drives_the_grid_choice(gpu):
-    t = gpu.benchmark_fft([192, 200, 240, 256, 320], trials=3, batch=8)
+    # every even size of the search window, as select_grid requires (planner.cpp:118-121)
+    sizes = list(range(192, 258, 2))
+    t = gpu.benchmark_fft(sizes, trials=2, batch=4)
     assert all(v > 0 for v in t.entries_us.values())
     # a size without a fused line engine (200 = 8 x 25) runs the direct DFT and loses
     assert t.entries_us[200] > t.entries_us[256]
-    G, gamma = gpu.select_grid(80, t, 1.2, 2.0)
-    assert G in (192, 240, 256, 320) and gpu.grid_supported(G)
-    assert gamma == G / 160
+    G, gamma = gpu.select_grid(64, t, 1.5, 2.0)
+    assert gpu.grid_supported(G) and gamma == G / 128
+    p = gpu.plan_from_table(64, 4, t, 1.5, 2.0)
+    assert (p.G, p.N, p.Gc) == (G, 64, G // 4)
 
 
 @pytest.mark.gpu
