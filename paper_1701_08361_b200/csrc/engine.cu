@@ -104,7 +104,7 @@ struct Registry {
   std::vector<Engine::Ops> ops;
   std::vector<std::pair<int, void (*)()>> attrs;  // per G, run once per device
   std::vector<std::vector<int>> attrs_done;       // [device] -> list of G
-  std::vector<std::pair<std::pair<int, int>, float2*>> twG;  // (device, G) -> table
+  std::vector<std::pair<std::pair<int, int>, float4*>> twG;  // (device, G) -> table
   std::vector<std::pair<std::pair<int, int>, double2*>> twD;  // (device, n*sign) -> direct table
 };
 
@@ -142,20 +142,24 @@ const Engine::Ops* ops_for(int G, int dev) {
   return found;
 }
 
-float2* twiddles_for(int G, int dev) {
+// W_G^e, e < G, as packed operand pairs {w.x, w.y, -w.y, w.x} (cmul_pk), for the
+// forward sign, then their conjugates {w.x, -w.y, w.y, w.x} for the inverse
+float4* twiddles_for(int G, int dev) {
   Registry& r = registry();
   std::lock_guard<std::mutex> lock(r.mu);
   for (auto& e : r.twG) {
     if (e.first == std::make_pair(dev, G)) return e.second;
   }
-  std::vector<float2> h(static_cast<size_t>(G));
+  std::vector<float4> h(2 * static_cast<size_t>(G));
   for (int e = 0; e < G; ++e) {
     const double a = -2.0 * std::numbers::pi * e / G;
-    h[static_cast<size_t>(e)] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+    const float c = static_cast<float>(std::cos(a)), sn = static_cast<float>(std::sin(a));
+    h[static_cast<size_t>(e)] = make_float4(c, sn, -sn, c);
+    h[static_cast<size_t>(G + e)] = make_float4(c, -sn, sn, c);
   }
-  float2* d = nullptr;
-  check_cuda(cudaMalloc(&d, sizeof(float2) * G), "twiddle alloc");
-  check_cuda(cudaMemcpy(d, h.data(), sizeof(float2) * G, cudaMemcpyHostToDevice), "twiddle upload");
+  float4* d = nullptr;
+  check_cuda(cudaMalloc(&d, sizeof(float4) * h.size()), "twiddle alloc");
+  check_cuda(cudaMemcpy(d, h.data(), sizeof(float4) * h.size(), cudaMemcpyHostToDevice), "twiddle upload");
   r.twG.push_back({{dev, G}, d});
   return d;
 }
@@ -199,7 +203,7 @@ void fft2_device(float2* data, int n, int batch, int sign, cudaStream_t s) {
   check_cuda(cudaGetDevice(&dev), "get device");
   const Engine::Ops* ops = (n % 2 == 0) ? ops_for(n, dev) : nullptr;
   if (ops) {
-    const float2* tw = twiddles_for(n, dev);
+    const float4* tw = twiddles_for(n, dev);
     const int grid = batch * ((n + ops->LPB - 1) / ops->LPB);
     ops->fft(s, grid, sign, data, batch, 1, tw, 1.0f);
     ops->fft(s, grid, sign, data, batch, 0, tw, 1.0f / n);

@@ -216,7 +216,7 @@ class Engine : public FrameWorker {
 
   std::vector<float> winv_host_;
   float* winv_ = nullptr;
-  float2* twG_ = nullptr;
+  float4* twG_ = nullptr;  // packed twiddles (twiddles_for)
   float2* P_ = nullptr;
   float2* z_ = nullptr;
   float2* x_ = nullptr;

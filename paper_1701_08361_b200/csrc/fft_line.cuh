@@ -26,9 +26,10 @@
 
 namespace rtnb {
 
-// exp(-2 pi i k / N) for N = 1..32, k = 0..N-1, at offset N(N-1)/2. Filled from
-// double-precision values by the host (engine.cu, the one TU that includes this).
-static __constant__ float2 c_small_tw[528];
+// exp(-2 pi i k / N) for N = 1..32, k = 0..N-1, at offset N(N-1)/2, as float4
+// {w.x, w.y, -w.y, w.x}: the two packed operands of a twiddle product (cmul_pk).
+// Filled from double-precision values by the host (ops.cuh, once per translation unit).
+static __constant__ float4 c_small_tw[528];
 
 __host__ __device__ constexpr int small_tw_offset(int n) { return n * (n - 1) / 2; }
 
@@ -46,21 +47,66 @@ __host__ __device__ constexpr int split_factor(int n) {
   return n;
 }
 
+// Packed FP32 (sm_100a FADD2 / FMUL2 / FFMA2): one instruction per complex add and two
+// per twiddle product. RTNB_PACKED=0 selects the scalar forms.
+#ifndef RTNB_PACKED
+#define RTNB_PACKED 1
+#endif
+__device__ __forceinline__ unsigned long long pk2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return make_float2(lo, hi);
+}
+
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+#if RTNB_PACKED
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return upk2(r);
+#else
+  return make_float2(a.x + b.x, a.y + b.y);
+#endif
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+#if RTNB_PACKED
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return upk2(r);
+#else
+  return make_float2(a.x - b.x, a.y - b.y);
+#endif
+}
+// a * w with the twiddle pre-split as t = {w.x, w.y, -w.y, w.x}:
+// a.x * (w.x, w.y) + a.y * (-w.y, w.x), a.x and a.y broadcast into both lanes
+__device__ __forceinline__ float2 cmul_pk(float2 a, float4 t) {
+#if RTNB_PACKED
+  unsigned long long m, r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(m) : "l"(pk2(a.x, a.x)), "l"(pk2(t.x, t.y)));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a.y, a.y)), "l"(pk2(t.z, t.w)), "l"(m));
+  return upk2(r);
+#else
+  return make_float2(a.x * t.x + a.y * t.z, a.x * t.y + a.y * t.w);
+#endif
+}
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 __device__ __forceinline__ float2 cneg(float2 a) { return make_float2(-a.x, -a.y); }
 
 // W_N^k for sign S (S = -1 forward: exp(-2 pi i k/N); S = +1 inverse: conjugate)
+// (as the packed operand pair of cmul_pk)
 template <int N, int S>
-__device__ __forceinline__ float2 small_w(int k) {
-  float2 w = c_small_tw[small_tw_offset(N) + (k % N)];
-  if (S > 0) w.y = -w.y;
-  return w;
+__device__ __forceinline__ float4 small_w(int k) {
+  const float4 t = c_small_tw[small_tw_offset(N) + (k % N)];
+  // conj(w) = {w.x, -w.y, w.y, w.x}
+  return S > 0 ? make_float4(t.x, t.z, t.y, t.w) : t;
 }
 
 // multiply by -i*S... i.e. by W_4^1 = exp(S * 2 pi i / 4) = S*i
@@ -80,11 +126,7 @@ __device__ __forceinline__ void dft_direct(float2 (&x)[N]) {
   for (int k = 0; k < N; ++k) {
     float2 acc = x[0];
 #pragma unroll
-    for (int t = 1; t < N; ++t) {
-      const float2 w = small_w<N, S>((k * t) % N);
-      acc.x += x[t].x * w.x - x[t].y * w.y;
-      acc.y += x[t].x * w.y + x[t].y * w.x;
-    }
+    for (int t = 1; t < N; ++t) acc = cadd(acc, cmul_pk(x[t], small_w<N, S>((k * t) % N)));
     y[k] = acc;
   }
 #pragma unroll
@@ -138,7 +180,7 @@ __device__ __forceinline__ void dft(float2 (&x)[N]) {
       float2 t[P];
       t[0] = sub[0][k];
 #pragma unroll
-      for (int p = 1; p < P; ++p) t[p] = cmul(sub[p][k], small_w<N, S>(p * k));
+      for (int p = 1; p < P; ++p) t[p] = cmul_pk(sub[p][k], small_w<N, S>(p * k));
       dft<P, S>(t);
 #pragma unroll
       for (int m = 0; m < P; ++m) x[k + Q * m] = t[m];
@@ -214,7 +256,7 @@ __device__ __forceinline__ float2 mul_wn(float2 v) {
       return make_float2(v.y, -v.x);  // * -i
     }
   } else {
-    return cmul(v, small_w<N, S>(e));
+    return cmul_pk(v, small_w<N, S>(e));
   }
 }
 
@@ -339,14 +381,13 @@ struct Item {
 // step 1 on registers: v[n1] = x[N2*n1 + n2] -> DFT_N1 -> twiddle W_G^{n2 k1};
 // IN: which n1 may be nonzero
 template <class Geo, int S, uint32_t IN = Geo::ALL_N1>
-__device__ __forceinline__ void fft_step1(float2 (&v)[Geo::N1], int n2, const float2* __restrict__ twG) {
+// twG: 2G packed twiddles {w.x, w.y, -w.y, w.x} of W_G^e, e < G, for S = -1, then the
+// conjugates for S = +1 (twiddles_for, engine.cu)
+__device__ __forceinline__ void fft_step1(float2 (&v)[Geo::N1], int n2, const float4* __restrict__ twG) {
   dft_m<Geo::N1, S, IN, Geo::ALL_N1>(v);
+  const float4* tw = twG + (S > 0 ? Geo::G : 0);
 #pragma unroll
-  for (int k1 = 1; k1 < Geo::N1; ++k1) {
-    float2 w = __ldg(twG + n2 * k1);
-    if (S > 0) w.y = -w.y;
-    v[k1] = cmul(v[k1], w);
-  }
+  for (int k1 = 1; k1 < Geo::N1; ++k1) v[k1] = cmul_pk(v[k1], __ldg(tw + n2 * k1));
 }
 
 template <class Geo>

@@ -160,7 +160,7 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
 // Gc centered k-rows, output rows [r0, r0+nr) of U_j (G x Gc, row-major).
 template <class Geo>
 __global__ void RTNB_PASS_BOUNDS_LIGHT k_colA(Dims d, const float* __restrict__ winv,
-                                                  const float2* __restrict__ twG,
+                                                  const float4* __restrict__ twG,
                                                   const float2* __restrict__ chat, float2* __restrict__ U,
                                                   int r0, int nr, const DevState* st, int use_halt) {
   pdl_enter();
@@ -214,7 +214,7 @@ enum Rows1Mode : int { R1_DECODE = 0, R1_OP = 1, R1_SETUP = 2 };
 //          forward row FFT -> V_j (L x G).
 //  SETUP:  window rows: t = rho*c_j (nlinv.cpp:252) -> forward row FFT -> V_j.
 template <class Geo>
-__global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float2* __restrict__ twG,
+__global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restrict__ twG,
                                                    const float2* __restrict__ U,
                                                    const float2* __restrict__ coils,
                                                    const float2* __restrict__ rhom,
@@ -320,7 +320,7 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float2* __restr
 // Toeplitz column pass: forward column FFT of the window rows of V_j, * P/G, inverse
 // column FFT, keep the window rows (in place in V_j). Lines: (j, column q).
 template <class Geo>
-__global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float2* __restrict__ twG,
+__global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
                                                    const float2* __restrict__ P, float2* __restrict__ V,
                                                    const DevState* st, int use_halt) {
   pdl_enter();
@@ -424,7 +424,7 @@ __device__ __forceinline__ void finish_elem(const ColsWArgs& a, size_t e, float2
 // decomp.cpp:26-39; k_colsW adds the groups in order); rt = conj(rho) T -> forward
 // W^-H row pass keeping the Gc coil k-columns -> Y_j (L x Gc).
 template <class Geo>
-__global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float2* __restrict__ twG,
+__global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* __restrict__ twG,
                                                    const float2* __restrict__ V,
                                                    const float2* __restrict__ coils,
                                                    const float2* __restrict__ rhom,
@@ -524,7 +524,7 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float2* 
 // k_rows2, whose reduction partial (st->scal[1]) is folded into the totals here.
 template <class Geo>
 __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float* __restrict__ winv,
-                                                   const float2* __restrict__ twG,
+                                                   const float4* __restrict__ twG,
                                                    const float2* __restrict__ Y,
                                                    const double2* __restrict__ RP,
                                                    const float2* __restrict__ coils,
@@ -1049,7 +1049,7 @@ __global__ void __launch_bounds__(kThreads) k_image(Dims d, const float2* __rest
 // or columns (COLS = true, axis 0); scale applied on output
 template <class Geo, int S, bool COLS>
 __global__ void __launch_bounds__(Geo::NT) k_fft_pass(float2* __restrict__ data, int batch,
-                                                      const float2* __restrict__ twG, float scale) {
+                                                      const float4* __restrict__ twG, float scale) {
   RTNB_TILE_SETUP(COLS);
   constexpr int tiles = (G + Geo::LPB - 1) / Geo::LPB;
   const int img = blockIdx.x / tiles;

@@ -16,17 +16,17 @@ namespace rtnb {
 struct Engine::Ops {
   int G = 0, N1 = 0, N2 = 0, LPB = 0, NT = 0;
   size_t smem = 0;
-  void (*colA)(cudaStream_t, int, Dims, const float*, const float2*, const float2*, float2*, int, int,
+  void (*colA)(cudaStream_t, int, Dims, const float*, const float4*, const float2*, float2*, int, int,
                const DevState*, int) = nullptr;
-  void (*rows1)(cudaStream_t, int, Dims, int, const float2*, const float2*, const float2*, const float2*,
+  void (*rows1)(cudaStream_t, int, Dims, int, const float4*, const float2*, const float2*, const float2*,
                 const float2*, float2*, float2*, const float2*, float2*, const DevState*, int) = nullptr;
-  void (*colsT)(cudaStream_t, int, Dims, const float2*, const float2*, float2*, const DevState*, int) = nullptr;
-  void (*rows2)(cudaStream_t, int, Dims, int, const float2*, const float2*, const float2*,
+  void (*colsT)(cudaStream_t, int, Dims, const float4*, const float2*, float2*, const DevState*, int) = nullptr;
+  void (*rows2)(cudaStream_t, int, Dims, int, const float4*, const float2*, const float2*,
                 const float2*, const float2*, float2*, double2*, double*, DevState*, int) = nullptr;
-  void (*colsW)(cudaStream_t, int, Dims, ColsWArgs, const float*, const float2*, const float2*,
+  void (*colsW)(cudaStream_t, int, Dims, ColsWArgs, const float*, const float4*, const float2*,
                 const double2*, const float2*, const float2*, int, double*, DevState*, CrScalars, int,
                 const GroupView&) = nullptr;
-  void (*fft)(cudaStream_t, int, int, float2*, int, int, const float2*, float) = nullptr;
+  void (*fft)(cudaStream_t, int, int, float2*, int, int, const float4*, float) = nullptr;
 };
 
 namespace {
@@ -56,11 +56,12 @@ void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStre
 }
 
 inline void upload_small_twiddles() {
-  float2 tw[528];
+  float4 tw[528];
   for (int n = 1; n <= 32; ++n) {
     for (int k = 0; k < n; ++k) {
       const double a = -2.0 * 3.14159265358979323846 * k / n;
-      tw[small_tw_offset(n) + k] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+      const float c = static_cast<float>(std::cos(a)), sn = static_cast<float>(std::sin(a));
+      tw[small_tw_offset(n) + k] = make_float4(c, sn, -sn, c);
     }
   }
   check_cuda(cudaMemcpyToSymbol(c_small_tw, tw, sizeof(tw)), "upload small twiddles");
@@ -108,31 +109,31 @@ Engine::Ops Inst<N1, N2>::make() {
   o.LPB = Geo::LPB;
   o.smem = kSmem;
   o.NT = kNT;
-  o.colA = [](cudaStream_t s, int grid, Dims d, const float* winv, const float2* tw, const float2* chat,
+  o.colA = [](cudaStream_t s, int grid, Dims d, const float* winv, const float4* tw, const float2* chat,
               float2* U, int r0, int nr, const DevState* st, int h) {
     launch_k(k_colA<Geo>, grid, kNT, kSmem, s, d, winv, tw, chat, U, r0, nr, st, h);
   };
-  o.rows1 = [](cudaStream_t s, int grid, Dims d, int mode, const float2* tw, const float2* U,
+  o.rows1 = [](cudaStream_t s, int grid, Dims d, int mode, const float4* tw, const float2* U,
                const float2* coils, const float2* rhom, const float2* drho, float2* V, float2* coils_out,
                const float2* rho_src, float2* rhom_out, const DevState* st, int h) {
     launch_k(k_rows1<Geo>, grid, kNT, kSmem, s, d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
              rhom_out, st, h);
   };
-  o.colsT = [](cudaStream_t s, int grid, Dims d, const float2* tw, const float2* P, float2* V,
+  o.colsT = [](cudaStream_t s, int grid, Dims d, const float4* tw, const float2* P, float2* V,
                const DevState* st, int h) {
     launch_k(k_colsT<Geo>, grid, kNT, kSmem, s, d, tw, P, V, st, h);
   };
-  o.rows2 = [](cudaStream_t s, int grid, Dims d, int setup, const float2* tw, const float2* V,
+  o.rows2 = [](cudaStream_t s, int grid, Dims d, int setup, const float4* tw, const float2* V,
                const float2* coils, const float2* rhom, const float2* z, float2* Y, double2* RP,
                double* partials, DevState* st, int h) {
     launch_k(k_rows2<Geo>, grid, kNT, kSmem2, s, d, setup, tw, V, coils, rhom, z, Y, RP, partials, st, h);
   };
-  o.colsW = [](cudaStream_t s, int grid, Dims d, ColsWArgs a, const float* winv, const float2* tw,
+  o.colsW = [](cudaStream_t s, int grid, Dims d, ColsWArgs a, const float* winv, const float4* tw,
                const float2* Y, const double2* RP, const float2* coils, const float2* z, int nbw,
                double* partials, DevState* st, CrScalars cr, int h, const GroupView& gv) {
     launch_k(k_colsW<Geo>, grid, kNT, kSmem, s, d, a, winv, tw, Y, RP, coils, z, nbw, partials, st, cr, h, gv);
   };
-  o.fft = [](cudaStream_t s, int grid, int sign, float2* data, int batch, int axis, const float2* tw,
+  o.fft = [](cudaStream_t s, int grid, int sign, float2* data, int batch, int axis, const float4* tw,
              float scale) {
     if (sign < 0) {
       if (axis == 0) {
