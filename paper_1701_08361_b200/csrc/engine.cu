@@ -425,6 +425,7 @@ void Engine::enq_apply_back(const float2* dx, float2* out, int cw_mode, float al
   a.dx = dx;
   a.out = out;
   a.ap_prev = ap_prev;
+  a.win_only_ok = win_only_ok_;
   const int nbw = J * tGc;
   ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, use_halt, gv_);
 }
@@ -465,12 +466,14 @@ void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
   ensure_cr_capacity(cap);
   if (!sync_each && fused_cr_) {
     // budget-mode graphs: one fused recurrence kernel per iteration (k_cr_fused)
+    win_only_ok_ = 1;
     enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1, nullptr);
     enq_cr_fused(0, tol);
     for (int it = 1; it < cap; ++it) {
       enq_apply(r_, ar_, CW_OPALPHA, alpha, it, 1, ap_);
       enq_cr_fused(it, tol);
     }
+    win_only_ok_ = 0;
     return;
   }
   enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1);
@@ -510,7 +513,7 @@ void Engine::enq_image(const float2* est, float2* img, float scale, bool apply_s
 void Engine::enq_cr_fused(int it, float tol) {
   const int rho_skip = (dims_.grp && !dims_.count_rho) ? plan_.G * plan_.G : 0;
   launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, static_cast<const float2*>(ar_),
-           partials_, st_, cr_, it, tol, rho_skip, dims_.grp);
+           partials_, st_, cr_, it, tol, rho_skip, dims_.grp, plan_.G);
 }
 
 void Engine::join_group(int rank, const GroupView& gv, const GroupScal& gs) {
@@ -899,7 +902,7 @@ double Engine::time_kernel(const char* which, int reps) {
       launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], p_, ap_, partials_, st_, cr_, 1, 0.f);
     } else if (w == "cr_fused") {
       launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], p_, ap_,
-               static_cast<const float2*>(ar_), partials_, st_, cr_, 1, 0.f, 0, 0);
+               static_cast<const float2*>(ar_), partials_, st_, cr_, 1, 0.f, 0, 0, plan_.G);
     } else if (w == "cr_pap") {
       launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], r_, ar_, partials_, st_, cr_, 1);
     } else if (w == "colA") {

@@ -251,7 +251,8 @@ class Engine : public FrameWorker {
   std::vector<int> caps_;       // budget-mode per-step caps
   std::vector<float> alphas_;   // per-step alpha schedule
   bool use_graphs_ = true;
-  bool fused_cr_ = true;   // RTN_FUSED_CR=0 selects the two-kernel recurrence in graphs too
+  bool fused_cr_ = true;
+  int win_only_ok_ = 0;    // the applications being enqueued belong to a fused CR solve   // RTN_FUSED_CR=0 selects the two-kernel recurrence in graphs too
   cudaGraphExec_t step_graph_[kMaxSteps] = {};
   cudaGraphExec_t frame_graph_ = nullptr;
   float2* frame_graph_img_ = nullptr;

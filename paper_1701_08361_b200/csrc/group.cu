@@ -213,6 +213,8 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
     run_cr = !mem_[0]->st_host_->cr_halt;
   }
   if (run_cr) {
+    // the fused recurrence handles every CR vector, so the window-only skip is exact
+    each([&](int, Engine& e) { e.win_only_ok_ = 1; });
     for (int it = 0; it < cap; ++it) {
       each([&](int, Engine& e) { e.enq_apply_front(e.r_, 1); });
       barrier();
@@ -233,6 +235,7 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
       barrier();
       each([&](int, Engine& e) { e.enq_grp_fin(0, -1, cap - 1, tol); });
     }
+    each([&](int, Engine& e) { e.win_only_ok_ = 0; });
   }
   each([&](int, Engine& e) { e.enq_axpy1(); });
 }

@@ -58,11 +58,11 @@ struct DevState {
   int status;     // sticky error for the frame (ST_SOLVER on non-finite values)
   int cr_halt;    // skip the remaining CR work of the current step
   int cur_step;
-  int pad_;
+  int rho_out_known;  // the current step's setup has classified rhs.rho outside the window
   unsigned int counter;  // last-block reduction ticket
   unsigned int pad2_;
   int z_out;      // the loaded data has a nonzero sample outside the window (k_z_outside)
-  int pad3_;
+  int rho_out_nz; // the setup wrote a nonzero rhs.rho entry outside the window
   StepRec steps[kMaxSteps];
   double scal[8];        // scratch scalar outputs (op-level calls)
   double gp[4];          // group mode: this member's SETUP partials {|rhs|^2, resid_out, resid_win, -}

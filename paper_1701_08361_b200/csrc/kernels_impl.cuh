@@ -390,12 +390,23 @@ struct ColsWArgs {
   float2* out2;       // SETUP: p (= r)
   float2* out3;       // SETUP: x_cg (zeroed)
   const float2* ap_prev;  // fused CR: also reduce |out|^2 and Re<ap_prev, out> (nullable)
+  int win_only_ok;        // fused CR: rho entries outside the window may be skipped when the
+                          // step's setup left them exactly zero (see rho_window_only)
 };
+
+// Outside the field-of-view window the normal operator's rho output is zero (T is
+// masked, preproc.cpp:442), so if the Newton step's rhs.rho is exactly zero there, every
+// CR vector (r, p, ap, ar, x_cg) stays exactly zero there for the whole solve
+// (nlinv.cpp:188-232 only combines them linearly). The setup records that (the common
+// case: window-masked data and estimates); the fused CR kernels then skip those entries.
+__device__ __forceinline__ bool rho_window_only(const DevState* st) {
+  return st->rho_out_known && !st->rho_out_nz;
+}
 
 // combine the normal-operator value n at flat index e with the CR / rhs terms and
 // accumulate the reduction the caller needs (Re<dx,out> or |rhs|^2)
-__device__ __forceinline__ void finish_elem(const ColsWArgs& a, size_t e, float2 n, double& acc, double& aa,
-                                            double& pa) {
+__device__ __forceinline__ float2 finish_elem(const ColsWArgs& a, size_t e, float2 n, double& acc, double& aa,
+                                             double& pa) {
   if (a.mode == CW_SETUP) {
     float2 v = axpy_rn(n, a.a_x, a.x[e]);
     v = axpy_rn(v, a.a_reg, a.reg[e]);
@@ -403,6 +414,7 @@ __device__ __forceinline__ void finish_elem(const ColsWArgs& a, size_t e, float2
     a.out2[e] = v;
     a.out3[e] = make_float2(0.f, 0.f);
     acc += nrm2(v);
+    return v;
   } else {
     float2 v = n;
     const float2 p = a.dx[e];
@@ -414,6 +426,7 @@ __device__ __forceinline__ void finish_elem(const ColsWArgs& a, size_t e, float2
       const float2 q = a.ap_prev[e];
       pa += (double)q.x * v.x + (double)q.y * v.y;
     }
+    return v;
   }
 }
 
@@ -577,8 +590,20 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
     // data term sum_j conj(c_j) z_j, in channel order in FP64
     const int H = d.H;
     double dummy0 = 0.0, dummy1 = 0.0, dummy2 = 0.0;
-    for (int e = (blockIdx.x - nbw) * blockDim.x + threadIdx.x; e < D0; e += (gridDim.x - nbw) * blockDim.x) {
-      const int r = e / G, c = e - (e / G) * G;
+    const bool win_only = a.mode != CW_SETUP && a.win_only_ok && rho_window_only(st);
+    const int nv = win_only ? d.L * d.L : D0;
+    int nz = 0;  // SETUP: a nonzero rhs.rho entry outside the window
+    for (int v = (blockIdx.x - nbw) * blockDim.x + threadIdx.x; v < nv; v += (gridDim.x - nbw) * blockDim.x) {
+      int e, r, c;
+      if (win_only) {
+        r = d.lo + v / d.L;
+        c = d.lo + v - (v / d.L) * d.L;
+        e = r * G + c;
+      } else {
+        e = v;
+        r = e / G;
+        c = e - (e / G) * G;
+      }
       double sx = 0.0, sy = 0.0;
       if (d.grp) {
         // channel decomposition: every member's partials, in member order, loaded
@@ -600,11 +625,13 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
           }
         }
         // the rho part of every dot product is replicated: counted on one member
+        float2 o;
         if (d.count_rho) {
-          finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), acc0, aa, pa);
+          o = finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), acc0, aa, pa);
         } else {
-          finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), dummy0, dummy1, dummy2);
+          o = finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), dummy0, dummy1, dummy2);
         }
+        if (a.mode == CW_SETUP && !in_win(d, r, c) && (o.x != 0.f || o.y != 0.f)) nz = 1;
         continue;
       }
       if (in_win(d, r, c)) {
@@ -623,12 +650,15 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
           acc1 += nrm2(zz);
         }
       }
-      finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), acc0, aa, pa);
+      const float2 o = finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), acc0, aa, pa);
+      if (a.mode == CW_SETUP && !in_win(d, r, c) && (o.x != 0.f || o.y != 0.f)) nz = 1;
     }
+    if (a.mode == CW_SETUP && __syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&st->rho_out_nz, 1);
   }
   double vv[4] = {acc0, acc1, aa, pa}, tot[4];
   if (grid_reduce<4>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
     const double total = tot[0];
+    if (a.mode == CW_SETUP) st->rho_out_known = 1;  // every block's atomicOr precedes its ticket
     if (d.grp) {
       // member partials; k_grp_fin forms the totals once every member has them
       if (a.mode == CW_SETUP) {
@@ -674,6 +704,8 @@ __global__ void k_step_begin(DevState* st, int m) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     st->cur_step = m;
     st->cr_halt = 0;
+    st->rho_out_known = 0;
+    st->rho_out_nz = 0;
     StepRec& s = st->steps[m];
     s.iters = 0;
     s.zero_rhs = 0;
@@ -788,7 +820,7 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
                                                        float2* __restrict__ p, float2* __restrict__ ap,
                                                        const float2* __restrict__ ar, double* partials,
                                                        DevState* st, CrScalars cr, int it, float tol,
-                                                       int rho_skip, int grp) {
+                                                       int rho_skip, int grp, int G) {
   pdl_enter();
   if (st->status || st->cr_halt) return;
   const double rar_new = cr.rar[it];
@@ -813,7 +845,13 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
   const double a = upd ? rar_new / denom : 0.0;
   const float bf = (float)b, af = (float)a, naf = (float)(-a);
   double acc_ap = 0.0, acc_r = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
+  // rho entries outside the window are exactly zero in every vector: skip them
+  const bool win_only = rho_window_only(st);
+  const int L = G / 2, lo = (G - L) / 2, G2 = G * G;
+  const int nv = win_only ? D - G2 + L * L : D;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    int i = v;
+    if (win_only) i = v < L * L ? (lo + v / L) * G + lo + (v - (v / L) * L) : G2 + (v - L * L);
     const float2 pv = p[i], apv = ap[i], rv = r[i], arv = ar[i];
     const float2 np = make_float2(__fadd_rn(__fmul_rn(pv.x, bf), rv.x), __fadd_rn(__fmul_rn(pv.y, bf), rv.y));
     const float2 nap = make_float2(__fadd_rn(__fmul_rn(apv.x, bf), arv.x), __fadd_rn(__fmul_rn(apv.y, bf), arv.y));
