@@ -13,6 +13,7 @@ GPU is visible.
 from __future__ import annotations
 
 import ctypes
+import weakref
 import os
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
@@ -357,6 +358,9 @@ class Context:
         return [(out[2 * k], out[2 * k + 1]) for k in range(len(self.devices))]
 
     def close(self):
+        # a series borrows the context's engine: close every live one first
+        for ser in list(getattr(self, "_series", ())):
+            ser.close()
         if self._h:
             self.lib.rtn_ctx_destroy(self._h)
             self._h = ctypes.c_void_p()
@@ -572,6 +576,9 @@ class Series:
         self.lib = ctx.lib
         self.F = frames
         self._h = ctypes.c_void_p()
+        if not hasattr(ctx, "_series"):
+            ctx._series = weakref.WeakSet()
+        ctx._series.add(self)
         if devices:
             dv = (ctypes.c_int * len(devices))(*devices)
             _check(self.lib.rtn_series_create_multi(ctx._h, frames, n_psf, dv, len(devices), ctypes.byref(self._h)))

@@ -849,23 +849,46 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
   const bool win_only = rho_window_only(st);
   const int L = G / 2, lo = (G - L) / 2, G2 = G * G;
   const int nv = win_only ? D - G2 + L * L : D;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
-    int i = v;
-    if (win_only) i = v < L * L ? (lo + v / L) * G + lo + (v - (v / L) * L) : G2 + (v - L * L);
-    const float2 pv = p[i], apv = ap[i], rv = r[i], arv = ar[i];
-    const float2 np = make_float2(__fadd_rn(__fmul_rn(pv.x, bf), rv.x), __fadd_rn(__fmul_rn(pv.y, bf), rv.y));
-    const float2 nap = make_float2(__fadd_rn(__fmul_rn(apv.x, bf), arv.x), __fadd_rn(__fmul_rn(apv.y, bf), arv.y));
-    p[i] = np;
-    ap[i] = nap;
-    float2 nr = rv;
-    if (upd) {
-      x[i] = axpy_rn(x[i], af, np);
-      nr = axpy_rn(rv, naf, nap);
-      r[i] = nr;
+  // four entries per thread per round with every load issued up front (memory-level
+  // parallelism); per-thread accumulation order is unchanged
+  constexpr int kU = 4;
+  const int stride = gridDim.x * blockDim.x;
+  for (int v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < nv; v0 += kU * stride) {
+    int idx[kU];
+    float2 pv[kU], apv[kU], rv[kU], arv[kU], xv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int v = v0 + u * stride;
+      int i = v < nv ? v : -1;
+      if (win_only && i >= 0) i = v < L * L ? (lo + v / L) * G + lo + (v - (v / L) * L) : G2 + (v - L * L);
+      idx[u] = i;
+      if (i >= 0) {
+        pv[u] = p[i];
+        apv[u] = ap[i];
+        rv[u] = r[i];
+        arv[u] = ar[i];
+        if (upd) xv[u] = x[i];
+      }
     }
-    if (i >= rho_skip) {  // group members other than the first skip the replicated rho
-      acc_ap += nrm2(nap);
-      acc_r += nrm2(nr);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = idx[u];
+      if (i < 0) continue;
+      const float2 np = make_float2(__fadd_rn(__fmul_rn(pv[u].x, bf), rv[u].x), __fadd_rn(__fmul_rn(pv[u].y, bf), rv[u].y));
+      const float2 nap =
+          make_float2(__fadd_rn(__fmul_rn(apv[u].x, bf), arv[u].x), __fadd_rn(__fmul_rn(apv[u].y, bf), arv[u].y));
+      p[i] = np;
+      ap[i] = nap;
+      float2 nr = rv[u];
+      if (upd) {
+        x[i] = axpy_rn(xv[u], af, np);
+        nr = axpy_rn(rv[u], naf, nap);
+        r[i] = nr;
+      }
+      if (i >= rho_skip) {  // group members other than the first skip the replicated rho
+        acc_ap += nrm2(nap);
+        acc_r += nrm2(nr);
+      }
     }
   }
   double v[2] = {acc_ap, acc_r}, tot[2];
