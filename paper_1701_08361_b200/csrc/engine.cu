@@ -1,6 +1,7 @@
 // Engine: device buffers, size dispatch and kernel sequencing for one plan.
 #include "engine.hpp"
 
+#include <algorithm>
 #include <atomic>
 #include <cstddef>
 #include <chrono>
@@ -309,8 +310,13 @@ void Engine::alloc() {
     const char* e = std::getenv(k);
     return e ? std::max(1, std::atoi(e)) : dflt;
   };
-  vec_grid_ = std::min(blocks_for(D_, 1 << 20), env_int("RTN_VEC_BLOCKS", 2 * 148));
-  nbr_ = std::min(static_cast<int>((G2 + ops_->NT - 1) / ops_->NT), env_int("RTN_RHO_BLOCKS", 148));
+  // k_cr_fused handles four entries per thread per round
+  vec_grid_ = std::min(std::max(1, (D_ + 4 * kThreads - 1) / (4 * kThreads)), env_int("RTN_VEC_BLOCKS", 2 * 148));
+  // the CR applications touch only the window part of rho (L^2 entries): about 512
+  // entries per block keeps the grid reduction's ticket short (measured best at C3)
+  const int L2w = dims_.L * dims_.L;
+  nbr_ = std::min(static_cast<int>((G2 + ops_->NT - 1) / ops_->NT),
+                  env_int("RTN_RHO_BLOCKS", std::clamp(L2w / 512, 16, 148)));
   const int max_grid = std::max(vec_grid_, plan_.J * ((plan_.G + ops_->LPB - 1) / ops_->LPB) + nbr_ + 8);
   // grid_reduce<K> writes K doubles per block; K <= kMaxReduce
   check_cuda(cudaMalloc(&partials_, sizeof(double) * kMaxReduce * max_grid), "partials");
