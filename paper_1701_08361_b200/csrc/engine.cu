@@ -259,7 +259,7 @@ Engine::~Engine() {
   if (frame_graph_) cudaGraphExecDestroy(frame_graph_);
   void* bufs[] = {winv_, P_, z_, x_, xcg_, r_, p_, ap_, ar_, reg_, est_scratch_[0], est_scratch_[1],
                   est_scratch_[2], coils_, rhom_, U_, V_, Y_, RP_, gbuf_, img_, partials_, st_, cr_buf_,
-                  RPO_, SS_};
+                  RPO_, SS_, RC_, kpart_};
   for (void* b : bufs) {
     if (b) cudaFree(b);
   }
@@ -325,6 +325,17 @@ void Engine::alloc() {
   check_cuda(cudaMallocHost(&st_host_, sizeof(DevState)), "state mirror");
   std::memset(st_host_, 0, sizeof(DevState));
   ensure_cr_capacity(std::max({plan_.cg_max_iter, plan_.cg_iter_budget, 1}));
+  // one thread-block cluster per channel for every non-setup application where the
+  // geometry is instantiated (G = 16 x 16, Gc = G/4); RTN_CLUSTER=0 keeps five kernels
+  {
+    const char* e = std::getenv("RTN_CLUSTER");
+    use_cluster_ = ops_->apply_cluster && plan_.Gc * 4 == plan_.G && !(e && e[0] == '0');
+  }
+  if (use_cluster_) {
+    c2(&RC_, J * L * L, "cluster channel terms");
+    check_cuda(cudaMalloc(&kpart_, sizeof(double) * 3 * plan_.J * ops_->cluster_ctas), "cluster partials");
+    rho_grid_ = std::max(1, static_cast<int>((L * L + kThreads - 1) / kThreads));
+  }
   // alpha schedule and budget split are data independent (nlinv.cpp:295-313)
   float alpha = plan_.alpha0;
   int remaining = plan_.cg_iter_budget;
@@ -406,6 +417,20 @@ void Engine::enq_decode(const float2* est) {
 
 void Engine::enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
                        const float2* ap_prev) {
+  if (use_cluster_ && !dims_.grp && cw_mode != CW_SETUP) {
+    ColsWArgs a{};
+    a.mode = cw_mode;
+    a.alpha = alpha;
+    a.dot_slot = dot_slot;
+    a.dx = dx;
+    a.out = out;
+    a.ap_prev = ap_prev;
+    a.win_only_ok = win_only_ok_;
+    ops_->apply_cluster(s_, plan_.J, dims_, a, winv_, twG_, coils_, rhom_, P_, RC_, kpart_, st_, use_halt);
+    launch_k(k_rho_sum, rho_grid_, kThreads, 0, s_, dims_, a, static_cast<const float2*>(RC_),
+             static_cast<const double*>(kpart_), plan_.J * ops_->cluster_ctas, partials_, st_, cr_, use_halt);
+    return;
+  }
   enq_apply_front(dx, use_halt);
   enq_apply_back(dx, out, cw_mode, alpha, dot_slot, use_halt, ap_prev);
 }

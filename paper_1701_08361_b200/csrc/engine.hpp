@@ -247,6 +247,11 @@ class Engine : public FrameWorker {
   GroupScal gs_{};
   double2* RPO_ = nullptr;
   double* SS_ = nullptr;
+  // cluster-fused applications (kernels_cluster.cuh): channel terms rc_j and per-CTA dots
+  bool use_cluster_ = false;
+  float2* RC_ = nullptr;
+  double* kpart_ = nullptr;
+  int rho_grid_ = 0;
   bool have_cache_ = false;
   std::vector<int> caps_;       // budget-mode per-step caps
   std::vector<float> alphas_;   // per-step alpha schedule

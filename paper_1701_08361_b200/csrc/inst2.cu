@@ -6,7 +6,9 @@ namespace rtnb {
 
 void add_ops_2(std::vector<Engine::Ops>& ops, OpsAttrList& attrs) {
   RTNB_INST(12, 16)
-  RTNB_INST(16, 16)
+  ops.push_back(Inst<16, 16>::make());
+  Inst<16, 16>::add_cluster<8>(ops.back());
+  attrs.push_back({16 * 16, &Inst<16, 16>::set_attrs});
   RTNB_INST(16, 20)
 }
 

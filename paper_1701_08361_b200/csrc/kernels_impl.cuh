@@ -23,6 +23,8 @@
 // (nlinv.cpp:243-270) reuses the same kernels in SETUP mode, and the CR vector
 // recurrences (nlinv.cpp:197-232) are two fused kernels per iteration with
 // device-resident FP64 scalars.
+#pragma once
+
 #include <cuda_runtime.h>
 #include <math.h>
 

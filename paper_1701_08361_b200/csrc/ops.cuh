@@ -10,6 +10,7 @@
 
 #include "engine.hpp"
 #include "kernels_impl.cuh"
+#include "kernels_cluster.cuh"
 
 namespace rtnb {
 
@@ -27,6 +28,11 @@ struct Engine::Ops {
                 const double2*, const float2*, const float2*, int, double*, DevState*, CrScalars, int,
                 const GroupView&) = nullptr;
   void (*fft)(cudaStream_t, int, int, float2*, int, int, const float4*, float) = nullptr;
+  // whole application per channel in one thread-block cluster (kernels_cluster.cuh);
+  // nullptr where not instantiated (grid, tail, CTA count per channel)
+  void (*apply_cluster)(cudaStream_t, int J, Dims, ColsWArgs, const float*, const float4*, const float2*,
+                        const float2*, const float2*, float2*, double*, const DevState*, int) = nullptr;
+  int cluster_ctas = 0;
 };
 
 namespace {
@@ -96,6 +102,8 @@ struct Inst {
   }
 
   static Engine::Ops make();
+  template <int C>
+  static void add_cluster(Engine::Ops& o);
 };
 
 }  // namespace
@@ -152,6 +160,40 @@ Engine::Ops Inst<N1, N2>::make() {
   return o;
 }
 
+
+template <int N1, int N2>
+template <int C>
+void Inst<N1, N2>::add_cluster(Engine::Ops& o) {
+  using CG = ClusterGeom<Geo, C>;
+  o.cluster_ctas = C;
+  o.apply_cluster = [](cudaStream_t s, int J, Dims d, ColsWArgs a, const float* winv, const float4* tw,
+                       const float2* coils, const float2* rhom, const float2* P, float2* RC, double* kpart,
+                       const DevState* st, int h) {
+    static bool attr = [] {
+      check_cuda(cudaFuncSetAttribute(k_apply_cluster<Geo, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(CG::SMEM)),
+                 "attr cluster");
+      return true;
+    }();
+    (void)attr;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(J * C));
+    cfg.blockDim = dim3(static_cast<unsigned>(Geo::NT));
+    cfg.dynamicSmemBytes = CG::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, k_apply_cluster<Geo, C>, d, a, winv, tw, coils, rhom, P, RC, kpart, st, h),
+               "launch cluster apply");
+  };
+}
 
 using OpsAttrList = std::vector<std::pair<int, void (*)()>>;
 void add_ops_0(std::vector<Engine::Ops>& ops, OpsAttrList& attrs);

@@ -285,3 +285,41 @@ def test_shape_and_size_validation(gpu):
         gpu.Context(gpu.ReconPlan(N=8, G=16, Gc=32, J=1))
     with pytest.raises(gpu.UsageError):
         gpu.make_weights_inv(8, 4)
+
+
+@pytest.mark.parametrize("J", [4, 32])
+def test_cluster_fused_application_matches_reference(gpu, ref, J, monkeypatch):
+    # the one-cluster-per-channel application (kernels_cluster.cuh, G = 256, Gc = G/4)
+    # against the reference and against the five-kernel path
+    plan = gpu.raw_plan(256, J)
+    P = radial_psf(ref, plan, 9, J)
+    x = random_estimate(plan, 91 + J)
+    outs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RTN_CLUSTER", flag)
+        with gpu.Context(plan) as ctx:
+            ctx.set_psf(P)
+            ctx.make_step_cache(x)
+            outs[flag] = [ctx.apply_normal(random_estimate(plan, 500 + t)) for t in range(2)]
+    for t in range(2):
+        want = ref.apply_normal(plan, x, random_estimate(plan, 500 + t), P)
+        assert rel_err(outs["1"][t], want) < OP_TOL, t
+        assert rel_err(outs["1"][t], outs["0"][t]) < 1e-6, t
+
+
+def test_cluster_fused_frame_matches_reference(gpu, ref, monkeypatch):
+    # a C4-shaped frame (G = 256, 16 channels) through the cluster path in the budget graphs
+    monkeypatch.setenv("RTN_CLUSTER", "1")
+    plan = gpu.raw_plan(256, 16)
+    plan.newton_steps, plan.cg_iter_budget = 7, 50
+    inp = phantom_frame_inputs(ref, plan, K=15, U=5)
+    z, P = inp["z"][0], inp["P"][0]
+    init = gpu.initial_estimate(plan)
+    with gpu.Context(plan) as ctx:
+        ctx.set_psf(P)
+        ctx.set_data(z)
+        fr = ctx.reconstruct_frame(init)
+    img, est, per, _ = ref.reconstruct_frame(plan, z, P, init, A=4)
+    assert fr.cg_per_step == per
+    assert rel_err(fr.image, img) < FRAME_TOL
+    assert rel_err(fr.est, est) < FRAME_TOL
