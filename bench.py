@@ -557,6 +557,19 @@ def main():
                           "achieved_gbs": app_by / (app_ms / 1000.0) / 1e9},
                 "kernels": kern}
 
+    # latency mode: one frame at a time (T = 1) through the cluster-fused applications,
+    # the paper's per-frame latency figure (device time per frame)
+    latency_mode = None
+    try:
+        lo = pb.SeriesOptions(T=1, plain=True, sched=sched)
+        series.run(lo, first=W, count=NTUNE, want_images=False)
+        lout = series.run(lo, first=W + NTUNE, count=S, want_images=False)
+        lat_span = series.last_span_ms()
+        latency_mode = {"frames_in_flight": 1, "cluster_fused": True, "frames_per_s": S / (lat_span / 1000.0),
+                        "p50_latency_ms": statistics.median(float(v) for v in lout["gpu_ms"])}
+    except Exception as e:  # reported, never fatal
+        latency_mode = {"error": str(e)}
+
     decomp = None
     if world > 1:
         # the paper's decompositions across the GPUs of this node, driven from rank 0 in
@@ -587,6 +600,7 @@ def main():
         "p50_latency_ms": statistics.median(lat), "latency_ms_min_max": [min(lat), max(lat)],
         "e2e": e2e, "gpu_launches": launches_per_frame(caps, M) * S, "roofline": roofline, "autotune": tuning,
         "clocks": clk.summary(),
+        "latency_mode": latency_mode,
     }
     if decomp is not None:
         line["decompositions"] = decomp

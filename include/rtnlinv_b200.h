@@ -161,6 +161,8 @@ typedef struct rtn_series_opts_t {
   int chain;
   int normalize;
   int plain;
+  int cluster; /* cluster-fused applications (one thread-block cluster per channel):
+                  1 on, 0 off, -1 auto = on when T == 1 (latency mode) */
 } rtn_series_opts_t;
 
 int rtn_series_create(rtn_ctx* ctx, int frames, int n_psf, rtn_series** out);

@@ -62,7 +62,8 @@ class _Plan(ctypes.Structure):
 
 class _SeriesOpts(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int), ("A", ctypes.c_int), ("sched_l", ctypes.c_int), ("sched_o", ctypes.c_int),
-                ("chain", ctypes.c_int), ("normalize", ctypes.c_int), ("plain", ctypes.c_int)]
+                ("chain", ctypes.c_int), ("normalize", ctypes.c_int), ("plain", ctypes.c_int),
+                ("cluster", ctypes.c_int)]
 
 
 @dataclass
@@ -542,10 +543,11 @@ class SeriesOptions:
     chain: bool = True
     normalize: bool = True
     plain: bool = False
+    cluster: int = -1  # cluster-fused applications: 1 on, 0 off, -1 auto (on when T == 1)
 
     def to_c(self) -> _SeriesOpts:
         return _SeriesOpts(self.T, self.A, self.sched.l, self.sched.o, int(self.chain), int(self.normalize),
-                           int(self.plain))
+                           int(self.plain), int(self.cluster))
 
 
 @dataclass

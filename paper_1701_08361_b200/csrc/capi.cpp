@@ -494,6 +494,7 @@ static int series_run_impl(rtn_series* s, const rtn_series_opts_t* o, int first,
     so.chain = o->chain != 0;
     so.normalize = o->normalize != 0;
     so.plain = o->plain != 0;
+    so.cluster = o->cluster;
     std::vector<rtnb::SeriesFrameOut> out;
     ser(s).run(so, first, count, z_host, images, &out, raw);
     const int M = s->ctx->eng->plan().newton_steps;

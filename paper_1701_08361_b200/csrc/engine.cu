@@ -317,7 +317,7 @@ void Engine::alloc() {
   const int L2w = dims_.L * dims_.L;
   nbr_ = std::min(static_cast<int>((G2 + ops_->NT - 1) / ops_->NT),
                   env_int("RTN_RHO_BLOCKS", std::clamp(L2w / 512, 16, 148)));
-  const int max_grid = std::max(vec_grid_, plan_.J * ((plan_.G + ops_->LPB - 1) / ops_->LPB) + nbr_ + 8);
+  const int max_grid = std::max({vec_grid_, plan_.J * ((plan_.G + ops_->LPB - 1) / ops_->LPB) + nbr_ + 8, 4 * 148});
   // grid_reduce<K> writes K doubles per block; K <= kMaxReduce
   check_cuda(cudaMalloc(&partials_, sizeof(double) * kMaxReduce * max_grid), "partials");
   check_cuda(cudaMalloc(&st_, sizeof(DevState)), "state");
@@ -331,10 +331,11 @@ void Engine::alloc() {
     const char* e = std::getenv("RTN_CLUSTER");
     use_cluster_ = ops_->apply_cluster && plan_.Gc * 4 == plan_.G && !(e && e[0] == '0');
   }
-  if (use_cluster_) {
+  if (use_cluster_) {  // supported: latency mode by default
     c2(&RC_, J * L * L, "cluster channel terms");
     check_cuda(cudaMalloc(&kpart_, sizeof(double) * 3 * plan_.J * ops_->cluster_ctas), "cluster partials");
-    rho_grid_ = std::max(1, static_cast<int>((L * L + kThreads - 1) / kThreads));
+    // 32 window entries (x J channel terms) per block
+    rho_grid_ = std::max(1, std::min(static_cast<int>((L * L + kRhoTile - 1) / kRhoTile), 4 * 148));
   }
   // alpha schedule and budget split are data independent (nlinv.cpp:295-313)
   float alpha = plan_.alpha0;
@@ -371,6 +372,20 @@ void Engine::ensure_cr_capacity(int max_iter) {
 }
 
 void Engine::sync() { check_cuda(cudaStreamSynchronize(s_), "stream sync"); }
+
+void Engine::set_cluster(bool on) {
+  on = on && cluster_supported();
+  if (on == use_cluster_) return;
+  // captured graphs embed the kernel choice
+  sync();
+  for (auto& g : step_graph_) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
+  }
+  if (frame_graph_) cudaGraphExecDestroy(frame_graph_);
+  frame_graph_ = nullptr;
+  use_cluster_ = on;
+}
 
 void Engine::read_state() {
   check_cuda(cudaMemcpyAsync(st_host_, st_, sizeof(DevState), cudaMemcpyDeviceToHost, s_), "state read");

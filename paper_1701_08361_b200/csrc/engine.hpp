@@ -153,6 +153,11 @@ class Engine : public FrameWorker {
   float2* image_dev() override { return img_; }
   const std::vector<int>& budget_caps() const { return caps_; }
   void set_use_graphs(bool on) { use_graphs_ = on; }
+  // latency mode: every non-setup application as one thread-block cluster per channel
+  // (kernels_cluster.cuh) where the geometry supports it; throughput mode (several
+  // frames in flight): the five-kernel passes, which share the SMs better
+  void set_cluster(bool on);
+  bool cluster_supported() const { return RC_ != nullptr; }
 
   float2* x_dev() { return x_; }
   float2* reg_dev() { return reg_; }
@@ -248,7 +253,7 @@ class Engine : public FrameWorker {
   double2* RPO_ = nullptr;
   double* SS_ = nullptr;
   // cluster-fused applications (kernels_cluster.cuh): channel terms rc_j and per-CTA dots
-  bool use_cluster_ = false;
+  bool use_cluster_ = false;  // current mode (set_cluster); RC_ != nullptr: supported
   float2* RC_ = nullptr;
   double* kpart_ = nullptr;
   int rho_grid_ = 0;

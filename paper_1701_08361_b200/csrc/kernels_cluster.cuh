@@ -42,6 +42,12 @@ __device__ __forceinline__ void st_cluster(uint32_t addr, float2 v) {
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ int cluster_rank() {
   int r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -346,39 +352,67 @@ __global__ void __launch_bounds__(Geo::NT, 2)
 }
 
 #ifndef RTNB_PASS_ONLY
-// out.rho = sum_j rc_j (FP64, channel order) on the window (zero outside, where T is
-// masked), the CR "+alpha dx" and the dots of the rho part; the last block adds the
+// out.rho = sum_j rc_j on the window (zero outside, where T is masked) in FP64 in a
+// fixed order, the CR "+alpha dx" and the dots of the rho part; the last block adds the
 // coil-part partials of k_apply_cluster (fixed order) and publishes rar / saa / spa.
+// A block takes 32 consecutive entries: lane = entry (coalesced channel rows), warp w
+// sums channels w, w + 8, ... (independent loads in flight), the 8 warp partials are
+// added in warp order in shared memory.
+constexpr int kRhoTile = 32;
 __global__ void __launch_bounds__(kThreads) k_rho_sum(Dims d, ColsWArgs a, const float2* __restrict__ RC,
                                                       const double* __restrict__ kpart, int nk, double* partials,
                                                       DevState* st, CrScalars cr, int use_halt) {
   pdl_enter();
   if (st->status || (use_halt && st->cr_halt)) return;
+  __shared__ double2 part[kThreads / 32][kRhoTile];
   const int G = d.G, L = d.L, D0 = G * G;
   const bool win_only = a.win_only_ok && rho_window_only(st);
   const int nv = win_only ? L * L : D0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kThreads / 32;
   double acc = 0.0, aa = 0.0, pa = 0.0;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
-    int e, r, c;
-    if (win_only) {
-      r = d.lo + v / L;
-      c = d.lo + v - (v / L) * L;
-      e = r * G + c;
-    } else {
-      e = v;
-      r = e / G;
-      c = e - (e / G) * G;
-    }
-    double sx = 0.0, sy = 0.0;
-    if (in_win(d, r, c)) {
-      const float2* src = RC + (size_t)(r - d.lo) * L + (c - d.lo);
-      for (int j = 0; j < d.J; ++j) {
-        const float2 t = src[(size_t)j * L * L];
-        sx += t.x;
-        sy += t.y;
+  for (int v0 = blockIdx.x * kRhoTile; v0 < nv; v0 += gridDim.x * kRhoTile) {
+    const int v = v0 + lane;
+    int e = -1, r = 0, c = 0;
+    if (v < nv) {
+      if (win_only) {
+        r = d.lo + v / L;
+        c = d.lo + v - (v / L) * L;
+        e = r * G + c;
+      } else {
+        e = v;
+        r = e / G;
+        c = e - (e / G) * G;
       }
     }
-    finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), acc, aa, pa);
+    double sx = 0.0, sy = 0.0;
+    if (e >= 0 && in_win(d, r, c)) {
+      const float2* src = RC + (size_t)(r - d.lo) * L + (c - d.lo);
+      constexpr int kB = 4;
+      for (int j0 = warp; j0 < d.J; j0 += kB * nw) {
+        float2 t[kB];
+#pragma unroll
+        for (int q = 0; q < kB; ++q) {
+          const int jj = j0 + q * nw;
+          t[q] = jj < d.J ? __ldcg(src + (size_t)jj * L * L) : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < kB; ++q) {
+          sx += t[q].x;
+          sy += t[q].y;
+        }
+      }
+    }
+    part[warp][lane] = make_double2(sx, sy);
+    __syncthreads();
+    if (warp == 0 && e >= 0) {
+      double tx = 0.0, ty = 0.0;
+      for (int w = 0; w < nw; ++w) {
+        tx += part[w][lane].x;
+        ty += part[w][lane].y;
+      }
+      finish_elem(a, (size_t)e, make_float2((float)tx, (float)ty), acc, aa, pa);
+    }
+    __syncthreads();
   }
   double vv[3] = {acc, aa, pa}, tot[3];
   if (grid_reduce<3>(vv, partials, &st->counter, tot)) {
@@ -404,7 +438,6 @@ __global__ void __launch_bounds__(kThreads) k_rho_sum(Dims d, ColsWArgs a, const
     }
   }
 }
-
 #endif  // RTNB_PASS_ONLY
 
 }  // namespace rtnb

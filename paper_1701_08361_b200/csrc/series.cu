@@ -412,6 +412,13 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   }
   const int T = o.plain ? 1 : std::min(o.T, count);
   for (int t = 1; t < T; ++t) worker(t);
+  // one frame at a time: the latency-optimised cluster path; several in flight: the
+  // five-kernel passes, whose smaller blocks interleave across frames
+  const bool cl = o.cluster < 0 ? T == 1 : o.cluster != 0;
+  if (A_ == 1) {
+    eng0_.set_cluster(cl);
+    for (auto& ex : extra_) ex->set_cluster(cl);
+  }
   check_cuda(cudaEventRecord(span0_, copy_), "span event");
   for (int t = 0; t < T; ++t) check_cuda(cudaStreamWaitEvent(worker(t).stream(), span0_, 0), "span wait");
 

@@ -22,6 +22,7 @@ struct SeriesOptions {
   bool chain = true;
   bool normalize = true;
   bool plain = false;   // reconstruct_series_plain semantics (strictly sequential)
+  int cluster = -1;     // cluster-fused applications: 1 on, 0 off, -1 auto (on when T == 1)
 };
 
 // Raw acquisition input of the end-to-end path (KSpaceFrame per frame, seqsim.hpp:52-65):
