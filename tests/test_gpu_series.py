@@ -259,3 +259,27 @@ def test_raw_acquisitions_with_device_coil_compression(gpu, ref):
     got = _raw_series(gpu, plan, F, U, samples, angles, gpu.SeriesOptions(plain=True), cmat=m)
     for n in range(F):
         assert rel_err(got["images"][n], want["images"][n]) < FRAME_TOL, n
+
+
+@pytest.mark.parametrize("T,cluster", [(1, -1), (2, 1), (2, 0)])
+def test_g256_series_cluster_and_pass_paths_match_reference(gpu, ref, T, cluster):
+    # G = 256 instantiates the cluster-fused application (latency mode, on by default for
+    # T = 1); both paths replay the reference frame by frame
+    plan = gpu.raw_plan(256, 4)
+    plan.newton_steps, plan.cg_iter_budget = 3, 9
+    F = 4
+    _, _, z, P, idx = _series_inputs(ref, plan, F=F, K=15, U=2, noise=0.0, seed=4)
+    out = _run(gpu, plan, z, P, idx, gpu.SeriesOptions(T=T, plain=(T == 1), cluster=cluster,
+                                                       sched=gpu.TemporalSchedule(1, 1)))
+    M = plan.newton_steps
+    scale = out["series"].normalize()
+    zs = (z * np.float32(scale)).astype(np.complex64)
+    unity = gpu.initial_estimate(plan)
+    ests = {}
+    for n in range(F):
+        a = out["audit"][n]
+        init = unity if a.init_src < 0 else ests[a.init_src]
+        regs = [unity if a.init_src < 0 else ests[a.reg_src[m]] for m in range(M)]
+        img, est, _ = ref.reconstruct_frame_regs(plan, zs[n], P[idx[n]], init, regs)
+        ests[n] = est
+        assert rel_err(out["images"][n], img * np.float32(1.0 / scale)) < FRAME_TOL, n
