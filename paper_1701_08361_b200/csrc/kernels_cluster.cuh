@@ -75,6 +75,10 @@ struct ClusterGeom {
   static_assert(L % C == 0 && G % C == 0 && GC % C == 0, "cluster split");
   static_assert(OFF % N2 == 0 && GC % N2 == 0 && OFF % N1 == 0 && GC % N1 == 0, "coil band on the DFT grid");
   static_assert(RPC <= Geo::LPB && GCPC <= Geo::LPB && CPC % Geo::LPB == 0, "line batches");
+  // step-2 slots k2 of the window outputs p = k1 + N1 k2 in [LO, LO + L) and of the coil
+  // band [OFF, OFF + GC): the same for every k1 (prefetch indexing)
+  static_assert(LO % N1 == 0 && L % N1 == 0, "window on the DFT grid");
+  static constexpr int WK0 = LO / N1, WKN = L / N1, GK0 = OFF / N1, GKN = GC / N1;
 };
 
 namespace {
@@ -151,7 +155,21 @@ __global__ void __launch_bounds__(Geo::NT, 2)
       }
     }
   }
-  cluster_barrier();
+  // pass B's pointwise operands (c_j, drho on its window rows) load while the cluster
+  // barrier completes
+  constexpr int WK0 = CG::WK0, WKN = CG::WKN;
+  float2 pf0[WKN], pf1[WKN];
+  cluster_arrive();
+  if (r2.on && r2.l < RPC) {
+    const size_t row = (size_t)(LO + rank * RPC + r2.l) * G;
+#pragma unroll
+    for (int kk = 0; kk < WKN; ++kk) {
+      const size_t e = row + r2.k + N1 * (WK0 + kk);
+      pf0[kk] = cj[e];
+      pf1[kk] = dx[e];
+    }
+  }
+  cluster_wait();
 
   // ---- pass B: rows1 on this CTA's window rows -> V columns ------------------------------
   {
@@ -178,7 +196,7 @@ __global__ void __launch_bounds__(Geo::NT, 2)
           const size_t e = (size_t)R2 * G + p;
           const float2 aw = cscale(flip(u[k2], p), d.invG);
           // t = c_j * drho + rho * (W^-1 dchat_j)   (nlinv.cpp:163)
-          const float2 s1 = cmul_rn(cj[e], dx[e]);
+          const float2 s1 = cmul_rn(pf0[k2 - WK0], pf1[k2 - WK0]);
           const float2 s2 = cmul_rn(rhom[e], aw);
           w = flip(make_float2(__fadd_rn(s1.x, s2.x), __fadd_rn(s1.y, s2.y)), p);
         }
@@ -253,12 +271,22 @@ __global__ void __launch_bounds__(Geo::NT, 2)
     }
     __syncthreads();
   }
-  cluster_barrier();
+  cluster_arrive();
+  if (r2.on && r2.l < RPC) {
+    const size_t row = (size_t)(LO + rank * RPC + r2.l) * G;
+#pragma unroll
+    for (int kk = 0; kk < WKN; ++kk) {
+      const size_t e = row + r2.k + N1 * (WK0 + kk);
+      pf0[kk] = cj[e];
+      pf1[kk] = rhom[e];
+    }
+  }
+  cluster_wait();
 
   // ---- pass D: rows2 on this CTA's window rows -> rc_j (global), Y columns ---------------
   {
     const bool a1 = r1.on && r1.l < RPC, a2 = r2.on && r2.l < RPC;
-    const int r = rank * RPC + r2.l, R2 = LO + r;
+    const int r = rank * RPC + r2.l;
     if (a1) {
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) {
@@ -271,8 +299,6 @@ __global__ void __launch_bounds__(Geo::NT, 2)
     __syncthreads();
     if (a2) {
       fft_step2<Geo, +1, Geo::WIN_K2>(A, r2.l, r2.k, u);
-      const float2* cr = cj + (size_t)R2 * G;
-      const float2* rr = rhom + (size_t)R2 * G;
       float2* rc = RC + (size_t)j * L * L + (size_t)r * L;
 #pragma unroll
       for (int k2 = 0; k2 < N2; ++k2) {
@@ -280,8 +306,8 @@ __global__ void __launch_bounds__(Geo::NT, 2)
         float2 w = make_float2(0.f, 0.f);
         if (p >= LO && p < LO + L) {
           const float2 T = cscale(flip(u[k2], p), d.invG);
-          rc[p - LO] = cjmul_rn(cr[p], T);  // rc_j = conj(c_j) T_j   (nlinv.cpp:166)
-          w = flip(cjmul_rn(rr[p], T), p);  // rt_j = conj(rho) T_j   (nlinv.cpp:167)
+          rc[p - LO] = cjmul_rn(pf0[k2 - WK0], T);  // rc_j = conj(c_j) T_j   (nlinv.cpp:166)
+          w = flip(cjmul_rn(pf1[k2 - WK0], T), p);  // rt_j = conj(rho) T_j   (nlinv.cpp:167)
         }
         u[k2] = w;
       }
