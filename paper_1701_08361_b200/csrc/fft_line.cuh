@@ -358,6 +358,14 @@ struct LineGeom {
   static constexpr uint32_t ALL_N2 = full_mask(N2);
   static constexpr uint32_t WIN_N1 = ((G / 4) % N2 == 0) ? range_mask((G / 4) / N2, (3 * G / 4) / N2) : ALL_N1;
   static constexpr uint32_t WIN_K2 = ((G / 4) % N1 == 0) ? range_mask((G / 4) / N1, (3 * G / 4) / N1) : ALL_N2;
+  // The coil band [G/2 - Gc/2, G/2 + Gc/2) of the W^-1 / W^-H transforms for Gc = G/4
+  // (coil_grid_side, planner.hpp:66): the step-1 inputs a W^-1 line can have, the step-2
+  // outputs a W^-H line needs, when the band lies on the DFT grid (else: all)
+  static constexpr int OFFC = G / 2 - (G / 4) / 2;
+  static constexpr uint32_t GC_N1 =
+      (OFFC % N2 == 0 && (G / 4) % N2 == 0) ? range_mask(OFFC / N2, (OFFC + G / 4) / N2) : ALL_N1;
+  static constexpr uint32_t GC_K2 =
+      (OFFC % N1 == 0 && (G / 4) % N1 == 0) ? range_mask(OFFC / N1, (OFFC + G / 4) / N1) : ALL_N2;
   __device__ __forceinline__ static int a(int l, int q) { return l * LS + q + q / N2; }
 };
 

@@ -187,7 +187,11 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colA(Dims d, const float* __restrict__ 
         v[n1] = flip(make_float2(c.x * w, c.y * w), t);  // chat * winv.real() (nlinv.cpp:121)
       }
     }
-    fft_step1<Geo, +1>(v, i1.k, twG);
+    if (d.Gc * 4 == G) {  // pruned: only the coil band can be nonzero
+      fft_step1<Geo, +1, Geo::GC_N1>(v, i1.k, twG);
+    } else {
+      fft_step1<Geo, +1>(v, i1.k, twG);
+    }
     park_step1<Geo>(A, i1.l, i1.k, v);
   }
   __syncthreads();
@@ -247,7 +251,11 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restr
         const int qk = t - d.off;
         v[n1] = (qk >= 0 && qk < d.Gc) ? flip(Uj[(size_t)r1 * d.Gc + qk], t) : make_float2(0.f, 0.f);
       }
-      fft_step1<Geo, +1>(v, i1.k, twG);
+      if (d.Gc * 4 == G) {  // pruned: only the coil band can be nonzero
+        fft_step1<Geo, +1, Geo::GC_N1>(v, i1.k, twG);
+      } else {
+        fft_step1<Geo, +1>(v, i1.k, twG);
+      }
       park_step1<Geo>(A, i1.l, i1.k, v);
     }
     __syncthreads();
@@ -513,7 +521,11 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
   }
   __syncthreads();
   if (a2) {
-    fft_step2<Geo, -1>(A, i2.l, i2.k, u);
+    if (d.Gc * 4 == G) {  // pruned: only the coil band is kept
+      fft_step2<Geo, -1, Geo::GC_K2>(A, i2.l, i2.k, u);
+    } else {
+      fft_step2<Geo, -1>(A, i2.l, i2.k, u);
+    }
     float2* Yr = Y + (size_t)(j0 + i2.l) * d.L * d.Gc + (size_t)rl * d.Gc;
 #pragma unroll
     for (int k2 = 0; k2 < N2; ++k2) {
@@ -571,7 +583,11 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
     __syncthreads();
     if (a2) {
       float2 u[N2];
-      fft_step2<Geo, -1>(A, i2.l, i2.k, u);
+      if (d.Gc * 4 == G) {  // pruned: only the coil band is kept
+        fft_step2<Geo, -1, Geo::GC_K2>(A, i2.l, i2.k, u);
+      } else {
+        fft_step2<Geo, -1>(A, i2.l, i2.k, u);
+      }
       const int q = q0 + i2.l;
 #pragma unroll
       for (int k2 = 0; k2 < N2; ++k2) {
