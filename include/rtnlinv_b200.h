@@ -68,6 +68,19 @@ void rtn_ctx_destroy(rtn_ctx* ctx);
  * rtn_make_step_cache (rho_out = coils_out = NULL), rtn_apply_normal and
  * rtn_reconstruct_frame; the other per-context entry points return 2. */
 int rtn_ctx_create_group(const rtn_plan_t* plan, const int* devices, int n_devices, int a_cap, rtn_ctx** out);
+/* The same decomposition with one process per GPU (torchrun layout): this process
+ * owns member `rank` of `members` on `device`. Each member exports its cross-member
+ * buffers as CUDA IPC handles (rtn_ctx_proc_handles: call with out = NULL to get the
+ * size), the caller exchanges them (e.g. an all-gather over torch.distributed) and
+ * hands every member's handles in rank order to rtn_ctx_proc_attach. Barriers are
+ * device-side epoch flags, so every member must make the same calls in the same
+ * order. Supports rtn_set_psf, rtn_set_data (full J*G*G arrays; each member takes its
+ * block) and rtn_reconstruct_frame (full-layout init / reg; every member returns the
+ * full image and estimate). */
+int rtn_ctx_create_proc_member(const rtn_plan_t* plan, int device, int rank, int members, int a_cap,
+                               rtn_ctx** out);
+int rtn_ctx_proc_handles(rtn_ctx* ctx, void* out, int* nbytes);
+int rtn_ctx_proc_attach(rtn_ctx* ctx, const void* all, int nbytes);
 /* the members' channel blocks, 2*n_devices ints {j0, j1} */
 int rtn_ctx_group_blocks(rtn_ctx* ctx, int* out_pairs);
 

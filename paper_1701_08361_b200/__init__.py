@@ -136,6 +136,10 @@ def load_library(path: str = LIB_PATH):
         "rtn_ctx_create_group": ([ctypes.POINTER(_Plan), i, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
                                  ctypes.c_int),
         "rtn_ctx_group_blocks": ([vp, i], ctypes.c_int),
+        "rtn_ctx_create_proc_member": ([ctypes.POINTER(_Plan), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(vp)], ctypes.c_int),
+        "rtn_ctx_proc_handles": ([vp, vp, i], ctypes.c_int),
+        "rtn_ctx_proc_attach": ([vp, vp, ctypes.c_int], ctypes.c_int),
         "rtn_grid_adjoint": ([vp, f, ctypes.c_int, d, ctypes.c_int, ctypes.c_int, ctypes.c_double, f], ctypes.c_int),
         "rtn_grid_spread": ([vp, f, ctypes.c_int, d, ctypes.c_int, ctypes.c_int, ctypes.c_double, f], ctypes.c_int),
         "rtn_build_psf": ([vp, d, ctypes.c_int, ctypes.c_int, f], ctypes.c_int),
@@ -336,18 +340,37 @@ class Context:
     on device devices[k]; a device may repeat (members then share that GPU)."""
 
     def __init__(self, plan: ReconPlan, device: int = 0, devices: Optional[Sequence[int]] = None,
-                 a_cap: int = 8):
+                 a_cap: int = 8, member: Optional[Sequence[int]] = None):
+        """member=(rank, members): this process's member of a one-process-per-GPU channel
+        group (connect the members with connect_members)"""
         self.lib = load_library()
         self.plan = plan
         self._h = ctypes.c_void_p()
         self.devices = None if devices is None else [int(d) for d in devices]
+        self.member = None if member is None else (int(member[0]), int(member[1]))
         c = plan.to_c()
-        if self.devices is None:
+        if self.member is not None:
+            _check(self.lib.rtn_ctx_create_proc_member(ctypes.byref(c), device, self.member[0], self.member[1], a_cap,
+                                                       ctypes.byref(self._h)))
+        elif self.devices is None:
             _check(self.lib.rtn_ctx_create(ctypes.byref(c), device, ctypes.byref(self._h)))
         else:
             arr = (ctypes.c_int * len(self.devices))(*self.devices)
             _check(self.lib.rtn_ctx_create_group(ctypes.byref(c), arr, len(self.devices), a_cap,
                                                  ctypes.byref(self._h)))
+
+    def ipc_handles(self) -> bytes:
+        """this member's CUDA IPC handles (process-group members)"""
+        n = ctypes.c_int(0)
+        _check(self.lib.rtn_ctx_proc_handles(self._h, None, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        _check(self.lib.rtn_ctx_proc_handles(self._h, buf, ctypes.byref(n)))
+        return buf.raw
+
+    def attach(self, handles: Sequence[bytes]):
+        """every member's ipc_handles() in rank order"""
+        blob = b"".join(handles)
+        _check(self.lib.rtn_ctx_proc_attach(self._h, blob, len(blob)))
 
     @property
     def group_blocks(self):
@@ -814,6 +837,16 @@ def median3_sequence(mags) -> np.ndarray:
 def grid_supported(G: int) -> bool:
     """the fused line engine covers grid side G (else transforms fall back to the direct DFT kernel)"""
     return bool(load_library().rtn_grid_supported(G))
+
+
+def connect_members(ctx: "Context", group=None):
+    """exchange the members' IPC handles over torch.distributed (any backend; the
+    handles are small host objects) and attach them"""
+    import torch.distributed as dist
+    mine = ctx.ipc_handles()
+    allh = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allh, mine, group=group)
+    ctx.attach(allh)
 
 
 def psf_angle_key(angles, S: int, G: int) -> int:

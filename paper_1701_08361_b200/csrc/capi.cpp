@@ -12,6 +12,7 @@
 #include "../../include/rtnlinv_b200.h"
 #include "engine.hpp"
 #include "group.hpp"
+#include "procgroup.hpp"
 #include "preproc.hpp"
 #include "post.hpp"
 #include "sched.hpp"
@@ -20,6 +21,7 @@
 struct rtn_ctx {
   rtnb::Engine* eng = nullptr;
   rtnb::Group* grp = nullptr;  // channel-decomposed context (rtn_ctx_create_group)
+  rtnb::ProcGroup* pg = nullptr;  // one member of a one-process-per-GPU group
   std::unique_ptr<rtnb::Preproc> pre;  // pre stage, created on first use
 };
 
@@ -63,7 +65,7 @@ rtnb::Plan to_plan(const rtn_plan_t* p) {
 }
 
 rtnb::Engine& eng(rtn_ctx* c) {
-  if (c && c->grp) rtnb::fail(2, "this entry point is not available on a channel-group context");
+  if (c && (c->grp || c->pg)) rtnb::fail(2, "this entry point is not available on a channel-group context");
   if (!c || !c->eng) rtnb::fail(2, "null context");
   return *c->eng;
 }
@@ -140,6 +142,45 @@ int rtn_ctx_create_group(const rtn_plan_t* plan, const int* devices, int n_devic
   });
 }
 
+int rtn_ctx_create_proc_member(const rtn_plan_t* plan, int device, int rank, int members, int a_cap,
+                               rtn_ctx** out) {
+  return guarded([&] {
+    if (!plan || !out) rtnb::fail(2, "rtn_ctx_create_proc_member: null argument");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) rtnb::fail(5, "no CUDA device available");
+    if (device < 0 || device >= n) rtnb::fail(2, "rtn_ctx_create_proc_member: device index out of range");
+    auto* c = new rtn_ctx;
+    try {
+      c->pg = new rtnb::ProcGroup(to_plan(plan), device, rank, members, a_cap);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int rtn_ctx_proc_handles(rtn_ctx* ctx, void* out, int* nbytes) {
+  return guarded([&] {
+    if (!ctx || !ctx->pg || !nbytes) rtnb::fail(2, "rtn_ctx_proc_handles: not a process-group member");
+    const int need = static_cast<int>(sizeof(cudaIpcMemHandle_t)) * rtnb::ProcGroup::kHandles;
+    if (out) {
+      if (*nbytes < need) rtnb::fail(2, "rtn_ctx_proc_handles: buffer too small");
+      ctx->pg->export_handles(static_cast<cudaIpcMemHandle_t*>(out));
+    }
+    *nbytes = need;
+  });
+}
+
+int rtn_ctx_proc_attach(rtn_ctx* ctx, const void* all, int nbytes) {
+  return guarded([&] {
+    if (!ctx || !ctx->pg || !all) rtnb::fail(2, "rtn_ctx_proc_attach: not a process-group member");
+    const int need = static_cast<int>(sizeof(cudaIpcMemHandle_t)) * rtnb::ProcGroup::kHandles * ctx->pg->members();
+    if (nbytes != need) rtnb::fail(2, "rtn_ctx_proc_attach: expected every member's handles in rank order");
+    ctx->pg->attach(static_cast<const cudaIpcMemHandle_t*>(all));
+  });
+}
+
 int rtn_ctx_group_blocks(rtn_ctx* ctx, int* out_pairs) {
   return guarded([&] {
     if (!ctx || !ctx->grp) rtnb::fail(2, "rtn_ctx_group_blocks: not a channel-group context");
@@ -152,10 +193,12 @@ int rtn_ctx_group_blocks(rtn_ctx* ctx, int* out_pairs) {
 }
 
 static rtnb::Preproc& pre(rtn_ctx* c) {
-  if (!c || (!c->eng && !c->grp)) rtnb::fail(2, "null context");
+  if (!c || (!c->eng && !c->grp && !c->pg)) rtnb::fail(2, "null context");
   if (!c->pre) {
     if (c->grp) {
       c->pre = std::make_unique<rtnb::Preproc>(c->grp->plan(), c->grp->device());
+    } else if (c->pg) {
+      c->pre = std::make_unique<rtnb::Preproc>(c->pg->plan(), c->pg->device());
     } else {
       c->pre = std::make_unique<rtnb::Preproc>(c->eng->plan(), c->eng->device());
     }
@@ -295,6 +338,7 @@ uint64_t rtn_psf_angle_key(const double* angles, int K, int S, int G) {
 void rtn_ctx_destroy(rtn_ctx* ctx) {
   if (!ctx) return;
   ctx->pre.reset();
+  delete ctx->pg;
   delete ctx->grp;
   delete ctx->eng;
   delete ctx;
@@ -343,6 +387,8 @@ int rtn_set_psf(rtn_ctx* ctx, const float* P) {
   return guarded([&] {
     if (ctx && ctx->grp) {
       ctx->grp->set_psf(P);
+    } else if (ctx && ctx->pg) {
+      ctx->pg->set_psf(P);
     } else {
       eng(ctx).set_psf(P);
     }
@@ -352,6 +398,8 @@ int rtn_set_data(rtn_ctx* ctx, const float* z) {
   return guarded([&] {
     if (ctx && ctx->grp) {
       ctx->grp->set_data(z);
+    } else if (ctx && ctx->pg) {
+      ctx->pg->set_data(z);
     } else {
       eng(ctx).set_data(z);
     }
@@ -403,6 +451,8 @@ int rtn_reconstruct_frame(rtn_ctx* ctx, const float* init, const float* reg, flo
     rtnb::FrameStats st;
     if (ctx && ctx->grp) {
       ctx->grp->reconstruct_frame(init, reg, image, est_out, &st);
+    } else if (ctx && ctx->pg) {
+      ctx->pg->reconstruct_frame(init, reg, image, est_out, &st);
     } else {
       eng(ctx).reconstruct_frame(init, reg, image, est_out, &st);
     }

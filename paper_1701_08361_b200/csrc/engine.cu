@@ -373,6 +373,8 @@ void Engine::ensure_cr_capacity(int max_iter) {
 
 void Engine::sync() { check_cuda(cudaStreamSynchronize(s_), "stream sync"); }
 
+int Engine::line_batch() const { return ops_->LPB; }
+
 void Engine::set_cluster(bool on) {
   on = on && cluster_supported();
   if (on == use_cluster_) return;
@@ -581,6 +583,10 @@ void Engine::enq_z_scan() {
   check_cuda(cudaMemsetAsync(&st_->z_out, 0, sizeof(int), s_), "z scan reset");
   launch_k(k_z_outside, blocks_for(static_cast<long long>(plan_.J) * plan_.G * plan_.G, 148 * 4), kThreads, 0, s_,
            dims_, static_cast<const float2*>(z_), st_);
+}
+
+void Engine::enq_pg_barrier(int* own_flags, const GroupFlags& f) {
+  launch_k(k_pg_barrier, 1, 32, 0, s_, own_flags, f);
 }
 
 void Engine::enq_state_reset() { check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset"); }

@@ -158,6 +158,7 @@ class Engine : public FrameWorker {
   // frames in flight): the five-kernel passes, which share the SMs better
   void set_cluster(bool on);
   bool cluster_supported() const { return RC_ != nullptr; }
+  int line_batch() const;  // lines per block of the pass kernels (channel-group size of k_rows2)
 
   float2* x_dev() { return x_; }
   float2* reg_dev() { return reg_; }
@@ -179,6 +180,7 @@ class Engine : public FrameWorker {
 
  private:
   friend class Group;
+  friend class ProcGroup;
   void alloc();
   void ensure_cr_capacity(int max_iter);
   void enq_step_begin(int m);
@@ -203,6 +205,7 @@ class Engine : public FrameWorker {
   void enq_z_scan();  // st->z_out for the data now in z_ (stream ordered)
   void enq_coil_ss();
   void enq_image_grp(float2* img, float scale, bool apply_scale);
+  void enq_pg_barrier(int* own_flags, const GroupFlags& f);
   void enq_cr(float alpha, float tol, int cap, bool sync_each);
   void enq_newton_step(int m, float2* x, const float2* reg, float alpha, float tol, int cap,
                        bool sync_each);

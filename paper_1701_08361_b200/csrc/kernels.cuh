@@ -76,6 +76,12 @@ struct GroupScal {
   const double* ss[kMaxGroup];      // final image: per-member sum_j |c_j|^2 (N x N)
 };
 
+// One-process-per-GPU groups (procgroup.hpp): every member's published barrier epoch
+struct GroupFlags {
+  int A;
+  const int* flag[kMaxGroup];
+};
+
 // CR scalars of the current step: rar[k] = <r, A r> after apply k, ap2[k] = |ap|^2
 // after update k, rn[k] = |r| after iteration k (cg_solve nlinv.cpp:179-234).
 struct CrScalars {

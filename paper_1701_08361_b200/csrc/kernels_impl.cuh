@@ -1084,6 +1084,35 @@ __global__ void __launch_bounds__(kThreads) k_z_outside(Dims d, const float2* __
   if (__syncthreads_or(any) && threadIdx.x == 0) st->z_out = 1;
 }
 
+// All-member barrier of a one-process-per-GPU group (procgroup.hpp): bump this
+// member's epoch counter, publish it with a system-scope release (after the stream's
+// earlier kernels, whose writes the fence makes visible to the peers), then poll every
+// member's published epoch with acquire loads until all have reached it. Every member
+// runs the same barrier sequence, so the counters advance in lockstep and captured
+// graphs replay correctly.
+__global__ void k_pg_barrier(int* own, GroupFlags f) {
+  pdl_enter();
+  __shared__ int epoch;
+  if (threadIdx.x == 0) {
+    const int e = own[1] + 1;
+    own[1] = e;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(own), "r"(e) : "memory");
+    epoch = e;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < f.A) {
+    const int e = epoch;
+    for (;;) {
+      int v;
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(f.flag[threadIdx.x]) : "memory");
+      if (v >= e) break;
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+}
+
 // x += 1.0 * x_cg  (newton_step, nlinv.cpp:281)
 __global__ void __launch_bounds__(kThreads) k_axpy1(int D, float2* __restrict__ x, const float2* __restrict__ d,
                                                     const DevState* st) {
