@@ -396,6 +396,28 @@ def decompositions(pb, plan, frames, P, U, sched, ngpu):
     return res
 
 
+def channel_processes(pb, plan, frames, P, world, rank, local, S):
+    """frames/s of one frame sequence reconstructed by all ranks as one channel group"""
+    ctx = pb.Context(plan, device=local, member=(rank, world), a_cap=8)
+    pb.connect_members(ctx)
+    z = frames[0]
+    nsq = float(np.sum(np.abs(z.astype(np.complex128)) ** 2))
+    z = (z * np.float32(100.0 / math.sqrt(nsq))).astype(np.complex64)
+    ctx.set_psf(P[0])
+    ctx.set_data(z)
+    est = pb.initial_estimate(plan)
+    for _ in range(2):
+        est = ctx.reconstruct_frame(est, est).est
+    barrier(world, local)
+    t0 = time.perf_counter()
+    for _ in range(S):
+        est = ctx.reconstruct_frame(est, est).est
+    wall = max_over_ranks(time.perf_counter() - t0, world, local)
+    ctx.close()
+    return {"members": world, "frames_per_s": S / wall, "ms_per_frame": 1000.0 * wall / S,
+            "path": "rtn_reconstruct_frame per frame (host in / out), chained, wall clock, max over ranks"}
+
+
 # ------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------
@@ -583,6 +605,15 @@ def main():
             except Exception as e:  # reported, never fatal for the headline line
                 decomp = {"error": str(e)}
         barrier(world, local)
+        # the same channel decomposition with one process per GPU: every rank is one
+        # member (CUDA IPC views of the peers, device-side barriers), one chained frame
+        # sequence for the whole job (strong scaling), host in / host out per frame
+        try:
+            procs = channel_processes(pb, plan, frames, P, world, rank, local, S)
+        except Exception as e:
+            procs = {"error": str(e)}
+        if rank == 0 and decomp is not None:
+            decomp["channel_processes"] = procs
 
     if rank != 0:
         return
