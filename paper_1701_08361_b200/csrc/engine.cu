@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <numbers>
@@ -112,10 +113,23 @@ struct Registry {
 Registry& registry() {
   static Registry* r = [] {
     auto* reg = new Registry;
-add_ops_0(reg->ops, reg->attrs);
+    add_ops_0(reg->ops, reg->attrs);
     add_ops_1(reg->ops, reg->attrs);
     add_ops_2(reg->ops, reg->attrs);
     add_ops_3(reg->ops, reg->attrs);
+    // Per-kernel factorisation preferences (measured, scripts/prof_kernels.py): the last
+    // registration of a grid side is its default; a kernel may come from another
+    // factorisation with the same lines per block (same k_rows2 channel grouping)
+    auto prefer_rows2 = [&](int G, int N1, int N2) {
+      Engine::Ops* dflt = nullptr;
+      const Engine::Ops* alt = nullptr;
+      for (auto& o : reg->ops) {
+        if (o.G == G) dflt = &o;
+        if (o.G == G && o.N1 == N1 && o.N2 == N2) alt = &o;
+      }
+      if (dflt && alt && dflt != alt && dflt->LPB == alt->LPB) dflt->rows2 = alt->rows2;
+    };
+    prefer_rows2(320, 20, 16);
     return reg;
   }();
   return *r;
@@ -126,8 +140,11 @@ const Engine::Ops* ops_for(int G, int dev) {
   Registry& r = registry();
   std::lock_guard<std::mutex> lock(r.mu);
   const Engine::Ops* found = nullptr;
+  // RTN_GEO_<G>=N1xN2 picks one of several factorisations of G (tuning)
+  int want1 = 0, want2 = 0;
+  if (const char* e = std::getenv(("RTN_GEO_" + std::to_string(G)).c_str())) std::sscanf(e, "%dx%d", &want1, &want2);
   for (const auto& o : r.ops) {
-    if (o.G == G) found = &o;
+    if (o.G == G && (!want1 || (o.N1 == want1 && o.N2 == want2))) found = &o;
   }
   if (!found) return nullptr;
   if (dev < 0 || dev >= 64) fail(2, "device index out of range");

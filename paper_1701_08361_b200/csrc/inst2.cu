@@ -9,6 +9,7 @@ void add_ops_2(std::vector<Engine::Ops>& ops, OpsAttrList& attrs) {
   ops.push_back(Inst<16, 16>::make());
   Inst<16, 16>::add_cluster<8>(ops.back());
   attrs.push_back({16 * 16, &Inst<16, 16>::set_attrs});
+  RTNB_INST(20, 16)  // k_rows2 at G = 320 (C2): faster than 16 x 20 (ops_for merges)
   RTNB_INST(16, 20)
 }
 
