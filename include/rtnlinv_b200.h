@@ -209,6 +209,10 @@ int rtn_series_run_raw(rtn_series* s, const rtn_series_opts_t* opts, int first, 
                        int* audit, uint64_t* seqs, int* cg_iters, float* gpu_ms);
 /* distinct PSFs built by rtn_series_run_raw so far */
 int rtn_series_psf_cache_size(rtn_series* s);
+/* PsfCache::save / load (preproc.cpp:346-388): the series' device PSF cache as the
+ * reference's "PSFC" v1 sidecar file (interchangeable); 3 on I/O or format errors */
+int rtn_series_psf_cache_save(rtn_series* s, const char* path);
+int rtn_series_psf_cache_load(rtn_series* s, const char* path);
 /* postprocessing of the device-resident images [first, first+count) to host floats:
  * mode 0 magnitude (count*N*N), 1 magnitude + temporal median-of-3 (count*N*N),
  * 2 phase difference of frame pairs (count/2 * N*N) */

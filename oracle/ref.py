@@ -304,6 +304,21 @@ def reconstruct_series(plan, samples, angles, T=1, A=1, sched=(1, 1), chain=True
     return dict(images=images, audit=audit, seqs=seqs, cg_iters=cg, seconds=secs, data_scale=scale.value)
 
 
+def psf_cache_save(plan, angle_sets, S, path):
+    a = np.ascontiguousarray(angle_sets, np.float64)
+    _chk(lib().ref_psf_cache_save(ctypes.byref(plan_c(plan)), _dp(a), a.shape[0], a.shape[1], S, str(path).encode()))
+
+
+def psf_cache_get(plan, path, angles, S):
+    """(P, hits, size) after loading the sidecar and asking for one angle set"""
+    a = np.ascontiguousarray(angles, np.float64)
+    P = np.zeros((plan.G, plan.G), np.complex64)
+    hits, size = ctypes.c_int(0), ctypes.c_int(0)
+    _chk(lib().ref_psf_cache_get(ctypes.byref(plan_c(plan)), str(path).encode(), _dp(a), len(a), S, _fp(P),
+                                 ctypes.byref(hits), ctypes.byref(size)))
+    return P, hits.value, size.value
+
+
 # ---- planner / postprocessing -------------------------------------------------------------------
 def select_grid(N, table, gamma_min=1.4, gamma_max=2.0):
     sizes = np.array(sorted(table), np.int32)

@@ -377,6 +377,27 @@ int ref_median_filter(const float* mags, int F, int N, float* out) {
   });
 }
 
+// PsfCache (preproc.cpp:315-388): build the kernels of `nsets` angle sets, save them
+int ref_psf_cache_save(const ref_plan_t* p, const double* angles, int nsets, int K, int S, const char* path) {
+  return guarded([&] {
+    PsfCache c(to_plan(p));
+    for (int n = 0; n < nsets; ++n) c.get(std::vector<double>(angles + static_cast<size_t>(n) * K, angles + static_cast<size_t>(n + 1) * K), S);
+    if (!c.save(path)) throw DataError("psf cache save failed");
+  });
+}
+// load a sidecar and return the kernel of one angle set (build it if absent: count hits)
+int ref_psf_cache_get(const ref_plan_t* p, const char* path, const double* angles, int K, int S, float* P_out,
+                      int* hits, int* size) {
+  return guarded([&] {
+    PsfCache c(to_plan(p));
+    if (!c.load(path)) throw DataError("psf cache load failed");
+    const auto k = c.get(std::vector<double>(angles, angles + K), S);
+    store_img(k->P, P_out);
+    *hits = static_cast<int>(c.hits());
+    *size = static_cast<int>(c.size());
+  });
+}
+
 // ---- primitives ---------------------------------------------------------------------
 
 int ref_fft(float* data, int n, int sign) {

@@ -186,6 +186,8 @@ def load_library(path: str = LIB_PATH):
                                 ctypes.c_int, ctypes.c_double, vp, ctypes.c_int, vp, i,
                                 ctypes.POINTER(ctypes.c_uint64), i, f], ctypes.c_int),
         "rtn_series_psf_cache_size": ([vp], ctypes.c_int),
+        "rtn_series_psf_cache_save": ([vp, ctypes.c_char_p], ctypes.c_int),
+        "rtn_series_psf_cache_load": ([vp, ctypes.c_char_p], ctypes.c_int),
         "rtn_series_estimate": ([vp, ctypes.c_int, f], ctypes.c_int),
         "rtn_series_last_span_ms": ([vp], ctypes.c_float),
         "rtn_partition_channels": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, i], ctypes.c_int),
@@ -701,6 +703,12 @@ class Series:
         out = np.zeros((n, p.N, p.N), np.float32)
         _check(self.lib.rtn_series_post(self._h, first, count, m, _fp(out)))
         return out
+
+    def save_psf_cache(self, path):
+        _check(self.lib.rtn_series_psf_cache_save(self._h, str(path).encode()))
+
+    def load_psf_cache(self, path):
+        _check(self.lib.rtn_series_psf_cache_load(self._h, str(path).encode()))
 
     def psf_cache_size(self) -> int:
         return int(self.lib.rtn_series_psf_cache_size(self._h))

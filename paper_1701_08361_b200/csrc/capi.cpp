@@ -591,6 +591,17 @@ int rtn_series_run_raw(rtn_series* s, const rtn_series_opts_t* o, int first, int
 
 int rtn_series_psf_cache_size(rtn_series* s) { return (s && s->s) ? s->s->psf_cache_size() : 0; }
 
+int rtn_series_psf_cache_save(rtn_series* s, const char* path) {
+  return guarded([&] {
+    if (!path || !ser(s).save_psf_cache(path)) rtnb::fail(3, "psf cache: cannot write " + std::string(path ? path : ""));
+  });
+}
+int rtn_series_psf_cache_load(rtn_series* s, const char* path) {
+  return guarded([&] {
+    if (!path || !ser(s).load_psf_cache(path)) rtnb::fail(3, "psf cache: cannot read " + std::string(path ? path : ""));
+  });
+}
+
 int rtn_series_post(rtn_series* s, int first, int count, int mode, float* out) {
   return guarded([&] { ser(s).post(first, count, mode, out); });
 }

@@ -1,9 +1,12 @@
 // Series drivers over device-resident frames (nlinv.cpp:366-526).
 #include "series.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "post.hpp"
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
@@ -159,8 +162,18 @@ double Series::normalize() {
   return scale_;
 }
 
+namespace {
+// NVTX range for a profiler timeline (SURVEY.md §5 "tracing"); no-op without a tool
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& ledger, SeriesFrameOut& out,
                        cudaEvent_t ready) {
+  const std::string label = "frame " + std::to_string(n) + " worker " + std::to_string(t);
+  NvtxRange range(label.c_str());
   FrameWorker& e = worker(t);
   const Plan& p = e.plan();
   const int M = p.newton_steps;
@@ -275,6 +288,56 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   ledger.mark_complete(n);
 }
 
+// PsfCache::save / load (preproc.cpp:346-388): "PSFC" v1, G, count, then per entry the
+// angle key and the G x G complex64 kernel; the file is interchangeable with the reference's
+bool Series::save_psf_cache(const std::string& path) {
+  const uint32_t magic = 0x43465350u, version = 1, G = static_cast<uint32_t>(eng0_.plan().G);
+  const uint32_t count = static_cast<uint32_t>(psf_keys_.size());
+  std::vector<float2> host(psz_);
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) return false;
+  bool ok = std::fwrite(&magic, 4, 1, f) == 1 && std::fwrite(&version, 4, 1, f) == 1 &&
+            std::fwrite(&G, 4, 1, f) == 1 && std::fwrite(&count, 4, 1, f) == 1;
+  check_cuda(cudaSetDevice(eng0_.device()), "set device");
+  for (uint32_t e = 0; ok && e < count; ++e) {
+    check_cuda(cudaMemcpy(host.data(), psf_ + psz_ * e, sizeof(float2) * psz_, cudaMemcpyDeviceToHost), "psf d2h");
+    ok = std::fwrite(&psf_keys_[e], 8, 1, f) == 1 && std::fwrite(host.data(), sizeof(float2), psz_, f) == psz_;
+  }
+  return std::fclose(f) == 0 && ok;
+}
+
+bool Series::load_psf_cache(const std::string& path) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return false;
+  uint32_t magic = 0, version = 0, G = 0, count = 0;
+  bool ok = std::fread(&magic, 4, 1, f) == 1 && std::fread(&version, 4, 1, f) == 1 && std::fread(&G, 4, 1, f) == 1 &&
+            std::fread(&count, 4, 1, f) == 1 && magic == 0x43465350u && version == 1 &&
+            G == static_cast<uint32_t>(eng0_.plan().G);
+  std::vector<std::pair<uint64_t, std::vector<float2>>> entries;
+  for (uint32_t e = 0; ok && e < count; ++e) {
+    uint64_t key = 0;
+    std::vector<float2> P(psz_);
+    ok = std::fread(&key, 8, 1, f) == 1 && std::fread(P.data(), sizeof(float2), psz_, f) == psz_;
+    if (ok) entries.emplace_back(key, std::move(P));
+  }
+  std::fclose(f);
+  if (!ok) return false;
+  check_cuda(cudaSetDevice(eng0_.device()), "set device");
+  for (auto& [key, P] : entries) {  // insert or replace, like the reference's map
+    int slot = -1;
+    for (size_t i = 0; i < psf_keys_.size(); ++i) {
+      if (psf_keys_[i] == key) slot = static_cast<int>(i);
+    }
+    if (slot < 0) {
+      if (static_cast<int>(psf_keys_.size()) >= n_psf_) fail(2, "load_psf_cache: more kernels than PSF slots");
+      slot = static_cast<int>(psf_keys_.size());
+      psf_keys_.push_back(key);
+    }
+    check_cuda(cudaMemcpy(psf_ + psz_ * slot, P.data(), sizeof(float2) * psz_, cudaMemcpyHostToDevice), "psf h2d");
+  }
+  return true;
+}
+
 void Series::post(int first, int count, int mode, float* out) {
   if (first < 0 || count < 1 || first + count > F_) fail(2, "series post: frame range out of bounds");
   if (mode < 0 || mode > 2) fail(2, "series post: unknown mode");
@@ -307,6 +370,7 @@ void Series::post(int first, int count, int mode, float* out) {
 
 void Series::produce_frames(const SeriesOptions& o, int first, int count, const float* z_host,
                             const RawInput* raw, std::vector<cudaEvent_t>& ready) {
+  NvtxRange range(raw ? "pre stage (raw acquisitions)" : "frame upload");
   const Plan& p = eng0_.plan();
   const size_t nsamp = raw ? static_cast<size_t>(raw->K) * raw->S : 0;
   if (raw) {

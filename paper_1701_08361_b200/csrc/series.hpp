@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "engine.hpp"
@@ -83,6 +84,9 @@ class Series {
   void run(const SeriesOptions& o, int first, int count, const float* z_host, float* images_host,
            std::vector<SeriesFrameOut>* out, const RawInput* raw = nullptr);
   int psf_cache_size() const { return static_cast<int>(psf_keys_.size()); }
+  // the device PSF cache in the reference's sidecar format (PsfCache::save / load)
+  bool save_psf_cache(const std::string& path);
+  bool load_psf_cache(const std::string& path);
   // postprocessing of the device-resident images [first, first + count) into host floats:
   // mode 0 magnitude, 1 magnitude + temporal median-of-3 (MedianFilter3 over the range),
   // 2 phase difference of consecutive frame pairs (count/2 images); pipeline.cpp:60-137

@@ -283,3 +283,33 @@ def test_g256_series_cluster_and_pass_paths_match_reference(gpu, ref, T, cluster
         img, est, _ = ref.reconstruct_frame_regs(plan, zs[n], P[idx[n]], init, regs)
         ests[n] = est
         assert rel_err(out["images"][n], img * np.float32(1.0 / scale)) < FRAME_TOL, n
+
+
+def test_psf_cache_sidecar_interchanges_with_the_reference(gpu, ref, tmp_path):
+    # PsfCache::save / load (preproc.cpp:346-388): the device cache writes and reads the
+    # reference's "PSFC" v1 file
+    plan = gpu.make_plan(24, 3)
+    plan.newton_steps, plan.cg_iter_budget = 3, 9
+    F, U = 5, 5
+    samples, angles = ref.phantom_series(3, F, 11, U, plan.N, 1e-3, 41)
+    s = gpu.Series(gpu.Context(plan), F, U)
+    s.run(gpu.SeriesOptions(plain=True), raw=dict(samples=samples, angles=angles))
+    ours = tmp_path / "ours.psfc"
+    s.save_psf_cache(ours)
+    for n in range(U):  # the reference loads our file and finds every kernel (no rebuild)
+        P, hits, size = ref.psf_cache_get(plan, ours, angles[n], 2 * plan.N)
+        assert hits == 1 and size == U
+        assert rel_err(P, ref.build_psf(plan, angles[n], 2 * plan.N)) < 1e-5
+    theirs = tmp_path / "theirs.psfc"
+    ref.psf_cache_save(plan, angles[:U], 2 * plan.N, theirs)
+    s2 = gpu.Series(gpu.Context(plan), F, U)
+    s2.load_psf_cache(theirs)
+    assert s2.psf_cache_size() == U
+    out = s2.run(gpu.SeriesOptions(plain=True), raw=dict(samples=samples, angles=angles))
+    assert s2.psf_cache_size() == U  # every angle set hit the loaded cache
+    want = ref.reconstruct_series(plan, samples, angles, plain=True)
+    for n in range(F):
+        assert rel_err(out["images"][n], want["images"][n]) < FRAME_TOL, n
+    (tmp_path / "bad.psfc").write_bytes(b"nope")
+    with pytest.raises(gpu.DataError):
+        s2.load_psf_cache(tmp_path / "bad.psfc")
