@@ -398,8 +398,18 @@ def decompositions(pb, plan, frames, P, U, sched, ngpu):
 
 def channel_processes(pb, plan, frames, P, world, rank, local, S):
     """frames/s of one frame sequence reconstructed by all ranks as one channel group"""
-    ctx = pb.Context(plan, device=local, member=(rank, world), a_cap=8)
-    pb.connect_members(ctx)
+    # every rank must have its member before any enters the device-side barriers (a
+    # missing member would otherwise only surface at the barrier deadline)
+    ctx, err = None, ""
+    try:
+        ctx = pb.Context(plan, device=local, member=(rank, world), a_cap=8)
+        pb.connect_members(ctx)
+    except Exception as e:
+        err = str(e)
+    if max_over_ranks(1.0 if err else 0.0, world, local) > 0:
+        if ctx is not None:
+            ctx.close()
+        raise RuntimeError("process-group setup failed on some rank" + (f": {err}" if err else ""))
     z = frames[0]
     nsq = float(np.sum(np.abs(z.astype(np.complex128)) ** 2))
     z = (z * np.float32(100.0 / math.sqrt(nsq))).astype(np.complex64)

@@ -413,6 +413,7 @@ void Engine::read_state() {
 
 void Engine::raise_status(const char* where) {
   if (st_host_->status == ST_SOLVER) fail(4, std::string(where) + ": iteration diverged or produced non-finite values");
+  if (st_host_->status == ST_DEADLINE) fail(4, std::string(where) + ": a group member missed the barrier deadline");
   if (st_host_->status != ST_OK) fail(st_host_->status, std::string(where) + ": device error");
 }
 
@@ -603,7 +604,7 @@ void Engine::enq_z_scan() {
 }
 
 void Engine::enq_pg_barrier(int* own_flags, const GroupFlags& f) {
-  launch_k(k_pg_barrier, 1, 32, 0, s_, own_flags, f);
+  launch_k(k_pg_barrier, 1, 32, 0, s_, own_flags, f, st_);
 }
 
 void Engine::enq_state_reset() { check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset"); }

@@ -40,7 +40,7 @@ enum ColsWMode : int { CW_OP = 0, CW_OPALPHA = 1, CW_SETUP = 2 };
 // largest K of any grid_reduce<K> (sizes the per-block partials buffer)
 constexpr int kMaxReduce = 4;
 
-enum Status : int { ST_OK = 0, ST_USAGE = 2, ST_DATA = 3, ST_SOLVER = 4 };
+enum Status : int { ST_OK = 0, ST_USAGE = 2, ST_DATA = 3, ST_SOLVER = 4, ST_DEADLINE = 6 };
 
 // Per-frame device state. Scalars are indexed by Newton step m and CR iteration.
 // All reductions are FP64 (types.hpp:47-59) and deterministic (fixed-order

@@ -1090,23 +1090,41 @@ __global__ void __launch_bounds__(kThreads) k_z_outside(Dims d, const float2* __
 // member's published epoch with acquire loads until all have reached it. Every member
 // runs the same barrier sequence, so the counters advance in lockstep and captured
 // graphs replay correctly.
-__global__ void k_pg_barrier(int* own, GroupFlags f) {
+// A member that does not arrive within the deadline (about 10 s of SM clock) turns the
+// wait into the reference's DecompFault (WorkerGroup deadline, decomp.hpp:90-93): the
+// status goes to ST_DEADLINE, every later kernel of the frame skips, the host raises.
+constexpr long long kBarrierDeadlineCycles = 20000000000LL;
+constexpr int kBarrierPoison = 0x7fffffff;
+__global__ void k_pg_barrier(int* own, GroupFlags f, DevState* st) {
   pdl_enter();
   __shared__ int epoch;
   if (threadIdx.x == 0) {
     const int e = own[1] + 1;
     own[1] = e;
     __threadfence_system();
-    asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(own), "r"(e) : "memory");
+    if (own[0] != kBarrierPoison) {  // a poisoned member stays poisoned
+      asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(own), "r"(e) : "memory");
+    }
     epoch = e;
   }
   __syncthreads();
-  if ((int)threadIdx.x < f.A) {
+  // a member whose frame already failed only keeps its epoch count in step
+  if ((int)threadIdx.x < f.A && !st->status) {
     const int e = epoch;
+    const long long t0 = clock64();
     for (;;) {
       int v;
       asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(f.flag[threadIdx.x]) : "memory");
+      if (v == kBarrierPoison) {  // a member missed a deadline: the whole group fails
+        atomicExch(&st->status, (int)ST_DEADLINE);
+        break;
+      }
       if (v >= e) break;
+      if (clock64() - t0 > kBarrierDeadlineCycles) {
+        atomicExch(&st->status, (int)ST_DEADLINE);
+        asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(own), "r"(kBarrierPoison) : "memory");
+        break;
+      }
       __nanosleep(256);
     }
   }

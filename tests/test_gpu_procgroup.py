@@ -80,3 +80,57 @@ def test_two_process_channel_group_matches_in_process_group_and_reference(gpu, r
     rimg, rest, rper, _ = ref.reconstruct_frame(plan, z, P, init, A=2)
     assert cg0 == rper
     assert rel_err(img0, rimg) < 1e-3 and rel_err(est0, rest) < 1e-3
+
+
+def _member_absent(rank, world, port, plan_args, z, P, q):
+    # rank 1 connects but never reconstructs: rank 0 must fail at the barrier deadline
+    # (the reference's WorkerGroup deadline -> DecompFault), not hang
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import time
+        import torch.distributed as dist
+        import paper_1701_08361_b200 as pb
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        plan = pb.make_plan(*plan_args[:2])
+        plan.newton_steps, plan.cg_iter_budget = plan_args[2], plan_args[3]
+        ctx = pb.Context(plan, device=0, member=(rank, world))
+        pb.connect_members(ctx)
+        ctx.set_psf(P)
+        ctx.set_data(z)
+        if rank == 0:
+            t0 = time.time()
+            try:
+                ctx.reconstruct_frame(pb.initial_estimate(plan))
+                q.put((rank, "no error", time.time() - t0))
+            except pb.SolverError as e:
+                q.put((rank, "DecompFault", time.time() - t0))
+        else:
+            time.sleep(25)
+            q.put((rank, "idle", 0.0))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, "error", repr(e)))
+
+
+@pytest.mark.timeout(300)
+def test_missing_member_fails_at_the_barrier_deadline(gpu, ref):
+    plan = gpu.make_plan(16, 2)
+    plan.newton_steps, plan.cg_iter_budget = 2, 4
+    inp = phantom_frame_inputs(ref, plan, K=7, U=1)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_member_absent, args=(r, 2, port, (16, 2, 2, 4), inp["z"][0], inp["P"][0], q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        res = sorted([q.get(timeout=200) for _ in procs], key=lambda r: r[0])
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    assert res[0][1] == "DecompFault", res
+    assert res[0][2] < 60
