@@ -27,6 +27,8 @@ for k in range(U):
 s.set_psf_index([n % U for n in range(F)])
 s.normalize()
 sched = pb.TemporalSchedule.for_turns(U)
+if os.environ.get("RTN_SCHED"):  # "l,o" override of the reference default for_turns(U)
+    sched = pb.TemporalSchedule(*[int(v) for v in os.environ["RTN_SCHED"].split(",")])
 for T, A in pairs:
     o = pb.SeriesOptions(T=T, A=A, plain=(T == 1), sched=sched)
     s.run(o, first=0, count=8, want_images=False)
