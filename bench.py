@@ -462,7 +462,7 @@ def main():
     plan.newton_steps, plan.cg_iter_budget = 7, 50
     M = plan.newton_steps
     W, S = args.warmup, args.steps
-    NTUNE = 8 if args.T == "auto" else 0  # frames per autotune candidate, past the strict prefix
+    NTUNE = 16 if args.T == "auto" else 0  # frames per autotune candidate, past the strict prefix
     F = W + NTUNE + S
 
     z_unique, P = synth_series(G, J, K, U, n_unique=min(F, 10), seed=1234 + rank)
@@ -493,7 +493,8 @@ def main():
         space = [c for c in pb.legal_configs(6, a_cap=4)]
         for _ in space:
             T_try, A_try = pb.learn_step(key, db, 6, 4)
-            series.run(opts_for(T_try, A_try), first=W, count=2, want_images=False)  # graph capture
+            # graph capture on every worker (frame n runs on worker n mod T)
+            series.run(opts_for(T_try, A_try), first=W, count=T_try + 1, want_images=False)
             series.run(opts_for(T_try, A_try), first=W, count=NTUNE, want_images=False)
             ms = series.last_span_ms() / NTUNE
             db.append(key + (T_try, A_try, ms))
