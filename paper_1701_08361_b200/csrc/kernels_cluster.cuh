@@ -379,11 +379,12 @@ __global__ void __launch_bounds__(Geo::NT, 2)
 
 #ifndef RTNB_PASS_ONLY
 // out.rho = sum_j rc_j on the window (zero outside, where T is masked) in FP64 in a
-// fixed order, the CR "+alpha dx" and the dots of the rho part; the last block adds the
-// coil-part partials of k_apply_cluster (fixed order) and publishes rar / saa / spa.
-// A block takes 32 consecutive entries: lane = entry (coalesced channel rows), warp w
-// sums channels w, w + 8, ... (independent loads in flight), the 8 warp partials are
-// added in warp order in shared memory.
+// fixed order, the CR "+alpha dx" and the dots of the rho part, plus the coil-part
+// partials of k_apply_cluster (block b takes entries b, b + grid, ...); one grid
+// reduction publishes rar / saa / spa. A block takes 32 consecutive entries: lane =
+// entry (coalesced channel rows), warp w sums channels w, w + 8, ... (independent loads
+// in flight), the 8 warp partials are added in warp order in shared memory. Warp 0
+// loads the finish operands (dx, ap_prev) before the channel sums land.
 constexpr int kRhoTile = 32;
 __global__ void __launch_bounds__(kThreads) k_rho_sum(Dims d, ColsWArgs a, const float2* __restrict__ RC,
                                                       const double* __restrict__ kpart, int nk, double* partials,
@@ -396,6 +397,11 @@ __global__ void __launch_bounds__(kThreads) k_rho_sum(Dims d, ColsWArgs a, const
   const int nv = win_only ? L * L : D0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kThreads / 32;
   double acc = 0.0, aa = 0.0, pa = 0.0;
+  for (int i = blockIdx.x + threadIdx.x * gridDim.x; i < nk; i += blockDim.x * gridDim.x) {
+    acc += __ldcg(kpart + 3 * i);
+    aa += __ldcg(kpart + 3 * i + 1);
+    pa += __ldcg(kpart + 3 * i + 2);
+  }
   for (int v0 = blockIdx.x * kRhoTile; v0 < nv; v0 += gridDim.x * kRhoTile) {
     const int v = v0 + lane;
     int e = -1, r = 0, c = 0;
@@ -409,6 +415,11 @@ __global__ void __launch_bounds__(kThreads) k_rho_sum(Dims d, ColsWArgs a, const
         r = e / G;
         c = e - (e / G) * G;
       }
+    }
+    float2 pdx = make_float2(0.f, 0.f), pap = make_float2(0.f, 0.f);
+    if (warp == 0 && e >= 0) {
+      pdx = a.dx[e];
+      if (a.ap_prev) pap = a.ap_prev[e];
     }
     double sx = 0.0, sy = 0.0;
     if (e >= 0 && in_win(d, r, c)) {
@@ -436,31 +447,24 @@ __global__ void __launch_bounds__(kThreads) k_rho_sum(Dims d, ColsWArgs a, const
         tx += part[w][lane].x;
         ty += part[w][lane].y;
       }
-      finish_elem(a, (size_t)e, make_float2((float)tx, (float)ty), acc, aa, pa);
+      // finish_elem's operator branch with the operands loaded above
+      float2 o = make_float2((float)tx, (float)ty);
+      if (a.mode == CW_OPALPHA) o = axpy_rn(o, a.alpha, pdx);
+      a.out[e] = o;
+      acc += (double)pdx.x * o.x + (double)pdx.y * o.y;
+      aa += nrm2(o);
+      if (a.ap_prev) pa += (double)pap.x * o.x + (double)pap.y * o.y;
     }
     __syncthreads();
   }
   double vv[3] = {acc, aa, pa}, tot[3];
-  if (grid_reduce<3>(vv, partials, &st->counter, tot)) {
-    double k0 = 0.0, k1 = 0.0, k2 = 0.0;
-    for (int b = threadIdx.x; b < nk; b += blockDim.x) {
-      k0 += __ldcg(kpart + 3 * b);
-      k1 += __ldcg(kpart + 3 * b + 1);
-      k2 += __ldcg(kpart + 3 * b + 2);
-    }
-    __shared__ double red[32];
-    k0 = block_sum(k0, red);
-    k1 = block_sum(k1, red);
-    k2 = block_sum(k2, red);
-    if (threadIdx.x == 0) {
-      const double total = tot[0] + k0;
-      if (a.dot_slot >= 0) {
-        cr.rar[a.dot_slot] = total;
-        cr.saa[a.dot_slot] = tot[1] + k1;
-        cr.spa[a.dot_slot] = tot[2] + k2;
-      } else {
-        st->scal[0] = total;
-      }
+  if (grid_reduce<3>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
+    if (a.dot_slot >= 0) {
+      cr.rar[a.dot_slot] = tot[0];
+      cr.saa[a.dot_slot] = tot[1];
+      cr.spa[a.dot_slot] = tot[2];
+    } else {
+      st->scal[0] = tot[0];
     }
   }
 }
