@@ -447,13 +447,7 @@ __global__ void __launch_bounds__(kThreads) k_rho_sum(Dims d, ColsWArgs a, const
         tx += part[w][lane].x;
         ty += part[w][lane].y;
       }
-      // finish_elem's operator branch with the operands loaded above
-      float2 o = make_float2((float)tx, (float)ty);
-      if (a.mode == CW_OPALPHA) o = axpy_rn(o, a.alpha, pdx);
-      a.out[e] = o;
-      acc += (double)pdx.x * o.x + (double)pdx.y * o.y;
-      aa += nrm2(o);
-      if (a.ap_prev) pa += (double)pap.x * o.x + (double)pap.y * o.y;
+      finish_op(a, (size_t)e, make_float2((float)tx, (float)ty), pdx, pap, acc, aa, pa);
     }
     __syncthreads();
   }

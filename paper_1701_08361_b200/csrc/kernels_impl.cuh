@@ -440,6 +440,19 @@ __device__ __forceinline__ float2 finish_elem(const ColsWArgs& a, size_t e, floa
   }
 }
 
+// finish_elem's operator branch with its operands dx[e], ap_prev[e] already loaded
+// (issued ahead of the value they combine with)
+__device__ __forceinline__ float2 finish_op(const ColsWArgs& a, size_t e, float2 n, float2 p, float2 q,
+                                           double& acc, double& aa, double& pa) {
+  float2 v = n;
+  if (a.mode == CW_OPALPHA) v = axpy_rn(v, a.alpha, p);
+  a.out[e] = v;
+  acc += (double)p.x * v.x + (double)p.y * v.y;
+  aa += nrm2(v);
+  if (a.ap_prev) pa += (double)q.x * v.x + (double)q.y * v.y;
+  return v;
+}
+
 // Row pass 2. Block (window row r, channel group h of Geo::LPB channels): inverse
 // Toeplitz row pass -> T (window, 1/G); SETUP: e = z - T and the data residual
 // (nlinv.cpp:254-256); rc = conj(c_j) T summed over the group's channels in channel
@@ -569,6 +582,22 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
     const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
     const int nl = min(Geo::LPB, d.Gc - q0);
     const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
+    // pruned band (Gc = G/4 on the DFT grid): this thread's outputs are the step-2 slots
+    // k2 in [GK0, GK0 + GKN); their CR operands are loaded before the transform
+    constexpr bool kBand = Geo::GC_K2 != Geo::ALL_N2;
+    constexpr int GK0 = (G / 2 - (G / 4) / 2) / N1, GKN = kBand ? (G / 4) / N1 : 1;
+    const bool band = kBand && d.Gc * 4 == G && a.mode != CW_SETUP;
+    const size_t cbase = (size_t)D0 + (size_t)j * d.Gc * d.Gc;
+    float2 pdx[GKN], pap[GKN];
+    if (band && a2) {
+      const int q = q0 + i2.l;
+#pragma unroll
+      for (int kk = 0; kk < GKN; ++kk) {
+        const size_t e = cbase + (size_t)(i2.k + N1 * (GK0 + kk) - d.off) * d.Gc + q;
+        pdx[kk] = a.dx[e];
+        pap[kk] = a.ap_prev ? a.ap_prev[e] : make_float2(0.f, 0.f);
+      }
+    }
     if (a1) {
       const float2* col = Y + (size_t)j * d.L * d.Gc + q0 + i1.l;
       float2 v[N1];
@@ -589,16 +618,28 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
         fft_step2<Geo, -1>(A, i2.l, i2.k, u);
       }
       const int q = q0 + i2.l;
+      if (band) {
 #pragma unroll
-      for (int k2 = 0; k2 < N2; ++k2) {
-        const int p = i2.k + N1 * k2;
-        const int i = p - d.off;
-        if (i >= 0 && i < d.Gc) {
-          const int e = i * d.Gc + q;
+        for (int kk = 0; kk < GKN; ++kk) {
+          const int p = i2.k + N1 * (GK0 + kk);
+          const int e = (p - d.off) * d.Gc + q;
           const float w = winv[e];
-          const float2 f = cscale(flip(u[k2], p), d.invG);
+          const float2 f = cscale(flip(u[GK0 + kk], p), d.invG);
           // crop_k(FFT(u)) * winv   (nlinv.cpp:127-133)
-          finish_elem(a, (size_t)D0 + (size_t)j * d.Gc * d.Gc + e, make_float2(f.x * w, f.y * w), acc0, aa, pa);
+          finish_op(a, cbase + e, make_float2(f.x * w, f.y * w), pdx[kk], pap[kk], acc0, aa, pa);
+        }
+      } else {
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+          const int p = i2.k + N1 * k2;
+          const int i = p - d.off;
+          if (i >= 0 && i < d.Gc) {
+            const int e = i * d.Gc + q;
+            const float w = winv[e];
+            const float2 f = cscale(flip(u[k2], p), d.invG);
+            // crop_k(FFT(u)) * winv   (nlinv.cpp:127-133)
+            finish_elem(a, cbase + e, make_float2(f.x * w, f.y * w), acc0, aa, pa);
+          }
         }
       }
     }
@@ -652,6 +693,12 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
         if (a.mode == CW_SETUP && !in_win(d, r, c) && (o.x != 0.f || o.y != 0.f)) nz = 1;
         continue;
       }
+      const bool opm = a.mode != CW_SETUP;
+      float2 pdx = make_float2(0.f, 0.f), pap = make_float2(0.f, 0.f);
+      if (opm) {
+        pdx = a.dx[e];
+        if (a.ap_prev) pap = a.ap_prev[e];
+      }
       if (in_win(d, r, c)) {
         const double2* src = RP + (size_t)(r - d.lo) * d.L + (c - d.lo);
         for (int h = 0; h < H; ++h) {
@@ -668,7 +715,9 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
           acc1 += nrm2(zz);
         }
       }
-      const float2 o = finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), acc0, aa, pa);
+      const float2 n = make_float2((float)sx, (float)sy);
+      const float2 o = opm ? finish_op(a, (size_t)e, n, pdx, pap, acc0, aa, pa)
+                           : finish_elem(a, (size_t)e, n, acc0, aa, pa);
       if (a.mode == CW_SETUP && !in_win(d, r, c) && (o.x != 0.f || o.y != 0.f)) nz = 1;
     }
     if (a.mode == CW_SETUP && __syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&st->rho_out_nz, 1);
