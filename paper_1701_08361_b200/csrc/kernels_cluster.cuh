@@ -333,6 +333,22 @@ __global__ void __launch_bounds__(Geo::NT, 2)
       }
     }
   }
+  // pass E's CR operands and weights (its outputs are the coil band k2 in [GK0, GK0 + GKN)),
+  // requested before the barrier so they land during it
+  constexpr int GK0 = CG::GK0, GKN = CG::GKN;
+  const size_t cbase = (size_t)G * G + (size_t)j * GC * GC;
+  float2 edx[GKN], eap[GKN];
+  float ew[GKN];
+  if (c2.on && c2.l < GCPC) {
+    const int q = rank * GCPC + c2.l;
+#pragma unroll
+    for (int kk = 0; kk < GKN; ++kk) {
+      const int e = (c2.k + N1 * kk) * GC + q;  // k-row i = p - OFF of slot k2 = GK0 + kk
+      ew[kk] = winv[e];
+      edx[kk] = a.dx[cbase + e];
+      eap[kk] = a.ap_prev ? a.ap_prev[cbase + e] : make_float2(0.f, 0.f);
+    }
+  }
   cluster_barrier();
 
   // ---- pass E: W^-H column pass of this CTA's coil columns -> out.chat_j + dots ----------
@@ -353,16 +369,12 @@ __global__ void __launch_bounds__(Geo::NT, 2)
       fft_step2<Geo, -1, CG::GC_K2>(A, c2.l, c2.k, u);
       const int q = rank * GCPC + c2.l;
 #pragma unroll
-      for (int k2 = 0; k2 < N2; ++k2) {
-        const int p = c2.k + N1 * k2;
-        const int i = p - OFF;
-        if (i >= 0 && i < GC) {
-          const int e = i * GC + q;
-          const float w = winv[e];
-          const float2 f = cscale(flip(u[k2], p), d.invG);
-          // crop_k(FFT(u)) * winv   (nlinv.cpp:127-133)
-          finish_elem(a, (size_t)G * G + (size_t)j * GC * GC + e, make_float2(f.x * w, f.y * w), acc, aa, pa);
-        }
+      for (int kk = 0; kk < GKN; ++kk) {
+        const int p = c2.k + N1 * (GK0 + kk);
+        const int e = (p - OFF) * GC + q;
+        const float2 f = cscale(flip(u[GK0 + kk], p), d.invG);
+        // crop_k(FFT(u)) * winv   (nlinv.cpp:127-133)
+        finish_op(a, cbase + e, make_float2(f.x * ew[kk], f.y * ew[kk]), edx[kk], eap[kk], acc, aa, pa);
       }
     }
   }
