@@ -1,13 +1,15 @@
 #!/bin/bash
-# A/B of build_var/lib_base.so (committed tree) against the working tree's library on
-# the default-schedule decomposition probes; run under gpurun
-for n in base new base new; do
-  if [ $n = base ]; then export RTN_LIB=$PWD/build_var/lib_base.so; else unset RTN_LIB; fi
-  echo "== $n"
+# Same-box A/B of two builds of the library on the default-schedule probes (run under
+# gpurun): A = $AB_A (default build_var/lib_base.so), B = $AB_B (default: the
+# in-tree library of the working tree)
+A=${AB_A:-$PWD/build_var/lib_base.so}
+B=${AB_B:-$PWD/paper_1701_08361_b200/librtnlinv_b200.so}
+for lib in "$A" "$B" "$A" "$B"; do
+  export RTN_LIB=$lib
+  echo "== $(basename $lib)"
   timeout 100 python scripts/decomp_probe.py c3 3x1
   RTN_CLUSTER=0 timeout 100 python scripts/decomp_probe.py c3 1x1
   timeout 100 python scripts/decomp_probe.py c3 1x1
   timeout 100 python scripts/decomp_probe.py c4 3x1
-  timeout 100 python scripts/decomp_probe.py c2 3x1
   timeout 100 python scripts/decomp_probe.py c1 3x1
 done
