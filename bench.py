@@ -595,7 +595,7 @@ def main():
     latency_mode = None
     try:
         lo = pb.SeriesOptions(T=1, plain=True, sched=sched)
-        series.run(lo, first=W, count=NTUNE, want_images=False)
+        series.run(lo, first=0, count=W, want_images=False)  # graph capture for the cluster path
         lout = series.run(lo, first=W + NTUNE, count=S, want_images=False)
         lat_span = series.last_span_ms()
         latency_mode = {"frames_in_flight": 1, "cluster_fused": True, "frames_per_s": S / (lat_span / 1000.0),

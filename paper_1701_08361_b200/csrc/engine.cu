@@ -938,7 +938,6 @@ double Engine::kernel_bytes(const char* which) const {
   if (w == "colsW") return c8 * (J * L * Gc + 3.0 * (G * G + J * Gc * Gc)) + 16.0 * dims_.H * L * L + 4.0 * Gc * Gc;
   if (w == "cr_xr" || w == "cr_pap") return c8 * 6.0 * (G * G + J * Gc * Gc);
   if (w == "cr_fused") return c8 * 9.0 * (G * G + J * Gc * Gc);  // x,r,p,ap,ar in; x,r,p,ap out
-  if (w == "colsW") return c8 * (J * L * Gc + J * L * L + 2.0 * (G * G + J * Gc * Gc)) + 4.0 * Gc * Gc;
   if (w == "apply") {
     // one fused normal-operator application (SURVEY.md §8(d) B_op, window pruned)
     return 8.0 * L * L * (J + 3) + 8.0 * G * G + 16.0 * J * Gc * Gc + 4.0 * Gc * Gc;

@@ -1,5 +1,8 @@
 """Launch each hot-path kernel class a few times at a C3 linearisation point (eager
-launches on the engine stream) — the target for `ncu --set full`."""
+launches on the engine stream) — the target for `ncu --set full`. The launches sit
+between cudaProfilerStart/Stop, so `ncu --profile-from-start off` skips the frame
+reconstruction that builds the linearisation point."""
+import ctypes
 import os
 import sys
 
@@ -21,6 +24,9 @@ with pb.Context(plan) as ctx:
     ctx.set_data(z[0])
     fr = ctx.reconstruct_frame(pb.initial_estimate(plan))
     ctx.make_step_cache(fr.est)
+    rt = ctypes.CDLL("libcudart.so.12")
+    rt.cudaProfilerStart()
     for n in names:
         ms, by = ctx.time_kernel(n, int(os.environ.get("REPS", "50")))
         print(f"{n}: {ms * 1000:.1f} us, {by / 1e6:.2f} MB algorithmic, {by / ms / 1e6:.0f} GB/s", flush=True)
+    rt.cudaProfilerStop()
