@@ -598,7 +598,8 @@ def main():
         series.run(lo, first=0, count=W, want_images=False)  # graph capture for the cluster path
         lout = series.run(lo, first=W + NTUNE, count=S, want_images=False)
         lat_span = series.last_span_ms()
-        latency_mode = {"frames_in_flight": 1, "cluster_fused": True, "frames_per_s": S / (lat_span / 1000.0),
+        latency_mode = {"frames_in_flight": 1, "cluster_fused": ctx.cluster_supported(),
+                        "frames_per_s": S / (lat_span / 1000.0),
                         "p50_latency_ms": statistics.median(float(v) for v in lout["gpu_ms"])}
     except Exception as e:  # reported, never fatal
         latency_mode = {"error": str(e)}

@@ -254,6 +254,9 @@ int rtn_tunedb_load(const char* path, int* rows6, double* runtime_ms, int64_t* t
 /* average ms per launch of one kernel class ("colsT", "rows1", "rows2", "colA",
  * "apply") at the cached linearisation point, and its algorithmic bytes */
 int rtn_time_kernel(rtn_ctx* ctx, const char* which, int reps, double* ms, double* bytes);
+/* 1 when this plan's grid has the cluster-fused application (latency mode; one
+ * thread-block cluster per channel), else 0 (the five-kernel passes always run) */
+int rtn_cluster_supported(rtn_ctx* ctx, int* supported);
 
 #ifdef __cplusplus
 }

@@ -210,6 +210,7 @@ def load_library(path: str = LIB_PATH):
         "rtn_tunedb_load": ([ctypes.c_char_p, i, d, ctypes.POINTER(ctypes.c_int64), ctypes.c_int, i, i],
                             ctypes.c_int),
         "rtn_time_kernel": ([vp, ctypes.c_char_p, ctypes.c_int, d, d], ctypes.c_int),
+        "rtn_cluster_supported": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -538,6 +539,12 @@ class Context:
         out = np.zeros((Jv,) + samples.shape[1:], np.complex64)
         _check(self.lib.rtn_apply_compression(self._h, _fp(m), Jv, Jp, _fp(samples), n, _fp(out)))
         return out
+
+    def cluster_supported(self) -> bool:
+        """whether this plan's grid has the cluster-fused application (latency mode)"""
+        v = ctypes.c_int(0)
+        _check(self.lib.rtn_cluster_supported(self._h, ctypes.byref(v)))
+        return bool(v.value)
 
     def time_kernel(self, which: str, reps: int = 20):
         """(average ms per launch, algorithmic bytes per launch) of one kernel class"""

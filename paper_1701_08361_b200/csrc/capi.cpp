@@ -773,4 +773,11 @@ int rtn_time_kernel(rtn_ctx* ctx, const char* which, int reps, double* ms, doubl
   });
 }
 
+int rtn_cluster_supported(rtn_ctx* ctx, int* supported) {
+  return guarded([&] {
+    if (!supported) rtnb::fail(2, "cluster_supported: null output");
+    *supported = eng(ctx).cluster_supported() ? 1 : 0;
+  });
+}
+
 }  // extern "C"
