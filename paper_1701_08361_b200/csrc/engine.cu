@@ -968,12 +968,12 @@ double Engine::time_kernel(const char* which, int reps) {
       const int nbw = J * tGc;
       ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, 0, gv_);
     } else if (w == "cr_xr") {
-      launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], p_, ap_, partials_, st_, cr_, 1, 0.f);
+      launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, partials_, st_, cr_, 1, 0.f);
     } else if (w == "cr_fused") {
-      launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], p_, ap_,
+      launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_,
                static_cast<const float2*>(ar_), partials_, st_, cr_, 1, 0.f, 0, 0, plan_.G);
     } else if (w == "cr_pap") {
-      launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, est_scratch_[0], est_scratch_[1], r_, ar_, partials_, st_, cr_, 1);
+      launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, p_, ap_, r_, ar_, partials_, st_, cr_, 1);
     } else if (w == "colA") {
       ops_->colA(s_, J * tGc, dims_, winv_, twG_, r_ + static_cast<size_t>(G) * G, U_, dims_.lo, dims_.L, st_, 0);
     } else if (w == "apply") {
@@ -983,12 +983,19 @@ double Engine::time_kernel(const char* which, int reps) {
     }
   };
   if (w.rfind("cr_", 0) == 0) {
-    // finite scalars so the recurrences run their full vector passes
-    const double one[2] = {1.0, 1.0};
-    for (double* q : {cr_.rar, cr_.ap2, cr_.saa, cr_.spa}) {
+    // scalars of a stationary iteration (iteration 1: b = rar[1]/rar[0] = 0, step
+    // a = rar[1]/|ap|^2 = 0 with |ap|^2 = saa[1] = 1 > 0): every launch runs the full
+    // vector pass (loads, update, stores, norms) and the values stay finite however
+    // many times it repeats, so no launch exits early on a solver fault
+    const double rar[2] = {1.0, 0.0}, one[2] = {1.0, 1.0};
+    check_cuda(cudaMemcpyAsync(cr_.rar, rar, sizeof(rar), cudaMemcpyHostToDevice, s_), "scalars");
+    for (double* q : {cr_.ap2, cr_.saa, cr_.spa}) {
       check_cuda(cudaMemcpyAsync(q, one, sizeof(one), cudaMemcpyHostToDevice, s_), "scalars");
     }
   }
+  // fresh intermediates (U, V, Y, RP, ar) of one application at the linearisation
+  // point: the in-place passes (colsT on V) compound over a previous class's repeats
+  enq_apply(r_, ar_, CW_OP, 0.f, -1, 0);
   for (int i = 0; i < 3; ++i) launch();
   cudaEvent_t a, b;
   check_cuda(cudaEventCreate(&a), "event");
@@ -1001,6 +1008,12 @@ double Engine::time_kernel(const char* which, int reps) {
   check_cuda(cudaEventElapsedTime(&ms, a, b), "elapsed");
   cudaEventDestroy(a);
   cudaEventDestroy(b);
+  // a launch that returned early on a device fault would time nothing
+  read_state();
+  if (st_host_->status || st_host_->cr_halt) {
+    fail(4, "time_kernel: " + w + " stopped early (device status " + std::to_string(st_host_->status) +
+                ", halt " + std::to_string(st_host_->cr_halt) + ")");
+  }
   return ms / reps;
 }
 
