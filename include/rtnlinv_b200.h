@@ -160,6 +160,13 @@ int rtn_newton_step(rtn_ctx* ctx, float* x, const float* reg, float alpha, float
  * image: N*N, est_out: D (nullable), cg_per_step: newton_steps ints (nullable). */
 int rtn_reconstruct_frame(rtn_ctx* ctx, const float* init, const float* reg, float* image,
                           float* est_out, int* cg_per_step, double* seconds);
+/* reconstruct_frame with a RegProvider (nlinv.hpp:102, `const Estimate& reg(int m)`): the
+ * provider returns the host address of step m's regularisation target (D complex64),
+ * read before the step starts; NULL keeps the previous step's target (step 0: init).
+ * Runs step by step. Not available on process-group members (status 2). */
+typedef const float* (*rtn_reg_provider)(int m, void* user);
+int rtn_reconstruct_frame_provider(rtn_ctx* ctx, const float* init, rtn_reg_provider reg, void* user,
+                                   float* image, float* est_out, int* cg_per_step, double* seconds);
 
 /* --- nlinv.hpp:136-169: series drivers over device-resident frames ------------- */
 typedef struct rtn_series rtn_series;

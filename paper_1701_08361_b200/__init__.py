@@ -50,6 +50,9 @@ class DecompFault(RuntimeError):
 
 _ERRORS = {2: UsageError, 3: DataError, 4: SolverError}
 
+# rtn_reg_provider: const float* (*)(int m, void* user)
+_REG_PROVIDER = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p)
+
 
 class _Plan(ctypes.Structure):
     _fields_ = [
@@ -171,6 +174,7 @@ def load_library(path: str = LIB_PATH):
         "rtn_cg_solve": ([vp, f, ctypes.c_float, ctypes.c_float, ctypes.c_int, f, i, d], ctypes.c_int),
         "rtn_newton_step": ([vp, f, f, ctypes.c_float, ctypes.c_float, ctypes.c_int, i, d], ctypes.c_int),
         "rtn_reconstruct_frame": ([vp, f, f, f, f, i, d], ctypes.c_int),
+        "rtn_reconstruct_frame_provider": ([vp, f, _REG_PROVIDER, vp, f, f, i, d], ctypes.c_int),
         "rtn_series_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
         "rtn_series_destroy": ([vp], None),
         "rtn_series_create_multi": ([vp, ctypes.c_int, ctypes.c_int, i, ctypes.c_int, ctypes.POINTER(vp)],
@@ -469,7 +473,11 @@ class Context:
                                         ctypes.byref(iters), ctypes.byref(r0)))
         return x, iters.value, r0.value
 
-    def reconstruct_frame(self, init, reg=None) -> FrameResult:
+    def reconstruct_frame(self, init, reg=None, regs=None) -> FrameResult:
+        """nlinv.hpp:112. reg: one fixed target (None: init). regs: the RegProvider, a
+        callable m -> estimate (or None to keep the previous target) or a per-step list"""
+        if regs is not None:
+            return self._reconstruct_frame_provider(init, regs)
         init = _c64(init, (self.D,))
         regc = None if reg is None else _c64(reg, (self.D,))
         N = self.plan.N
@@ -479,6 +487,30 @@ class Context:
         secs = ctypes.c_double(0)
         _check(self.lib.rtn_reconstruct_frame(self._h, _fp(init), _fp(regc), _fp(img), _fp(est), per,
                                               ctypes.byref(secs)))
+        cg = [per[m] for m in range(self.plan.newton_steps)]
+        return FrameResult(img, est, cg, sum(cg), secs.value)
+
+    def _reconstruct_frame_provider(self, init, regs) -> FrameResult:
+        init = _c64(init, (self.D,))
+        fetch = regs if callable(regs) else (lambda m: regs[m])
+        keep = []
+
+        def provider(m, _user):
+            r = fetch(m)
+            if r is None:
+                return None
+            arr = _c64(r, (self.D,))
+            keep.append(arr)  # alive until the call returns
+            return arr.ctypes.data
+
+        cb = _REG_PROVIDER(provider)
+        N = self.plan.N
+        img = np.zeros((N, N), np.complex64)
+        est = np.zeros(self.D, np.complex64)
+        per = (ctypes.c_int * max(self.plan.newton_steps, 1))()
+        secs = ctypes.c_double(0)
+        _check(self.lib.rtn_reconstruct_frame_provider(self._h, _fp(init), cb, None, _fp(img), _fp(est), per,
+                                                       ctypes.byref(secs)))
         cg = [per[m] for m in range(self.plan.newton_steps)]
         return FrameResult(img, est, cg, sum(cg), secs.value)
 

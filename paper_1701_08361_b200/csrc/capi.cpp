@@ -463,6 +463,26 @@ int rtn_reconstruct_frame(rtn_ctx* ctx, const float* init, const float* reg, flo
   });
 }
 
+int rtn_reconstruct_frame_provider(rtn_ctx* ctx, const float* init, rtn_reg_provider reg, void* user,
+                                   float* image, float* est_out, int* cg_per_step, double* seconds) {
+  return guarded([&] {
+    if (!init || !image) rtnb::fail(2, "reconstruct_frame: null init or image");
+    rtnb::FrameStats st;
+    const rtnb::RegHostFn fn = [&](int m) -> const float* { return reg ? reg(m, user) : nullptr; };
+    if (ctx && ctx->grp) {
+      ctx->grp->reconstruct_frame_regs(init, fn, image, est_out, &st);
+    } else if (ctx && ctx->pg) {
+      rtnb::fail(2, "reconstruct_frame: a RegProvider needs a single-device or in-process group context");
+    } else {
+      eng(ctx).reconstruct_frame_regs(init, fn, image, est_out, &st);
+    }
+    if (cg_per_step) {
+      for (size_t m = 0; m < st.cg_per_step.size(); ++m) cg_per_step[m] = st.cg_per_step[m];
+    }
+    if (seconds) *seconds = st.seconds;
+  });
+}
+
 // ---- series -------------------------------------------------------------------------
 
 struct rtn_series {

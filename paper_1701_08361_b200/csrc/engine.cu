@@ -924,6 +924,26 @@ void Engine::reconstruct_frame(const float* init, const float* reg, float* image
   if (stats) stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+void Engine::reconstruct_frame_regs(const float* init, const RegHostFn& reg, float* image, float* est_out,
+                                    FrameStats* stats) {
+  const auto t0 = std::chrono::steady_clock::now();
+  check_cuda(cudaMemcpyAsync(x_, init, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
+  check_cuda(cudaMemcpyAsync(reg_, init, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
+  const RegFn dev = [&](int m) -> const float2* {
+    const float* h = reg ? reg(m) : nullptr;
+    if (!h) return nullptr;
+    check_cuda(cudaMemcpyAsync(reg_, h, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "reg h2d");
+    sync();  // the provider may reuse its buffer for the next step
+    return reg_;
+  };
+  frame_run_sync(dev, img_, 1.0f, false, stats);
+  check_cuda(cudaMemcpyAsync(image, img_, sizeof(float2) * plan_.N * plan_.N, cudaMemcpyDeviceToHost, s_), "d2h");
+  if (est_out) check_cuda(cudaMemcpyAsync(est_out, x_, sizeof(float2) * D_, cudaMemcpyDeviceToHost, s_), "d2h");
+  sync();
+  have_cache_ = true;
+  if (stats) stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 // ---- isolated kernel timing (bench roofline) ------------------------------------------
 
 double Engine::kernel_bytes(const char* which) const {

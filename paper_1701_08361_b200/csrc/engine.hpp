@@ -64,6 +64,9 @@ struct FrameStats {
 };
 
 using RegFn = std::function<const float2*(int m)>;  // device pointer of reg(m), or nullptr = keep reg
+// host-side RegProvider (nlinv.hpp:102): host pointer to the regularisation target of
+// Newton step m (D complex64), or nullptr = keep the previous step's target
+using RegHostFn = std::function<const float*(int m)>;
 
 // What a series driver needs from one frame worker: a single-device Engine, or a
 // channel-decomposed device Group (group.hpp). Estimates, frames and PSFs are in
@@ -127,6 +130,10 @@ class Engine : public FrameWorker {
   // reg == nullptr: every step regularises towards init (nlinv.cpp:425-429)
   void reconstruct_frame(const float* init, const float* reg, float* image, float* est_out,
                          FrameStats* stats);
+  // per-step regularisation targets from a RegProvider (step-by-step path; the target of
+  // step 0 defaults to init)
+  void reconstruct_frame_regs(const float* init, const RegHostFn& reg, float* image, float* est_out,
+                              FrameStats* stats);
 
   // ---- device-resident frame pipeline ----
   // A frame runs on the engine's own buffers: x (estimate; holds init on entry and

@@ -516,4 +516,35 @@ void Group::reconstruct_frame(const float* init, const float* reg, float* image,
   for (auto& m : mem_) m->have_cache_ = true;
 }
 
+void Group::reconstruct_frame_regs(const float* init, const RegHostFn& reg, float* image, float* est_out,
+                                   FrameStats* stats) {
+  DeviceRestore restore;
+  Engine& e0 = *mem_[0];
+  check_cuda(cudaSetDevice(e0.dev_), "set device");
+  auto stage_in = [&](const float* h, bool to_reg) {
+    check_cuda(cudaMemcpyAsync(h_stage_, h, sizeof(float2) * D_, cudaMemcpyHostToDevice, e0.s_), "h2d");
+    split_copy(h_stage_, to_reg);
+  };
+  stage_in(init, false);
+  stage_in(init, true);
+  const RegFn dev = [&](int m) -> const float2* {
+    const float* h = reg ? reg(m) : nullptr;
+    if (!h) return nullptr;
+    check_cuda(cudaSetDevice(e0.dev_), "set device");
+    check_cuda(cudaMemcpyAsync(h_stage_, h, sizeof(float2) * D_, cudaMemcpyHostToDevice, e0.s_), "reg h2d");
+    check_cuda(cudaStreamSynchronize(e0.s_), "reg h2d");  // the provider may reuse its buffer
+    return h_stage_;  // split to the members by load_reg on the same stream
+  };
+  frame_run_sync(dev, nullptr, 1.0f, false, stats);
+  check_cuda(cudaSetDevice(e0.dev_), "set device");
+  check_cuda(cudaMemcpyAsync(image, e0.img_, sizeof(float2) * plan_.N * plan_.N, cudaMemcpyDeviceToHost, e0.s_),
+             "d2h");
+  if (est_out) {
+    store_x(h_stage_);
+    check_cuda(cudaMemcpyAsync(est_out, h_stage_, sizeof(float2) * D_, cudaMemcpyDeviceToHost, e0.s_), "d2h");
+  }
+  sync();
+  for (auto& m : mem_) m->have_cache_ = true;
+}
+
 }  // namespace rtnb

@@ -64,6 +64,8 @@ class Group : public FrameWorker {
   void make_step_cache(const float* x);
   void apply_normal(const float* dx, float* out);
   void reconstruct_frame(const float* init, const float* reg, float* image, float* est_out, FrameStats* stats);
+  void reconstruct_frame_regs(const float* init, const RegHostFn& reg, float* image, float* est_out,
+                              FrameStats* stats);
 
  private:
   template <class F>

@@ -323,3 +323,26 @@ def test_cluster_fused_frame_matches_reference(gpu, ref, monkeypatch):
     assert fr.cg_per_step == per
     assert rel_err(fr.image, img) < FRAME_TOL
     assert rel_err(fr.est, est) < FRAME_TOL
+
+
+@pytest.mark.parametrize("A,budget", [(1, 12), (1, 0), (2, 12)])
+def test_reconstruct_frame_with_a_reg_provider_matches_reference(gpu, ref, A, budget):
+    # RegProvider (nlinv.hpp:102): a different regularisation target per Newton step,
+    # step 2 keeping step 1's (None); budget mode and tolerance mode (cg_tol 1e-3)
+    plan = gpu.make_plan(16, 3)
+    plan.newton_steps, plan.cg_iter_budget = 4, budget
+    inp = phantom_frame_inputs(ref, plan, K=7, U=1)
+    z, P = inp["z"][0], inp["P"][0]
+    init = gpu.initial_estimate(plan)
+    targets = [random_estimate(plan, 90 + m) * np.float32(0.01) for m in range(plan.newton_steps)]
+    provided = [targets[0], targets[1], None, targets[3]]
+    regs = [targets[0], targets[1], targets[1], targets[3]]
+    devices = [0] * A if A > 1 else None
+    with gpu.Context(plan, devices=devices) as ctx:
+        ctx.set_psf(P)
+        ctx.set_data(z)
+        fr = ctx.reconstruct_frame(init, regs=lambda m: provided[m])
+    img, est, per = ref.reconstruct_frame_regs(plan, z, P, init, regs)
+    assert fr.cg_per_step == per
+    assert rel_err(fr.image, img) < FRAME_TOL
+    assert rel_err(fr.est, est) < FRAME_TOL
