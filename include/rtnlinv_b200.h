@@ -232,6 +232,9 @@ int rtn_series_estimate(rtn_series* s, int n, float* est /* D */);
 /* --- decomp.hpp:25-130: decomposition and scheduling (host logic) ----------------- */
 /* cap = largest group (4 = reference kGroupSizeMax, 8 = NVSwitch) */
 int rtn_partition_channels(int J, int A, int cap, int* out_pairs /* 2*A */);
+/* all_reduce_sum (decomp.hpp:25-30): out = sum of n_terms G*G complex64 images in term
+ * order in FP64, one cast to float (bit-identical to the reference), on the device */
+int rtn_all_reduce_sum(const float* terms /* n_terms*G*G */, int n_terms, int G, float* out /* G*G */);
 typedef struct rtn_ledger rtn_ledger;
 int rtn_ledger_create(int frames, rtn_ledger** out);
 void rtn_ledger_destroy(rtn_ledger* l);

@@ -174,6 +174,7 @@ def load_library(path: str = LIB_PATH):
         "rtn_cg_solve": ([vp, f, ctypes.c_float, ctypes.c_float, ctypes.c_int, f, i, d], ctypes.c_int),
         "rtn_newton_step": ([vp, f, f, ctypes.c_float, ctypes.c_float, ctypes.c_int, i, d], ctypes.c_int),
         "rtn_reconstruct_frame": ([vp, f, f, f, f, i, d], ctypes.c_int),
+        "rtn_all_reduce_sum": ([f, ctypes.c_int, ctypes.c_int, f], ctypes.c_int),
         "rtn_reconstruct_frame_provider": ([vp, f, _REG_PROVIDER, vp, f, f, i, d], ctypes.c_int),
         "rtn_series_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
         "rtn_series_destroy": ([vp], None),
@@ -900,6 +901,16 @@ def psf_angle_key(angles, S: int, G: int) -> int:
     """PsfCache::angle_key (preproc.cpp:301-313)"""
     a = np.ascontiguousarray(angles, np.float64)
     return int(load_library().rtn_psf_angle_key(a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(a), S, G))
+
+
+def all_reduce_sum(terms):
+    """decomp.hpp:25-30: sum of the terms (n x G x G complex64) in order in FP64, on the device"""
+    terms = np.ascontiguousarray(terms, np.complex64)
+    if terms.ndim != 3 or terms.shape[1] != terms.shape[2]:
+        raise UsageError("all_reduce_sum: terms must be n x G x G")
+    out = np.zeros(terms.shape[1:], np.complex64)
+    _check(load_library().rtn_all_reduce_sum(_fp(terms), terms.shape[0], terms.shape[1], _fp(out)))
+    return out
 
 
 def partition_channels(J: int, A: int, cap: int = 4):

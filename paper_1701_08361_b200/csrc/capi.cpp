@@ -295,6 +295,18 @@ int rtn_fft_table_load(const char* path, int* sizes, double* us, int max_n, int*
 // ---- pipeline.cpp:60-137 postprocessing on the device -----------------------------------------
 
 
+int rtn_all_reduce_sum(const float* terms, int n_terms, int G, float* out) {
+  return guarded([&] {
+    if (!terms || !out || n_terms < 1 || G < 1) rtnb::fail(2, "all_reduce_sum: no terms or bad size");
+    const long long n = static_cast<long long>(G) * G;
+    with_device_buffers(sizeof(float2) * n * n_terms, sizeof(float2) * n, [&](void* a, void* b) {
+      rtnb::check_cuda(cudaMemcpy(a, terms, sizeof(float2) * n * n_terms, cudaMemcpyHostToDevice), "h2d");
+      rtnb::all_reduce_sum_device(static_cast<float2*>(a), n_terms, n, static_cast<float2*>(b), nullptr);
+      rtnb::check_cuda(cudaMemcpy(out, b, sizeof(float2) * n, cudaMemcpyDeviceToHost), "d2h");
+    });
+  });
+}
+
 int rtn_post_magnitude(const float* images, long long n, float* out) {
   return guarded([&] {
     if (!images || !out || n < 0) rtnb::fail(2, "magnitude_image: bad arguments");

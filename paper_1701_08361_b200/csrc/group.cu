@@ -547,4 +547,25 @@ void Group::reconstruct_frame_regs(const float* init, const RegHostFn& reg, floa
   for (auto& m : mem_) m->have_cache_ = true;
 }
 
+namespace {
+__global__ void k_all_reduce_sum(const float2* __restrict__ terms, int n_terms, long long n, float2* __restrict__ out) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    double sx = 0.0, sy = 0.0;
+    for (int t = 0; t < n_terms; ++t) {
+      const float2 v = terms[(size_t)t * n + e];
+      sx += (double)v.x;
+      sy += (double)v.y;
+    }
+    out[e] = make_float2((float)sx, (float)sy);
+  }
+}
+}  // namespace
+
+void all_reduce_sum_device(const float2* terms, int n_terms, long long n, float2* out, cudaStream_t s) {
+  if (n_terms < 1) fail(2, "all_reduce_sum: no terms");
+  const long long blocks = std::min<long long>((n + 255) / 256, 148 * 8);
+  k_all_reduce_sum<<<static_cast<unsigned>(std::max<long long>(blocks, 1)), 256, 0, s>>>(terms, n_terms, n, out);
+  check_cuda(cudaGetLastError(), "all_reduce_sum");
+}
+
 }  // namespace rtnb

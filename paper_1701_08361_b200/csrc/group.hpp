@@ -98,4 +98,8 @@ class Group : public FrameWorker {
   bool frame_graph_apply_ = false;
 };
 
+// all_reduce_sum (decomp.cpp:26-39) of n_terms device images of n elements: FP64 sums
+// in term order, one cast to float; bit-identical to the reference for any partition
+void all_reduce_sum_device(const float2* terms, int n_terms, long long n, float2* out, cudaStream_t s);
+
 }  // namespace rtnb

@@ -167,3 +167,21 @@ def test_hybrid_temporal_channel_series_replays_exactly(gpu, ref, T, A):
         ests[n] = est
         assert rel_err(out["images"][n], img * np.float32(1.0 / scale)) < FRAME_TOL, n
         assert rel_err(out["series"].estimate(n), est) < FRAME_TOL, n
+
+
+def test_all_reduce_sum_is_the_ordered_fp64_sum(gpu):
+    # test_decomp.cpp:82-106 on the device entry point: repeatable bit for bit, FP64
+    # accumulation in index order (here checked exactly, not just to 1e-6), zeros stay
+    # zero, no terms is a usage error
+    from helpers import random_image
+    terms = np.stack([random_image(12, 100 + j) for j in range(5)])
+    s1 = gpu.all_reduce_sum(terms)
+    s2 = gpu.all_reduce_sum(terms)
+    assert np.array_equal(s1.view(np.uint32), s2.view(np.uint32))
+    acc = np.zeros(terms.shape[1:], np.complex128)
+    for t in terms:
+        acc += t.astype(np.complex128)
+    assert np.array_equal(s1, acc.astype(np.complex64))
+    assert not np.any(gpu.all_reduce_sum(np.zeros((3, 8, 8), np.complex64)))
+    with pytest.raises(gpu.UsageError):
+        gpu.all_reduce_sum(np.zeros((0, 8, 8), np.complex64))
