@@ -158,6 +158,19 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
   (void)N1;                                                     \
   (void)N2
 
+// Barrier between the steps of a row-pass transform. Row lines map to consecutive thread
+// slots (Item<Geo, false>: line l = tid / n) in both steps; with N1 == N2 dividing 32 every
+// line stays inside one warp, so the exchange needs only a warp barrier and the warps of a
+// block run their lines independently. Column passes spread a line over the block.
+template <class Geo>
+__device__ __forceinline__ void row_line_sync() {
+  if constexpr (Geo::N1 == Geo::N2 && 32 % Geo::N1 == 0) {
+    __syncwarp();
+  } else {
+    __syncthreads();
+  }
+}
+
 // W^-1 column pass. Lines: (channel j, coil k-column q). Input chat_j*winv on the
 // Gc centered k-rows, output rows [r0, r0+nr) of U_j (G x Gc, row-major).
 template <class Geo>
@@ -258,7 +271,7 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restr
       }
       park_step1<Geo>(A, i1.l, i1.k, v);
     }
-    __syncthreads();
+    row_line_sync<Geo>();
     float2 u[N2];
     if (a2) {
       if (mode == R1_DECODE) {
@@ -295,9 +308,9 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restr
       }
     }
     if (mode == R1_DECODE) return;  // uniform across the block: no barrier follows
-    __syncthreads();
+    row_line_sync<Geo>();
     if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
-    __syncthreads();
+    row_line_sync<Geo>();
     if (a1) get_step1<Geo>(A, i1.l, i1.k, v);
   } else if (a1) {
 #pragma unroll
@@ -314,7 +327,7 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restr
     fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
   }
-  __syncthreads();
+  row_line_sync<Geo>();
   if (a2) {
     float2 u[N2];
     fft_step2<Geo, -1>(A, i2.l, i2.k, u);
@@ -490,7 +503,7 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
     fft_step1<Geo, +1>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
   }
-  __syncthreads();
+  row_line_sync<Geo>();
   float2 u[N2];
   if (a2) {
     fft_step2<Geo, +1, Geo::WIN_K2>(A, i2.l, i2.k, u);
@@ -526,13 +539,13 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
     }
     RP[((size_t)h * d.L + rl) * d.L + threadIdx.x] = make_double2(sx, sy);
   }
-  __syncthreads();
+  row_line_sync<Geo>();
   if (a1) {
     get_step1<Geo>(A, i1.l, i1.k, v);
     fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
   }
-  __syncthreads();
+  row_line_sync<Geo>();
   if (a2) {
     if (d.Gc * 4 == G) {  // pruned: only the coil band is kept
       fft_step2<Geo, -1, Geo::GC_K2>(A, i2.l, i2.k, u);
