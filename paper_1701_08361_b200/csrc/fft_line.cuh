@@ -371,18 +371,22 @@ struct LineGeom {
 
 // item decomposition of threadIdx.x for a step with `n` slots per line
 template <class Geo, bool COLS>
+// stride > 0 (row lines): line l owns the thread slots [l*stride, (l+1)*stride) whatever the
+// step's slot count n, so a line keeps the same threads in both steps
 struct Item {
   int l, k;
   bool on;
-  __device__ __forceinline__ Item(int tid, int n) {
+  __device__ __forceinline__ Item(int tid, int n, int stride = 0) {
     if (COLS) {
       l = tid % Geo::LPB;
       k = tid / Geo::LPB;
+      on = tid < Geo::LPB * n;
     } else {
-      l = tid / n;
-      k = tid - (tid / n) * n;
+      const int s = stride > 0 ? stride : n;
+      l = tid / s;
+      k = tid - l * s;
+      on = tid < Geo::LPB * s && k < n;
     }
-    on = tid < Geo::LPB * n;
   }
 };
 

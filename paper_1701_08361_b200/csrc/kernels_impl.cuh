@@ -150,21 +150,24 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
 #endif
 #define RTNB_PASS_BOUNDS_LIGHT __launch_bounds__(Geo::NT, (RTNB_MINB_LIGHT * 256 + Geo::NT - 1) / Geo::NT)
 
+template <class Geo, bool COLS>
+constexpr int kRowStride = (!COLS && 32 % Geo::NMAX == 0) ? Geo::NMAX : 0;
+
 #define RTNB_TILE_SETUP(COLS_)                                  \
   extern __shared__ float2 A[];                                 \
-  const Item<Geo, COLS_> i1(threadIdx.x, Geo::N2);              \
-  const Item<Geo, COLS_> i2(threadIdx.x, Geo::N1);              \
+  const Item<Geo, COLS_> i1(threadIdx.x, Geo::N2, kRowStride<Geo, COLS_>); \
+  const Item<Geo, COLS_> i2(threadIdx.x, Geo::N1, kRowStride<Geo, COLS_>); \
   constexpr int G = Geo::G, N1 = Geo::N1, N2 = Geo::N2;         \
   (void)N1;                                                     \
   (void)N2
 
-// Barrier between the steps of a row-pass transform. Row lines map to consecutive thread
-// slots (Item<Geo, false>: line l = tid / n) in both steps; with N1 == N2 dividing 32 every
-// line stays inside one warp, so the exchange needs only a warp barrier and the warps of a
-// block run their lines independently. Column passes spread a line over the block.
+// Barrier between the steps of a row-pass transform. A row line owns the same NMAX
+// consecutive thread slots in both steps (kRowStride); when NMAX divides 32 every line stays
+// inside one warp, so the exchange needs only a warp barrier and the warps of a block run
+// their lines independently. Column passes spread a line over the block.
 template <class Geo>
 __device__ __forceinline__ void row_line_sync() {
-  if constexpr (Geo::N1 == Geo::N2 && 32 % Geo::N1 == 0) {
+  if constexpr (32 % Geo::NMAX == 0) {
     __syncwarp();
   } else {
     __syncthreads();
