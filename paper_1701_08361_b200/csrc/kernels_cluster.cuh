@@ -117,6 +117,10 @@ __global__ void __launch_bounds__(Geo::NT, 2)
   const float2* dx = a.dx;
   const float2* cj = coils + (size_t)j * G * G;
   const Item<Geo, true> c1(threadIdx.x, N2), c2(threadIdx.x, N1);
+  // square factorisations (N1 == N2, C3/C4): a row line is the same warp-local thread slots
+  // in both steps, so the row passes exchange under warp barriers (measured: C1's 8 x 16
+  // is faster with its packed step-2 slots and block barriers)
+  constexpr bool kWarpRows = Geo::N1 == Geo::N2 && 32 % Geo::N1 == 0;
   const Item<Geo, false> r1(threadIdx.x, N2), r2(threadIdx.x, N1);
   float2 v[N1];
   float2 u[N2];
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(Geo::NT, 2)
       fft_step1<Geo, +1, CG::GC_N1>(v, r1.k, twG);
       park_step1<Geo>(A, r1.l, r1.k, v);
     }
-    __syncthreads();
+    step_sync<kWarpRows>();
     if (a2) {
       fft_step2<Geo, +1, Geo::WIN_K2>(A, r2.l, r2.k, u);
 #pragma unroll
@@ -203,15 +207,15 @@ __global__ void __launch_bounds__(Geo::NT, 2)
         u[k2] = w;
       }
     }
-    __syncthreads();
+    step_sync<kWarpRows>();
     if (a2) put_natural<Geo>(A, r2.l, r2.k, u);
-    __syncthreads();
+    step_sync<kWarpRows>();
     if (a1) {
       get_step1<Geo>(A, r1.l, r1.k, v);
       fft_step1<Geo, -1, Geo::WIN_N1>(v, r1.k, twG);
       park_step1<Geo>(A, r1.l, r1.k, v);
     }
-    __syncthreads();
+    step_sync<kWarpRows>();
     if (a2) {
       fft_step2<Geo, -1>(A, r2.l, r2.k, u);
       const int r = rank * RPC + r2.l;
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(Geo::NT, 2)
       fft_step1<Geo, +1>(v, r1.k, twG);
       park_step1<Geo>(A, r1.l, r1.k, v);
     }
-    __syncthreads();
+    step_sync<kWarpRows>();
     if (a2) {
       fft_step2<Geo, +1, Geo::WIN_K2>(A, r2.l, r2.k, u);
       float2* rc = RC + (size_t)j * L * L + (size_t)r * L;
@@ -312,15 +316,15 @@ __global__ void __launch_bounds__(Geo::NT, 2)
         u[k2] = w;
       }
     }
-    __syncthreads();
+    step_sync<kWarpRows>();
     if (a2) put_natural<Geo>(A, r2.l, r2.k, u);
-    __syncthreads();
+    step_sync<kWarpRows>();
     if (a1) {
       get_step1<Geo>(A, r1.l, r1.k, v);
       fft_step1<Geo, -1, Geo::WIN_N1>(v, r1.k, twG);
       park_step1<Geo>(A, r1.l, r1.k, v);
     }
-    __syncthreads();
+    step_sync<kWarpRows>();
     if (a2) {
       fft_step2<Geo, -1, CG::GC_K2>(A, r2.l, r2.k, u);
 #pragma unroll

@@ -165,6 +165,14 @@ constexpr int kRowStride = (!COLS && 32 % Geo::NMAX == 0) ? Geo::NMAX : 0;
 // consecutive thread slots in both steps (kRowStride); when NMAX divides 32 every line stays
 // inside one warp, so the exchange needs only a warp barrier and the warps of a block run
 // their lines independently. Column passes spread a line over the block.
+template <bool WARP>
+__device__ __forceinline__ void step_sync() {
+  if constexpr (WARP) {
+    __syncwarp();
+  } else {
+    __syncthreads();
+  }
+}
 template <class Geo>
 __device__ __forceinline__ void row_line_sync() {
   if constexpr (32 % Geo::NMAX == 0) {
