@@ -1268,7 +1268,7 @@ __global__ void __launch_bounds__(Geo::NT) k_fft_pass(float2* __restrict__ data,
     fft_step1<Geo, S>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
   }
-  __syncthreads();
+  step_sync<(kRowStride<Geo, COLS> > 0)>();  // row lines: warp-local exchange
   if (i2.on && i2.l < nl) {
     float2 u[N2];
     fft_step2<Geo, S>(A, i2.l, i2.k, u);
