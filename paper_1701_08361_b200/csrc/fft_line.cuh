@@ -8,6 +8,10 @@
 //           stride-N2 subsequence, then the inter-step twiddle W_G^{n2 k1};
 //   step 2: N1 threads per line, each an N2-point DFT in registers over a
 //           contiguous (padded) smem block, results in natural order.
+// Column lines interleave across the block (coalesced loads of adjacent columns), so
+// their step exchange is a block barrier. Row lines own NMAX consecutive thread slots
+// in both steps (idle slots when N1 != N2); when NMAX divides 32 a row line lives in
+// one warp and its exchange needs only a warp barrier (kernels_impl.cuh: row_line_sync).
 // The small DFTs are fully unrolled mixed-radix recursions (radix 2/3/4 closed
 // forms, direct sums for other primes) whose twiddles are compile-time constant
 // indices into a __constant__ table, so they become constant-bank FMA operands.
