@@ -539,17 +539,8 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
       u[k2] = w;
     }
   }
-  __syncthreads();
+  row_line_sync<Geo>();
   if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
-  if ((int)threadIdx.x < d.L) {
-    double sx = 0.0, sy = 0.0;
-    for (int l = 0; l < nl; ++l) {
-      const float2 t = RCs[l * L + threadIdx.x];
-      sx += t.x;
-      sy += t.y;
-    }
-    RP[((size_t)h * d.L + rl) * d.L + threadIdx.x] = make_double2(sx, sy);
-  }
   row_line_sync<Geo>();
   if (a1) {
     get_step1<Geo>(A, i1.l, i1.k, v);
@@ -570,6 +561,18 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
       const int q = p - d.off;
       if (q >= 0 && q < d.Gc) Yr[q] = flip(u[k2], p);
     }
+  }
+  // the group's channel terms, summed in channel order once every line has written them
+  // (the block's only barrier between its lines, placed after both transforms)
+  __syncthreads();
+  if ((int)threadIdx.x < d.L) {
+    double sx = 0.0, sy = 0.0;
+    for (int l = 0; l < nl; ++l) {
+      const float2 t = RCs[l * L + threadIdx.x];
+      sx += t.x;
+      sy += t.y;
+    }
+    RP[((size_t)h * d.L + rl) * d.L + threadIdx.x] = make_double2(sx, sy);
   }
   if (setup) {
     double vv[1] = {resid}, tot[1];
