@@ -422,6 +422,22 @@ __device__ __forceinline__ void fft_step2(const float2* A, int l, int k1, float2
   dft_m<Geo::N2, S, Geo::ALL_N2, OUT>(u);
 }
 
+// the inverse of a step-2 result without reordering (Toeplitz column pass): thread k1
+// holds X[k1 + N1*k2] over k2; the inverse's inner N2-point DFT over k2 runs in its
+// registers, then the twiddle W_G^{-S*...}: u[n2] *= W_G^{S-sign n2 k1}; the result is
+// written back to the thread's own step-2 block, where get_step1 reads it by n2 for the
+// outer N1-point DFT (in place: every thread reads and writes only its own block)
+template <class Geo, int S>
+__device__ __forceinline__ void inv_inner(float2* A, int l, int k1, float2 (&u)[Geo::N2],
+                                          const float4* __restrict__ twG) {
+  dft_m<Geo::N2, S, Geo::ALL_N2, Geo::ALL_N2>(u);
+  const float4* tw = twG + (S > 0 ? Geo::G : 0);
+  float2* dst = A + Geo::a(l, Geo::N2 * k1);
+  dst[0] = u[0];
+#pragma unroll
+  for (int n2 = 1; n2 < Geo::N2; ++n2) dst[n2] = cmul_pk(u[n2], __ldg(tw + n2 * k1));
+}
+
 // natural-order write / step-1-order read, for chaining two transforms in a block
 template <class Geo>
 __device__ __forceinline__ void put_natural(float2* A, int l, int k1, const float2 (&u)[Geo::N2]) {

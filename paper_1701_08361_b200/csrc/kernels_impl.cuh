@@ -389,23 +389,20 @@ __global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
       const int p = i2.k + N1 * k2;
       u[k2] = cscale(cmul(u[k2], Pc[(size_t)p * G]), d.invG);
     }
+    // the inverse transform in the reverse step order: its N2-point DFTs over k2 act on
+    // this thread's registers, so no reordering exchange is needed
+    inv_inner<Geo, +1>(A, i2.l, i2.k, u, twG);
   }
-  __syncthreads();
-  if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
   __syncthreads();
   if (a1) {
+    // outer N1-point DFT over k1 -> x[N2 n1 + n2], window rows only
     get_step1<Geo>(A, i1.l, i1.k, v);
-    fft_step1<Geo, +1>(v, i1.k, twG);
-    park_step1<Geo>(A, i1.l, i1.k, v);
-  }
-  __syncthreads();
-  if (a2) {
-    fft_step2<Geo, +1, Geo::WIN_K2>(A, i2.l, i2.k, u);
-    float2* col = Vj + q0 + i2.l;
+    dft_m<N1, +1, Geo::ALL_N1, Geo::WIN_N1>(v);
+    float2* col = Vj + q0 + i1.l;
 #pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) {
-      const int p = i2.k + N1 * k2;
-      if (p >= d.lo && p < d.lo + d.L) col[(size_t)(p - d.lo) * G] = flip(u[k2], p);
+    for (int n1 = 0; n1 < N1; ++n1) {
+      const int t = N2 * n1 + i1.k;
+      if (t >= d.lo && t < d.lo + d.L) col[(size_t)(t - d.lo) * G] = flip(v[n1], t);
     }
   }
 }
