@@ -251,25 +251,20 @@ __global__ void __launch_bounds__(Geo::NT, 2)
         const int p = c2.k + N1 * k2;
         u[k2] = cscale(cmul(u[k2], Pc[(size_t)p * G]), d.invG);
       }
+      // inverse in the reverse step order (as k_colsT): inner DFTs in registers
+      inv_inner<Geo, +1>(A, c2.l, c2.k, u, twG);
     }
-    __syncthreads();
-    if (c2.on) put_natural<Geo>(A, c2.l, c2.k, u);
     __syncthreads();
     if (c1.on) {
       get_step1<Geo>(A, c1.l, c1.k, v);
-      fft_step1<Geo, +1>(v, c1.k, twG);
-      park_step1<Geo>(A, c1.l, c1.k, v);
-    }
-    __syncthreads();
-    if (c2.on) {
-      fft_step2<Geo, +1, Geo::WIN_K2>(A, c2.l, c2.k, u);
-      const int q = rank * CPC + ql2;
+      dft_m<N1, +1, Geo::ALL_N1, Geo::WIN_N1>(v);
+      const int q = rank * CPC + ql1;
 #pragma unroll
-      for (int k2 = 0; k2 < N2; ++k2) {
-        const int p = c2.k + N1 * k2;
-        if (p >= LO && p < LO + L) {
-          const int r = p - LO;
-          st_cluster(cluster_map(ws_s + 8u * (uint32_t)((r % RPC) * G + q), r / RPC), flip(u[k2], p));
+      for (int n1 = 0; n1 < N1; ++n1) {
+        const int t = N2 * n1 + c1.k;
+        if (t >= LO && t < LO + L) {
+          const int r = t - LO;
+          st_cluster(cluster_map(ws_s + 8u * (uint32_t)((r % RPC) * G + q), r / RPC), flip(v[n1], t));
         }
       }
     }
