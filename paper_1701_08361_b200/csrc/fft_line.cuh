@@ -422,15 +422,16 @@ __device__ __forceinline__ void fft_step2(const float2* A, int l, int k1, float2
   dft_m<Geo::N2, S, Geo::ALL_N2, OUT>(u);
 }
 
-// the inverse of a step-2 result without reordering (Toeplitz column pass): thread k1
-// holds X[k1 + N1*k2] over k2; the inverse's inner N2-point DFT over k2 runs in its
-// registers, then the twiddle W_G^{-S*...}: u[n2] *= W_G^{S-sign n2 k1}; the result is
-// written back to the thread's own step-2 block, where get_step1 reads it by n2 for the
-// outer N1-point DFT (in place: every thread reads and writes only its own block)
-template <class Geo, int S>
+// A second transform of a step-2 result without reordering: thread k1 holds w[k1 + N1*k2]
+// over k2 (natural order). The transform's inner N2-point DFT over k2 runs in its
+// registers (IN: which k2 may be nonzero), then the twiddle W_G^{n2 k1} of sign S; the
+// result goes back to the thread's own step-2 block, where get_step1 reads it by n2 for
+// the outer N1-point DFT, whose output n1 is element N2*n1 + n2 (in place: every thread
+// reads and writes only its own block)
+template <class Geo, int S, uint32_t IN = Geo::ALL_N2>
 __device__ __forceinline__ void inv_inner(float2* A, int l, int k1, float2 (&u)[Geo::N2],
                                           const float4* __restrict__ twG) {
-  dft_m<Geo::N2, S, Geo::ALL_N2, Geo::ALL_N2>(u);
+  dft_m<Geo::N2, S, IN, Geo::ALL_N2>(u);
   const float4* tw = twG + (S > 0 ? Geo::G : 0);
   float2* dst = A + Geo::a(l, Geo::N2 * k1);
   dst[0] = u[0];

@@ -319,34 +319,48 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restr
       }
     }
     if (mode == R1_DECODE) return;  // uniform across the block: no barrier follows
+    // OP: the forward Toeplitz row transform in the reverse step order (inner DFTs over
+    // the window k2 on the registers, one exchange, outer DFT over k1)
+    if (a2) inv_inner<Geo, -1, Geo::WIN_K2>(A, i2.l, i2.k, u, twG);
     row_line_sync<Geo>();
-    if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
-    row_line_sync<Geo>();
-    if (a1) get_step1<Geo>(A, i1.l, i1.k, v);
-  } else if (a1) {
+    if (a1) {
+      get_step1<Geo>(A, i1.l, i1.k, v);
+      dft_m<N1, -1, Geo::ALL_N1, Geo::ALL_N1>(v);
+      float2* Vr = V + (size_t)j * d.L * G + (size_t)(rl0 + i1.l) * G;
 #pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) {
-      const int t = N2 * n1 + i1.k;
-      v[n1] = make_float2(0.f, 0.f);
-      if (t >= d.lo && t < d.lo + d.L) {
-        const size_t e = (size_t)r1 * G + t;
-        v[n1] = flip(cmul_rn(rhom[e], cj[e]), t);  // e = rho * c_j   (nlinv.cpp:252)
+      for (int n1 = 0; n1 < N1; ++n1) {
+        const int t = N2 * n1 + i1.k;
+        Vr[t] = flip(v[n1], t);
       }
     }
-  }
-  if (a1) {
-    fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
-    park_step1<Geo>(A, i1.l, i1.k, v);
-  }
-  row_line_sync<Geo>();
-  if (a2) {
-    float2 u[N2];
-    fft_step2<Geo, -1>(A, i2.l, i2.k, u);
-    float2* Vr = V + (size_t)j * d.L * G + (size_t)(rl0 + i2.l) * G;
+  } else {
+    // SETUP: e = rho * c_j on the window, forward Toeplitz row transform in the usual
+    // step order
+    if (a1) {
 #pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) {
-      const int p = i2.k + N1 * k2;
-      Vr[p] = flip(u[k2], p);
+      for (int n1 = 0; n1 < N1; ++n1) {
+        const int t = N2 * n1 + i1.k;
+        v[n1] = make_float2(0.f, 0.f);
+        if (t >= d.lo && t < d.lo + d.L) {
+          const size_t e = (size_t)r1 * G + t;
+          v[n1] = flip(cmul_rn(rhom[e], cj[e]), t);  // e = rho * c_j   (nlinv.cpp:252)
+        }
+      }
+    }
+    if (a1) {
+      fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
+      park_step1<Geo>(A, i1.l, i1.k, v);
+    }
+    row_line_sync<Geo>();
+    if (a2) {
+      float2 u[N2];
+      fft_step2<Geo, -1>(A, i2.l, i2.k, u);
+      float2* Vr = V + (size_t)j * d.L * G + (size_t)(rl0 + i2.l) * G;
+#pragma unroll
+      for (int k2 = 0; k2 < N2; ++k2) {
+        const int p = i2.k + N1 * k2;
+        Vr[p] = flip(u[k2], p);
+      }
     }
   }
 }
@@ -536,27 +550,50 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
       u[k2] = w;
     }
   }
-  row_line_sync<Geo>();
-  if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
-  row_line_sync<Geo>();
-  if (a1) {
-    get_step1<Geo>(A, i1.l, i1.k, v);
-    fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
-    park_step1<Geo>(A, i1.l, i1.k, v);
-  }
-  row_line_sync<Geo>();
-  if (a2) {
-    if (d.Gc * 4 == G) {  // pruned: only the coil band is kept
-      fft_step2<Geo, -1, Geo::GC_K2>(A, i2.l, i2.k, u);
-    } else {
-      fft_step2<Geo, -1>(A, i2.l, i2.k, u);
-    }
-    float2* Yr = Y + (size_t)(j0 + i2.l) * d.L * d.Gc + (size_t)rl * d.Gc;
+  if constexpr (32 % Geo::NMAX == 0) {
+    // the forward W^-H row transform in the reverse step order: inner DFTs over k2 on the
+    // registers (only window k2 nonzero), outer DFT over k1 after one exchange
+    if (a2) inv_inner<Geo, -1, Geo::WIN_K2>(A, i2.l, i2.k, u, twG);
+    row_line_sync<Geo>();
+    if (a1) {
+      get_step1<Geo>(A, i1.l, i1.k, v);
+      if (d.Gc * 4 == G) {  // pruned: only the coil band is kept
+        dft_m<N1, -1, Geo::ALL_N1, Geo::GC_N1>(v);
+      } else {
+        dft_m<N1, -1, Geo::ALL_N1, Geo::ALL_N1>(v);
+      }
+      float2* Yr = Y + (size_t)(j0 + i1.l) * d.L * d.Gc + (size_t)rl * d.Gc;
 #pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) {
-      const int p = i2.k + N1 * k2;
-      const int q = p - d.off;
-      if (q >= 0 && q < d.Gc) Yr[q] = flip(u[k2], p);
+      for (int n1 = 0; n1 < N1; ++n1) {
+        const int p = N2 * n1 + i1.k;
+        const int q = p - d.off;
+        if (q >= 0 && q < d.Gc) Yr[q] = flip(v[n1], p);
+      }
+    }
+  } else {
+    // 320/384-thread lines (block barriers): the usual step order spills less
+    __syncthreads();
+    if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
+    __syncthreads();
+    if (a1) {
+      get_step1<Geo>(A, i1.l, i1.k, v);
+      fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
+      park_step1<Geo>(A, i1.l, i1.k, v);
+    }
+    __syncthreads();
+    if (a2) {
+      if (d.Gc * 4 == G) {  // pruned: only the coil band is kept
+        fft_step2<Geo, -1, Geo::GC_K2>(A, i2.l, i2.k, u);
+      } else {
+        fft_step2<Geo, -1>(A, i2.l, i2.k, u);
+      }
+      float2* Yr = Y + (size_t)(j0 + i2.l) * d.L * d.Gc + (size_t)rl * d.Gc;
+#pragma unroll
+      for (int k2 = 0; k2 < N2; ++k2) {
+        const int p = i2.k + N1 * k2;
+        const int q = p - d.off;
+        if (q >= 0 && q < d.Gc) Yr[q] = flip(u[k2], p);
+      }
     }
   }
   // the group's channel terms, summed in channel order once every line has written them
