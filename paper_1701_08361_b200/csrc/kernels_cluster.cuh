@@ -207,22 +207,38 @@ __global__ void __launch_bounds__(Geo::NT, 2)
         u[k2] = w;
       }
     }
-    step_sync<kWarpRows>();
-    if (a2) put_natural<Geo>(A, r2.l, r2.k, u);
-    step_sync<kWarpRows>();
-    if (a1) {
-      get_step1<Geo>(A, r1.l, r1.k, v);
-      fft_step1<Geo, -1, Geo::WIN_N1>(v, r1.k, twG);
-      park_step1<Geo>(A, r1.l, r1.k, v);
-    }
-    step_sync<kWarpRows>();
-    if (a2) {
-      fft_step2<Geo, -1>(A, r2.l, r2.k, u);
-      const int r = rank * RPC + r2.l;
+    if constexpr (kWarpRows) {
+      // the forward Toeplitz row transform in the reverse step order (as k_rows1)
+      if (a2) inv_inner<Geo, -1, Geo::WIN_K2>(A, r2.l, r2.k, u, twG);
+      step_sync<kWarpRows>();
+      if (a1) {
+        get_step1<Geo>(A, r1.l, r1.k, v);
+        dft_m<N1, -1, Geo::ALL_N1, Geo::ALL_N1>(v);
+        const int r = rank * RPC + r1.l;
 #pragma unroll
-      for (int k2 = 0; k2 < N2; ++k2) {
-        const int p = r2.k + N1 * k2;
-        st_cluster(cluster_map(vs_s + 8u * (uint32_t)(r * VS + p % CPC), p / CPC), flip(u[k2], p));
+        for (int n1 = 0; n1 < N1; ++n1) {
+          const int p = N2 * n1 + r1.k;
+          st_cluster(cluster_map(vs_s + 8u * (uint32_t)(r * VS + p % CPC), p / CPC), flip(v[n1], p));
+        }
+      }
+    } else {
+      step_sync<kWarpRows>();
+      if (a2) put_natural<Geo>(A, r2.l, r2.k, u);
+      step_sync<kWarpRows>();
+      if (a1) {
+        get_step1<Geo>(A, r1.l, r1.k, v);
+        fft_step1<Geo, -1, Geo::WIN_N1>(v, r1.k, twG);
+        park_step1<Geo>(A, r1.l, r1.k, v);
+      }
+      step_sync<kWarpRows>();
+      if (a2) {
+        fft_step2<Geo, -1>(A, r2.l, r2.k, u);
+        const int r = rank * RPC + r2.l;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+          const int p = r2.k + N1 * k2;
+          st_cluster(cluster_map(vs_s + 8u * (uint32_t)(r * VS + p % CPC), p / CPC), flip(u[k2], p));
+        }
       }
     }
     (void)R1;
@@ -311,23 +327,42 @@ __global__ void __launch_bounds__(Geo::NT, 2)
         u[k2] = w;
       }
     }
-    step_sync<kWarpRows>();
-    if (a2) put_natural<Geo>(A, r2.l, r2.k, u);
-    step_sync<kWarpRows>();
-    if (a1) {
-      get_step1<Geo>(A, r1.l, r1.k, v);
-      fft_step1<Geo, -1, Geo::WIN_N1>(v, r1.k, twG);
-      park_step1<Geo>(A, r1.l, r1.k, v);
-    }
-    step_sync<kWarpRows>();
-    if (a2) {
-      fft_step2<Geo, -1, CG::GC_K2>(A, r2.l, r2.k, u);
+    if constexpr (kWarpRows) {
+      // the forward W^-H row transform in the reverse step order (as k_rows2)
+      if (a2) inv_inner<Geo, -1, Geo::WIN_K2>(A, r2.l, r2.k, u, twG);
+      step_sync<kWarpRows>();
+      if (a1) {
+        get_step1<Geo>(A, r1.l, r1.k, v);
+        dft_m<N1, -1, Geo::ALL_N1, CG::GC_N1>(v);
+        const int r1w = rank * RPC + r1.l;
 #pragma unroll
-      for (int k2 = 0; k2 < N2; ++k2) {
-        const int p = r2.k + N1 * k2;
-        const int q = p - OFF;
-        if (q >= 0 && q < GC) {
-          st_cluster(cluster_map(uy_s + 8u * (uint32_t)(r * GCPC + q % GCPC), q / GCPC), flip(u[k2], p));
+        for (int n1 = 0; n1 < N1; ++n1) {
+          const int p = N2 * n1 + r1.k;
+          const int q = p - OFF;
+          if (q >= 0 && q < GC) {
+            st_cluster(cluster_map(uy_s + 8u * (uint32_t)(r1w * GCPC + q % GCPC), q / GCPC), flip(v[n1], p));
+          }
+        }
+      }
+    } else {
+      step_sync<kWarpRows>();
+      if (a2) put_natural<Geo>(A, r2.l, r2.k, u);
+      step_sync<kWarpRows>();
+      if (a1) {
+        get_step1<Geo>(A, r1.l, r1.k, v);
+        fft_step1<Geo, -1, Geo::WIN_N1>(v, r1.k, twG);
+        park_step1<Geo>(A, r1.l, r1.k, v);
+      }
+      step_sync<kWarpRows>();
+      if (a2) {
+        fft_step2<Geo, -1, CG::GC_K2>(A, r2.l, r2.k, u);
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+          const int p = r2.k + N1 * k2;
+          const int q = p - OFF;
+          if (q >= 0 && q < GC) {
+            st_cluster(cluster_map(uy_s + 8u * (uint32_t)(r * GCPC + q % GCPC), q / GCPC), flip(u[k2], p));
+          }
         }
       }
     }
