@@ -361,6 +361,42 @@ def cpu_baseline(cfg, z, P, plan):
                       f"oracle shim FFT"}
 
 
+def check_timed_frames(pb, series, plan, frames, P, U, audit, first, n_check):
+    """Parity of the headline frames themselves (outside the timed region): each checked
+    frame of the timed run is replayed through the reference's reconstruct_frame with a
+    per-step RegProvider (nlinv.cpp:286-335) fed the device estimates of the sources its
+    audit recorded, and the device image / estimate must match within the north-star
+    frame tolerance (1e-3 relative L2), the CR iteration split exactly."""
+    from oracle import ref
+    scale = series.normalize()
+    lanes = max(1, min(4, os.cpu_count() or 1))
+    unity = pb.initial_estimate(plan)
+    M = plan.newton_steps
+    rows = []
+    for k in range(n_check):
+        n = first + k
+        a = audit[k]
+        src = lambda f: unity if f < 0 else series.estimate(f)  # noqa: E731
+        init = src(a.init_src)
+        regs = [src(a.reg_src[m]) if a.init_src >= 0 else unity for m in range(M)]
+        z = (frames[n] * np.float32(scale)).astype(np.complex64)
+        img, est, per = ref.reconstruct_frame_regs(plan, z, P[n % U], init, regs, A=lanes)
+        img = img * np.float32(1.0 / scale)
+        got_img = series.images(n, 1)[0]
+        got_est = series.estimate(n)
+
+        def rel(g, w):
+            g = np.asarray(g, np.complex128).ravel()
+            w = np.asarray(w, np.complex128).ravel()
+            return float(np.linalg.norm(g - w) / np.linalg.norm(w))
+
+        rows.append({"frame": n, "init_src": a.init_src, "reg_src": a.reg_src, "image_rel_err": rel(got_img, img),
+                     "estimate_rel_err": rel(got_est, est), "cg_per_step_ref": per})
+    worst = max(max(r["image_rel_err"], r["estimate_rel_err"]) for r in rows)
+    return {"frames": rows, "max_rel_err": worst, "tolerance": 1e-3, "pass": worst < 1e-3,
+            "oracle": "oracle/_ref reconstruct_frame with the audited per-step sources (device estimates)"}
+
+
 def decompositions(pb, plan, frames, P, U, sched, ngpu):
     """fps and p50 frame latency of each decomposition over ngpu GPUs (device time,
     CUDA events spanning every worker stream), plus the autotuner's hybrid pick"""
@@ -445,6 +481,8 @@ def main():
                     help="autotuner store (autotune.hpp TuneDb format)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-check", action="store_true",
+                    help="skip the parity check of the first two timed frames against the reference")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = args.config
@@ -528,6 +566,14 @@ def main():
         caps[m] = (rem + (M - m) - 1) // (M - m)
         rem -= caps[m]
     assert list(out["cg_iters"]) == [sum(caps)] * S
+
+    # the headline frames checked against the reference (after the timed region)
+    check = None
+    if rank == 0 and world == 1 and not args.no_check:
+        try:
+            check = check_timed_frames(pb, series, plan, frames, P, U, out["audit"], W + NTUNE, min(2, S))
+        except Exception as e:  # reported; the oracle may be absent on a stripped box
+            check = {"error": str(e)}
 
     # end to end: pinned host frames streamed through the public series call
     e2e = None
@@ -644,6 +690,7 @@ def main():
         "e2e": e2e, "gpu_launches": launches_per_frame(caps, M) * S, "roofline": roofline, "autotune": tuning,
         "clocks": clk.summary(),
         "latency_mode": latency_mode,
+        "check": check,
     }
     if decomp is not None:
         line["decompositions"] = decomp

@@ -274,14 +274,15 @@ def reconstruct_frame(plan, z, P, init, reg=None, A=1):
     return img, est, per[:plan.newton_steps].tolist(), secs.value
 
 
-def reconstruct_frame_regs(plan, z, P, init, regs):
-    """frame with a per-step regularisation target regs[m] (audit replay)"""
+def reconstruct_frame_regs(plan, z, P, init, regs, A=1):
+    """frame with a per-step regularisation target regs[m] (audit replay); A WorkerGroup
+    lanes (bit-identical results for every A, test_decomp.cpp:309-326)"""
     regs = _c64(np.stack([_c64(r) for r in regs]))
     img = np.zeros((plan.N, plan.N), np.complex64)
     est = np.zeros_like(_c64(init))
     per = np.zeros(max(plan.newton_steps, 1), np.int32)
     _chk(lib().ref_reconstruct_frame_regs(ctypes.byref(plan_c(plan)), _fp(_c64(z)), _fp(_c64(P)), _fp(_c64(init)),
-                                          _fp(regs), _fp(img), _fp(est), _ip(per)))
+                                          _fp(regs), A, _fp(img), _fp(est), _ip(per)))
     return img, est, per[:plan.newton_steps].tolist()
 
 

@@ -529,7 +529,7 @@ int ref_reconstruct_frame(const ref_plan_t* p, const float* z, const float* P, c
 // per-step regularisation targets regs[m] (M*D): replays a scheduled frame whose
 // sources were recorded in an audit (SURVEY.md §7 "audit replay")
 int ref_reconstruct_frame_regs(const ref_plan_t* p, const float* z, const float* P, const float* init,
-                               const float* regs, float* out_image, float* out_est, int* out_cg_per_step) {
+                               const float* regs, int A, float* out_image, float* out_est, int* out_cg_per_step) {
   return guarded([&] {
     const ReconPlan plan = to_plan(p);
     const PsfKernel psf = load_psf(P, plan.G);
@@ -538,7 +538,11 @@ int ref_reconstruct_frame_regs(const ref_plan_t* p, const float* z, const float*
     std::vector<Estimate> r;
     for (int m = 0; m < plan.newton_steps; ++m) r.push_back(load_est(regs + 2 * D * m, plan));
     const RegProvider rp = [&r](int m) -> const Estimate& { return r[static_cast<size_t>(m)]; };
-    const FrameResult fr = reconstruct_frame(load_z(z, plan), psf, plan, winv, load_est(init, plan), rp);
+    // A WorkerGroup lanes only speed the replay up: the reference is bit-identical across A
+    std::unique_ptr<WorkerGroup> wg;
+    if (A > 1) wg = std::make_unique<WorkerGroup>(A);
+    const FrameResult fr =
+        reconstruct_frame(load_z(z, plan), psf, plan, winv, load_est(init, plan), rp, wg.get());
     store_img(fr.image, out_image);
     if (out_est) store_est(fr.est, out_est);
     if (out_cg_per_step) {

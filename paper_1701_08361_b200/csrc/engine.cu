@@ -371,11 +371,18 @@ void Engine::alloc() {
 
 void Engine::ensure_cr_capacity(int max_iter) {
   if (max_iter + 2 <= cr_cap_) return;
+  if (grp_rank_ >= 0) fail(2, "cg capacity of a channel-group member is fixed when the group is built");
   if (cr_buf_) {
+    // the cached step / frame graphs captured the CR scalar pointers by value
     check_cuda(cudaStreamSynchronize(s_), "sync");
+    for (auto& g : step_graph_) {
+      if (g) cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+    if (frame_graph_) cudaGraphExecDestroy(frame_graph_);
+    frame_graph_ = nullptr;
     cudaFree(cr_buf_);
   }
-  if (grp_rank_ >= 0) fail(2, "cg capacity of a channel-group member is fixed when the group is built");
   cr_cap_ = max_iter + 2;
   check_cuda(cudaMalloc(&cr_buf_, sizeof(double) * 10 * cr_cap_), "cr scalars");
   check_cuda(cudaMemset(cr_buf_, 0, sizeof(double) * 10 * cr_cap_), "cr scalars");

@@ -236,6 +236,10 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
       each([&](int, Engine& e) { e.enq_grp_fin(0, -1, cap - 1, tol); });
     }
     each([&](int, Engine& e) { e.win_only_ok_ = 0; });
+  } else {
+    // no CR iteration follows: a lagging member may still be reading this step's setup
+    // partials in its k_grp_fin when the next step's setup_front overwrites them
+    barrier();
   }
   each([&](int, Engine& e) { e.enq_axpy1(); });
 }

@@ -186,6 +186,10 @@ void ProcGroup::enq_newton_step(int m, float tol, int cap, bool sync_each) {
       e.enq_grp_fin(0, -1, cap - 1, tol);
     }
     e.win_only_ok_ = 0;
+  } else {
+    // no CR iteration follows: a lagging member may still be reading this step's setup
+    // partials in its k_grp_fin when the next step's setup_front overwrites them
+    barrier();
   }
   e.enq_axpy1();
 }

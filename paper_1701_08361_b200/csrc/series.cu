@@ -535,7 +535,9 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
       ledger.poison();
       enq.poison();
     } catch (...) {
-      {
+      // once a worker asked for the safe-mode re-run, the other workers' failures are
+      // the poisoned ledgers' "series aborted" faults: the re-run supersedes them
+      if (!redo.load()) {
         std::lock_guard<std::mutex> g(err_mu);
         if (!first_err) first_err = std::current_exception();
       }

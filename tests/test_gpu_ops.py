@@ -346,3 +346,24 @@ def test_reconstruct_frame_with_a_reg_provider_matches_reference(gpu, ref, A, bu
     assert fr.cg_per_step == per
     assert rel_err(fr.image, img) < FRAME_TOL
     assert rel_err(fr.est, est) < FRAME_TOL
+
+
+def test_cg_capacity_growth_keeps_cached_frame_graphs_valid(gpu, ref):
+    """a cg_solve with max_iter above the plan's CR capacity reallocates the
+    device CR scalars; the frame graphs captured earlier hold the old pointers and must
+    be rebuilt, so a frame after the solve equals the frame before it bit for bit"""
+    plan = gpu.make_plan(16, 2)
+    plan.newton_steps, plan.cg_iter_budget = 3, 9
+    inp = phantom_frame_inputs(ref, plan, K=7, U=1)
+    init = gpu.initial_estimate(plan)
+    with gpu.Context(plan) as ctx:
+        ctx.set_psf(inp["P"][0])
+        ctx.set_data(inp["z"][0])
+        before = ctx.reconstruct_frame(init)
+        ctx.make_step_cache(before.est)
+        rhs = random_estimate(plan, 9)
+        _, iters, _ = ctx.cg_solve(rhs, 0.5, 0.0, 400)  # capacity grows past max(200, 9)
+        assert iters == 400
+        after = ctx.reconstruct_frame(init)
+    assert np.array_equal(before.image, after.image)
+    assert np.array_equal(before.est, after.est)

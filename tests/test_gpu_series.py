@@ -313,3 +313,24 @@ def test_psf_cache_sidecar_interchanges_with_the_reference(gpu, ref, tmp_path):
     (tmp_path / "bad.psfc").write_bytes(b"nope")
     with pytest.raises(gpu.DataError):
         s2.load_psf_cache(tmp_path / "bad.psfc")
+
+
+@pytest.mark.parametrize("T", [2, 3])
+def test_zero_rhs_frames_recover_through_the_safe_mode_rerun(gpu, ref, T):
+    """a speculative budget split that meets an exactly-zero right-hand side
+    (frame_verify fails) while other workers wait on the poisoned ledgers must end in the
+    safe-mode re-run, not in a spurious DecompFault. All-zero frames chained from the
+    initial estimate give zero rhs in every step (nlinv.cpp:182-186: 0 iterations)."""
+    plan = _small_plan(gpu, 16, 2, 3, 9)
+    F = 6
+    samples = np.zeros((F, plan.J, 5, 2 * plan.N), np.complex64)
+    _, angles = ref.phantom_series(plan.J, F, 5, 3, plan.N, 0.0, 3)
+    z = np.zeros((F, plan.J, plan.G, plan.G), np.complex64)
+    P = np.stack([ref.build_psf(plan, angles[n], 2 * plan.N) for n in range(3)])
+    out = _run(gpu, plan, z, P, [n % 3 for n in range(F)],
+               gpu.SeriesOptions(T=T, sched=gpu.TemporalSchedule(1, 1)))
+    want = ref.reconstruct_series(plan, samples, angles, T=1, sched=(1, 1))
+    assert list(out["cg_iters"]) == list(want["cg_iters"]) == [0] * F
+    assert np.array_equal(out["images"], want["images"])
+    for n in range(1, F):
+        assert out["audit"][n].reg_final_src == n - 1
