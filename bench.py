@@ -299,48 +299,105 @@ def weak_scaling_value(world, frames_per_rank, span_ms_max):
 # ------------------------------------------------------------------------------------
 # reference arm: the reference's own CPU path (oracle/_ref) on the same workload
 # ------------------------------------------------------------------------------------
+def host_info():
+    """nproc and the CPU model of this host (state the cores the CPU arm had)"""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"nproc": os.cpu_count() or 1, "cpu_model": model}
+
+
+def reference_inputs(cfg, plan, F):
+    """the reference's own pre stage (grid_adjoint per frame, build_psf per angle set,
+    prep_series normalisation of frame 0) on the bench's raw acquisitions, outside any
+    timed region"""
+    from oracle import ref
+    G, J, K, U, _ = CONFIGS[cfg]
+    raw, angles = synth_raw(G, J, K, U, n_unique=U)
+    P = np.stack([ref.build_psf(plan, angles[t], 2 * plan.N) for t in range(U)])
+    zu = np.stack([ref.grid_adjoint(plan, raw[t], angles[t]) for t in range(U)])
+    scale = np.float32(100.0 / math.sqrt(float(np.sum(np.abs(zu[0].astype(np.complex128)) ** 2))))
+    z = np.stack([(zu[n % U] * scale).astype(np.complex64) for n in range(F)])
+    return z, P, [n % U for n in range(F)]
+
+
 def reference_arm(args, cfg):
+    """BASELINE.md CPU-baseline plan: the reference's scheduled series driver
+    (reconstruct_series, nlinv.cpp:446-526, with TemporalSchedule::for_turns(U) like our
+    arm) on this host. (T, A) comes from the reference's own autotuner (learn_step /
+    select_config, autotune.cpp:40-88) over legal_configs(nproc), pruned for time to the
+    A = min(4, nproc) row with T <= 4 (the schedule keeps at most o + 1 = 4 frames
+    progressing, so more threads only wait), each candidate timed on 2T frames past the
+    strict prefix; plus T = 1, A = 1 (reconstruct_series_plain on one core) for reference."""
     G, J, K, U, _ = CONFIGS[cfg]
     from oracle import ref
     import paper_1701_08361_b200 as pb
     plan = pb.raw_plan(G, J)
     plan.newton_steps, plan.cg_iter_budget = 7, 50
-    nproc = os.cpu_count() or 1
-    A = max(1, min(4, nproc, J))  # the reference's WorkerGroup cap (decomp.hpp:21)
-    # the reference pipeline's pre + rec stages on raw acquisitions: grid_adjoint per
-    # frame, PSFs from a PsfCache (built once per angle set, outside the timed region),
-    # prep_series normalisation of frame 0, reconstruct_frame chained
-    raw, angles = synth_raw(G, J, K, U, n_unique=min(U, args.steps + args.warmup))
-    P = [ref.build_psf(plan, angles[t], 2 * plan.N) for t in range(len(angles))]
-    z0 = ref.grid_adjoint(plan, raw[0], angles[0])
-    scale = np.float32(100.0 / math.sqrt(float(np.sum(np.abs(z0.astype(np.complex128)) ** 2))))
-    est = ref.initial_estimate(plan)
-    budget_s = float(os.environ.get("RTN_REF_BUDGET_S", "150"))
-    times = []
-    t_all = time.time()
-    total = args.warmup + args.steps
-    for n in range(total):
-        t0 = time.perf_counter()
-        u = n % len(raw)
-        z = (ref.grid_adjoint(plan, raw[u], angles[u]) * scale).astype(np.complex64)
-        _, est, _, _ = ref.reconstruct_frame(plan, z, P[u], est, est, A=A)
-        dt = time.perf_counter() - t0
-        if n >= args.warmup:
-            times.append(dt)
-        if time.time() - t_all > budget_s and len(times) >= 1:
-            break
-    fps = len(times) / sum(times)
-    sample = (f"{len(times)} chained {cfg.upper()} frames from raw radial samples (grid_adjoint + "
-              f"reconstruct_frame: 7 Newton steps, 50 CR iterations each; PSFs cached) after "
-              f"{min(args.warmup, total)} warm-up; reference reconstruct_frame, A={A} WorkerGroup lanes; "
+    host = host_info()
+    nproc = host["nproc"]
+    sched = (U, (U + 1) // 2)
+    A = max(1, min(4, nproc, J))
+    cands = [(T, A) for T in range(1, 5) if T * A <= nproc] or [(1, 1)]
+    pre = sched[0] + 1  # the strict prefix (frames 1..l wait for n-1) plus frame 0
+    F = pre + sum(2 * T for T, _ in cands) + 1 + args.warmup + args.steps
+    z, P, idx = reference_inputs(cfg, plan, F)
+    D = plan.D
+    ests = np.zeros((F, D), np.complex64)
+    # the strict prefix once (its frames run one after another whatever T is)
+    _, _, _, e = ref.time_series(plan, z[:pre], P, idx[:pre], 1, A, sched)
+    ests[:pre] = e
+    first = pre
+    key = (0, plan.N, 2, J)  # single_slice, N, frames bucket, J (autotune.hpp:13-31)
+    db, sweep = [], {}
+    for T, A_ in cands:
+        cnt = 2 * T
+        w, lat, cg, e = ref.time_series(plan, z[:first + cnt], P, idx[:first + cnt], T, A_, sched, first=first,
+                                        ests=ests[:first + cnt])
+        ests[:first + cnt] = e
+        first += cnt
+        ms = 1000.0 * w / cnt
+        db.append(key + (T, A_, ms))
+        sweep[f"T{T}xA{A_}"] = round(1000.0 / ms, 4)
+    T_best, A_best = ref.select_config(key, db)  # exact-key argmin (autotune.cpp:15-38)
+    # single core, one frame (reconstruct_series_plain with A = 1)
+    w1, _, _, e = ref.time_series(plan, z[:first + 1], P, idx[:first + 1], 1, 1, sched, first=first,
+                                  ests=ests[:first + 1])
+    ests[:first + 1] = e
+    first += 1
+    single = 1.0 / w1
+    # timed: warm-up, then args.steps frames with the selected configuration
+    if args.warmup:
+        _, _, _, e = ref.time_series(plan, z[:first + args.warmup], P, idx[:first + args.warmup], T_best, A_best,
+                                     sched, first=first, ests=ests[:first + args.warmup])
+        ests[:first + args.warmup] = e
+        first += args.warmup
+    w, lat, cg, _ = ref.time_series(plan, z[:first + args.steps], P, idx[:first + args.steps], T_best, A_best,
+                                    sched, first=first, ests=ests[:first + args.steps])
+    assert int(cg.sum()) == 50 * args.steps
+    fps = args.steps / w
+    sample = (f"{args.steps} chained {cfg.upper()} frames (7 Newton steps, 50 CR iterations each) through the "
+              f"reference's scheduled series driver (reconstruct_series loop, for_turns({U})) with T={T_best} "
+              f"threads x A={A_best} WorkerGroup lanes, after {args.warmup} warm-up frames; (T, A) = "
+              f"select_config over the sweep {sweep} (frames/s; candidates: the A={A} row of legal_configs({nproc}) with T<=4, 2T frames "
+              f"each); single core (T=1, A=1): {single:.3f} frames/s; gridding and PSFs outside the timed region; "
               f"FFTW replaced by the oracle shim FFT (oracle/shim, pocketfft-class speed)")
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
-        "steps": len(times), "warmup": args.warmup, "ms_per_step": 1000.0 / fps, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * w / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c64/f64", "data": "synthetic",
         "config": {"workload": cfg, "description": CONFIGS[cfg][4], "G": G, "J": J, "newton_steps": 7,
-                   "cg_iter_budget": 50},
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": A, "kind": "reference", "sample": sample},
+                   "cg_iter_budget": 50, "frames_in_flight": T_best, "channel_group": A_best,
+                   "temporal_schedule": {"l": sched[0], "o": sched[1]}},
+        "p50_latency_ms": 1000.0 * float(np.median(lat)),
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": T_best * A_best, "kind": "reference",
+                         "sample": sample, "host": host, "sweep_frames_per_s": sweep,
+                         "single_core_frames_per_s": single, "selected": {"T": T_best, "A": A_best}},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -355,10 +412,10 @@ def cpu_baseline(cfg, z, P, plan):
     t0 = time.perf_counter()
     ref.reconstruct_frame(plan, z, P, est, est, A=A)
     dt = time.perf_counter() - t0
-    return {"value": 1.0 / dt, "unit": "frames/s", "cores": A, "kind": "reference",
+    return {"value": 1.0 / dt, "unit": "frames/s", "cores": A, "kind": "reference", "host": host_info(),
             "sample": f"1 {cfg.upper()} frame (7 Newton steps, 50 CR iterations) through the reference "
                       f"reconstruct_frame with A={A} WorkerGroup lanes, {dt:.1f} s; FFTW replaced by the "
-                      f"oracle shim FFT"}
+                      f"oracle shim FFT; the scheduled (T, A) figure is the --impl reference arm's"}
 
 
 def check_timed_frames(pb, series, plan, frames, P, U, audit, first, n_check):
@@ -477,6 +534,9 @@ def main():
     ap.add_argument("--T", default="auto",
                     help="frames in flight (temporal decomposition): 1 = plain chain, N, or auto = autotuner")
     ap.add_argument("--A", default="1", help="channel-group width per frame worker (with --T N)")
+    ap.add_argument("--sched", default=None,
+                    help="temporal schedule 'l,o' (decomp.hpp:70-76); default for_turns(U) = (U, ceil(U/2)); "
+                         "C4's relaxed t-k schedule with 8 frames in flight: --config c4 --T 8 --sched 5,8")
     ap.add_argument("--tune-db", default=os.path.join(ROOT, "profiles", "tune_db.tsv"),
                     help="autotuner store (autotune.hpp TuneDb format)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -513,6 +573,9 @@ def main():
     series.set_psf_index([n % U for n in range(F)])
     series.normalize()
     sched = pb.TemporalSchedule.for_turns(U)
+    if args.sched:
+        l_, o_ = (int(v) for v in args.sched.split(","))
+        sched = pb.TemporalSchedule(l_, o_)
 
     def opts_for(T, A=1):
         return pb.SeriesOptions(T=T, A=A, plain=(T == 1), sched=sched)

@@ -415,3 +415,25 @@ def learn_step(key, db, total=8):
     out = np.zeros(2, np.int32)
     _chk(lib().ref_learn_step(_ip(k), _ip(rows), _dp(ms), len(db), total, _ip(out)))
     return int(out[0]), int(out[1])
+
+
+def time_series(plan, z, P, psf_idx, T, A, sched, first=0, ests=None):
+    """the reference's scheduled series driver on pre-gridded, normalised frames (bench
+    reference arm). Frames [0, first) are taken as complete with estimates ests[:first]
+    (a continuing series); frames [first, F) run with T threads x A lanes. Returns wall
+    seconds, per-frame latency seconds, CR iterations and the (updated) estimates."""
+    z = _c64(z)
+    P = _c64(P)
+    if P.ndim == 2:
+        P = P[None]
+    F = z.shape[0]
+    D = plan.G * plan.G + plan.J * plan.Gc * plan.Gc
+    ests = np.zeros((F, D), np.complex64) if ests is None else np.ascontiguousarray(ests, np.complex64)
+    idx = np.ascontiguousarray(np.asarray(psf_idx, np.int32))
+    wall = ctypes.c_double(0)
+    lat = np.zeros(F, np.float64)
+    cg = np.zeros(F, np.int32)
+    _chk(lib().ref_time_series(ctypes.byref(plan_c(plan)), _fp(z), _fp(P), P.shape[0], _ip(idx), F, int(first),
+                               int(T), int(A), int(sched[0]), int(sched[1]), _fp(ests), ctypes.byref(wall), _dp(lat),
+                               _ip(cg)))
+    return wall.value, lat[first:], cg[first:], ests

@@ -18,6 +18,8 @@
 // Status codes follow the CLI mapping (rtnlinv_main.cpp:381-391): 0 ok, 2 UsageError,
 // 3 DataError, 4 SolverError / DecompFault, 5 other.
 #include <array>
+#include <chrono>
+#include <mutex>
 #include <complex>
 #include <cstdint>
 #include <cstring>
@@ -691,6 +693,91 @@ int ref_learn_step(const int* key, const int* rows, const double* ms, int n, int
                    load_records(rows, ms, n), total);
     out_ta[0] = sel.first;
     out_ta[1] = sel.second;
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// Timing leg of bench.py's reference arm (BASELINE.md "CPU-baseline plan"): the
+// reference's scheduled series driver (reconstruct_series, nlinv.cpp:446-526: T threads
+// taking frames round-robin, h_choose / CompletionLedger, A WorkerGroup lanes per
+// thread) on frames that were gridded and normalised beforehand, so PSF construction
+// and gridding stay outside the timed region as the plan prescribes. The per-thread
+// loop below is the reference's own thread_main with prep_series factored out; it calls
+// only the reference's public API (reconstruct_frame, h_choose, CompletionLedger,
+// WorkerGroup). z: F*J*G*G (normalised), P: U*G*G, psf_idx: F. Outputs: wall seconds of
+// the whole run, per-frame wall latency (start -> finish) and per-frame CR iterations.
+// Frames [0, first) count as already reconstructed (a continuing series: their
+// estimates come from ests_io, F*D complex64); frames [first, F) are timed and their
+// estimates written back to ests_io.
+int ref_time_series(const ref_plan_t* p, const float* z, const float* P, int U, const int* psf_idx, int F,
+                    int first, int T, int A, int sched_l, int sched_o, float* ests_io, double* out_wall,
+                    double* out_latency, int* out_cg) {
+  return guarded([&] {
+    const ReconPlan plan = to_plan(p);
+    if (T < 1 || A < 1 || F < 1 || first < 0 || first >= F) throw UsageError("ref_time_series: bad T, A or range");
+    const CImage winv = make_weights_inv(plan.Gc, plan.G);
+    std::vector<PsfKernel> psfs;
+    for (int u = 0; u < U; ++u) psfs.push_back(load_psf(P + 2 * static_cast<size_t>(plan.G) * plan.G * u, plan.G));
+    const size_t zsz = 2 * static_cast<size_t>(plan.J) * plan.G * plan.G;
+    std::vector<GriddedData> frames;
+    for (int n = 0; n < F; ++n) frames.push_back(n >= first ? load_z(z + zsz * n, plan) : GriddedData{});
+    const TemporalSchedule sched{sched_l, sched_o};
+    const int M = plan.newton_steps;
+    const int TT = std::min(T, F - first);
+    const size_t D = static_cast<size_t>(plan.G) * plan.G + static_cast<size_t>(plan.J) * plan.Gc * plan.Gc;
+    std::vector<Estimate> ests(static_cast<size_t>(F));
+    CompletionLedger ledger(F);
+    for (int n = 0; n < first; ++n) {
+      ests[static_cast<size_t>(n)] = load_est(ests_io + 2 * D * n, plan);
+      ledger.mark_complete(n);
+    }
+    const Estimate unity = initial_estimate(plan);
+    std::mutex err_mu;
+    std::exception_ptr first_err;
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto thread_main = [&](int t) {
+      try {
+        std::unique_ptr<WorkerGroup> wg;
+        if (A > 1) wg = std::make_unique<WorkerGroup>(A);
+        for (int n = first + t; n < F; n += TT) {
+          if (ledger.poisoned()) return;
+          const auto ts = std::chrono::steady_clock::now();
+          const bool chained = n > 0;
+          if (chained && n <= sched.l) ledger.wait_complete(n - 1);
+          const int init_src = chained ? h_choose(n, 0, M, sched, ledger) : -1;
+          const Estimate init = init_src >= 0 ? ests[static_cast<size_t>(init_src)] : unity;
+          const RegProvider reg = [&](int m) -> const Estimate& {
+            if (!chained) return unity;
+            return ests[static_cast<size_t>(h_choose(n, m, M, sched, ledger))];
+          };
+          FrameResult fr = reconstruct_frame(frames[static_cast<size_t>(n)], psfs[static_cast<size_t>(psf_idx[n])],
+                                             plan, winv, init, reg, wg.get(),
+                                             [&](int m) { ledger.mark_step(n, m); });
+          ests[static_cast<size_t>(n)] = std::move(fr.est);
+          if (out_cg) out_cg[n] = fr.cg_iters;
+          if (out_latency) {
+            out_latency[n] = std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count();
+          }
+          ledger.mark_complete(n);
+        }
+      } catch (...) {
+        {
+          std::lock_guard<std::mutex> lock(err_mu);
+          if (!first_err) first_err = std::current_exception();
+        }
+        ledger.poison();
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < TT; ++t) pool.emplace_back(thread_main, t);
+    thread_main(0);
+    for (std::thread& th : pool) th.join();
+    if (first_err) std::rethrow_exception(first_err);
+    *out_wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int n = first; n < F; ++n) store_est(ests[static_cast<size_t>(n)], ests_io + 2 * D * n);
   });
 }
 
