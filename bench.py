@@ -341,7 +341,7 @@ def reference_arm(args, cfg):
     plan.newton_steps, plan.cg_iter_budget = 7, 50
     host = host_info()
     nproc = host["nproc"]
-    sched = (U, (U + 1) // 2)
+    sched = tuple(int(v) for v in args.sched.split(",")) if args.sched else (U, (U + 1) // 2)
     A = max(1, min(4, nproc, J))
     cands = [(T, A) for T in range(1, 5) if T * A <= nproc] or [(1, 1)]
     pre = sched[0] + 1  # the strict prefix (frames 1..l wait for n-1) plus frame 0
