@@ -51,6 +51,9 @@ typedef struct rtn_ctx rtn_ctx;
 
 int rtn_abi_version(void);
 const char* rtn_last_error(void);
+/* the exception type behind the calling thread's last failure: 2 UsageError, 3 DataError,
+ * 4 SolverError, 6 DecompFault (both reported as status 4), 5 runtime (types.hpp:12-25) */
+int rtn_last_error_kind(void);
 /* 1 if the fused line-FFT kernels cover grid side G (rtnlinv::make_plan sizes) */
 int rtn_grid_supported(int G);
 int rtn_device_count(void);
@@ -144,6 +147,12 @@ int rtn_post_median3(const float* mags, int frames, long long npix, float* out);
 uint64_t rtn_psf_angle_key(const double* angles, int K, int S, int G);
 
 /* --- nlinv.hpp:61-98 ----------------------------------------------------------- */
+/* the `winv` argument of the W^-1 functions (nlinv.hpp:41-116): Gc*Gc real weights (the
+ * context starts with make_weights_inv(Gc, G)); single-device and in-process group contexts */
+int rtn_set_weights(rtn_ctx* ctx, const float* winv);
+/* a StepCache given by its parts (nlinv.hpp:53-60): masked rho (G*G) and decoded coils
+ * (J*G*G), as make_step_cache returns them; apply_normal / cg_solve then linearise there */
+int rtn_set_step_cache(rtn_ctx* ctx, const float* rho, const float* coils);
 /* make_step_cache: linearise at estimate x; optional outputs masked rho (G*G), coils (J*G*G) */
 int rtn_make_step_cache(rtn_ctx* ctx, const float* x, float* rho_out, float* coils_out);
 /* apply_normal at the cached linearisation point */

@@ -65,6 +65,22 @@ def build(force=False, verbose=False, out=None):
     return OUT
 
 
+def build_compat(force=False):
+    """The C++ drop-in (compat/rtnlinv_compat.cpp) and the reference's own test programs
+    linked against it. Needs the reference headers (/root/reference, this container) and
+    the in-place oracle objects; the GPU box uses the prebuilt compat/_build files."""
+    ref = os.environ.get("RTN_REFERENCE", "/root/reference/proj")
+    if not os.path.isdir(ref):
+        return None
+    cmd = ["make", "-C", os.path.join(HERE, "compat"), "-j8", f"REF={ref}"]
+    if force:
+        cmd.insert(1, "-B")
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("compat build failed:\n" + out.stdout[-4000:] + out.stderr[-4000:])
+    return os.path.join(HERE, "compat", "_build")
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(OUT)

@@ -28,6 +28,7 @@ struct rtn_ctx {
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_kind = 0;
 
 template <typename F>
 int guarded(F&& f) {
@@ -36,12 +37,15 @@ int guarded(F&& f) {
     return 0;
   } catch (const rtnb::Error& e) {
     g_err = e.what();
+    g_kind = e.decomp ? 6 : e.code;
     return e.code;
   } catch (const std::bad_alloc&) {
     g_err = "out of memory";
+    g_kind = 5;
     return 5;
   } catch (const std::exception& e) {
     g_err = e.what();
+    g_kind = 5;
     return 5;
   }
 }
@@ -99,6 +103,7 @@ extern "C" {
 
 int rtn_abi_version(void) { return 1; }
 const char* rtn_last_error(void) { return g_err.c_str(); }
+int rtn_last_error_kind(void) { return g_kind; }
 int rtn_grid_supported(int G) { return rtnb::grid_supported(G) ? 1 : 0; }
 
 int rtn_device_count(void) {
@@ -425,6 +430,24 @@ int rtn_apply_W_invH(rtn_ctx* ctx, const float* u, float* out) {
 }
 int rtn_toeplitz_apply(rtn_ctx* ctx, float* x) {
   return guarded([&] { eng(ctx).toeplitz_apply(x); });
+}
+int rtn_set_weights(rtn_ctx* ctx, const float* winv) {
+  return guarded([&] {
+    if (!winv) rtnb::fail(2, "set_weights: null weights");
+    if (ctx && ctx->grp) {
+      ctx->grp->set_weights(winv);
+    } else if (ctx && ctx->pg) {
+      rtnb::fail(2, "set_weights: not available on a process-group member");
+    } else {
+      eng(ctx).set_weights(winv);
+    }
+  });
+}
+int rtn_set_step_cache(rtn_ctx* ctx, const float* rho, const float* coils) {
+  return guarded([&] {
+    if (!rho || !coils) rtnb::fail(2, "set_step_cache: null rho or coils");
+    eng(ctx).set_step_cache(rho, coils);
+  });
 }
 int rtn_make_step_cache(rtn_ctx* ctx, const float* x, float* rho_out, float* coils_out) {
   return guarded([&] {

@@ -22,6 +22,7 @@ namespace rtnb {
 // ------------------------------------------------------------------------------
 
 void fail(int code, const std::string& msg) { throw Error(code, msg); }
+void fail_decomp(const std::string& msg) { throw Error(4, msg, true); }
 
 void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(5, std::string(what) + ": " + cudaGetErrorString(e));
@@ -420,7 +421,7 @@ void Engine::read_state() {
 
 void Engine::raise_status(const char* where) {
   if (st_host_->status == ST_SOLVER) fail(4, std::string(where) + ": iteration diverged or produced non-finite values");
-  if (st_host_->status == ST_DEADLINE) fail(4, std::string(where) + ": a group member missed the barrier deadline");
+  if (st_host_->status == ST_DEADLINE) fail_decomp(std::string(where) + ": a group member missed the barrier deadline");
   if (st_host_->status != ST_OK) fail(st_host_->status, std::string(where) + ": device error");
 }
 
@@ -436,6 +437,20 @@ void Engine::set_data(const float* z) {
 }
 void Engine::set_psf_device(const float2* P) {
   check_cuda(cudaMemcpyAsync(P_, P, sizeof(float2) * plan_.G * plan_.G, cudaMemcpyDeviceToDevice, s_), "psf copy");
+}
+void Engine::set_weights(const float* w) {
+  std::memcpy(winv_host_.data(), w, sizeof(float) * winv_host_.size());
+  check_cuda(cudaMemcpyAsync(winv_, winv_host_.data(), sizeof(float) * winv_host_.size(), cudaMemcpyHostToDevice, s_),
+             "weights upload");
+  sync();
+}
+void Engine::set_step_cache(const float* rho, const float* coils) {
+  const size_t G2 = static_cast<size_t>(plan_.G) * plan_.G;
+  check_cuda(cudaMemcpyAsync(rhom_, rho, sizeof(float2) * G2, cudaMemcpyHostToDevice, s_), "rho upload");
+  check_cuda(cudaMemcpyAsync(coils_, coils, sizeof(float2) * G2 * plan_.J, cudaMemcpyHostToDevice, s_),
+             "coils upload");
+  sync();
+  have_cache_ = true;
 }
 void Engine::set_data_device(const float2* z) {
   check_cuda(cudaMemcpyAsync(z_, z, sizeof(float2) * plan_.J * plan_.G * plan_.G, cudaMemcpyDeviceToDevice, s_),

@@ -37,9 +37,12 @@ struct Plan {
 // rtnlinv_main.cpp:381-391): 2 usage, 3 data, 4 solver / decomposition fault.
 struct Error : std::runtime_error {
   int code;
-  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+  bool decomp;  // a decomposition fault (DecompFault, decomp.hpp:25-66), reported with code 4
+  Error(int c, const std::string& m, bool d = false) : std::runtime_error(m), code(c), decomp(d) {}
 };
 [[noreturn]] void fail(int code, const std::string& msg);
+// DecompFault: a worker missed its deadline or the series ledger was poisoned (status 4)
+[[noreturn]] void fail_decomp(const std::string& msg);
 void check_cuda(cudaError_t e, const char* what);
 
 bool grid_supported(int G);
@@ -116,6 +119,12 @@ class Engine : public FrameWorker {
   void set_psf_device(const float2* P);
   void set_data_device(const float2* z);
   const float* winv_host() const { return winv_host_.data(); }
+  // caller-supplied W^-1 weights (Gc*Gc real; the `winv` argument of apply_W_inv /
+  // make_step_cache / newton_step / reconstruct_frame, nlinv.hpp:41-116)
+  void set_weights(const float* w);
+  // a linearisation point given as its decoded parts (StepCache::rho masked, G*G, and
+  // StepCache::coils, J*G*G; nlinv.hpp:53-60) instead of an estimate to decode
+  void set_step_cache(const float* rho, const float* coils);
 
   // ---- op-level, synchronous, host in / host out (nlinv.hpp:41-98) ----
   void apply_W_inv(const float* chat, float* out);

@@ -432,6 +432,14 @@ void Group::set_data(const float* z) {
   }
 }
 
+void Group::set_weights(const float* w) {
+  DeviceRestore restore;
+  for (auto& m : mem_) {
+    check_cuda(cudaSetDevice(m->dev_), "set device");
+    m->set_weights(w);
+  }
+}
+
 void Group::make_step_cache(const float* x) {
   DeviceRestore restore;
   Engine& e0 = *mem_[0];

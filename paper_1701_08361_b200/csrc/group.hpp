@@ -60,6 +60,7 @@ class Group : public FrameWorker {
 
   // host in / host out (parity boundary)
   void set_psf(const float* P);
+  void set_weights(const float* w);  // every member (nlinv.hpp `winv`)
   void set_data(const float* z);
   void make_step_cache(const float* x);
   void apply_normal(const float* dx, float* out);

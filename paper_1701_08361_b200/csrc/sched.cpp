@@ -65,8 +65,8 @@ void CompletionLedger::wait_complete(int n, std::chrono::milliseconds deadline) 
   const size_t idx = static_cast<size_t>(n);
   if (idx >= complete_.size()) fail(2, "CompletionLedger: frame index out of range");
   const bool ready = cv_.wait_for(g, deadline, [&] { return poisoned_ || complete_[idx] != 0; });
-  if (poisoned_) fail(4, "series aborted by an earlier fault");
-  if (!ready) fail(4, "timed out waiting for a predecessor frame");
+  if (poisoned_) fail_decomp("series aborted by an earlier fault");
+  if (!ready) fail_decomp("timed out waiting for a predecessor frame");
 }
 
 void CompletionLedger::poison() {

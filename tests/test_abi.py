@@ -54,3 +54,20 @@ def test_size_coverage_table():
         assert lib.rtn_grid_supported(G) == 1, G
     for G in (34, 130, 1000):
         assert lib.rtn_grid_supported(G) == 0, G
+
+
+def test_cpp_drop_in_links_against_the_c_abi():
+    """the C++ drop-in (the reference's nlinv.hpp / fft.hpp API over include/rtnlinv_b200.h)
+    is built and defines the reference's hot-path symbols; no device call is made"""
+    import subprocess
+    so = os.path.join(ROOT, "paper_1701_08361_b200", "compat", "_build", "librtnlinv_compat.so")
+    if not os.path.exists(so):
+        import pytest
+        pytest.skip("compat library not built (needs the reference headers)")
+    syms = subprocess.run(["nm", "-DC", "--defined-only", so], capture_output=True, text=True).stdout
+    for name in ("rtnlinv::apply_normal(", "rtnlinv::cg_solve(", "rtnlinv::newton_step(",
+                 "rtnlinv::reconstruct_frame(", "rtnlinv::reconstruct_series(", "rtnlinv::make_step_cache(",
+                 "rtnlinv::fft::forward(", "rtnlinv::fft::count("):
+        assert name in syms, name
+    deps = subprocess.run(["ldd", so], capture_output=True, text=True).stdout
+    assert "librtnlinv_b200.so" in deps
