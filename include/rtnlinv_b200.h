@@ -234,6 +234,21 @@ int rtn_series_psf_cache_load(rtn_series* s, const char* path);
  * 2 phase difference of frame pairs (count/2 * N*N) */
 int rtn_series_post(rtn_series* s, int first, int count, int mode, float* out);
 int rtn_series_images(rtn_series* s, int first, int count, float* images);
+
+/* --- ingest.hpp:105-126: the .rti image sink (RtiWriter format) ---------------------
+ * header9 = DatasetHeader {version, N, J_physical, K, U, frames, slices, mode, samples},
+ * mode 0 single_slice, 1 multi_slice, 2 flow. Images are N*N float32, kind 0 magnitude,
+ * 1 phase_difference; with strict_order frame indices must increase per slice. The
+ * files (and the "<path>.idx" sidecar) are interchangeable with the reference's. */
+typedef struct rtn_rti rtn_rti;
+int rtn_rti_open(const char* path, const int* header9, int strict_order, rtn_rti** out);
+int rtn_rti_write(rtn_rti* w, int frame, int slice, int kind, const float* pixels);
+int rtn_rti_count(rtn_rti* w);
+int rtn_rti_close(rtn_rti* w); /* flushes and frees */
+/* the device postprocessing of series images [first, first+count) (mode as
+ * rtn_series_post) written to the sink as slice `slice`: frame indices first.., or the
+ * pair index first/2.. for phase differences (pipeline.cpp:60-137 + the snk stage) */
+int rtn_series_write_rti(rtn_series* s, rtn_rti* w, int first, int count, int mode, int slice);
 /* device time (ms) of the last rtn_series_run: CUDA events spanning all worker streams */
 float rtn_series_last_span_ms(rtn_series* s);
 int rtn_series_estimate(rtn_series* s, int n, float* est /* D */);

@@ -437,3 +437,29 @@ def time_series(plan, z, P, psf_idx, T, A, sched, first=0, ests=None):
                                int(T), int(A), int(sched[0]), int(sched[1]), _fp(ests), ctypes.byref(wall), _dp(lat),
                                _ip(cg)))
     return wall.value, lat[first:], cg[first:], ests
+
+
+def rti_write(path, header, records, pixels):
+    """the reference's RtiWriter: header = 9 ints (DatasetHeader), records [(frame, slice,
+    kind)], pixels (n, N, N) float32"""
+    h = np.ascontiguousarray(header, np.int32)
+    rec = np.asarray(records, np.int32).reshape(-1, 3)
+    px = np.ascontiguousarray(pixels, np.float32)
+    fr, sl, kd = (np.ascontiguousarray(rec[:, k]) for k in range(3))
+    _chk(lib().ref_rti_write(str(path).encode(), _ip(h), len(rec), _ip(fr), _ip(sl), _ip(kd),
+                             px.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+
+
+def rti_read(path, max_records=4096):
+    """the reference's RtiReader: (header 9 ints, records [(frame, slice, kind)], pixels)"""
+    h = np.zeros(9, np.int32)
+    n = ctypes.c_int(0)
+    probe = np.zeros(3, np.int32)
+    _chk(lib().ref_rti_read(str(path).encode(), _ip(h), 0, ctypes.byref(n), _ip(probe), None))
+    N = int(h[1])
+    cnt = min(n.value, max_records)
+    rec = np.zeros((max(cnt, 1), 3), np.int32)
+    px = np.zeros((max(cnt, 1), N, N), np.float32)
+    _chk(lib().ref_rti_read(str(path).encode(), _ip(h), cnt, ctypes.byref(n), _ip(rec),
+                            px.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+    return h.tolist(), [tuple(int(v) for v in r) for r in rec[:cnt]], px[:cnt]

@@ -32,6 +32,7 @@
 #include "rtnlinv/autotune.hpp"
 #include "rtnlinv/decomp.hpp"
 #include "rtnlinv/fft.hpp"
+#include "rtnlinv/ingest.hpp"
 #include "rtnlinv/nlinv.hpp"
 #include "rtnlinv/pipeline.hpp"
 #include "rtnlinv/planner.hpp"
@@ -778,6 +779,68 @@ int ref_time_series(const ref_plan_t* p, const float* z, const float* P, int U, 
     if (first_err) std::rethrow_exception(first_err);
     *out_wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     for (int n = first; n < F; ++n) store_est(ests[static_cast<size_t>(n)], ests_io + 2 * D * n);
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// .rti sink (ingest.cpp:240-320): the reference's RtiWriter / RtiReader on flat
+// buffers. header9 = {version, N, J_physical, K, U, frames, slices, mode, samples}.
+static DatasetHeader rti_header(const int* h) {
+  DatasetHeader d;
+  d.version = h[0];
+  d.N = h[1];
+  d.J_physical = h[2];
+  d.K = h[3];
+  d.U = h[4];
+  d.frames = h[5];
+  d.slices = h[6];
+  d.mode = h[7] == 1 ? ImagingMode::multi_slice : (h[7] == 2 ? ImagingMode::flow : ImagingMode::single_slice);
+  d.samples_per_spoke = h[8];
+  return d;
+}
+
+int ref_rti_write(const char* path, const int* header9, int n, const int* frames, const int* slices,
+                  const int* kinds, const float* pixels) {
+  return guarded([&] {
+    const DatasetHeader h = rti_header(header9);
+    RtiWriter w(path, h);
+    const size_t npix = static_cast<size_t>(h.N) * h.N;
+    for (int i = 0; i < n; ++i) {
+      ImageOut img;
+      img.frame_index = frames[i];
+      img.slice_id = slices[i];
+      img.n = h.N;
+      img.kind = kinds[i] == 1 ? ImageKind::phase_difference : ImageKind::magnitude;
+      img.pixels.assign(pixels + npix * i, pixels + npix * (i + 1));
+      w.write_image(img);
+    }
+    w.close();
+  });
+}
+
+// header9 out; records {frame, slice, kind} (3 ints each) and pixels (npix each), at
+// most max_records; *n_records = the file's record count
+int ref_rti_read(const char* path, int* header9, int max_records, int* n_records, int* records, float* pixels) {
+  return guarded([&] {
+    RtiReader r(path);
+    const DatasetHeader& h = r.header();
+    const int hv[9] = {h.version, h.N, h.J_physical, h.K, h.U, h.frames, h.slices,
+                       h.mode == ImagingMode::multi_slice ? 1 : (h.mode == ImagingMode::flow ? 2 : 0),
+                       h.samples_per_spoke};
+    std::memcpy(header9, hv, sizeof(hv));
+    *n_records = static_cast<int>(r.records().size());
+    const size_t npix = static_cast<size_t>(h.N) * h.N;
+    for (int i = 0; i < std::min(*n_records, max_records); ++i) {
+      const RtiRecord& rec = r.records()[static_cast<size_t>(i)];
+      records[3 * i] = rec.frame_index;
+      records[3 * i + 1] = rec.slice_id;
+      records[3 * i + 2] = rec.kind == ImageKind::phase_difference ? 1 : 0;
+      const ImageOut img = r.read_image(static_cast<size_t>(i));
+      std::memcpy(pixels + npix * i, img.pixels.data(), sizeof(float) * npix);
+    }
   });
 }
 

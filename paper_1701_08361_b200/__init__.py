@@ -216,6 +216,14 @@ def load_library(path: str = LIB_PATH):
                             ctypes.c_int),
         "rtn_time_kernel": ([vp, ctypes.c_char_p, ctypes.c_int, d, d], ctypes.c_int),
         "rtn_cluster_supported": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+        "rtn_last_error_kind": ([], ctypes.c_int),
+        "rtn_set_weights": ([vp, f], ctypes.c_int),
+        "rtn_set_step_cache": ([vp, f, f], ctypes.c_int),
+        "rtn_rti_open": ([ctypes.c_char_p, i, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
+        "rtn_rti_write": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, f], ctypes.c_int),
+        "rtn_rti_count": ([vp], ctypes.c_int),
+        "rtn_rti_close": ([vp], ctypes.c_int),
+        "rtn_series_write_rti": ([vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -233,6 +241,8 @@ def _check(status: int):
     if status == 0:
         return
     msg = _lib.rtn_last_error().decode(errors="replace")
+    if status == 4 and _lib.rtn_last_error_kind() == 6:
+        raise DecompFault(msg)
     raise _ERRORS.get(status, RuntimeError)(msg)
 
 
@@ -744,6 +754,14 @@ class Series:
         _check(self.lib.rtn_series_post(self._h, first, count, m, _fp(out)))
         return out
 
+    def write_rti(self, sink: "RtiSink", first: int = 0, count: Optional[int] = None, mode: str = "magnitude",
+                  slice_id: int = 0):
+        """device postprocessing of the stored images into an .rti sink (the pipeline's
+        pst + snk stages, pipeline.cpp:60-137)"""
+        count = self.F - first if count is None else count
+        m = {"magnitude": 0, "median3": 1, "phase_difference": 2}[mode]
+        _check(self.lib.rtn_series_write_rti(self._h, sink._h, first, count, m, slice_id))
+
     def save_psf_cache(self, path):
         _check(self.lib.rtn_series_psf_cache_save(self._h, str(path).encode()))
 
@@ -768,6 +786,51 @@ class Series:
         out = np.zeros(self.ctx.D, np.complex64)
         _check(self.lib.rtn_series_estimate(self._h, n, _fp(out)))
         return out
+
+
+class RtiSink:
+    """.rti image sink in the reference's RtiWriter format (ingest.hpp:105-126). header:
+    DatasetHeader fields {version, N, J_physical, K, U, frames, slices, mode, samples}
+    (mode 0 single_slice, 1 multi_slice, 2 flow)."""
+
+    KINDS = {"magnitude": 0, "phase_difference": 1}
+
+    def __init__(self, path, header, strict_order: bool = True):
+        self.lib = load_library()
+        self._h = ctypes.c_void_p()
+        h = np.ascontiguousarray(header, np.int32)
+        if h.size != 9:
+            raise UsageError("rti header needs 9 fields")
+        _check(self.lib.rtn_rti_open(str(path).encode(), h.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                     int(strict_order), ctypes.byref(self._h)))
+        self.N = int(h[1])
+
+    def write(self, frame: int, slice_id: int, kind: str, pixels):
+        px = np.ascontiguousarray(pixels, np.float32)
+        if px.size != self.N * self.N:
+            raise UsageError("rti image does not match the header's N")
+        _check(self.lib.rtn_rti_write(self._h, frame, slice_id, self.KINDS[kind], _fp(px)))
+
+    @property
+    def count(self) -> int:
+        return int(self.lib.rtn_rti_count(self._h))
+
+    def close(self):
+        if self._h:
+            h, self._h = self._h, ctypes.c_void_p()
+            _check(self.lib.rtn_rti_close(h))
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def reconstruct_series(ctx: Context, z, P, opts: SeriesOptions, psf_index=None):

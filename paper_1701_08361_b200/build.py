@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "librtnlinv_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["engine.cu", "inst0.cu", "inst1.cu", "inst2.cu", "inst3.cu", "group.cu", "procgroup.cu", "preproc.cu", "post.cu", "series.cu", "sched.cpp", "capi.cpp"]
+SOURCES = ["engine.cu", "inst0.cu", "inst1.cu", "inst2.cu", "inst3.cu", "group.cu", "procgroup.cu", "preproc.cu", "post.cu", "series.cu", "sched.cpp", "rti.cpp", "capi.cpp"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++20",

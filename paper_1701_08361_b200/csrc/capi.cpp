@@ -15,6 +15,7 @@
 #include "procgroup.hpp"
 #include "preproc.hpp"
 #include "post.hpp"
+#include "rti.hpp"
 #include "sched.hpp"
 #include "series.hpp"
 
@@ -659,6 +660,70 @@ int rtn_series_psf_cache_load(rtn_series* s, const char* path) {
 
 int rtn_series_post(rtn_series* s, int first, int count, int mode, float* out) {
   return guarded([&] { ser(s).post(first, count, mode, out); });
+}
+
+struct rtn_rti {
+  rtnb::RtiSink* w = nullptr;
+};
+
+int rtn_rti_open(const char* path, const int* header9, int strict_order, rtn_rti** out) {
+  return guarded([&] {
+    if (!path || !header9 || !out) rtnb::fail(2, "rti_open: null argument");
+    rtnb::RtiHeader h;
+    h.version = header9[0];
+    h.N = header9[1];
+    h.J_physical = header9[2];
+    h.K = header9[3];
+    h.U = header9[4];
+    h.frames = header9[5];
+    h.slices = header9[6];
+    h.mode = header9[7];
+    h.samples = header9[8];
+    auto* r = new rtn_rti;
+    try {
+      r->w = new rtnb::RtiSink(path, h, strict_order != 0);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    *out = r;
+  });
+}
+
+int rtn_rti_write(rtn_rti* w, int frame, int slice, int kind, const float* pixels) {
+  return guarded([&] {
+    if (!w || !w->w || !pixels) rtnb::fail(2, "rti_write: null argument");
+    w->w->write(frame, slice, kind, pixels);
+  });
+}
+
+int rtn_rti_count(rtn_rti* w) { return (w && w->w) ? w->w->count() : 0; }
+
+int rtn_rti_close(rtn_rti* w) {
+  if (!w) return 0;
+  const int st = guarded([&] {
+    if (w->w) w->w->close();
+  });
+  delete w->w;
+  delete w;
+  return st;
+}
+
+int rtn_series_write_rti(rtn_series* s, rtn_rti* w, int first, int count, int mode, int slice) {
+  return guarded([&] {
+    if (!w || !w->w) rtnb::fail(2, "series_write_rti: null sink");
+    const rtnb::Plan& p = s->ctx->eng->plan();
+    if (w->w->header().N != p.N) rtnb::fail(2, "series_write_rti: image side does not match the sink header");
+    const size_t npix = static_cast<size_t>(p.N) * p.N;
+    const int n_out = mode == 2 ? count / 2 : count;
+    std::vector<float> host(npix * static_cast<size_t>(std::max(n_out, 1)));
+    ser(s).post(first, count, mode, host.data());
+    for (int k = 0; k < n_out; ++k) {
+      // phase-difference images carry the pair index (pipeline.cpp:98-111)
+      const int frame = mode == 2 ? first / 2 + k : first + k;
+      w->w->write(frame, slice, mode == 2 ? 1 : 0, host.data() + npix * k);
+    }
+  });
 }
 
 int rtn_series_images(rtn_series* s, int first, int count, float* images) {

@@ -1,6 +1,6 @@
 // Host-side engine: one device context per (GPU, stream) that owns every device
 // buffer of a plan and enqueues the fused kernels of kernels_impl.cuh. The C-ABI
-// (capi.cpp) and the C++ drop-in API (api.cpp) are thin layers over this.
+// (capi.cpp) and the C++ drop-in over it (compat/rtnlinv_compat.cpp) are thin layers.
 #pragma once
 
 #include <cuda_runtime.h>

@@ -334,3 +334,35 @@ def test_zero_rhs_frames_recover_through_the_safe_mode_rerun(gpu, ref, T):
     assert np.array_equal(out["images"], want["images"])
     for n in range(1, F):
         assert out["audit"][n].reg_final_src == n - 1
+
+
+@pytest.mark.parametrize("mode", ["magnitude", "median3", "phase_difference"])
+def test_series_images_through_the_device_post_stage_into_an_rti_sink(gpu, ref, tmp_path, mode):
+    """device postprocessing of the series images straight into the
+    .rti sink; the reference's RtiReader reads the file and the pixels match the
+    reference's own postprocessing of the reference's images (pipeline.cpp:60-137)"""
+    plan = _small_plan(gpu, 24, 3, 3, 9)
+    F = 6
+    samples, angles = ref.phantom_series(3, F, 11, 5, plan.N, 1e-3, 19)
+    want = ref.reconstruct_series(plan, samples, angles, plain=True)
+    s = gpu.Series(gpu.Context(plan), F, 5)
+    s.run(gpu.SeriesOptions(plain=True), raw=dict(samples=samples, angles=angles))
+    header = [1, plan.N, 3, 11, 5, F, 2, 2 if mode == "phase_difference" else 1, 2 * plan.N]
+    path = tmp_path / "out.rti"
+    with gpu.RtiSink(path, header) as sink:
+        s.write_rti(sink, 0, F, mode=mode, slice_id=1)
+    h, recs, px = ref.rti_read(path)
+    assert h == header
+    if mode == "phase_difference":
+        assert recs == [(k, 1, 1) for k in range(F // 2)]
+        expect = np.stack([ref.phase_difference_image(want["images"][2 * k], want["images"][2 * k + 1])
+                           for k in range(F // 2)])
+        # phases: compare on the unit circle where the magnitude is meaningful
+        mag = np.abs(want["images"][0::2]) * np.abs(want["images"][1::2])
+        keep = mag > 1e-3 * mag.max()
+        assert np.max(np.abs(np.angle(np.exp(1j * (px - expect)))[keep])) < 1e-2
+    else:
+        assert recs == [(n, 1, 0) for n in range(F)]
+        mags = np.stack([ref.magnitude_image(want["images"][n]) for n in range(F)])
+        expect = ref.median_filter(mags) if mode == "median3" else mags
+        assert rel_err(px, expect) < FRAME_TOL
