@@ -205,7 +205,15 @@ void rtn_series_destroy(rtn_series* s);
 int rtn_series_upload_frames(rtn_series* s, int first, int count, const float* z);
 int rtn_series_upload_psf(rtn_series* s, int k, const float* P);
 int rtn_series_set_psf_index(rtn_series* s, const int* idx /* frames */);
-/* prep_series normalisation: frame 0 scaled to norm 100 (nlinv.cpp:390-400) */
+/* multi-slice acquisitions (pipeline.cpp:315-334, 429-434, 503): the store holds
+ * `slices` interleaved chains, store index g = frame * slices + slice (the pipeline's
+ * delivery order); each slice has its own ledger, estimates, temporal schedule and
+ * normalisation (its frame 0 scaled to norm 100). Frame workers take store indices
+ * round-robin across the slices. Default 1. */
+int rtn_series_set_slices(rtn_series* s, int slices);
+int rtn_series_slice_scale(rtn_series* s, int slice, double* scale);
+/* prep_series normalisation: frame 0 scaled to norm 100 (nlinv.cpp:390-400); per slice
+ * with rtn_series_set_slices; returns slice 0's scale */
 int rtn_series_normalize(rtn_series* s, double* data_scale);
 /* reconstruct frames [first, first+count). z_host != NULL streams those frames from
  * host memory inside the call (end-to-end path). Outputs (all nullable):

@@ -217,6 +217,8 @@ def load_library(path: str = LIB_PATH):
         "rtn_time_kernel": ([vp, ctypes.c_char_p, ctypes.c_int, d, d], ctypes.c_int),
         "rtn_cluster_supported": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
         "rtn_last_error_kind": ([], ctypes.c_int),
+        "rtn_series_set_slices": ([vp, ctypes.c_int], ctypes.c_int),
+        "rtn_series_slice_scale": ([vp, ctypes.c_int, d], ctypes.c_int),
         "rtn_set_weights": ([vp, f], ctypes.c_int),
         "rtn_set_step_cache": ([vp, f, f], ctypes.c_int),
         "rtn_rti_open": ([ctypes.c_char_p, i, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
@@ -686,6 +688,16 @@ class Series:
     def set_psf_index(self, idx):
         a = np.ascontiguousarray(np.asarray(idx, np.int32))
         _check(self.lib.rtn_series_set_psf_index(self._h, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int))))
+
+    def set_slices(self, slices: int):
+        """interleaved slice chains: store index g = frame * slices + slice (pipeline.cpp:315-334)"""
+        _check(self.lib.rtn_series_set_slices(self._h, slices))
+        self.slices = slices
+
+    def slice_scale(self, sl: int) -> float:
+        v = ctypes.c_double(0)
+        _check(self.lib.rtn_series_slice_scale(self._h, sl, ctypes.byref(v)))
+        return v.value
 
     def normalize(self) -> float:
         v = ctypes.c_double(0)

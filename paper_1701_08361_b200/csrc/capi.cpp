@@ -581,6 +581,15 @@ int rtn_series_upload_psf(rtn_series* s, int k, const float* P) {
 int rtn_series_set_psf_index(rtn_series* s, const int* idx) {
   return guarded([&] { ser(s).set_psf_index(idx); });
 }
+int rtn_series_set_slices(rtn_series* s, int slices) {
+  return guarded([&] { ser(s).set_slices(slices); });
+}
+int rtn_series_slice_scale(rtn_series* s, int slice, double* scale) {
+  return guarded([&] {
+    if (slice < 0 || slice >= ser(s).slices()) rtnb::fail(2, "series_slice_scale: slice out of range");
+    if (scale) *scale = ser(s).slice_scale(slice);
+  });
+}
 int rtn_series_normalize(rtn_series* s, double* scale) {
   return guarded([&] {
     const double v = ser(s).normalize();

@@ -146,18 +146,32 @@ void Series::set_psf_index(const int* idx) {
   }
 }
 
+void Series::set_slices(int Sl) {
+  if (Sl < 1 || Sl > F_) fail(2, "reconstruct_series: slice count out of range");
+  Sl_ = Sl;
+  slice_scale_.assign(static_cast<size_t>(Sl), 1.0);
+  normalized_ = false;
+}
+
 double Series::normalize() {
   if (normalized_) return scale_;
   check_cuda(cudaSetDevice(eng0_.device()), "set device");
-  k_nrm2_frame<<<1, 256>>>(z_, static_cast<long long>(zsz_), nsq_);
-  double nsq = 0;
-  check_cuda(cudaMemcpy(&nsq, nsq_, sizeof(double), cudaMemcpyDeviceToHost), "nsq read");
-  scale_ = 1.0;
-  if (nsq > 0) {
-    scale_ = 100.0 / std::sqrt(nsq);
-    k_scale_frames<<<148 * 8, 256>>>(z_, static_cast<long long>(zsz_) * F_, static_cast<float>(scale_));
-    check_cuda(cudaDeviceSynchronize(), "normalise");
+  for (int sl = 0; sl < Sl_; ++sl) {
+    // frame 0 of the slice sets its scale (pipeline.cpp:429-434; nlinv.cpp:390-400 for Sl = 1)
+    k_nrm2_frame<<<1, 256>>>(z_ + zsz_ * sl, static_cast<long long>(zsz_), nsq_);
+    double nsq = 0;
+    check_cuda(cudaMemcpy(&nsq, nsq_, sizeof(double), cudaMemcpyDeviceToHost), "nsq read");
+    double sc = 1.0;
+    if (nsq > 0) {
+      sc = 100.0 / std::sqrt(nsq);
+      for (int g = sl; g < F_; g += Sl_) {
+        k_scale_frames<<<148 * 2, 256>>>(z_ + zsz_ * g, static_cast<long long>(zsz_), static_cast<float>(sc));
+      }
+    }
+    slice_scale_[static_cast<size_t>(sl)] = sc;
   }
+  check_cuda(cudaDeviceSynchronize(), "normalise");
+  scale_ = slice_scale_[0];
   normalized_ = true;
   return scale_;
 }
@@ -170,9 +184,15 @@ struct NvtxRange {
 };
 }  // namespace
 
-void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& ledger, SeriesFrameOut& out,
-                       cudaEvent_t ready) {
-  const std::string label = "frame " + std::to_string(n) + " worker " + std::to_string(t);
+void Series::run_frame(int t, int g, const SeriesOptions& o, SeriesFrameOut& out, cudaEvent_t ready) {
+  // frame n of slice sl; its chain (ledger, estimates, schedule) is the slice's own
+  const int n = g / Sl_, sl = g % Sl_;
+  CompletionLedger& ledger = *ledgers_[static_cast<size_t>(sl)];
+  CompletionLedger& enq = *enqs_[static_cast<size_t>(sl)];
+  auto est_of = [&](int frame) { return estimate_dev(frame * Sl_ + sl); };
+  const double scale = slice_scale_[static_cast<size_t>(sl)];
+  const std::string label = "frame " + std::to_string(n) + " slice " + std::to_string(sl) + " worker " +
+                            std::to_string(t);
   NvtxRange range(label.c_str());
   FrameWorker& e = worker(t);
   const Plan& p = e.plan();
@@ -190,11 +210,11 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
     a.start_seq = ledger.next_seq();
   }
   if (chained) a.init_src = o.plain ? n - 1 : h_choose(n, 0, M, o.sched, ledger);
-  const float2* init = chained ? estimate_dev(a.init_src) : unity_;
+  const float2* init = chained ? est_of(a.init_src) : unity_;
 
   if (ready) check_cuda(cudaStreamWaitEvent(s, ready, 0), "wait frame upload");
   check_cuda(cudaSetDevice(e.device()), "set device");
-  e.load_frame(z_ + zsz_ * n, psf_ + psz_ * psf_idx_[static_cast<size_t>(n)]);
+  e.load_frame(z_ + zsz_ * g, psf_ + psz_ * psf_idx_[static_cast<size_t>(g)]);
   e.load_x(init);
   cudaEvent_t ev0, ev1;
   check_cuda(cudaEventCreate(&ev0), "event");
@@ -203,9 +223,9 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   // the image lands in the store directly on the store's device, via the worker's
   // own buffer (then one peer copy) elsewhere
   const bool local = e.device() == eng0_.device();
-  float2* img = local ? images_ + isz_ * n : e.image_dev();
-  const float iscale = static_cast<float>(1.0 / scale_);
-  const bool undo = o.normalize && scale_ != 1.0;
+  float2* img = local ? images_ + isz_ * g : e.image_dev();
+  const float iscale = static_cast<float>(1.0 / scale);
+  const bool undo = o.normalize && scale != 1.0;
   const bool fixed_reg = o.plain || !chained;  // every step regularises towards init
   const bool chain_events = !safe_mode_ && !o.plain && o.T > 1;
   if (fixed_reg) {
@@ -228,17 +248,18 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
         // n-1's final work is enqueued; the stream waits on n-1's completion event, so
         // the serial chain of closing steps runs device-side with no host round trip.
         src = n - 1;
-        if (n - 1 >= run_first_) enq_->wait_complete(n - 1);
+        const int gp = g - Sl_;  // store index of frame n-1 of this slice
+        if (gp >= run_first_) enq.wait_complete(n - 1);
         a.reg_final_seq = ledger.next_seq();
-        if (n - 1 >= run_first_) {
-          check_cuda(cudaStreamWaitEvent(s, done_[static_cast<size_t>(n - 1 - run_first_)], 0), "chain wait");
+        if (gp >= run_first_) {
+          check_cuda(cudaStreamWaitEvent(s, done_[static_cast<size_t>(gp - run_first_)], 0), "chain wait");
         }
       } else {
         src = h_choose(n, m, M, o.sched, ledger);
         if (m == M - 1) a.reg_final_seq = ledger.next_seq();
       }
       a.reg_src[static_cast<size_t>(m)] = src;
-      e.frame_step(m, estimate_dev(src));
+      e.frame_step(m, est_of(src));
       // Sources are chosen when a step is enqueued; h_choose blocks the host thread
       // only when Eq. 10 requires it (empty window, closing step), while this frame's
       // queued steps keep the device busy. step_sync_ re-creates the reference's
@@ -253,10 +274,10 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
   if (chain_events) {
     // publish the estimate and its completion event before this thread blocks, so the
     // next frame's closing step can be queued behind it on the device
-    e.store_x(estimate_dev(n));
-    check_cuda(cudaEventRecord(done_[static_cast<size_t>(n - run_first_)], s), "done event");
+    e.store_x(estimate_dev(g));
+    check_cuda(cudaEventRecord(done_[static_cast<size_t>(g - run_first_)], s), "done event");
     a.finish_seq = ledger.next_seq();
-    enq_->mark_complete(n);
+    enq.mark_complete(n);
     if (!e.frame_verify(&fs)) throw RedoSeries{};  // consumers may hold the speculative estimate
   } else if (!e.frame_verify(&fs)) {
     // a step met an exactly-zero right-hand side: redo with the true budget split,
@@ -264,16 +285,16 @@ void Series::run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& l
     e.load_x(init);
     const std::vector<int> srcs = a.reg_src;
     const float2* u = unity_;
-    RegFn rf = [this, srcs, u](int m) -> const float2* {
+    RegFn rf = [this, srcs, u, sl](int m) -> const float2* {
       const int sidx = srcs[static_cast<size_t>(m)];
-      return sidx >= 0 ? estimate_dev(sidx) : u;
+      return sidx >= 0 ? estimate_dev(sidx * Sl_ + sl) : u;
     };
     e.frame_run_sync(rf, img, iscale, undo, &fs);
     check_cuda(cudaEventRecord(ev1, s), "event");
   }
-  if (!chain_events) e.store_x(estimate_dev(n));
+  if (!chain_events) e.store_x(estimate_dev(g));
   if (!local) {
-    check_cuda(cudaMemcpyAsync(images_ + isz_ * n, img, sizeof(float2) * isz_, cudaMemcpyDefault, s), "image");
+    check_cuda(cudaMemcpyAsync(images_ + isz_ * g, img, sizeof(float2) * isz_, cudaMemcpyDefault, s), "image");
   }
   e.sync();
   float ms = 0;
@@ -434,25 +455,27 @@ void Series::produce_frames(const SeriesOptions& o, int first, int count, const 
   };
   ready.resize(static_cast<size_t>(count));
   check_cuda(cudaSetDevice(eng0_.device()), "set device");
-  if (first == 0) {
-    produce(0);
-    normalized_ = false;
-    if (o.normalize) {
-      k_nrm2_frame<<<1, 256, 0, copy_>>>(z_, static_cast<long long>(zsz_), nsq_);
-      double nsq = 0;
-      check_cuda(cudaMemcpyAsync(&nsq, nsq_, sizeof(double), cudaMemcpyDeviceToHost, copy_), "nsq");
-      check_cuda(cudaStreamSynchronize(copy_), "nsq");
-      scale_ = nsq > 0 ? 100.0 / std::sqrt(nsq) : 1.0;
-    } else {
-      scale_ = 1.0;
-    }
-  }
+  if (first == 0) normalized_ = false;
   for (int k = 0; k < count; ++k) {
-    const int n = first + k;
-    if (!(n == 0 && first == 0)) produce(k);
-    if (o.normalize && scale_ != 1.0) {
-      k_scale_frames<<<148 * 2, 256, 0, copy_>>>(z_ + zsz_ * n, static_cast<long long>(zsz_),
-                                                 static_cast<float>(scale_));
+    const int g = first + k, sl = g % Sl_;
+    produce(k);
+    if (g < Sl_) {
+      // frame 0 of slice sl arrived: it sets the slice's scale (pipeline.cpp:429-434)
+      double sc = 1.0;
+      if (o.normalize) {
+        k_nrm2_frame<<<1, 256, 0, copy_>>>(z_ + zsz_ * g, static_cast<long long>(zsz_), nsq_);
+        double nsq = 0;
+        check_cuda(cudaMemcpyAsync(&nsq, nsq_, sizeof(double), cudaMemcpyDeviceToHost, copy_), "nsq");
+        check_cuda(cudaStreamSynchronize(copy_), "nsq");
+        sc = nsq > 0 ? 100.0 / std::sqrt(nsq) : 1.0;
+      }
+      slice_scale_[static_cast<size_t>(sl)] = sc;
+      if (sl == 0) scale_ = sc;
+    }
+    const double sc = slice_scale_[static_cast<size_t>(sl)];
+    if (o.normalize && sc != 1.0) {
+      k_scale_frames<<<148 * 2, 256, 0, copy_>>>(z_ + zsz_ * g, static_cast<long long>(zsz_),
+                                                 static_cast<float>(sc));
     }
     check_cuda(cudaEventCreateWithFlags(&ready[static_cast<size_t>(k)], cudaEventDisableTiming), "event");
     check_cuda(cudaEventRecord(ready[static_cast<size_t>(k)], copy_), "event");
@@ -495,15 +518,25 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
     normalize();
   } else if (first == 0) {
     scale_ = 1.0;
+    slice_scale_.assign(static_cast<size_t>(Sl_), 1.0);
   }
 
-  CompletionLedger ledger(F_);
-  CompletionLedger enq(F_);
-  for (int n = 0; n < first; ++n) {
-    ledger.mark_complete(n);
-    enq.mark_complete(n);
+  // one chain per slice; store indices before `first` are complete
+  const int Fs = (F_ + Sl_ - 1) / Sl_;
+  ledgers_.clear();
+  enqs_.clear();
+  for (int sl = 0; sl < Sl_; ++sl) {
+    ledgers_.push_back(std::make_unique<CompletionLedger>(Fs));
+    enqs_.push_back(std::make_unique<CompletionLedger>(Fs));
   }
-  enq_ = &enq;
+  for (int g = 0; g < first; ++g) {
+    ledgers_[static_cast<size_t>(g % Sl_)]->mark_complete(g / Sl_);
+    enqs_[static_cast<size_t>(g % Sl_)]->mark_complete(g / Sl_);
+  }
+  auto poison_all = [&] {
+    for (auto& l : ledgers_) l->poison();
+    for (auto& l : enqs_) l->poison();
+  };
   run_first_ = first;
   done_.assign(static_cast<size_t>(count), nullptr);
   for (int k = 0; k < count; ++k) {
@@ -519,8 +552,8 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
     try {
       check_cuda(cudaSetDevice(worker(t).device()), "set device");
       for (int k = t; k < count; k += T) {
-        if (ledger.poisoned()) return;
-        run_frame(t, first + k, o, ledger, (*out)[static_cast<size_t>(k)],
+        if (ledgers_[static_cast<size_t>((first + k) % Sl_)]->poisoned()) return;
+        run_frame(t, first + k, o, (*out)[static_cast<size_t>(k)],
                   ready.empty() ? nullptr : ready[static_cast<size_t>(k)]);
         if (images_host) {
           FrameWorker& e = worker(t);
@@ -532,8 +565,7 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
       }
     } catch (const RedoSeries&) {
       redo = true;
-      ledger.poison();
-      enq.poison();
+      poison_all();
     } catch (...) {
       // once a worker asked for the safe-mode re-run, the other workers' failures are
       // the poisoned ledgers' "series aborted" faults: the re-run supersedes them
@@ -541,8 +573,7 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
         std::lock_guard<std::mutex> g(err_mu);
         if (!first_err) first_err = std::current_exception();
       }
-      ledger.poison();
-      enq.poison();
+      poison_all();
     }
   };
   if (T == 1) {
@@ -557,7 +588,6 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   for (int t = 0; t < T; ++t) worker(t).sync();
   for (cudaEvent_t ev : done_) cudaEventDestroy(ev);
   done_.clear();
-  enq_ = nullptr;
   if (redo && !first_err) {
     // a speculative budget split was wrong (exactly-zero right-hand side) while later
     // frames already consumed the estimate: re-run the range with per-frame

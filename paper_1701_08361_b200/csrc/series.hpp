@@ -64,6 +64,14 @@ class Series {
   Series& operator=(const Series&) = delete;
 
   int frames() const { return F_; }
+  // Multi-slice acquisitions (pipeline.cpp:315-334, 429-434, 503): the store holds Sl
+  // interleaved slice chains, store index g = frame * Sl + slice, as the pipeline
+  // numbers its deliveries. Each slice is its own chain (ledger, estimates, temporal
+  // schedule) with its own normalisation (frame 0 of the slice scaled to norm 100);
+  // the T frame workers take store indices round-robin across slices.
+  void set_slices(int Sl);
+  int slices() const { return Sl_; }
+  double slice_scale(int sl) const { return slice_scale_[static_cast<size_t>(sl)]; }
   void upload_frames(int first, int count, const float* z_host);  // synchronous H2D
   void upload_psf(int k, const float* P_host);
   void set_psf_index(const int* idx);
@@ -100,8 +108,8 @@ class Series {
 
  private:
   FrameWorker& worker(int t);
-  void run_frame(int t, int n, const SeriesOptions& o, CompletionLedger& ledger, SeriesFrameOut& out,
-                 cudaEvent_t ready);
+  // g: store index (frame g / Sl of slice g % Sl)
+  void run_frame(int t, int g, const SeriesOptions& o, SeriesFrameOut& out, cudaEvent_t ready);
 
   Engine& eng0_;
   std::vector<std::unique_ptr<Engine>> extra_;
@@ -132,7 +140,10 @@ class Series {
   float span_ms_ = 0.f;
   bool step_sync_ = false;
   bool safe_mode_ = false;                 // no device-side chaining of closing steps
-  CompletionLedger* enq_ = nullptr;        // frames whose final work is enqueued
+  int Sl_ = 1;                             // interleaved slice chains
+  std::vector<double> slice_scale_{1.0};   // prep normalisation per slice
+  std::vector<std::unique_ptr<CompletionLedger>> ledgers_;  // per slice, current run
+  std::vector<std::unique_ptr<CompletionLedger>> enqs_;     // per slice: final work enqueued
   int run_first_ = 0;
   std::vector<cudaEvent_t> done_;          // per frame of the current run: estimate published
 };

@@ -366,3 +366,71 @@ def test_series_images_through_the_device_post_stage_into_an_rti_sink(gpu, ref, 
         mags = np.stack([ref.magnitude_image(want["images"][n]) for n in range(F)])
         expect = ref.median_filter(mags) if mode == "median3" else mags
         assert rel_err(px, expect) < FRAME_TOL
+
+
+def _slice_inputs(ref, plan, Sl, F, K, U, seeds):
+    """Sl slices of F frames each (a different phantom seed per slice), interleaved in
+    the pipeline's delivery order g = frame * Sl + slice"""
+    per = [ref.phantom_series(plan.J, F, K, U, plan.N, 1e-4, seeds[sl]) for sl in range(Sl)]
+    samples = np.stack([per[g % Sl][0][g // Sl] for g in range(F * Sl)])
+    angles = np.stack([per[g % Sl][1][g // Sl] for g in range(F * Sl)])
+    return per, samples, angles
+
+
+def test_interleaved_slices_equal_independent_series_bit_for_bit(gpu, ref):
+    """per-slice chains in one device series (pipeline.cpp:315-334).
+    Each slice is its own chain with its own normalisation, so a 2-slice interleaved
+    series reproduces two separate single-slice series bit for bit, and each slice
+    matches the reference's own series on that slice's frames."""
+    plan = _small_plan(gpu, 24, 3, 3, 9)
+    Sl, F, U = 2, 5, 5
+    per, samples, angles = _slice_inputs(ref, plan, Sl, F, 11, U, [21, 22])
+    s = gpu.Series(gpu.Context(plan), F * Sl, F * Sl)
+    s.set_slices(Sl)
+    out = s.run(gpu.SeriesOptions(plain=True), raw=dict(samples=samples, angles=angles))
+    for sl in range(Sl):
+        single = gpu.Series(gpu.Context(plan), F, U)
+        alone = single.run(gpu.SeriesOptions(plain=True), raw=dict(samples=per[sl][0], angles=per[sl][1]))
+        got = out["images"][sl::Sl]
+        assert np.array_equal(got, alone["images"]), sl
+        assert s.slice_scale(sl) == single.normalize()
+        want = ref.reconstruct_series(plan, per[sl][0], per[sl][1], plain=True)
+        assert want["data_scale"] == pytest.approx(s.slice_scale(sl), rel=1e-6)
+        for n in range(F):
+            assert rel_err(got[n], want["images"][n]) < FRAME_TOL, (sl, n)
+    assert [a.frame for a in out["audit"]] == [g // Sl for g in range(F * Sl)]
+
+
+def test_interleaved_slices_with_frames_in_flight_replay_per_slice(gpu, ref):
+    """T = 3 workers over 2 interleaved slices with a short strict prefix: every slice
+    keeps the ordering contract on its own chain and replays through the reference"""
+    plan = _small_plan(gpu, 16, 3, 3, 6)
+    Sl, F, U = 2, 6, 3
+    per, samples, angles = _slice_inputs(ref, plan, Sl, F, 5, U, [31, 32])
+    sched = gpu.TemporalSchedule(2, 2)
+    s = gpu.Series(gpu.Context(plan), F * Sl, F * Sl)
+    s.set_slices(Sl)
+    out = s.run(gpu.SeriesOptions(T=3, sched=sched), raw=dict(samples=samples, angles=angles))
+    M = plan.newton_steps
+    unity = gpu.initial_estimate(plan)
+    for sl in range(Sl):
+        audit = out["audit"][sl::Sl]
+        z = np.stack([ref.grid_adjoint(plan, per[sl][0][n], per[sl][1][n]) for n in range(F)])
+        P = np.stack([ref.build_psf(plan, per[sl][1][n], 2 * plan.N) for n in range(F)])
+        scale = s.slice_scale(sl)
+        zs = (z * np.float32(scale)).astype(np.complex64)
+        ests = {}
+        for n in range(F):
+            a = audit[n]
+            assert a.frame == n
+            if n > 0:
+                assert 0 <= a.init_src < n and a.reg_final_src == n - 1
+                assert a.reg_final_seq > audit[n - 1].finish_seq
+                if n <= sched.l:
+                    assert a.start_seq > audit[n - 1].finish_seq
+            init = unity if a.init_src < 0 else ests[a.init_src]
+            regs = [unity if a.init_src < 0 else ests[a.reg_src[m]] for m in range(M)]
+            img, est, _ = ref.reconstruct_frame_regs(plan, zs[n], P[n], init, regs)
+            ests[n] = est
+            assert rel_err(out["images"][n * Sl + sl], img * np.float32(1.0 / scale)) < FRAME_TOL, (sl, n)
+            assert rel_err(s.estimate(n * Sl + sl), est) < FRAME_TOL, (sl, n)
