@@ -277,7 +277,7 @@ Engine::~Engine() {
   if (frame_graph_) cudaGraphExecDestroy(frame_graph_);
   void* bufs[] = {winv_, P_, z_, x_, xcg_, r_, p_, ap_, ar_, reg_, est_scratch_[0], est_scratch_[1],
                   est_scratch_[2], coils_, rhom_, U_, V_, Y_, RP_, gbuf_, img_, partials_, st_, cr_buf_,
-                  RPO_, SS_, RC_, kpart_, flow_ctl_};
+                  RPO_, SS_, RC_, kpart_};
   for (void* b : bufs) {
     if (b) cudaFree(b);
   }
@@ -354,21 +354,6 @@ void Engine::alloc() {
     check_cuda(cudaMalloc(&kpart_, sizeof(double) * 3 * plan_.J * ops_->cluster_ctas), "cluster partials");
     // 32 window entries (x J channel terms) per block
     rho_grid_ = std::max(1, std::min(static_cast<int>((L * L + kRhoTile - 1) / kRhoTile), 4 * 148));
-  }
-  // persistent iteration kernel (k_flow) for the fused-CR applications of a stand-alone
-  // engine in throughput mode; RTN_FLOW=0 keeps the five pass kernels + k_cr_fused
-  if (ops_->flow) {
-    const char* e = std::getenv("RTN_FLOW");
-    use_flow_ = !(e && e[0] == '0');
-    if (use_flow_) {
-      const int words = flow_ctl_words(plan_.J, dims_.H);
-      check_cuda(cudaMalloc(&flow_ctl_, sizeof(unsigned int) * words), "flow control");
-      check_cuda(cudaMemset(flow_ctl_, 0, sizeof(unsigned int) * words), "flow control");
-      int sms = 0;
-      check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_), "sm count");
-      const int per_sm = std::max(1, ops_->flow_blocks_per_sm());
-      flow_grid_ = std::max(1, env_int("RTN_FLOW_CTAS", per_sm * sms));
-    }
   }
   // alpha schedule and budget split are data independent (nlinv.cpp:295-313)
   float alpha = plan_.alpha0;
@@ -567,11 +552,6 @@ void Engine::enq_setup_back(const float2* x, const float2* reg, float alpha) {
 
 void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
   ensure_cr_capacity(cap);
-  if (!sync_each && fused_cr_ && use_flow_ && !dims_.grp && !use_cluster_) {
-    // throughput mode: each iteration is one persistent dataflow launch (k_flow)
-    for (int it = 0; it < cap; ++it) enq_flow_iter(it, alpha, tol);
-    return;
-  }
   if (!sync_each && fused_cr_) {
     // budget-mode graphs: one fused recurrence kernel per iteration (k_cr_fused)
     win_only_ok_ = 1;
@@ -616,43 +596,6 @@ void Engine::enq_image(const float2* est, float2* img, float scale, bool apply_s
   enq_decode(est);
   launch_k(k_image, blocks_for(static_cast<long long>(plan_.N) * plan_.N, 148 * 4), kThreads, 0, s_, dims_,
            est, coils_, scale, apply_scale ? 1 : 0, img, st_);
-}
-
-void Engine::enq_flow_iter(int it, float alpha, float tol) {
-  FlowArgs f{};
-  f.d = dims_;
-  f.a.mode = CW_OPALPHA;
-  f.a.alpha = alpha;
-  f.a.dot_slot = it;
-  f.a.dx = r_;
-  f.a.out = ar_;
-  f.a.ap_prev = it > 0 ? ap_ : nullptr;
-  f.a.win_only_ok = 1;
-  f.winv = winv_;
-  f.twG = twG_;
-  f.coils = coils_;
-  f.rhom = rhom_;
-  f.P = P_;
-  f.dx = r_;
-  f.U = U_;
-  f.V = V_;
-  f.Y = Y_;
-  f.RP = RP_;
-  f.partials = partials_;
-  f.st = st_;
-  f.cr = cr_;
-  f.x = xcg_;
-  f.r = r_;
-  f.p = p_;
-  f.ap = ap_;
-  f.ar = ar_;
-  f.D = D_;
-  f.it = it;
-  f.tol = tol;
-  f.nbr = nbr_;
-  f.nvec = vec_grid_;
-  f.ctl = flow_ctl_;
-  ops_->flow(s_, flow_grid_, f);
 }
 
 void Engine::enq_cr_fused(int it, float tol) {
@@ -1037,11 +980,9 @@ double Engine::kernel_bytes(const char* which) const {
   if (w == "colsW") return c8 * (J * L * Gc + 3.0 * (G * G + J * Gc * Gc)) + 16.0 * dims_.H * L * L + 4.0 * Gc * Gc;
   if (w == "cr_xr" || w == "cr_pap") return c8 * 6.0 * (G * G + J * Gc * Gc);
   if (w == "cr_fused") return c8 * 9.0 * (G * G + J * Gc * Gc);  // x,r,p,ap,ar in; x,r,p,ap out
-  if (w == "apply" || w == "flow") {
-    // one fused normal-operator application (SURVEY.md §8(d) B_op, window pruned);
-    // k_flow adds the CR update, B_cg = 72 D_w
-    const double bop = 8.0 * L * L * (J + 3) + 8.0 * G * G + 16.0 * J * Gc * Gc + 4.0 * Gc * Gc;
-    return w == "apply" ? bop : bop + 72.0 * (L * L + J * Gc * Gc);
+  if (w == "apply") {
+    // one fused normal-operator application (SURVEY.md §8(d) B_op, window pruned)
+    return 8.0 * L * L * (J + 3) + 8.0 * G * G + 16.0 * J * Gc * Gc + 4.0 * Gc * Gc;
   }
   return 0.0;
 }
@@ -1079,9 +1020,6 @@ double Engine::time_kernel(const char* which, int reps) {
       ops_->colA(s_, J * tGc, dims_, winv_, twG_, r_ + static_cast<size_t>(G) * G, U_, dims_.lo, dims_.L, st_, 0);
     } else if (w == "apply") {
       enq_apply(r_, ar_, CW_OP, 0.f, -1, 0);
-    } else if (w == "flow") {
-      if (!use_flow_) fail(2, "time_kernel: the persistent iteration kernel is off for this plan");
-      enq_flow_iter(0, 0.5f, 0.f);  // a minimal-residual step: stationary, finite
     } else {
       fail(2, "time_kernel: unknown kernel " + w);
     }

@@ -280,11 +280,6 @@ class Engine : public FrameWorker {
   std::vector<int> caps_;       // budget-mode per-step caps
   std::vector<float> alphas_;   // per-step alpha schedule
   bool use_graphs_ = true;
-  // persistent iteration kernel for the fused-CR applications (throughput mode)
-  bool use_flow_ = false;
-  int flow_grid_ = 0;
-  unsigned int* flow_ctl_ = nullptr;
-  void enq_flow_iter(int it, float alpha, float tol);
   bool fused_cr_ = true;
   int win_only_ok_ = 0;    // the applications being enqueued belong to a fused CR solve   // RTN_FUSED_CR=0 selects the two-kernel recurrence in graphs too
   cudaGraphExec_t step_graph_[kMaxSteps] = {};

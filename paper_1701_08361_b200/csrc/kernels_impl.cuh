@@ -79,34 +79,11 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Grid-wide deterministic sum of K doubles: per-block partials, then the last
+// block to arrive reduces them in a fixed order. Returns true in that block,
+// with the totals in tot[] (all threads).
 template <int K>
-__device__ bool grid_reduce_at(double (&v)[K], double* partials, unsigned int* counter, double (&tot)[K], int bid,
-                               int nb);
-
-template <int K>
-__device__ __forceinline__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* counter,
-                                            double (&tot)[K]) {
-  return grid_reduce_at<K>(v, partials, counter, tot, (int)blockIdx.x, (int)gridDim.x);
-}
-
-// intermediate loads: plain inside the pass kernels (a kernel boundary orders producer
-// and consumer); L2-only (ld.global.cg) inside the persistent iteration kernel, where
-// the producer is another CTA of the same grid and a stale L1 line must not be read
-template <bool CG, class T>
-__device__ __forceinline__ T ldi(const T* p) {
-  if constexpr (CG) {
-    return __ldcg(p);
-  } else {
-    return *p;
-  }
-}
-
-// Grid-wide deterministic sum of K doubles over nb participating blocks (block index
-// bid): per-block partials, then the last block to arrive reduces them in a fixed
-// order. Returns true in that block, with the totals in tot[] (all threads).
-template <int K>
-__device__ bool grid_reduce_at(double (&v)[K], double* partials, unsigned int* counter, double (&tot)[K], int bid,
-                               int nb) {
+__device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* counter, double (&tot)[K]) {
   static_assert(K <= kMaxReduce, "partials buffer holds kMaxReduce doubles per block");
   __shared__ double red[K][32];
   __shared__ int s_last;
@@ -122,11 +99,11 @@ __device__ bool grid_reduce_at(double (&v)[K], double* partials, unsigned int* c
     for (int k = 0; k < K; ++k) {
       double s = 0;
       for (int w = 0; w < nw; ++w) s += red[k][w];
-      partials[bid * K + k] = s;
+      partials[blockIdx.x * K + k] = s;
     }
     __threadfence();
     const unsigned int t = atomicAdd(counter, 1u);
-    s_last = (t == (unsigned)nb - 1);
+    s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return false;
@@ -134,7 +111,7 @@ __device__ bool grid_reduce_at(double (&v)[K], double* partials, unsigned int* c
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     double s = 0;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) s += __ldcg(partials + b * K + k);
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) s += __ldcg(partials + b * K + k);
     s = warp_sum(s);
     __syncthreads();
     if (lane == 0) red[k][warp] = s;
@@ -208,13 +185,16 @@ __device__ __forceinline__ void row_line_sync() {
 // W^-1 column pass. Lines: (channel j, coil k-column q). Input chat_j*winv on the
 // Gc centered k-rows, output rows [r0, r0+nr) of U_j (G x Gc, row-major).
 template <class Geo>
-__device__ __forceinline__ void colA_body(int bid, Dims d, const float* __restrict__ winv,
-                                          const float4* __restrict__ twG, const float2* __restrict__ chat,
-                                          float2* __restrict__ U, int r0, int nr) {
+__global__ void RTNB_PASS_BOUNDS_LIGHT k_colA(Dims d, const float* __restrict__ winv,
+                                                  const float4* __restrict__ twG,
+                                                  const float2* __restrict__ chat, float2* __restrict__ U,
+                                                  int r0, int nr, const DevState* st, int use_halt) {
+  pdl_enter();
+  if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(true);
   const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
-  const int j = bid / tiles;
-  const int q0 = (bid - j * tiles) * Geo::LPB;
+  const int j = blockIdx.x / tiles;
+  const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
   const int nl = min(Geo::LPB, d.Gc - q0);
   const float2* src = chat + (size_t)j * d.Gc * d.Gc;
   if (i1.on && i1.l < nl) {
@@ -255,16 +235,6 @@ __device__ __forceinline__ void colA_body(int bid, Dims d, const float* __restri
   }
 }
 
-template <class Geo>
-__global__ void RTNB_PASS_BOUNDS_LIGHT k_colA(Dims d, const float* __restrict__ winv,
-                                                  const float4* __restrict__ twG,
-                                                  const float2* __restrict__ chat, float2* __restrict__ U,
-                                                  int r0, int nr, const DevState* st, int use_halt) {
-  pdl_enter();
-  if (st->status || (use_halt && st->cr_halt)) return;
-  colA_body<Geo>(blockIdx.x, d, winv, twG, chat, U, r0, nr);
-}
-
 enum Rows1Mode : int { R1_DECODE = 0, R1_OP = 1, R1_SETUP = 2 };
 
 // Row pass 1.
@@ -273,18 +243,24 @@ enum Rows1Mode : int { R1_DECODE = 0, R1_OP = 1, R1_SETUP = 2 };
 //  OP:     window rows: W^-1 row pass of U_j, t = c_j*drho + rho*a on the window,
 //          forward row FFT -> V_j (L x G).
 //  SETUP:  window rows: t = rho*c_j (nlinv.cpp:252) -> forward row FFT -> V_j.
-template <class Geo, bool CG>
-__device__ __forceinline__ void rows1_body(int bid, Dims d, int mode, const float4* __restrict__ twG,
-                                           const float2* __restrict__ U, const float2* __restrict__ coils,
-                                           const float2* __restrict__ rhom, const float2* __restrict__ drho,
-                                           float2* __restrict__ V, float2* __restrict__ coils_out,
-                                           const float2* __restrict__ rho_src, float2* __restrict__ rhom_out) {
+template <class Geo>
+__global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restrict__ twG,
+                                                   const float2* __restrict__ U,
+                                                   const float2* __restrict__ coils,
+                                                   const float2* __restrict__ rhom,
+                                                   const float2* __restrict__ drho, float2* __restrict__ V,
+                                                   float2* __restrict__ coils_out,
+                                                   const float2* __restrict__ rho_src,
+                                                   float2* __restrict__ rhom_out, const DevState* st,
+                                                   int use_halt) {
+  pdl_enter();
+  if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(false);
   const int nrows = (mode == R1_DECODE) ? G : d.L;
   const int row0 = (mode == R1_DECODE) ? 0 : d.lo;
   const int tiles = (nrows + Geo::LPB - 1) / Geo::LPB;
-  const int j = bid / tiles;
-  const int rl0 = (bid - j * tiles) * Geo::LPB;
+  const int j = blockIdx.x / tiles;
+  const int rl0 = (blockIdx.x - j * tiles) * Geo::LPB;
   const int nl = min(Geo::LPB, nrows - rl0);
   const float2* Uj = U + (size_t)j * G * d.Gc;
   const float2* cj = coils + (size_t)j * G * G;
@@ -297,7 +273,7 @@ __device__ __forceinline__ void rows1_body(int bid, Dims d, int mode, const floa
       for (int n1 = 0; n1 < N1; ++n1) {
         const int t = N2 * n1 + i1.k;
         const int qk = t - d.off;
-        v[n1] = (qk >= 0 && qk < d.Gc) ? flip(ldi<CG>(Uj + (size_t)r1 * d.Gc + qk), t) : make_float2(0.f, 0.f);
+        v[n1] = (qk >= 0 && qk < d.Gc) ? flip(Uj[(size_t)r1 * d.Gc + qk], t) : make_float2(0.f, 0.f);
       }
       if (d.Gc * 4 == G) {  // pruned: only the coil band can be nonzero
         fft_step1<Geo, +1, Geo::GC_N1>(v, i1.k, twG);
@@ -389,30 +365,18 @@ __device__ __forceinline__ void rows1_body(int bid, Dims d, int mode, const floa
   }
 }
 
-template <class Geo>
-__global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restrict__ twG,
-                                                   const float2* __restrict__ U,
-                                                   const float2* __restrict__ coils,
-                                                   const float2* __restrict__ rhom,
-                                                   const float2* __restrict__ drho, float2* __restrict__ V,
-                                                   float2* __restrict__ coils_out,
-                                                   const float2* __restrict__ rho_src,
-                                                   float2* __restrict__ rhom_out, const DevState* st,
-                                                   int use_halt) {
-  pdl_enter();
-  if (st->status || (use_halt && st->cr_halt)) return;
-  rows1_body<Geo, false>(blockIdx.x, d, mode, twG, U, coils, rhom, drho, V, coils_out, rho_src, rhom_out);
-}
-
 // Toeplitz column pass: forward column FFT of the window rows of V_j, * P/G, inverse
 // column FFT, keep the window rows (in place in V_j). Lines: (j, column q).
-template <class Geo, bool CG>
-__device__ __forceinline__ void colsT_body(int bid, Dims d, const float4* __restrict__ twG,
-                                           const float2* __restrict__ P, float2* __restrict__ V) {
+template <class Geo>
+__global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
+                                                   const float2* __restrict__ P, float2* __restrict__ V,
+                                                   const DevState* st, int use_halt) {
+  pdl_enter();
+  if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(true);
   constexpr int tiles = (G + Geo::LPB - 1) / Geo::LPB;
-  const int j = bid / tiles;
-  const int q0 = (bid - j * tiles) * Geo::LPB;
+  const int j = blockIdx.x / tiles;
+  const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
   const int nl = min(Geo::LPB, G - q0);
   const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
   float2* Vj = V + (size_t)j * d.L * G;
@@ -422,7 +386,7 @@ __device__ __forceinline__ void colsT_body(int bid, Dims d, const float4* __rest
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) {
       const int t = N2 * n1 + i1.k;
-      v[n1] = (t >= d.lo && t < d.lo + d.L) ? flip(ldi<CG>(col + (size_t)(t - d.lo) * G), t) : make_float2(0.f, 0.f);
+      v[n1] = (t >= d.lo && t < d.lo + d.L) ? flip(col[(size_t)(t - d.lo) * G], t) : make_float2(0.f, 0.f);
     }
     fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
@@ -457,15 +421,6 @@ __device__ __forceinline__ void colsT_body(int bid, Dims d, const float4* __rest
   }
 }
 
-
-template <class Geo>
-__global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
-                                                   const float2* __restrict__ P, float2* __restrict__ V,
-                                                   const DevState* st, int use_halt) {
-  pdl_enter();
-  if (st->status || (use_halt && st->cr_halt)) return;
-  colsT_body<Geo, false>(blockIdx.x, d, twG, P, V);
-}
 
 struct ColsWArgs {
   int mode;
@@ -539,17 +494,21 @@ __device__ __forceinline__ float2 finish_op(const ColsWArgs& a, size_t e, float2
 // order in FP64 in shared memory -> RP[h][r] (double2 partial of all_reduce_sum,
 // decomp.cpp:26-39; k_colsW adds the groups in order); rt = conj(rho) T -> forward
 // W^-H row pass keeping the Gc coil k-columns -> Y_j (L x Gc).
-template <class Geo, bool CG>
-__device__ __forceinline__ void rows2_body(int bid, int nb, Dims d, int setup, const float4* __restrict__ twG,
-                                           const float2* __restrict__ V, const float2* __restrict__ coils,
-                                           const float2* __restrict__ rhom, const float2* __restrict__ z,
-                                           float2* __restrict__ Y, double2* __restrict__ RP, double* partials,
-                                           DevState* st) {
+template <class Geo>
+__global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* __restrict__ twG,
+                                                   const float2* __restrict__ V,
+                                                   const float2* __restrict__ coils,
+                                                   const float2* __restrict__ rhom,
+                                                   const float2* __restrict__ z, float2* __restrict__ Y,
+                                                   double2* __restrict__ RP, double* partials, DevState* st,
+                                                   int use_halt) {
+  pdl_enter();
+  if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(false);
   constexpr int L = G / 2;
   float2* RCs = A + Geo::SMEM_FLOAT2;  // LPB x L channel terms of this row
-  const int rl = bid % d.L;
-  const int h = bid / d.L;
+  const int rl = blockIdx.x % d.L;
+  const int h = blockIdx.x / d.L;
   const int r = d.lo + rl;
   const int j0 = h * Geo::LPB;
   const int nl = min(Geo::LPB, d.J - j0);
@@ -561,7 +520,7 @@ __device__ __forceinline__ void rows2_body(int bid, int nb, Dims d, int setup, c
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) {
       const int t = N2 * n1 + i1.k;
-      v[n1] = flip(ldi<CG>(Vr + t), t);
+      v[n1] = flip(Vr[t], t);
     }
     fft_step1<Geo, +1>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
@@ -651,7 +610,7 @@ __device__ __forceinline__ void rows2_body(int bid, int nb, Dims d, int setup, c
   }
   if (setup) {
     double vv[1] = {resid}, tot[1];
-    if (grid_reduce_at<1>(vv, partials, &st->counter, tot, bid, nb) && threadIdx.x == 0) {
+    if (grid_reduce<1>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
       if (d.grp) {
         st->gp[2] = tot[0];  // member partial, summed by k_grp_fin
       } else {
@@ -661,37 +620,27 @@ __device__ __forceinline__ void rows2_body(int bid, int nb, Dims d, int setup, c
   }
 }
 
-template <class Geo>
-__global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* __restrict__ twG,
-                                                   const float2* __restrict__ V,
-                                                   const float2* __restrict__ coils,
-                                                   const float2* __restrict__ rhom,
-                                                   const float2* __restrict__ z, float2* __restrict__ Y,
-                                                   double2* __restrict__ RP, double* partials, DevState* st,
-                                                   int use_halt) {
-  pdl_enter();
-  if (st->status || (use_halt && st->cr_halt)) return;
-  rows2_body<Geo, false>(blockIdx.x, gridDim.x, d, setup, twG, V, coils, rhom, z, Y, RP, partials, st);
-}
-
 // Last pass of an application: W^-H column pass (blocks [0, nbw)) and out.rho
 // outside the window (blocks [nbw, grid)); the window part of out.rho came from
 // k_rows2, whose reduction partial (st->scal[1]) is folded into the totals here.
-// returns true in the block that formed the totals (after writing them)
-template <class Geo, bool CG>
-__device__ __forceinline__ bool colsW_body(int bid, int nb, Dims d, const ColsWArgs& a,
-                                           const float* __restrict__ winv, const float4* __restrict__ twG,
-                                           const float2* __restrict__ Y, const double2* __restrict__ RP,
-                                           const float2* __restrict__ coils, const float2* __restrict__ z,
-                                           int nbw, double* partials, DevState* st, const CrScalars& cr,
-                                           const GroupView& gv) {
+template <class Geo>
+__global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float* __restrict__ winv,
+                                                   const float4* __restrict__ twG,
+                                                   const float2* __restrict__ Y,
+                                                   const double2* __restrict__ RP,
+                                                   const float2* __restrict__ coils,
+                                                   const float2* __restrict__ z, int nbw,
+                                                   double* partials, DevState* st, CrScalars cr,
+                                                   int use_halt, GroupView gv) {
+  pdl_enter();
+  if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(true);
   const int D0 = G * G;
   double acc0 = 0.0, acc1 = 0.0, aa = 0.0, pa = 0.0;
-  if (bid < nbw) {
+  if ((int)blockIdx.x < nbw) {
     const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
-    const int j = bid / tiles;
-    const int q0 = (bid - j * tiles) * Geo::LPB;
+    const int j = blockIdx.x / tiles;
+    const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
     const int nl = min(Geo::LPB, d.Gc - q0);
     const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
     // pruned band (Gc = G/4 on the DFT grid): this thread's outputs are the step-2 slots
@@ -716,7 +665,7 @@ __device__ __forceinline__ bool colsW_body(int bid, int nb, Dims d, const ColsWA
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) {
         const int t = N2 * n1 + i1.k;
-        v[n1] = (t >= d.lo && t < d.lo + d.L) ? flip(ldi<CG>(col + (size_t)(t - d.lo) * d.Gc), t) : make_float2(0.f, 0.f);
+        v[n1] = (t >= d.lo && t < d.lo + d.L) ? flip(col[(size_t)(t - d.lo) * d.Gc], t) : make_float2(0.f, 0.f);
       }
       fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
       park_step1<Geo>(A, i1.l, i1.k, v);
@@ -764,7 +713,7 @@ __device__ __forceinline__ bool colsW_body(int bid, int nb, Dims d, const ColsWA
     const bool win_only = a.mode != CW_SETUP && a.win_only_ok && rho_window_only(st);
     const int nv = win_only ? d.L * d.L : D0;
     int nz = 0;  // SETUP: a nonzero rhs.rho entry outside the window
-    for (int v = (bid - nbw) * blockDim.x + threadIdx.x; v < nv; v += (nb - nbw) * blockDim.x) {
+    for (int v = (blockIdx.x - nbw) * blockDim.x + threadIdx.x; v < nv; v += (gridDim.x - nbw) * blockDim.x) {
       int e, r, c;
       if (win_only) {
         r = d.lo + v / d.L;
@@ -814,7 +763,7 @@ __device__ __forceinline__ bool colsW_body(int bid, int nb, Dims d, const ColsWA
       if (in_win(d, r, c)) {
         const double2* src = RP + (size_t)(r - d.lo) * d.L + (c - d.lo);
         for (int h = 0; h < H; ++h) {
-          const double2 t = ldi<CG>(src + (size_t)h * d.L * d.L);
+          const double2 t = src[(size_t)h * d.L * d.L];
           sx += t.x;
           sy += t.y;
         }
@@ -835,8 +784,7 @@ __device__ __forceinline__ bool colsW_body(int bid, int nb, Dims d, const ColsWA
     if (a.mode == CW_SETUP && __syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&st->rho_out_nz, 1);
   }
   double vv[4] = {acc0, acc1, aa, pa}, tot[4];
-  const bool last = grid_reduce_at<4>(vv, partials, &st->counter, tot, bid, nb);
-  if (last && threadIdx.x == 0) {
+  if (grid_reduce<4>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
     const double total = tot[0];
     if (a.mode == CW_SETUP) st->rho_out_known = 1;  // every block's atomicOr precedes its ticket
     if (d.grp) {
@@ -869,377 +817,6 @@ __device__ __forceinline__ bool colsW_body(int bid, int nb, Dims d, const ColsWA
       cr.spa[a.dot_slot] = tot[3];
     } else {
       st->scal[0] = total;
-    }
-  }
-  return last;
-}
-
-template <class Geo>
-__global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float* __restrict__ winv,
-                                                   const float4* __restrict__ twG,
-                                                   const float2* __restrict__ Y,
-                                                   const double2* __restrict__ RP,
-                                                   const float2* __restrict__ coils,
-                                                   const float2* __restrict__ z, int nbw,
-                                                   double* partials, DevState* st, CrScalars cr,
-                                                   int use_halt, GroupView gv) {
-  pdl_enter();
-  if (st->status || (use_halt && st->cr_halt)) return;
-  colsW_body<Geo, false>(blockIdx.x, gridDim.x, d, a, winv, twG, Y, RP, coils, z, nbw, partials, st, cr, gv);
-}
-
-// Fused CR recurrence for the budget-mode frame graphs: iteration `it` second half
-// and iteration it+1 first half in one pass (one kernel and one grid reduction fewer
-// per iteration than k_cr_pap + k_cr_xr):
-//   b = rar[it]/rar[it-1] (b = 0 for it = 0, the priming step);
-//   p = b p + r; ap = b ap + ar;                          (nlinv.cpp:225-230)
-//   |ap|^2 = b^2 |ap_prev|^2 + 2b Re<ap_prev, ar> + |ar|^2  from the exact norm of the
-//     previous ap and the application's dots (exact for it = 0);
-//   a = rar[it]/|ap|^2; x += a p; r -= a ap; rn[it+1] = |r|  (nlinv.cpp:205-220)
-// The exact |ap|^2 of this pass is reduced for the next iteration.
-template <bool CG>
-__device__ __forceinline__ void cr_fused_body(int bid, int nb, int D, float2* __restrict__ x,
-                                              float2* __restrict__ r, float2* __restrict__ p,
-                                              float2* __restrict__ ap, const float2* __restrict__ ar,
-                                              double* partials, DevState* st, const CrScalars& cr, int it,
-                                              float tol, int rho_skip, int grp, int G) {
-  const double rar_new = ldi<CG>(cr.rar + it);
-  double b = 0.0, denom = ldi<CG>(cr.saa);
-  if (it > 0) {
-    const double rar_old = ldi<CG>(cr.rar + it - 1);
-    b = (rar_old != 0.0) ? rar_new / rar_old : 0.0;
-    denom = b * b * ldi<CG>(cr.ap2 + it - 1) + 2.0 * b * ldi<CG>(cr.spa + it) + ldi<CG>(cr.saa + it);
-  }
-  if (!isfinite(denom) || !isfinite(rar_new)) {
-    if (bid == 0 && threadIdx.x == 0) {
-      st->status = ST_SOLVER;
-      st->cr_halt = 1;
-    }
-    return;
-  }
-  if (denom <= 0.0 && tol > 0.0f) {
-    if (bid == 0 && threadIdx.x == 0) st->cr_halt = 1;
-    return;
-  }
-  const bool upd = denom > 0.0;
-  const double a = upd ? rar_new / denom : 0.0;
-  const float bf = (float)b, af = (float)a, naf = (float)(-a);
-  double acc_ap = 0.0, acc_r = 0.0;
-  // rho entries outside the window are exactly zero in every vector: skip them
-  const bool win_only = rho_window_only(st);
-  const int L = G / 2, lo = (G - L) / 2, G2 = G * G;
-  const int nv = win_only ? D - G2 + L * L : D;
-  // four entries per thread per round with every load issued up front (memory-level
-  // parallelism); per-thread accumulation order is unchanged
-  constexpr int kU = 4;
-  const int stride = nb * blockDim.x;
-  for (int v0 = bid * blockDim.x + threadIdx.x; v0 < nv; v0 += kU * stride) {
-    int idx[kU];
-    float2 pv[kU], apv[kU], rv[kU], arv[kU], xv[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int v = v0 + u * stride;
-      int i = v < nv ? v : -1;
-      if (win_only && i >= 0) i = v < L * L ? (lo + v / L) * G + lo + (v - (v / L) * L) : G2 + (v - L * L);
-      idx[u] = i;
-      if (i >= 0) {
-        pv[u] = p[i];
-        apv[u] = ap[i];
-        rv[u] = r[i];
-        arv[u] = ldi<CG>(ar + i);
-        if (upd) xv[u] = x[i];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int i = idx[u];
-      if (i < 0) continue;
-      const float2 np = make_float2(__fadd_rn(__fmul_rn(pv[u].x, bf), rv[u].x), __fadd_rn(__fmul_rn(pv[u].y, bf), rv[u].y));
-      const float2 nap =
-          make_float2(__fadd_rn(__fmul_rn(apv[u].x, bf), arv[u].x), __fadd_rn(__fmul_rn(apv[u].y, bf), arv[u].y));
-      p[i] = np;
-      ap[i] = nap;
-      float2 nr = rv[u];
-      if (upd) {
-        x[i] = axpy_rn(xv[u], af, np);
-        nr = axpy_rn(rv[u], naf, nap);
-        r[i] = nr;
-      }
-      if (i >= rho_skip) {  // group members other than the first skip the replicated rho
-        acc_ap += nrm2(nap);
-        acc_r += nrm2(nr);
-      }
-    }
-  }
-  double v[2] = {acc_ap, acc_r}, tot[2];
-  if (grid_reduce_at<2>(v, partials, &st->counter, tot, bid, nb) && threadIdx.x == 0) {
-    if (grp) {
-      cr.pcr[2 * it + 0] = tot[0];
-      cr.pcr[2 * it + 1] = tot[1];
-      return;
-    }
-    cr.ap2[it] = tot[0];
-    const double rn = sqrt(tot[1]);
-    cr.rn[it + 1] = rn;
-    StepRec& s = st->steps[st->cur_step];
-    if (!isfinite(rn)) {
-      st->status = ST_SOLVER;
-      st->cr_halt = 1;
-      return;
-    }
-    s.iters = it + 1;
-    const double target = (double)tol * sqrt(s.rhs_nrm2);
-    if (tol > 0.0f && (rn == 0.0 || rn <= target)) st->cr_halt = 1;
-  }
-}
-
-
-// ---------------------------------------------------------------------------------
-// Persistent iteration kernel (throughput mode, single device): one CR iteration --
-// the normal-operator application (colA, rows1, colsT, rows2, colsW) and the fused
-// recurrence -- as ONE launch of resident CTAs that pull tiles from a ticket counter
-// in a dependency-respecting order and wait only on the tiles they read:
-//   rows1(j)  after colA(j)           colsT(j) after rows1(j)
-//   rows2(h)  after colsT(j in h)     colsW(j) after rows2(h(j))
-//   rho part  after every rows2       recurrence after colsW's totals
-// so channel group h+1 fills the SMs while group h drains, and no tile waits for a
-// grid-wide kernel boundary. The tile bodies are the pass kernels' own (same
-// arithmetic, same results bit for bit); intermediates written by other CTAs of the
-// grid are read through L2 (ldi<true>), and every completed tile publishes with a
-// gpu-scope fence before its counter increment. Tickets are handed out in increasing
-// order and a tile only waits on tiles with smaller tickets, which were claimed by
-// CTAs already running, so the wait graph is acyclic whatever the residency.
-// ---------------------------------------------------------------------------------
-
-struct FlowArgs {
-  Dims d;
-  ColsWArgs a;          // the CW_OPALPHA application of iteration `it`
-  const float* winv;
-  const float4* twG;
-  const float2* coils;
-  const float2* rhom;
-  const float2* P;
-  const float2* dx;     // the operand r (rho then chat)
-  float2* U;
-  float2* V;
-  float2* Y;
-  double2* RP;
-  double* partials;
-  DevState* st;
-  CrScalars cr;
-  float2* x;            // CR vectors for the recurrence
-  float2* r;
-  float2* p;
-  float2* ap;
-  float2* ar;
-  int D;
-  int it;
-  float tol;
-  int nbr;              // rho-part tiles of colsW
-  int nvec;             // recurrence tiles
-  unsigned int* ctl;    // FlowCtl words (zero between launches)
-};
-
-// FlowCtl layout: [0] ticket, [1] CTAs done, [2] colsW totals written, [3] rows2 tiles
-// done (all groups), then colA done per channel (J), rows1 done per channel (J), colsT
-// done per group (H), rows2 done per group (H)
-constexpr int kFlowHead = 4;
-__host__ __device__ constexpr int flow_ctl_words(int J, int H) { return kFlowHead + 2 * J + 2 * H; }
-
-__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// thread 0 waits until *p >= target; then the block proceeds (cumulative acquire)
-__device__ __forceinline__ void flow_wait(const unsigned int* p, unsigned int target) {
-  if (threadIdx.x == 0) {
-    while (ld_acquire(p) < target) __nanosleep(32);
-  }
-  __syncthreads();
-}
-
-// every thread's stores of the tile, then one release increment: the CTA barrier
-// orders the threads' stores before thread 0's gpu-scope release (fences are
-// cumulative; the pattern of cooperative-groups' grid sync)
-__device__ __forceinline__ void flow_done(unsigned int* p) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    atomicAdd(p, 1u);
-  }
-}
-
-// One function per tile kind (RTNB_FLOW_NOINLINE=1: separately register-allocated
-// calls; 0: inlined into the dispatch loop).
-#ifndef RTNB_FLOW_NOINLINE
-#define RTNB_FLOW_NOINLINE 1
-#endif
-#if RTNB_FLOW_NOINLINE
-#define RTNB_FLOW_FN __device__ __noinline__
-#else
-#define RTNB_FLOW_FN __device__ __forceinline__
-#endif
-#ifndef RTNB_FLOW_ORDER
-#define RTNB_FLOW_ORDER 1
-#endif
-// resident CTAs per SM the persistent kernel asks the register allocator for
-#ifndef RTNB_FLOW_MINB
-#define RTNB_FLOW_MINB 3
-#endif
-template <class Geo>
-RTNB_FLOW_FN void flow_colA(int bid, const FlowArgs& f) {
-  colA_body<Geo>(bid, f.d, f.winv, f.twG, f.dx + (size_t)Geo::G * Geo::G, f.U, f.d.lo, f.d.L);
-}
-template <class Geo>
-RTNB_FLOW_FN void flow_rows1(int bid, const FlowArgs& f) {
-  rows1_body<Geo, true>(bid, f.d, R1_OP, f.twG, f.U, f.coils, f.rhom, f.dx, f.V, nullptr, nullptr, nullptr);
-}
-template <class Geo>
-RTNB_FLOW_FN void flow_colsT(int bid, const FlowArgs& f) {
-  colsT_body<Geo, true>(bid, f.d, f.twG, f.P, f.V);
-}
-template <class Geo>
-RTNB_FLOW_FN void flow_rows2(int bid, const FlowArgs& f) {
-  rows2_body<Geo, true>(bid, f.d.H * f.d.L, f.d, 0, f.twG, f.V, f.coils, f.rhom, nullptr, f.Y, f.RP, f.partials,
-                        f.st);
-}
-template <class Geo>
-RTNB_FLOW_FN bool flow_colsW(int bid, int nbw, const FlowArgs& f) {
-  GroupView gv{};
-  return colsW_body<Geo, true>(bid, nbw + f.nbr, f.d, f.a, f.winv, f.twG, f.Y, f.RP, f.coils, nullptr, nbw,
-                               f.partials, f.st, f.cr, gv);
-}
-template <class Geo>
-RTNB_FLOW_FN void flow_cr(int bid, const FlowArgs& f) {
-  cr_fused_body<true>(bid, f.nvec, f.D, f.x, f.r, f.p, f.ap, f.ar, f.partials, f.st, f.cr, f.it, f.tol, 0, 0,
-                      Geo::G);
-}
-
-template <class Geo>
-__global__ void __launch_bounds__(Geo::NT, (RTNB_FLOW_MINB * 256 + Geo::NT - 1) / Geo::NT) k_flow(FlowArgs f) {
-  pdl_enter();
-  constexpr int LPB = Geo::LPB, G = Geo::G;
-  const Dims& d = f.d;
-  unsigned int* ctl = f.ctl;
-  unsigned int* c_colA = ctl + kFlowHead;
-  unsigned int* c_rows1 = c_colA + d.J;
-  unsigned int* c_colsT = c_rows1 + d.J;
-  unsigned int* c_rows2 = c_colsT + d.H;
-  const int tGc = (d.Gc + LPB - 1) / LPB, tL = (d.L + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB;
-  const int nbw = d.J * tGc;
-  // tiles per channel group: colA, rows1, colsT, rows2 rows, colsW (W^-H)
-  const int per_ch = tGc + tL + tG + tGc;
-  const int groups_total = d.J * per_ch + d.H * d.L;
-  const int total = groups_total + f.nbr + f.nvec;
-  // RTNB_FLOW_ORDER 1: tickets phase by phase (all colA, all rows1, ...), each phase's
-  // tiles channel-major, so a consumer is claimed only after every producer tile of its
-  // phase was; 0: channel group by channel group (consumers of group h right behind h)
-  constexpr bool kPhaseMajor = RTNB_FLOW_ORDER != 0;
-  __shared__ int s_t;
-  const volatile DevState* vst = f.st;
-  const bool live = !(vst->status || vst->cr_halt);
-  while (live) {
-    if (threadIdx.x == 0) s_t = (int)atomicAdd(ctl, 1u);
-    __syncthreads();
-    int t = s_t;
-    __syncthreads();
-    if (t >= total) break;
-    if (t < groups_total) {
-      int h = 0, jb = 0, nh = d.J, u = t;
-      if constexpr (kPhaseMajor) {
-        // map the phase-major ticket onto (group h, offset u inside the group's layout)
-        int k = t;
-        int ph = 0, cnt[5] = {d.J * tGc, d.J * tL, d.J * tG, d.H * d.L, d.J * tGc};
-        while (k >= cnt[ph]) {
-          k -= cnt[ph];
-          ++ph;
-        }
-        const int per[5] = {tGc, tL, tG, 0, tGc};
-        if (ph == 3) {
-          h = k / d.L;
-          k -= h * d.L;
-        } else {
-          h = (k / per[ph]) / LPB;
-          k -= h * LPB * per[ph];
-        }
-        jb = h * LPB;
-        nh = min(LPB, d.J - jb);
-        const int off[5] = {0, nh * tGc, nh * (tGc + tL), nh * (tGc + tL + tG), nh * (tGc + tL + tG) + d.L};
-        u = off[ph] + k;
-      } else {
-        // locate the channel group: groups are LPB channels (the last may be short)
-        int base = 0;
-        for (;; ++h) {
-          const int nhh = min(LPB, d.J - h * LPB);
-          const int sz = nhh * per_ch + d.L;
-          if (t < base + sz) break;
-          base += sz;
-        }
-        jb = h * LPB;
-        nh = min(LPB, d.J - jb);
-        u = t - base;
-      }
-      if (u < nh * tGc) {  // colA (j, coil-column tile)
-        const int j = jb + u / tGc;
-        flow_colA<Geo>(jb * tGc + u, f);
-        flow_done(c_colA + j);
-        continue;
-      }
-      u -= nh * tGc;
-      if (u < nh * tL) {  // rows1 (j, window-row tile)
-        const int j = jb + u / tL;
-        flow_wait(c_colA + j, tGc);
-        flow_rows1<Geo>(jb * tL + u, f);
-        flow_done(c_rows1 + j);
-        continue;
-      }
-      u -= nh * tL;
-      if (u < nh * tG) {  // colsT (j, column tile)
-        const int j = jb + u / tG;
-        flow_wait(c_rows1 + j, tL);
-        flow_colsT<Geo>(jb * tG + u, f);
-        flow_done(c_colsT + h);
-        continue;
-      }
-      u -= nh * tG;
-      if (u < d.L) {  // rows2 (group h, window row u)
-        flow_wait(c_colsT + h, nh * tG);
-        flow_rows2<Geo>(h * d.L + u, f);
-        flow_done(c_rows2 + h);
-        if (threadIdx.x == 0) atomicAdd(ctl + 3, 1u);  // ordered after the fence above
-        continue;
-      }
-      u -= d.L;
-      {  // colsW W^-H (j, coil-column tile)
-        flow_wait(c_rows2 + h, d.L);
-        const bool last = flow_colsW<Geo>(jb * tGc + u, nbw, f);
-        if (last) flow_done(ctl + 2);
-        continue;
-      }
-    }
-    t -= groups_total;
-    if (t < f.nbr) {  // colsW rho part: the channel-group sums of every group
-      flow_wait(ctl + 3, d.H * d.L);
-      const bool last = flow_colsW<Geo>(nbw + t, nbw, f);
-      if (last) flow_done(ctl + 2);
-      continue;
-    }
-    t -= f.nbr;
-    // the fused CR recurrence (needs the application's totals)
-    flow_wait(ctl + 2, 1);
-    if (vst->status) continue;
-    flow_cr<Geo>(t, f);
-  }
-  // the last CTA out clears the control words for the next launch (stream ordered)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(ctl + 1, 1u) == gridDim.x - 1) {
-      const int n = flow_ctl_words(d.J, d.H);
-      for (int k = 0; k < n; ++k) ctl[k] = 0u;
-      __threadfence();
     }
   }
 }
@@ -1358,7 +935,15 @@ __global__ void __launch_bounds__(kThreads) k_cr_pap(int D, float2* __restrict__
   if (grid_reduce<1>(v, partials, &st->counter, tot) && threadIdx.x == 0) cr.ap2[it] = tot[0];
 }
 
-
+// Fused CR recurrence for the budget-mode frame graphs: iteration `it` second half
+// and iteration it+1 first half in one pass (one kernel and one grid reduction fewer
+// per iteration than k_cr_pap + k_cr_xr):
+//   b = rar[it]/rar[it-1] (b = 0 for it = 0, the priming step);
+//   p = b p + r; ap = b ap + ar;                          (nlinv.cpp:225-230)
+//   |ap|^2 = b^2 |ap_prev|^2 + 2b Re<ap_prev, ar> + |ar|^2  from the exact norm of the
+//     previous ap and the application's dots (exact for it = 0);
+//   a = rar[it]/|ap|^2; x += a p; r -= a ap; rn[it+1] = |r|  (nlinv.cpp:205-220)
+// The exact |ap|^2 of this pass is reduced for the next iteration.
 __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict__ x, float2* __restrict__ r,
                                                        float2* __restrict__ p, float2* __restrict__ ap,
                                                        const float2* __restrict__ ar, double* partials,
@@ -1366,7 +951,94 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
                                                        int rho_skip, int grp, int G) {
   pdl_enter();
   if (st->status || st->cr_halt) return;
-  cr_fused_body<false>(blockIdx.x, gridDim.x, D, x, r, p, ap, ar, partials, st, cr, it, tol, rho_skip, grp, G);
+  const double rar_new = cr.rar[it];
+  double b = 0.0, denom = cr.saa[0];
+  if (it > 0) {
+    const double rar_old = cr.rar[it - 1];
+    b = (rar_old != 0.0) ? rar_new / rar_old : 0.0;
+    denom = b * b * cr.ap2[it - 1] + 2.0 * b * cr.spa[it] + cr.saa[it];
+  }
+  if (!isfinite(denom) || !isfinite(rar_new)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->status = ST_SOLVER;
+      st->cr_halt = 1;
+    }
+    return;
+  }
+  if (denom <= 0.0 && tol > 0.0f) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->cr_halt = 1;
+    return;
+  }
+  const bool upd = denom > 0.0;
+  const double a = upd ? rar_new / denom : 0.0;
+  const float bf = (float)b, af = (float)a, naf = (float)(-a);
+  double acc_ap = 0.0, acc_r = 0.0;
+  // rho entries outside the window are exactly zero in every vector: skip them
+  const bool win_only = rho_window_only(st);
+  const int L = G / 2, lo = (G - L) / 2, G2 = G * G;
+  const int nv = win_only ? D - G2 + L * L : D;
+  // four entries per thread per round with every load issued up front (memory-level
+  // parallelism); per-thread accumulation order is unchanged
+  constexpr int kU = 4;
+  const int stride = gridDim.x * blockDim.x;
+  for (int v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < nv; v0 += kU * stride) {
+    int idx[kU];
+    float2 pv[kU], apv[kU], rv[kU], arv[kU], xv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int v = v0 + u * stride;
+      int i = v < nv ? v : -1;
+      if (win_only && i >= 0) i = v < L * L ? (lo + v / L) * G + lo + (v - (v / L) * L) : G2 + (v - L * L);
+      idx[u] = i;
+      if (i >= 0) {
+        pv[u] = p[i];
+        apv[u] = ap[i];
+        rv[u] = r[i];
+        arv[u] = ar[i];
+        if (upd) xv[u] = x[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = idx[u];
+      if (i < 0) continue;
+      const float2 np = make_float2(__fadd_rn(__fmul_rn(pv[u].x, bf), rv[u].x), __fadd_rn(__fmul_rn(pv[u].y, bf), rv[u].y));
+      const float2 nap =
+          make_float2(__fadd_rn(__fmul_rn(apv[u].x, bf), arv[u].x), __fadd_rn(__fmul_rn(apv[u].y, bf), arv[u].y));
+      p[i] = np;
+      ap[i] = nap;
+      float2 nr = rv[u];
+      if (upd) {
+        x[i] = axpy_rn(xv[u], af, np);
+        nr = axpy_rn(rv[u], naf, nap);
+        r[i] = nr;
+      }
+      if (i >= rho_skip) {  // group members other than the first skip the replicated rho
+        acc_ap += nrm2(nap);
+        acc_r += nrm2(nr);
+      }
+    }
+  }
+  double v[2] = {acc_ap, acc_r}, tot[2];
+  if (grid_reduce<2>(v, partials, &st->counter, tot) && threadIdx.x == 0) {
+    if (grp) {
+      cr.pcr[2 * it + 0] = tot[0];
+      cr.pcr[2 * it + 1] = tot[1];
+      return;
+    }
+    cr.ap2[it] = tot[0];
+    const double rn = sqrt(tot[1]);
+    cr.rn[it + 1] = rn;
+    StepRec& s = st->steps[st->cur_step];
+    if (!isfinite(rn)) {
+      st->status = ST_SOLVER;
+      st->cr_halt = 1;
+      return;
+    }
+    s.iters = it + 1;
+    const double target = (double)tol * sqrt(s.rhs_nrm2);
+    if (tol > 0.0f && (rn == 0.0 || rn <= target)) st->cr_halt = 1;
+  }
 }
 
 // ---------------------------------------------------------------------------------

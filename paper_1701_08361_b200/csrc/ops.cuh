@@ -33,10 +33,6 @@ struct Engine::Ops {
   void (*apply_cluster)(cudaStream_t, int J, Dims, ColsWArgs, const float*, const float4*, const float2*,
                         const float2*, const float2*, float2*, double*, const DevState*, int) = nullptr;
   int cluster_ctas = 0;
-  // persistent iteration kernel (k_flow): one CR iteration per launch; resident CTAs
-  // per SM at its register / shared-memory footprint
-  void (*flow)(cudaStream_t, int grid, const FlowArgs&) = nullptr;
-  int (*flow_blocks_per_sm)() = nullptr;
 };
 
 namespace {
@@ -99,9 +95,6 @@ struct Inst {
                                     static_cast<int>(kSmem2)),
                "attr rows2");
     check_cuda(cudaFuncSetAttribute(k_colsW<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsW");
-    check_cuda(cudaFuncSetAttribute(k_flow<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kSmem2)),
-               "attr flow");
     check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
     check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, +1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr ifft");
     check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
@@ -147,14 +140,6 @@ Engine::Ops Inst<N1, N2>::make() {
                const float2* Y, const double2* RP, const float2* coils, const float2* z, int nbw,
                double* partials, DevState* st, CrScalars cr, int h, const GroupView& gv) {
     launch_k(k_colsW<Geo>, grid, kNT, kSmem, s, d, a, winv, tw, Y, RP, coils, z, nbw, partials, st, cr, h, gv);
-  };
-  o.flow = [](cudaStream_t s, int grid, const FlowArgs& f) {
-    launch_k(k_flow<Geo>, grid, kNT, kSmem2, s, f);
-  };
-  o.flow_blocks_per_sm = [] {
-    int n = 0;
-    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_flow<Geo>, kNT, kSmem2), "flow occupancy");
-    return n;
   };
   o.fft = [](cudaStream_t s, int grid, int sign, float2* data, int batch, int axis, const float4* tw,
              float scale) {
