@@ -293,12 +293,16 @@ int rtn_tunedb_load(const char* path, int* rows6, double* runtime_ms, int64_t* t
                     int* n_rows, int* skipped);
 
 /* --- measurement --------------------------------------------------------------------- */
-/* average ms per launch of one kernel class ("colsT", "rows1", "rows2", "colA",
- * "apply") at the cached linearisation point, and its algorithmic bytes */
+/* average ms per launch of one kernel class ("colsT", "rows1", "rows2", "colA", "colsW",
+ * "cr_fused", "crA", "apply") at the cached linearisation point, and its algorithmic
+ * bytes; "<name>:cold" times every launch alone after a write larger than L2 */
 int rtn_time_kernel(rtn_ctx* ctx, const char* which, int reps, double* ms, double* bytes);
 /* 1 when this plan's grid has the cluster-fused application (latency mode; one
  * thread-block cluster per channel), else 0 (the five-kernel passes always run) */
 int rtn_cluster_supported(rtn_ctx* ctx, int* supported);
+/* 1 when the budget-mode CR solve on the five-kernel path fuses the recurrence with
+ * the next application's W^-1 column pass (k_crA), else 0 */
+int rtn_fused_cra(rtn_ctx* ctx, int* on);
 
 #ifdef __cplusplus
 }

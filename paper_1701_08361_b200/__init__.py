@@ -216,6 +216,7 @@ def load_library(path: str = LIB_PATH):
                             ctypes.c_int),
         "rtn_time_kernel": ([vp, ctypes.c_char_p, ctypes.c_int, d, d], ctypes.c_int),
         "rtn_cluster_supported": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+        "rtn_fused_cra": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
         "rtn_last_error_kind": ([], ctypes.c_int),
         "rtn_series_set_slices": ([vp, ctypes.c_int], ctypes.c_int),
         "rtn_series_slice_scale": ([vp, ctypes.c_int, d], ctypes.c_int),
@@ -589,6 +590,13 @@ class Context:
         """whether this plan's grid has the cluster-fused application (latency mode)"""
         v = ctypes.c_int(0)
         _check(self.lib.rtn_cluster_supported(self._h, ctypes.byref(v)))
+        return bool(v.value)
+
+    def fused_cra(self) -> bool:
+        """whether the budget-mode CR solve fuses the recurrence with the next
+        application's W^-1 column pass (k_crA) on the five-kernel path"""
+        v = ctypes.c_int(0)
+        _check(self.lib.rtn_fused_cra(self._h, ctypes.byref(v)))
         return bool(v.value)
 
     def time_kernel(self, which: str, reps: int = 20):

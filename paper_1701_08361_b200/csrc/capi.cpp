@@ -909,4 +909,11 @@ int rtn_cluster_supported(rtn_ctx* ctx, int* supported) {
   });
 }
 
+int rtn_fused_cra(rtn_ctx* ctx, int* on) {
+  return guarded([&] {
+    if (!on) rtnb::fail(2, "fused_cra: null output");
+    *on = eng(ctx).fused_crA() ? 1 : 0;
+  });
+}
+
 }  // extern "C"

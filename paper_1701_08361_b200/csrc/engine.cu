@@ -265,6 +265,10 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), dev_(device) {
   D_ = plan.G * plan.G + plan.J * plan.Gc * plan.Gc;
   check_cuda(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
   if (const char* e = std::getenv("RTN_FUSED_CR")) fused_cr_ = e[0] != '0';
+  // k_crA by measurement: +4 % at C3 and C4 (16 x 16); the 24-point step-1 geometries
+  // (C5's 24 x 16) hold too many CR operands with their DFT and lose 2 %
+  fused_crA_ = ops_->N1 <= 16;
+  if (const char* e = std::getenv("RTN_CRA")) fused_crA_ = e[0] != '0';
   alloc();
 }
 
@@ -492,11 +496,13 @@ void Engine::enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, 
   enq_apply_back(dx, out, cw_mode, alpha, dot_slot, use_halt, ap_prev);
 }
 
-void Engine::enq_apply_front(const float2* dx, int use_halt) {
+void Engine::enq_apply_front(const float2* dx, int use_halt, bool skip_colA) {
   const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
   const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
-  ops_->colA(s_, J * tGc, dims_, winv_, twG_, dx + static_cast<size_t>(G) * G, U_, dims_.lo, dims_.L, st_,
-             use_halt);
+  if (!skip_colA) {
+    ops_->colA(s_, J * tGc, dims_, winv_, twG_, dx + static_cast<size_t>(G) * G, U_, dims_.lo, dims_.L, st_,
+               use_halt);
+  }
   ops_->rows1(s_, J * tL, dims_, R1_OP, twG_, U_, coils_, rhom_, dx, V_, nullptr, nullptr, nullptr, st_, use_halt);
   ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, use_halt);
   ops_->rows2(s_, dims_.L * dims_.H, dims_, 0, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, use_halt);
@@ -554,12 +560,19 @@ void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
   ensure_cr_capacity(cap);
   if (!sync_each && fused_cr_) {
     // budget-mode graphs: one fused recurrence kernel per iteration (k_cr_fused)
+    // on the pass path the recurrence also runs the next application's W^-1 column pass
+    const bool crA = fused_crA() && !use_cluster_;
     win_only_ok_ = 1;
     enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1, nullptr);
-    enq_cr_fused(0, tol);
-    for (int it = 1; it < cap; ++it) {
-      enq_apply(r_, ar_, CW_OPALPHA, alpha, it, 1, ap_);
-      enq_cr_fused(it, tol);
+    for (int it = 0; it < cap; ++it) {
+      if (!crA || it + 1 == cap) {
+        enq_cr_fused(it, tol);
+        if (it + 1 < cap) enq_apply(r_, ar_, CW_OPALPHA, alpha, it + 1, 1, ap_);
+      } else {
+        enq_crA(it, tol);
+        enq_apply_front(r_, 1, true);
+        enq_apply_back(r_, ar_, CW_OPALPHA, alpha, it + 1, 1, ap_);
+      }
     }
     win_only_ok_ = 0;
     return;
@@ -602,6 +615,15 @@ void Engine::enq_cr_fused(int it, float tol) {
   const int rho_skip = (dims_.grp && !dims_.count_rho) ? plan_.G * plan_.G : 0;
   launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, static_cast<const float2*>(ar_),
            partials_, st_, cr_, it, tol, rho_skip, dims_.grp, plan_.G);
+}
+
+bool Engine::fused_crA() const { return fused_crA_ && fused_cr_ && ops_->crA != nullptr && !dims_.grp; }
+
+void Engine::enq_crA(int it, float tol) {
+  const int nbc = plan_.J * ((plan_.Gc + ops_->LPB - 1) / ops_->LPB);
+  // rho part: the window's L^2 entries at four per thread (all G^2 when it is not window-only)
+  const int nbr = std::max(1, std::min(vec_grid_, (dims_.L * dims_.L + 4 * kThreads - 1) / (4 * kThreads)));
+  ops_->crA(s_, nbc + nbr, nbc, dims_, xcg_, r_, p_, ap_, ar_, winv_, twG_, U_, partials_, st_, cr_, it, tol);
 }
 
 void Engine::join_group(int rank, const GroupView& gv, const GroupScal& gs) {
@@ -980,6 +1002,8 @@ double Engine::kernel_bytes(const char* which) const {
   if (w == "colsW") return c8 * (J * L * Gc + 3.0 * (G * G + J * Gc * Gc)) + 16.0 * dims_.H * L * L + 4.0 * Gc * Gc;
   if (w == "cr_xr" || w == "cr_pap") return c8 * 6.0 * (G * G + J * Gc * Gc);
   if (w == "cr_fused") return c8 * 9.0 * (G * G + J * Gc * Gc);  // x,r,p,ap,ar in; x,r,p,ap out
+  // k_crA: the recurrence on the window-only rho and every coil entry, the weights, U's window rows
+  if (w == "crA") return c8 * (9.0 * (L * L + J * Gc * Gc) + J * L * Gc) + 4.0 * Gc * Gc;
   if (w == "apply") {
     // one fused normal-operator application (SURVEY.md §8(d) B_op, window pruned)
     return 8.0 * L * L * (J + 3) + 8.0 * G * G + 16.0 * J * Gc * Gc + 4.0 * Gc * Gc;
@@ -989,7 +1013,11 @@ double Engine::kernel_bytes(const char* which) const {
 
 double Engine::time_kernel(const char* which, int reps) {
   if (!have_cache_) fail(2, "time_kernel: no step cache");
-  const std::string w(which);
+  // "<kernel>:cold": every launch timed on its own after a write of a buffer larger than
+  // L2 (cold-cache operands); otherwise back-to-back launches on L2-resident operands
+  std::string w(which);
+  const bool cold = w.size() > 5 && w.compare(w.size() - 5, 5, ":cold") == 0;
+  if (cold) w.resize(w.size() - 5);
   const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
   const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
   check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
@@ -1014,6 +1042,10 @@ double Engine::time_kernel(const char* which, int reps) {
     } else if (w == "cr_fused") {
       launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_,
                static_cast<const float2*>(ar_), partials_, st_, cr_, 1, 0.f, 0, 0, plan_.G);
+    } else if (w == "crA") {
+      const int nbc = J * tGc;
+      const int nbr = std::max(1, std::min(vec_grid_, (dims_.L * dims_.L + 4 * kThreads - 1) / (4 * kThreads)));
+      ops_->crA(s_, nbc + nbr, nbc, dims_, xcg_, r_, p_, ap_, ar_, winv_, twG_, U_, partials_, st_, cr_, 1, 0.f);
     } else if (w == "cr_pap") {
       launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, p_, ap_, r_, ar_, partials_, st_, cr_, 1);
     } else if (w == "colA") {
@@ -1024,7 +1056,7 @@ double Engine::time_kernel(const char* which, int reps) {
       fail(2, "time_kernel: unknown kernel " + w);
     }
   };
-  if (w.rfind("cr_", 0) == 0) {
+  if (w.rfind("cr", 0) == 0) {
     // scalars of a stationary iteration (iteration 1: b = rar[1]/rar[0] = 0, step
     // a = rar[1]/|ap|^2 = 0 with |ap|^2 = saa[1] = 1 > 0): every launch runs the full
     // vector pass (loads, update, stores, norms) and the values stay finite however
@@ -1042,12 +1074,29 @@ double Engine::time_kernel(const char* which, int reps) {
   cudaEvent_t a, b;
   check_cuda(cudaEventCreate(&a), "event");
   check_cuda(cudaEventCreate(&b), "event");
-  check_cuda(cudaEventRecord(a, s_), "event");
-  for (int i = 0; i < reps; ++i) launch();
-  check_cuda(cudaEventRecord(b, s_), "event");
-  check_cuda(cudaEventSynchronize(b), "event sync");
   float ms = 0;
-  check_cuda(cudaEventElapsedTime(&ms, a, b), "elapsed");
+  if (!cold) {
+    check_cuda(cudaEventRecord(a, s_), "event");
+    for (int i = 0; i < reps; ++i) launch();
+    check_cuda(cudaEventRecord(b, s_), "event");
+    check_cuda(cudaEventSynchronize(b), "event sync");
+    check_cuda(cudaEventElapsedTime(&ms, a, b), "elapsed");
+  } else {
+    const size_t flush_bytes = size_t(256) << 20;  // 2x the 126 MB L2
+    void* flush = nullptr;
+    check_cuda(cudaMalloc(&flush, flush_bytes), "l2 flush buffer");
+    for (int i = 0; i < reps; ++i) {
+      check_cuda(cudaMemsetAsync(flush, i & 0xff, flush_bytes, s_), "l2 flush");
+      check_cuda(cudaEventRecord(a, s_), "event");
+      launch();
+      check_cuda(cudaEventRecord(b, s_), "event");
+      check_cuda(cudaEventSynchronize(b), "event sync");
+      float one = 0;
+      check_cuda(cudaEventElapsedTime(&one, a, b), "elapsed");
+      ms += one;
+    }
+    cudaFree(flush);
+  }
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   // a launch that returned early on a device fault would time nothing

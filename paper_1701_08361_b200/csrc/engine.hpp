@@ -174,6 +174,7 @@ class Engine : public FrameWorker {
   // frames in flight): the five-kernel passes, which share the SMs better
   void set_cluster(bool on);
   bool cluster_supported() const { return RC_ != nullptr; }
+  bool fused_crA() const;  // budget-mode CR solves use k_crA on the five-kernel path
   int line_batch() const;  // lines per block of the pass kernels (channel-group size of k_rows2)
 
   float2* x_dev() { return x_; }
@@ -206,7 +207,8 @@ class Engine : public FrameWorker {
   // the two halves of an application / a Newton-step setup: everything up to the
   // channel-sum partials (front), and the W^-H column pass + rho sum (back). A
   // channel group puts its all-member barrier between them.
-  void enq_apply_front(const float2* dx, int use_halt);
+  // skip_colA: U already holds dx's W^-1 column pass (k_crA wrote it)
+  void enq_apply_front(const float2* dx, int use_halt, bool skip_colA = false);
   void enq_apply_back(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
                       const float2* ap_prev);
   void enq_setup_front(const float2* x);
@@ -216,6 +218,7 @@ class Engine : public FrameWorker {
   void join_group(int rank, const GroupView& gv, const GroupScal& gs);
   void enq_grp_fin(int setup, int op_slot, int cr_slot, float tol);
   void enq_cr_fused(int it, float tol);
+  void enq_crA(int it, float tol);
   void enq_axpy1();
   void enq_state_reset();
   void enq_z_scan();  // st->z_out for the data now in z_ (stream ordered)
@@ -280,8 +283,9 @@ class Engine : public FrameWorker {
   std::vector<int> caps_;       // budget-mode per-step caps
   std::vector<float> alphas_;   // per-step alpha schedule
   bool use_graphs_ = true;
-  bool fused_cr_ = true;
-  int win_only_ok_ = 0;    // the applications being enqueued belong to a fused CR solve   // RTN_FUSED_CR=0 selects the two-kernel recurrence in graphs too
+  bool fused_cr_ = true;   // RTN_FUSED_CR=0 selects the two-kernel recurrence in graphs too
+  bool fused_crA_ = true;  // RTN_CRA=0: k_cr_fused + k_colA instead of k_crA on the pass path
+  int win_only_ok_ = 0;    // the applications being enqueued belong to a fused CR solve
   cudaGraphExec_t step_graph_[kMaxSteps] = {};
   cudaGraphExec_t frame_graph_ = nullptr;
   float2* frame_graph_img_ = nullptr;

@@ -821,6 +821,208 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
   }
 }
 
+// CR step coefficients of iteration `it` of the fused recurrence (k_cr_fused, k_crA):
+// b = rar[it]/rar[it-1] (0 for the priming step), the step denominator |ap|^2 from the
+// previous exact norm and the application's dots, and a = rar[it]/|ap|^2. Returns false
+// (after recording the decision once) when the iteration must not run.
+struct CrCoef {
+  double b, a;
+  bool upd;
+};
+__device__ __forceinline__ bool cr_coef(DevState* st, const CrScalars& cr, int it, float tol, CrCoef& c) {
+  const double rar_new = cr.rar[it];
+  double b = 0.0, denom = cr.saa[0];
+  if (it > 0) {
+    const double rar_old = cr.rar[it - 1];
+    b = (rar_old != 0.0) ? rar_new / rar_old : 0.0;
+    denom = b * b * cr.ap2[it - 1] + 2.0 * b * cr.spa[it] + cr.saa[it];
+  }
+  if (!isfinite(denom) || !isfinite(rar_new)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->status = ST_SOLVER;
+      st->cr_halt = 1;
+    }
+    return false;
+  }
+  if (denom <= 0.0 && tol > 0.0f) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->cr_halt = 1;
+    return false;
+  }
+  c.b = b;
+  c.upd = denom > 0.0;
+  c.a = c.upd ? rar_new / denom : 0.0;
+  return true;
+}
+
+// the single-device epilogue of the fused recurrence (last block): |ap|^2 for the next
+// iteration's denominator, |r|, iteration count, tolerance stop (nlinv.cpp:205-220)
+__device__ __forceinline__ void cr_fused_tail(DevState* st, const CrScalars& cr, int it, float tol,
+                                              double ap2, double r2) {
+  cr.ap2[it] = ap2;
+  const double rn = sqrt(r2);
+  cr.rn[it + 1] = rn;
+  StepRec& s = st->steps[st->cur_step];
+  if (!isfinite(rn)) {
+    st->status = ST_SOLVER;
+    st->cr_halt = 1;
+    return;
+  }
+  s.iters = it + 1;
+  const double target = (double)tol * sqrt(s.rhs_nrm2);
+  if (tol > 0.0f && (rn == 0.0 || rn <= target)) st->cr_halt = 1;
+}
+
+// one CR vector entry of the fused recurrence: p = b p + r; ap = b ap + ar;
+// x += a p; r -= a ap (nlinv.cpp:205-230, the reference's float roundings). Returns r.
+__device__ __forceinline__ float2 cr_update(float2 pv, float2 apv, float2 rv, float2 arv, float2 xv, float bf,
+                                            float af, float naf, bool upd, float2& np, float2& nap,
+                                            float2& nx) {
+  np = make_float2(__fadd_rn(__fmul_rn(pv.x, bf), rv.x), __fadd_rn(__fmul_rn(pv.y, bf), rv.y));
+  nap = make_float2(__fadd_rn(__fmul_rn(apv.x, bf), arv.x), __fadd_rn(__fmul_rn(apv.y, bf), arv.y));
+  if (!upd) return rv;
+  nx = axpy_rn(xv, af, np);
+  return axpy_rn(rv, naf, nap);
+}
+
+// Fused CR recurrence of iteration `it` (as k_cr_fused) + the W^-1 column pass (k_colA)
+// of the next application, whose operand is the updated residual r. Blocks [0, nbc) own
+// one (channel j, coil column tile) as k_colA does: each thread updates the CR vectors on
+// the coil entries of its column's step-1 subsequence and transforms r_new * winv
+// straight from its registers into U. Blocks [nbc, grid) update the rho entries (the
+// window only when the step's setup left them zero outside, rho_window_only). The same
+// values as k_cr_fused followed by k_colA: one launch, and the r re-read, fewer per
+// iteration.
+template <class Geo>
+__global__ void RTNB_PASS_BOUNDS k_crA(Dims d, float2* __restrict__ x, float2* __restrict__ r,
+                                       float2* __restrict__ p, float2* __restrict__ ap,
+                                       const float2* __restrict__ ar, const float* __restrict__ winv,
+                                       const float4* __restrict__ twG, float2* __restrict__ U, int nbc,
+                                       double* partials, DevState* st, CrScalars cr, int it, float tol) {
+  pdl_enter();
+  if (st->status || st->cr_halt) return;
+  CrCoef c;
+  if (!cr_coef(st, cr, it, tol, c)) return;
+  const float bf = (float)c.b, af = (float)c.a, naf = (float)(-c.a);
+  double acc_ap = 0.0, acc_r = 0.0;
+  extern __shared__ float2 A[];
+  constexpr int G = Geo::G, N1 = Geo::N1, N2 = Geo::N2;
+  const int G2 = G * G;
+  if ((int)blockIdx.x < nbc) {
+    const Item<Geo, true> i1(threadIdx.x, N2), i2(threadIdx.x, N1);
+    const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
+    const int j = blockIdx.x / tiles;
+    const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
+    const int nl = min(Geo::LPB, d.Gc - q0);
+    const size_t cbase = (size_t)G2 + (size_t)j * d.Gc * d.Gc;
+    if (i1.on && i1.l < nl) {
+      const int q = q0 + i1.l;
+      float2 v[N1];
+#pragma unroll
+      for (int n1 = 0; n1 < N1; ++n1) v[n1] = make_float2(0.f, 0.f);
+      // the CR update of entry (k-row i, column q), step-1 slot n1; returns r_new * winv
+      auto entry = [&](int n1, float2 pv, float2 apv, float2 rv, float2 arv, float2 xv) {
+        const int t = N2 * n1 + i1.k;
+        const int i = t - d.off;
+        const size_t e = cbase + (size_t)i * d.Gc + q;
+        float2 np, nap, nx;
+        const float2 nr = cr_update(pv, apv, rv, arv, xv, bf, af, naf, c.upd, np, nap, nx);
+        p[e] = np;
+        ap[e] = nap;
+        if (c.upd) {
+          x[e] = nx;
+          r[e] = nr;
+        }
+        acc_ap += nrm2(nap);
+        acc_r += nrm2(nr);
+        const float w = winv[i * d.Gc + q];
+        v[n1] = flip(make_float2(nr.x * w, nr.y * w), t);  // chat * winv.real() (nlinv.cpp:121)
+      };
+      constexpr uint32_t BAND = Geo::GC_N1;
+      if (BAND != Geo::ALL_N1 && d.Gc * 4 == G) {
+        // the coil band's step-1 slots are compile-time: every load issued up front
+        constexpr int B0 = __builtin_ctz(BAND), BN = __builtin_popcount(BAND);
+        float2 pv[BN], apv[BN], rv[BN], arv[BN], xv[BN];
+#pragma unroll
+        for (int b = 0; b < BN; ++b) {
+          const size_t e = cbase + (size_t)(N2 * (B0 + b) + i1.k - d.off) * d.Gc + q;
+          pv[b] = p[e];
+          apv[b] = ap[e];
+          rv[b] = r[e];
+          arv[b] = ar[e];
+          xv[b] = c.upd ? x[e] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int b = 0; b < BN; ++b) entry(B0 + b, pv[b], apv[b], rv[b], arv[b], xv[b]);
+        fft_step1<Geo, +1, BAND>(v, i1.k, twG);
+      } else {
+#pragma unroll
+        for (int n1 = 0; n1 < N1; ++n1) {
+          const int i = N2 * n1 + i1.k - d.off;
+          if (i >= 0 && i < d.Gc) {
+            const size_t e = cbase + (size_t)i * d.Gc + q;
+            entry(n1, p[e], ap[e], r[e], ar[e], c.upd ? x[e] : make_float2(0.f, 0.f));
+          }
+        }
+        fft_step1<Geo, +1>(v, i1.k, twG);
+      }
+      park_step1<Geo>(A, i1.l, i1.k, v);
+    }
+    __syncthreads();
+    if (i2.on && i2.l < nl) {
+      float2 u[N2];
+      fft_step2<Geo, +1, Geo::WIN_K2>(A, i2.l, i2.k, u);  // window rows of U
+      float2* dst = U + (size_t)j * G * d.Gc + q0 + i2.l;
+#pragma unroll
+      for (int k2 = 0; k2 < N2; ++k2) {
+        const int pp = i2.k + N1 * k2;
+        if (pp >= d.lo && pp < d.lo + d.L) dst[(size_t)pp * d.Gc] = flip(u[k2], pp);
+      }
+    }
+  } else {
+    const bool win_only = rho_window_only(st);
+    const int L = d.L, lo = d.lo;
+    const int nv = win_only ? L * L : G2;
+    constexpr int kU = 4;
+    const int nbr = gridDim.x - nbc;
+    const int stride = nbr * blockDim.x;
+    for (int v0 = (blockIdx.x - nbc) * blockDim.x + threadIdx.x; v0 < nv; v0 += kU * stride) {
+      int idx[kU];
+      float2 pv[kU], apv[kU], rv[kU], arv[kU], xv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int v = v0 + u * stride;
+        int i = v < nv ? v : -1;
+        if (win_only && i >= 0) i = (lo + v / L) * G + lo + (v - (v / L) * L);
+        idx[u] = i;
+        if (i >= 0) {
+          pv[u] = p[i];
+          apv[u] = ap[i];
+          rv[u] = r[i];
+          arv[u] = ar[i];
+          if (c.upd) xv[u] = x[i];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = idx[u];
+        if (i < 0) continue;
+        float2 np, nap, nx;
+        const float2 nr = cr_update(pv[u], apv[u], rv[u], arv[u], xv[u], bf, af, naf, c.upd, np, nap, nx);
+        p[i] = np;
+        ap[i] = nap;
+        if (c.upd) {
+          x[i] = nx;
+          r[i] = nr;
+        }
+        acc_ap += nrm2(nap);
+        acc_r += nrm2(nr);
+      }
+    }
+  }
+  double vv[2] = {acc_ap, acc_r}, tot[2];
+  if (grid_reduce<2>(vv, partials, &st->counter, tot) && threadIdx.x == 0) cr_fused_tail(st, cr, it, tol, tot[0], tot[1]);
+}
+
 #ifndef RTNB_PASS_ONLY  // non-template kernels: compiled once (engine.cu)
 // ---------------------------------------------------------------------------------
 // CR recurrences (nlinv.cpp:197-232). D = G*G + J*Gc*Gc complex entries.
@@ -951,27 +1153,9 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
                                                        int rho_skip, int grp, int G) {
   pdl_enter();
   if (st->status || st->cr_halt) return;
-  const double rar_new = cr.rar[it];
-  double b = 0.0, denom = cr.saa[0];
-  if (it > 0) {
-    const double rar_old = cr.rar[it - 1];
-    b = (rar_old != 0.0) ? rar_new / rar_old : 0.0;
-    denom = b * b * cr.ap2[it - 1] + 2.0 * b * cr.spa[it] + cr.saa[it];
-  }
-  if (!isfinite(denom) || !isfinite(rar_new)) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      st->status = ST_SOLVER;
-      st->cr_halt = 1;
-    }
-    return;
-  }
-  if (denom <= 0.0 && tol > 0.0f) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->cr_halt = 1;
-    return;
-  }
-  const bool upd = denom > 0.0;
-  const double a = upd ? rar_new / denom : 0.0;
-  const float bf = (float)b, af = (float)a, naf = (float)(-a);
+  CrCoef c;
+  if (!cr_coef(st, cr, it, tol, c)) return;
+  const float bf = (float)c.b, af = (float)c.a, naf = (float)(-c.a);
   double acc_ap = 0.0, acc_r = 0.0;
   // rho entries outside the window are exactly zero in every vector: skip them
   const bool win_only = rho_window_only(st);
@@ -995,22 +1179,19 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
         apv[u] = ap[i];
         rv[u] = r[i];
         arv[u] = ar[i];
-        if (upd) xv[u] = x[i];
+        if (c.upd) xv[u] = x[i];
       }
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int i = idx[u];
       if (i < 0) continue;
-      const float2 np = make_float2(__fadd_rn(__fmul_rn(pv[u].x, bf), rv[u].x), __fadd_rn(__fmul_rn(pv[u].y, bf), rv[u].y));
-      const float2 nap =
-          make_float2(__fadd_rn(__fmul_rn(apv[u].x, bf), arv[u].x), __fadd_rn(__fmul_rn(apv[u].y, bf), arv[u].y));
+      float2 np, nap, nx;
+      const float2 nr = cr_update(pv[u], apv[u], rv[u], arv[u], xv[u], bf, af, naf, c.upd, np, nap, nx);
       p[i] = np;
       ap[i] = nap;
-      float2 nr = rv[u];
-      if (upd) {
-        x[i] = axpy_rn(xv[u], af, np);
-        nr = axpy_rn(rv[u], naf, nap);
+      if (c.upd) {
+        x[i] = nx;
         r[i] = nr;
       }
       if (i >= rho_skip) {  // group members other than the first skip the replicated rho
@@ -1026,18 +1207,7 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
       cr.pcr[2 * it + 1] = tot[1];
       return;
     }
-    cr.ap2[it] = tot[0];
-    const double rn = sqrt(tot[1]);
-    cr.rn[it + 1] = rn;
-    StepRec& s = st->steps[st->cur_step];
-    if (!isfinite(rn)) {
-      st->status = ST_SOLVER;
-      st->cr_halt = 1;
-      return;
-    }
-    s.iters = it + 1;
-    const double target = (double)tol * sqrt(s.rhs_nrm2);
-    if (tol > 0.0f && (rn == 0.0 || rn <= target)) st->cr_halt = 1;
+    cr_fused_tail(st, cr, it, tol, tot[0], tot[1]);
   }
 }
 

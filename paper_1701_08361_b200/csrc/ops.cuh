@@ -28,6 +28,9 @@ struct Engine::Ops {
                 const double2*, const float2*, const float2*, int, double*, DevState*, CrScalars, int,
                 const GroupView&) = nullptr;
   void (*fft)(cudaStream_t, int, int, float2*, int, int, const float4*, float) = nullptr;
+  // CR recurrence + the next application's W^-1 column pass (k_crA)
+  void (*crA)(cudaStream_t, int grid, int nbc, Dims, float2*, float2*, float2*, float2*, const float2*,
+              const float*, const float4*, float2*, double*, DevState*, CrScalars, int, float) = nullptr;
   // whole application per channel in one thread-block cluster (kernels_cluster.cuh);
   // nullptr where not instantiated (grid, tail, CTA count per channel)
   void (*apply_cluster)(cudaStream_t, int J, Dims, ColsWArgs, const float*, const float4*, const float2*,
@@ -95,6 +98,7 @@ struct Inst {
                                     static_cast<int>(kSmem2)),
                "attr rows2");
     check_cuda(cudaFuncSetAttribute(k_colsW<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsW");
+    check_cuda(cudaFuncSetAttribute(k_crA<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr crA");
     check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
     check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, +1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr ifft");
     check_cuda(cudaFuncSetAttribute(k_fft_pass<Geo, -1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr fft");
@@ -140,6 +144,11 @@ Engine::Ops Inst<N1, N2>::make() {
                const float2* Y, const double2* RP, const float2* coils, const float2* z, int nbw,
                double* partials, DevState* st, CrScalars cr, int h, const GroupView& gv) {
     launch_k(k_colsW<Geo>, grid, kNT, kSmem, s, d, a, winv, tw, Y, RP, coils, z, nbw, partials, st, cr, h, gv);
+  };
+  o.crA = [](cudaStream_t s, int grid, int nbc, Dims d, float2* x, float2* r, float2* p, float2* ap,
+             const float2* ar, const float* winv, const float4* tw, float2* U, double* partials, DevState* st,
+             CrScalars cr, int it, float tol) {
+    launch_k(k_crA<Geo>, grid, kNT, kSmem, s, d, x, r, p, ap, ar, winv, tw, U, nbc, partials, st, cr, it, tol);
   };
   o.fft = [](cudaStream_t s, int grid, int sign, float2* data, int batch, int axis, const float4* tw,
              float scale) {

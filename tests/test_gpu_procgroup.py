@@ -67,7 +67,7 @@ def test_two_process_channel_group_matches_in_process_group_and_reference(gpu, r
             if p.is_alive():
                 p.kill()
     for r in res:
-        assert r[1] is not "error", r
+        assert not isinstance(r[1], str), r
     (_, img0, est0, cg0, replay0), (_, img1, est1, cg1, replay1) = res
     assert replay0 and replay1
     assert np.array_equal(img0, img1) and np.array_equal(est0, est1) and cg0 == cg1
@@ -103,7 +103,7 @@ def _member_absent(rank, world, port, plan_args, z, P, q):
             try:
                 ctx.reconstruct_frame(pb.initial_estimate(plan))
                 q.put((rank, "no error", time.time() - t0))
-            except pb.SolverError as e:
+            except pb.DecompFault:
                 q.put((rank, "DecompFault", time.time() - t0))
         else:
             time.sleep(25)
