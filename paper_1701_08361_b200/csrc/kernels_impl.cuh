@@ -44,6 +44,11 @@ __device__ __forceinline__ float2 flip(float2 v, int t) {
 __device__ __forceinline__ bool in_win(const Dims& d, int r, int c) {
   return r >= d.lo && r < d.lo + d.L && c >= d.lo && c < d.lo + d.L;
 }
+// the same with the window of a compile-time grid side (Dims: L = G/2, lo = (G - L)/2 = G/4)
+template <int G>
+__device__ __forceinline__ bool in_win_c(int r, int c) {
+  return r >= G / 4 && r < G / 4 + G / 2 && c >= G / 4 && c < G / 4 + G / 2;
+}
 // exact IEEE float ops (no contraction) where the reference's rounding is mirrored
 __device__ __forceinline__ float2 axpy_rn(float2 y, float a, float2 x) {
   return make_float2(__fadd_rn(y.x, __fmul_rn(a, x.x)), __fadd_rn(y.y, __fmul_rn(a, x.y)));
@@ -149,6 +154,14 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
 #define RTNB_MINB_LIGHT 4
 #endif
 #define RTNB_PASS_BOUNDS_LIGHT __launch_bounds__(Geo::NT, (RTNB_MINB_LIGHT * 256 + Geo::NT - 1) / Geo::NT)
+// per-kernel residency targets (256-thread blocks per SM) of the heavy passes
+#ifndef RTNB_MINB_ROWS1
+#define RTNB_MINB_ROWS1 RTNB_MINB
+#endif
+#ifndef RTNB_MINB_CRA
+#define RTNB_MINB_CRA RTNB_MINB
+#endif
+#define RTNB_BOUNDS_N(M) __launch_bounds__(Geo::NT, ((M) * 256 + Geo::NT - 1) / Geo::NT)
 
 template <class Geo, bool COLS>
 constexpr int kRowStride = (!COLS && 32 % Geo::NMAX == 0) ? Geo::NMAX : 0;
@@ -158,8 +171,11 @@ constexpr int kRowStride = (!COLS && 32 % Geo::NMAX == 0) ? Geo::NMAX : 0;
   const Item<Geo, COLS_> i1(threadIdx.x, Geo::N2, kRowStride<Geo, COLS_>); \
   const Item<Geo, COLS_> i2(threadIdx.x, Geo::N1, kRowStride<Geo, COLS_>); \
   constexpr int G = Geo::G, N1 = Geo::N1, N2 = Geo::N2;         \
+  constexpr int LO = G / 4, LW = G / 2; /* window (Dims lo, L) */ \
   (void)N1;                                                     \
-  (void)N2
+  (void)N2;                                                     \
+  (void)LO;                                                     \
+  (void)LW
 
 // Barrier between the steps of a row-pass transform. A row line owns the same NMAX
 // consecutive thread slots in both steps (kRowStride); when NMAX divides 32 every line stays
@@ -244,7 +260,7 @@ enum Rows1Mode : int { R1_DECODE = 0, R1_OP = 1, R1_SETUP = 2 };
 //          forward row FFT -> V_j (L x G).
 //  SETUP:  window rows: t = rho*c_j (nlinv.cpp:252) -> forward row FFT -> V_j.
 template <class Geo>
-__global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restrict__ twG,
+__global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const float4* __restrict__ twG,
                                                    const float2* __restrict__ U,
                                                    const float2* __restrict__ coils,
                                                    const float2* __restrict__ rhom,
@@ -256,8 +272,8 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restr
   pdl_enter();
   if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(false);
-  const int nrows = (mode == R1_DECODE) ? G : d.L;
-  const int row0 = (mode == R1_DECODE) ? 0 : d.lo;
+  const int nrows = (mode == R1_DECODE) ? G : LW;
+  const int row0 = (mode == R1_DECODE) ? 0 : LO;
   const int tiles = (nrows + Geo::LPB - 1) / Geo::LPB;
   const int j = blockIdx.x / tiles;
   const int rl0 = (blockIdx.x - j * tiles) * Geo::LPB;
@@ -298,7 +314,7 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restr
           out[p] = cscale(flip(u[k2], p), d.invG);
           if (j == 0) {
             const float2 x = rho_src[(size_t)r2 * G + p];
-            rhom_out[(size_t)r2 * G + p] = in_win(d, r2, p) ? x : make_float2(0.f, 0.f);
+            rhom_out[(size_t)r2 * G + p] = in_win_c<G>(r2, p) ? x : make_float2(0.f, 0.f);
           }
         }
       } else {
@@ -306,7 +322,7 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restr
         for (int k2 = 0; k2 < N2; ++k2) {
           const int p = i2.k + N1 * k2;
           float2 w = make_float2(0.f, 0.f);
-          if (p >= d.lo && p < d.lo + d.L) {
+          if (p >= LO && p < LO + LW) {
             const size_t e = (size_t)r2 * G + p;
             const float2 aw = cscale(flip(u[k2], p), d.invG);
             // t = c_j * drho + rho * (W^-1 dchat_j)   (nlinv.cpp:163)
@@ -326,7 +342,7 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restr
     if (a1) {
       get_step1<Geo>(A, i1.l, i1.k, v);
       dft_m<N1, -1, Geo::ALL_N1, Geo::ALL_N1>(v);
-      float2* Vr = V + (size_t)j * d.L * G + (size_t)(rl0 + i1.l) * G;
+      float2* Vr = V + (size_t)j * LW * G + (size_t)(rl0 + i1.l) * G;
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) {
         const int t = N2 * n1 + i1.k;
@@ -341,7 +357,7 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restr
       for (int n1 = 0; n1 < N1; ++n1) {
         const int t = N2 * n1 + i1.k;
         v[n1] = make_float2(0.f, 0.f);
-        if (t >= d.lo && t < d.lo + d.L) {
+        if (t >= LO && t < LO + LW) {
           const size_t e = (size_t)r1 * G + t;
           v[n1] = flip(cmul_rn(rhom[e], cj[e]), t);  // e = rho * c_j   (nlinv.cpp:252)
         }
@@ -355,7 +371,7 @@ __global__ void RTNB_PASS_BOUNDS k_rows1(Dims d, int mode, const float4* __restr
     if (a2) {
       float2 u[N2];
       fft_step2<Geo, -1>(A, i2.l, i2.k, u);
-      float2* Vr = V + (size_t)j * d.L * G + (size_t)(rl0 + i2.l) * G;
+      float2* Vr = V + (size_t)j * LW * G + (size_t)(rl0 + i2.l) * G;
 #pragma unroll
       for (int k2 = 0; k2 < N2; ++k2) {
         const int p = i2.k + N1 * k2;
@@ -379,14 +395,14 @@ __global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
   const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
   const int nl = min(Geo::LPB, G - q0);
   const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
-  float2* Vj = V + (size_t)j * d.L * G;
+  float2* Vj = V + (size_t)j * LW * G;
   float2 v[N1];
   if (a1) {
     const float2* col = Vj + q0 + i1.l;
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) {
       const int t = N2 * n1 + i1.k;
-      v[n1] = (t >= d.lo && t < d.lo + d.L) ? flip(col[(size_t)(t - d.lo) * G], t) : make_float2(0.f, 0.f);
+      v[n1] = (t >= LO && t < LO + LW) ? flip(col[(size_t)(t - LO) * G], t) : make_float2(0.f, 0.f);
     }
     fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
@@ -416,7 +432,7 @@ __global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) {
       const int t = N2 * n1 + i1.k;
-      if (t >= d.lo && t < d.lo + d.L) col[(size_t)(t - d.lo) * G] = flip(v[n1], t);
+      if (t >= LO && t < LO + LW) col[(size_t)(t - LO) * G] = flip(v[n1], t);
     }
   }
 }
@@ -507,16 +523,16 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
   RTNB_TILE_SETUP(false);
   constexpr int L = G / 2;
   float2* RCs = A + Geo::SMEM_FLOAT2;  // LPB x L channel terms of this row
-  const int rl = blockIdx.x % d.L;
-  const int h = blockIdx.x / d.L;
-  const int r = d.lo + rl;
+  const int rl = blockIdx.x % LW;
+  const int h = blockIdx.x / LW;
+  const int r = LO + rl;
   const int j0 = h * Geo::LPB;
   const int nl = min(Geo::LPB, d.J - j0);
   const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
   double resid = 0.0;
   float2 v[N1];
   if (a1) {
-    const float2* Vr = V + (size_t)(j0 + i1.l) * d.L * G + (size_t)rl * G;
+    const float2* Vr = V + (size_t)(j0 + i1.l) * LW * G + (size_t)rl * G;
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) {
       const int t = N2 * n1 + i1.k;
@@ -537,14 +553,14 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
     for (int k2 = 0; k2 < N2; ++k2) {
       const int p = i2.k + N1 * k2;
       float2 w = make_float2(0.f, 0.f);
-      if (p >= d.lo && p < d.lo + d.L) {
+      if (p >= LO && p < LO + LW) {
         float2 T = cscale(flip(u[k2], p), d.invG);
         if (setup) {
           const float2 zz = zj[p];
           T = make_float2(__fsub_rn(zz.x, T.x), __fsub_rn(zz.y, T.y));
           resid += nrm2(T);
         }
-        RCs[i2.l * L + (p - d.lo)] = cjmul_rn(cj[p], T);
+        RCs[i2.l * L + (p - LO)] = cjmul_rn(cj[p], T);
         w = flip(cjmul_rn(rr[p], T), p);
       }
       u[k2] = w;
@@ -562,7 +578,7 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
       } else {
         dft_m<N1, -1, Geo::ALL_N1, Geo::ALL_N1>(v);
       }
-      float2* Yr = Y + (size_t)(j0 + i1.l) * d.L * d.Gc + (size_t)rl * d.Gc;
+      float2* Yr = Y + (size_t)(j0 + i1.l) * LW * d.Gc + (size_t)rl * d.Gc;
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) {
         const int p = N2 * n1 + i1.k;
@@ -587,7 +603,7 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
       } else {
         fft_step2<Geo, -1>(A, i2.l, i2.k, u);
       }
-      float2* Yr = Y + (size_t)(j0 + i2.l) * d.L * d.Gc + (size_t)rl * d.Gc;
+      float2* Yr = Y + (size_t)(j0 + i2.l) * LW * d.Gc + (size_t)rl * d.Gc;
 #pragma unroll
       for (int k2 = 0; k2 < N2; ++k2) {
         const int p = i2.k + N1 * k2;
@@ -599,14 +615,14 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
   // the group's channel terms, summed in channel order once every line has written them
   // (the block's only barrier between its lines, placed after both transforms)
   __syncthreads();
-  if ((int)threadIdx.x < d.L) {
+  if ((int)threadIdx.x < LW) {
     double sx = 0.0, sy = 0.0;
     for (int l = 0; l < nl; ++l) {
       const float2 t = RCs[l * L + threadIdx.x];
       sx += t.x;
       sy += t.y;
     }
-    RP[((size_t)h * d.L + rl) * d.L + threadIdx.x] = make_double2(sx, sy);
+    RP[((size_t)h * LW + rl) * LW + threadIdx.x] = make_double2(sx, sy);
   }
   if (setup) {
     double vv[1] = {resid}, tot[1];
@@ -660,12 +676,12 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
       }
     }
     if (a1) {
-      const float2* col = Y + (size_t)j * d.L * d.Gc + q0 + i1.l;
+      const float2* col = Y + (size_t)j * LW * d.Gc + q0 + i1.l;
       float2 v[N1];
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) {
         const int t = N2 * n1 + i1.k;
-        v[n1] = (t >= d.lo && t < d.lo + d.L) ? flip(col[(size_t)(t - d.lo) * d.Gc], t) : make_float2(0.f, 0.f);
+        v[n1] = (t >= LO && t < LO + LW) ? flip(col[(size_t)(t - LO) * d.Gc], t) : make_float2(0.f, 0.f);
       }
       fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
       park_step1<Geo>(A, i1.l, i1.k, v);
@@ -711,13 +727,13 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
     const int H = d.H;
     double dummy0 = 0.0, dummy1 = 0.0, dummy2 = 0.0;
     const bool win_only = a.mode != CW_SETUP && a.win_only_ok && rho_window_only(st);
-    const int nv = win_only ? d.L * d.L : D0;
+    const int nv = win_only ? LW * LW : D0;
     int nz = 0;  // SETUP: a nonzero rhs.rho entry outside the window
     for (int v = (blockIdx.x - nbw) * blockDim.x + threadIdx.x; v < nv; v += (gridDim.x - nbw) * blockDim.x) {
       int e, r, c;
       if (win_only) {
-        r = d.lo + v / d.L;
-        c = d.lo + v - (v / d.L) * d.L;
+        r = LO + v / LW;
+        c = LO + v - (v / LW) * LW;
         e = r * G + c;
       } else {
         e = v;
@@ -728,11 +744,11 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
       if (d.grp) {
         // channel decomposition: every member's partials, in member order, loaded
         // from the peers' memory (the all_reduce_sum of decomp.cpp:26-39)
-        if (in_win(d, r, c)) {
-          const size_t w = (size_t)(r - d.lo) * d.L + (c - d.lo);
+        if (in_win_c<G>(r, c)) {
+          const size_t w = (size_t)(r - LO) * LW + (c - LO);
           for (int m = 0; m < gv.A; ++m) {
             for (int h = 0; h < gv.h[m]; ++h) {
-              const double2 t = __ldcg(gv.rp[m] + (size_t)h * d.L * d.L + w);
+              const double2 t = __ldcg(gv.rp[m] + (size_t)h * LW * LW + w);
               sx += t.x;
               sy += t.y;
             }
@@ -751,7 +767,7 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
         } else {
           o = finish_elem(a, (size_t)e, make_float2((float)sx, (float)sy), dummy0, dummy1, dummy2);
         }
-        if (a.mode == CW_SETUP && !in_win(d, r, c) && (o.x != 0.f || o.y != 0.f)) nz = 1;
+        if (a.mode == CW_SETUP && !in_win_c<G>(r, c) && (o.x != 0.f || o.y != 0.f)) nz = 1;
         continue;
       }
       const bool opm = a.mode != CW_SETUP;
@@ -760,10 +776,10 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
         pdx = a.dx[e];
         if (a.ap_prev) pap = a.ap_prev[e];
       }
-      if (in_win(d, r, c)) {
-        const double2* src = RP + (size_t)(r - d.lo) * d.L + (c - d.lo);
+      if (in_win_c<G>(r, c)) {
+        const double2* src = RP + (size_t)(r - LO) * LW + (c - LO);
         for (int h = 0; h < H; ++h) {
-          const double2 t = src[(size_t)h * d.L * d.L];
+          const double2 t = src[(size_t)h * LW * LW];
           sx += t.x;
           sy += t.y;
         }
@@ -779,7 +795,7 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
       const float2 n = make_float2((float)sx, (float)sy);
       const float2 o = opm ? finish_op(a, (size_t)e, n, pdx, pap, acc0, aa, pa)
                            : finish_elem(a, (size_t)e, n, acc0, aa, pa);
-      if (a.mode == CW_SETUP && !in_win(d, r, c) && (o.x != 0.f || o.y != 0.f)) nz = 1;
+      if (a.mode == CW_SETUP && !in_win_c<G>(r, c) && (o.x != 0.f || o.y != 0.f)) nz = 1;
     }
     if (a.mode == CW_SETUP && __syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&st->rho_out_nz, 1);
   }
@@ -893,7 +909,7 @@ __device__ __forceinline__ float2 cr_update(float2 pv, float2 apv, float2 rv, fl
 // values as k_cr_fused followed by k_colA: one launch, and the r re-read, fewer per
 // iteration.
 template <class Geo>
-__global__ void RTNB_PASS_BOUNDS k_crA(Dims d, float2* __restrict__ x, float2* __restrict__ r,
+__global__ void RTNB_BOUNDS_N(RTNB_MINB_CRA) k_crA(Dims d, float2* __restrict__ x, float2* __restrict__ r,
                                        float2* __restrict__ p, float2* __restrict__ ap,
                                        const float2* __restrict__ ar, const float* __restrict__ winv,
                                        const float4* __restrict__ twG, float2* __restrict__ U, int nbc,
@@ -905,7 +921,7 @@ __global__ void RTNB_PASS_BOUNDS k_crA(Dims d, float2* __restrict__ x, float2* _
   const float bf = (float)c.b, af = (float)c.a, naf = (float)(-c.a);
   double acc_ap = 0.0, acc_r = 0.0;
   extern __shared__ float2 A[];
-  constexpr int G = Geo::G, N1 = Geo::N1, N2 = Geo::N2;
+  constexpr int G = Geo::G, N1 = Geo::N1, N2 = Geo::N2, LO = G / 4, LW = G / 2;
   const int G2 = G * G;
   if ((int)blockIdx.x < nbc) {
     const Item<Geo, true> i1(threadIdx.x, N2), i2(threadIdx.x, N1);
@@ -975,12 +991,12 @@ __global__ void RTNB_PASS_BOUNDS k_crA(Dims d, float2* __restrict__ x, float2* _
 #pragma unroll
       for (int k2 = 0; k2 < N2; ++k2) {
         const int pp = i2.k + N1 * k2;
-        if (pp >= d.lo && pp < d.lo + d.L) dst[(size_t)pp * d.Gc] = flip(u[k2], pp);
+        if (pp >= LO && pp < LO + LW) dst[(size_t)pp * d.Gc] = flip(u[k2], pp);
       }
     }
   } else {
     const bool win_only = rho_window_only(st);
-    const int L = d.L, lo = d.lo;
+    const int L = LW, lo = LO;
     const int nv = win_only ? L * L : G2;
     constexpr int kU = 4;
     const int nbr = gridDim.x - nbc;

@@ -31,6 +31,8 @@ if os.environ.get("RTN_SCHED"):  # "l,o" override of the reference default for_t
     sched = pb.TemporalSchedule(*[int(v) for v in os.environ["RTN_SCHED"].split(",")])
 for T, A in pairs:
     o = pb.SeriesOptions(T=T, A=A, plain=(T == 1), sched=sched)
+    if os.environ.get("RTN_SERIES_CLUSTER"):  # 1 / 0: force the cluster-fused applications on / off
+        o.cluster = int(os.environ["RTN_SERIES_CLUSTER"])
     s.run(o, first=0, count=8, want_images=False)
     out = s.run(o, first=8, count=16, want_images=False)
     ms = s.last_span_ms() / 16
