@@ -246,6 +246,17 @@ def launches_per_frame(caps, M, cra=False):
     return n + 3
 
 
+def launches_per_frame_group(caps, M, A):
+    """kernels one frame launches on a channel group of A members (group.cu enqueue order,
+    all members): per step and member 1 step_begin + 2 decode + 3 setup passes + 1
+    k_rho_out + 1 k_colsW + 1 k_grp_fin + cap x (5 apply passes + k_grp_fin + k_cr_fused)
+    + 1 closing k_grp_fin + 1 axpy; then per member 2 decode + 1 k_coil_ss, + 1 k_image_grp"""
+    n = 0
+    for m in range(M):
+        n += A * (1 + 2 + 3 + 1 + 1 + 1 + 7 * caps[m] + (1 if caps[m] else 0) + 1)
+    return n + 3 * A + 1
+
+
 def dist_setup(n_gpus, backend=None):
     """one process per GPU (torchrun env); NCCL on GPUs, gloo for the CPU tests"""
     rank, world, local = 0, 1, 0
@@ -457,39 +468,104 @@ def check_timed_frames(pb, series, plan, frames, P, U, audit, first, n_check):
             "oracle": "oracle/_ref reconstruct_frame with the audited per-step sources (device estimates)"}
 
 
-def decompositions(pb, plan, frames, P, U, sched, ngpu):
-    """fps and p50 frame latency of each decomposition over ngpu GPUs (device time,
-    CUDA events spanning every worker stream), plus the autotuner's hybrid pick"""
-    F = frames.shape[0]
+def e2e_raw(pb, make_series, plan, opts, cfg, F, S, world, local):
+    """frames/s end to end through the public series call: raw acquisitions (J x K x S
+    samples per frame) from pinned host memory through rtn_series_run_raw -- H2D, device
+    pre stage (gridding, cached PSFs, normalisation), reconstruction, images D2H to pinned
+    host -- all inside the timed region (wall clock, max over ranks). world = the ranks
+    that call it together (each its own series: weak scaling); a single series over
+    several GPUs is called on rank 0 alone with world = 1"""
+    import torch
+    G, J, K, U, _ = CONFIGS[cfg]
+    raw, angles = synth_raw(G, J, K, U, n_unique=U)
+    Ssp = raw.shape[-1]
+    FR = F + S  # one more range of S frames: the untimed e2e warm-up range
+    rt = torch.empty((FR, J, K, Ssp), dtype=torch.complex64, pin_memory=True)
+    rt.numpy()[:] = np.stack([raw[n % U] for n in range(FR)])
+    ang = np.stack([angles[n % U] for n in range(FR)])
+    imt = torch.empty((FR, plan.N, plan.N), dtype=torch.complex64, pin_memory=True)
+    fb = rt[0].numel() * 8  # bytes of one raw frame
+    ib = plan.N * plan.N * 8
+    rs = make_series(FR)  # its own store and PSF cache
+    # frames [0, F - S) prime the chain, the normalisation scale, the PSF cache and the
+    # grid plans; the next S frames are the untimed e2e warm-up; the S after them are timed
+    T0 = F - S
+    rs.run(opts, first=0, count=T0, raw=dict(samples_ptr=rt.data_ptr(), S=Ssp, angles=ang[:T0]),
+           images_ptr=imt.data_ptr())
+    rs.run(opts, first=T0, count=S, raw=dict(samples_ptr=rt.data_ptr() + T0 * fb, S=Ssp, angles=ang[T0:T0 + S]),
+           images_ptr=imt.data_ptr() + T0 * ib)
+    T0 += S
+    raw_in = dict(samples_ptr=rt.data_ptr() + T0 * fb, S=Ssp, angles=ang[T0:T0 + S])
+    barrier(world, local)
+    t0 = time.perf_counter()
+    rs.run(opts, first=T0, count=S, raw=raw_in, images_ptr=imt.data_ptr() + T0 * ib)
+    wall = time.perf_counter() - t0
+    print(f"[bench] e2e wall {wall * 1e3:.1f} ms, device span {rs.last_span_ms():.1f} ms", file=sys.stderr,
+          flush=True)
+    barrier(world, local)
+    wall = max_over_ranks(wall, world, local)
+    rs.close()
+    return {"value": world * S / wall, "unit": "frames/s",
+            "h2d_bytes_per_step": J * K * Ssp * 8, "d2h_bytes_per_step": plan.N * plan.N * 8,
+            "path": "rtn_series_run_raw: pinned raw samples H2D on the copy stream, device gridding + "
+                    "cached PSFs + normalisation, reconstruction, images D2H to pinned host (wall clock)"}
+
+
+def single_series_multi_gpu(pb, plan, frames, P, U, sched, ngpu, cfg, W, S, with_e2e):
+    """The N > 1 headline: ONE acquisition (one frame series) reconstructed by all ngpu GPUs
+    of the node under the paper's decompositions -- channel groups over NVLink peer memory,
+    temporal decomposition, and the hybrid the autotuner picks (autotune.cpp:49-88 over
+    legal_configs) -- driven from rank 0 in one process (the reference's thread-per-worker
+    model; worker t's members on devices (t*A + k) % ngpu). Device time (CUDA events
+    spanning every worker stream) for the fps and p50 latency of each decomposition; the
+    selected hybrid is then timed on S frames (the headline, strong scaling) and end to end
+    through rtn_series_run_raw on the same devices."""
     nvis = pb.load_library().rtn_device_count()
-    s = pb.Series(pb.Context(plan, device=0), F, U, devices=[k % nvis for k in range(ngpu)])
+    devices = [k % nvis for k in range(ngpu)]
+    F = frames.shape[0]
+    s = pb.Series(pb.Context(plan, device=0), F, U, devices=devices)
     s.upload_frames(frames)
     for k in range(U):
         s.upload_psf(k, P[k])
     s.set_psf_index([n % U for n in range(F)])
     s.normalize()
-    nw, nt = min(6, F // 3), min(16, F - min(6, F // 3))
+    nw, nt = W, min(16, max(F - W - S, 4))
+
+    def opts(T, A):
+        return pb.SeriesOptions(T=T, A=A, plain=(T == 1), sched=sched)
 
     def measure(T, A):
-        o = pb.SeriesOptions(T=T, A=A, plain=(T == 1), sched=sched)
-        s.run(o, first=0, count=nw, want_images=False)
-        out = s.run(o, first=nw, count=nt, want_images=False)
+        s.run(opts(T, A), first=0, count=nw, want_images=False)
+        out = s.run(opts(T, A), first=nw, count=nt, want_images=False)
         ms = s.last_span_ms() / nt
         return {"T": T, "A": A, "frames_per_s": 1000.0 / ms, "ms_per_frame": ms,
                 "p50_latency_ms": statistics.median(float(v) for v in out["gpu_ms"])}
 
     res = {"gpus": ngpu, "single_gpu_plain": measure(1, 1), "channel": measure(1, min(ngpu, 8)),
            "temporal": measure(ngpu, 1)}
-    key = (pb.ImagingMode.single_slice, plan.N, pb.frames_bucket(nt), plan.J)
+    key = (pb.ImagingMode.single_slice, plan.N, pb.frames_bucket(S), plan.J)
     db = []
-    for _ in pb.legal_configs(ngpu, a_cap=8):
-        T, A = pb.learn_step(key, db, ngpu, 8)
-        r = measure(T, A)
-        db.append(key + (T, A, r["ms_per_frame"]))
+    slots = max(6, ngpu)  # worker slots: as on one GPU, several frames may share a device
+    for _ in pb.legal_configs(slots, a_cap=8):
+        T, A = pb.learn_step(key, db, slots, 8)
+        db.append(key + (T, A, measure(T, A)["ms_per_frame"]))
     T, A = pb.select_config(key, db)
     res["autotuned_hybrid"] = measure(T, A)
     res["tuned_space_ms_per_frame"] = {f"T{r[4]}xA{r[5]}": round(r[6], 3) for r in db}
-    return res
+    # the headline: the selected hybrid on the S frames after the warm-up and tuning ranges
+    o = opts(T, A)
+    s.run(o, first=0, count=nw, want_images=False)
+    with ClockSampler(0) as clk:
+        out = s.run(o, first=F - S, count=S, want_images=False)
+        span_ms = s.last_span_ms()
+    lat = [float(v) for v in out["gpu_ms"]]
+    head = {"T": T, "A": A, "span_ms": span_ms, "lat": lat, "clocks": clk.summary(), "decompositions": res,
+            "cg_iters": list(out["cg_iters"])}
+    s.close()
+    if with_e2e:
+        head["e2e"] = e2e_raw(pb, lambda n: pb.Series(pb.Context(plan, device=0), n, U, devices=devices), plan, o,
+                              cfg, F, S, 1, 0)
+    return head
 
 
 def channel_processes(pb, plan, frames, P, world, rank, local, S):
@@ -644,43 +720,7 @@ def main():
     # end to end: pinned host frames streamed through the public series call
     e2e = None
     if not args.no_e2e:
-        # raw acquisitions (J x K x S samples per frame) from pinned host memory through
-        # rtn_series_run_raw: H2D, device pre stage (gridding, cached PSFs, normalisation),
-        # reconstruction, images D2H to pinned host, all inside the timed region
-        import torch
-        raw, angles = synth_raw(G, J, K, U, n_unique=U)
-        Ssp = raw.shape[-1]
-        FR = F + S  # one more range of S frames: the untimed e2e warm-up range
-        rt = torch.empty((FR, J, K, Ssp), dtype=torch.complex64, pin_memory=True)
-        rt.numpy()[:] = np.stack([raw[n % U] for n in range(FR)])
-        ang = np.stack([angles[n % U] for n in range(FR)])
-        imt = torch.empty((FR, plan.N, plan.N), dtype=torch.complex64, pin_memory=True)
-        fb = rt[0].numel() * 8  # bytes of one raw frame
-        ib = plan.N * plan.N * 8
-        rs = pb.Series(ctx, FR, U)  # its own store and PSF cache
-        # frames [0, W + NTUNE) prime the chain, the normalisation scale, the PSF cache
-        # and the grid plans; the next S frames are the untimed e2e warm-up; the S after
-        # them are timed
-        T0 = W + NTUNE
-        rs.run(opts, first=0, count=T0, raw=dict(samples_ptr=rt.data_ptr(), S=Ssp, angles=ang[:T0]),
-               images_ptr=imt.data_ptr())
-        rs.run(opts, first=T0, count=S, raw=dict(samples_ptr=rt.data_ptr() + T0 * fb, S=Ssp, angles=ang[T0:T0 + S]),
-               images_ptr=imt.data_ptr() + T0 * ib)
-        T0 += S
-        raw_in = dict(samples_ptr=rt.data_ptr() + T0 * fb, S=Ssp, angles=ang[T0:T0 + S])
-        barrier(world, local)
-        t0 = time.perf_counter()
-        rs.run(opts, first=T0, count=S, raw=raw_in, images_ptr=imt.data_ptr() + T0 * ib)
-        wall = time.perf_counter() - t0
-        print(f"[bench] e2e wall {wall * 1e3:.1f} ms, device span {rs.last_span_ms():.1f} ms", file=sys.stderr,
-              flush=True)
-        barrier(world, local)
-        wall = max_over_ranks(wall, world, local)
-        e2e = {"value": world * S / wall, "unit": "frames/s", "h2d_bytes_per_step": J * K * Ssp * 8,
-               "d2h_bytes_per_step": plan.N * plan.N * 8,
-               "path": "rtn_series_run_raw: pinned raw samples H2D on the copy stream, device gridding + "
-                       "cached PSFs + normalisation, reconstruction, images D2H to pinned host (wall clock)"}
-        del rs
+        e2e = e2e_raw(pb, lambda n: pb.Series(ctx, n, U), plan, opts, cfg, F, S, world, local)
 
     # roofline of the dominant kernel (isolated CUDA-event timing on the engine stream)
     peak, peak_kind = measured_peaks()
@@ -728,18 +768,19 @@ def main():
     except Exception as e:  # reported, never fatal
         latency_mode = {"error": str(e)}
 
-    decomp = None
+    single = None
     if world > 1:
-        # the paper's decompositions across the GPUs of this node, driven from rank 0 in
-        # one process (the reference's thread-per-worker model): channel groups over
-        # NVLink peer memory, temporal decomposition, and the autotuned hybrid. The other
-        # ranks hold their GPUs idle meanwhile.
+        # the N > 1 headline: one acquisition over all the node's GPUs under the autotuned
+        # channel x temporal decomposition, driven from rank 0 in one process (the
+        # reference's thread-per-worker model); the other ranks hold their GPUs idle
+        # meanwhile. The per-rank slice series above stay as the multi-slice figure.
         barrier(world, local)
         if rank == 0:
             try:
-                decomp = decompositions(pb, plan, frames, P, U, sched, world)
-            except Exception as e:  # reported, never fatal for the headline line
-                decomp = {"error": str(e)}
+                single = single_series_multi_gpu(pb, plan, frames, P, U, sched, world, cfg, W, S,
+                                                 with_e2e=not args.no_e2e)
+            except Exception as e:  # reported; the headline then stays the multi-slice figure
+                single = {"error": str(e)}
         barrier(world, local)
         # the same channel decomposition with one process per GPU: every rank is one
         # member (CUDA IPC views of the peers, device-side barriers), one chained frame
@@ -748,8 +789,8 @@ def main():
             procs = channel_processes(pb, plan, frames, P, world, rank, local, S)
         except Exception as e:
             procs = {"error": str(e)}
-        if rank == 0 and decomp is not None:
-            decomp["channel_processes"] = procs
+        if rank == 0:
+            single["channel_processes"] = procs
 
     if rank != 0:
         return
@@ -770,8 +811,27 @@ def main():
         "latency_mode": latency_mode,
         "check": check,
     }
-    if decomp is not None:
-        line["decompositions"] = decomp
+    if single is not None:
+        multi_slice = {"value": value, "ms_per_step": span_ms / S, "scaling": "weak", "e2e": e2e,
+                       "frames_in_flight": T, "channel_group": A,
+                       "per_rank": "independent slice series (multi-slice acquisition), one per GPU"}
+        line["multi_slice"] = multi_slice
+        if "error" in single:
+            line["single_series_error"] = single["error"]
+            line["decompositions"] = {"channel_processes": single.get("channel_processes")}
+        else:
+            Ts, As = single["T"], single["A"]
+            line.update({
+                "value": S / (single["span_ms"] / 1000.0), "ms_per_step": single["span_ms"] / S, "scaling": "strong",
+                "p50_latency_ms": statistics.median(single["lat"]),
+                "latency_ms_min_max": [min(single["lat"]), max(single["lat"])],
+                "e2e": single.get("e2e"), "clocks": single["clocks"],
+                "gpu_launches": (launches_per_frame(caps, M, ctx.fused_cra() and Ts > 1) if As == 1
+                                 else launches_per_frame_group(caps, M, As)) * S,
+                "decompositions": dict(single["decompositions"], channel_processes=single.get("channel_processes")),
+            })
+            line["config"].update({"frames_in_flight": Ts, "channel_group": As,
+                                   "per_rank": "one frame series over all GPUs (rank 0 drives every device)"})
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, frames[0] * np.float32(100.0 / math.sqrt(

@@ -2,6 +2,7 @@
 #include "group.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -62,6 +63,23 @@ Group::Group(const Plan& plan, const std::vector<int>& devices, int a_cap) : pla
     cudaEvent_t ev;
     check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
     ev_.push_back(ev);
+    int* fl = nullptr;
+    check_cuda(cudaMalloc(&fl, sizeof(int) * 2), "group flags");
+    check_cuda(cudaMemset(fl, 0, sizeof(int) * 2), "group flags");
+    flags_.push_back(fl);
+    gf_.flag[d] = fl;
+  }
+  gf_.A = A_;
+  // all-member barriers: device-side epoch flags (k_pg_barrier, as the one-process-per-GPU
+  // group) when every member has its own GPU; CUDA graph edges between the streams when
+  // members share a device, where two spinning branches of one graph are not guaranteed
+  // to run concurrently. RTN_GROUP_BARRIER=flags|events overrides (the flag barrier's
+  // deadline turns a missing member into a DecompFault, never a hang).
+  {
+    std::vector<int> dv(devices);
+    std::sort(dv.begin(), dv.end());
+    flag_barrier_ = std::adjacent_find(dv.begin(), dv.end()) == dv.end();
+    if (const char* e = std::getenv("RTN_GROUP_BARRIER")) flag_barrier_ = std::strcmp(e, "flags") == 0;
   }
   for (int d = 0; d < A_; ++d) mem_[static_cast<size_t>(d)]->join_group(d, gv, gs);
   check_cuda(cudaSetDevice(mem_[0]->dev_), "set device");
@@ -80,6 +98,7 @@ Group::~Group() {
   for (size_t d = 0; d < ev_.size(); ++d) {
     cudaSetDevice(mem_[d]->dev_);
     cudaEventDestroy(ev_[d]);
+    if (d < flags_.size()) cudaFree(flags_[d]);
   }
   cudaSetDevice(mem_[0]->dev_);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
@@ -119,6 +138,12 @@ void Group::join() {
 
 void Group::barrier() {
   if (A_ == 1) return;
+  if (flag_barrier_) {
+    // each member bumps and publishes its epoch after its stream's earlier kernels, then
+    // polls every member's: no cross-stream dependency, no host involvement
+    each([&](int d, Engine& e) { e.enq_pg_barrier(flags_[static_cast<size_t>(d)], gf_); });
+    return;
+  }
   each([&](int d, Engine& e) { check_cuda(cudaEventRecord(ev_[static_cast<size_t>(d)], e.s_), "barrier record"); });
   each([&](int d, Engine& e) {
     for (int o = 0; o < A_; ++o) {

@@ -12,9 +12,10 @@
 // member order, fused with the W^-H column pass and the CR update), a second
 // barrier, and k_grp_fin, which forms the group totals of the CR scalars in member
 // order. Every member computes bit-identical totals and takes identical decisions;
-// there is no host round trip and no separate collective kernel. Barriers are CUDA
-// events (cross-device stream waits), captured into one multi-device graph per
-// frame in budget mode.
+// there is no host round trip and no separate collective kernel. Barriers are
+// device-side epoch flags (k_pg_barrier: release/acquire over NVLink) when every member
+// has its own GPU, CUDA events (stream edges) when members share one; either way a
+// frame is captured into one multi-device graph in budget mode.
 #pragma once
 
 #include <memory>
@@ -87,6 +88,9 @@ class Group : public FrameWorker {
   std::vector<std::pair<int, int>> blocks_;
   std::vector<std::unique_ptr<Engine>> mem_;
   std::vector<cudaEvent_t> ev_;      // per member, created on its device
+  std::vector<int*> flags_;          // per member: [0] published epoch, [1] local epoch counter
+  GroupFlags gf_{};
+  bool flag_barrier_ = false;        // device-side epoch barriers (k_pg_barrier) instead of graph edges
   cudaEvent_t ev_fork_ = nullptr;    // on the leader's device
   std::vector<float> alphas_;
   std::vector<int> caps_;

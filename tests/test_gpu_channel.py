@@ -87,6 +87,38 @@ def test_group_result_independent_of_member_placement(gpu, ref):
     assert np.array_equal(outs[0].est, outs[1].est)
 
 
+@pytest.mark.parametrize("A", [2, 4])
+def test_group_device_flag_barriers_match_event_barriers(gpu, ref, A, monkeypatch):
+    # the all-member barrier as device-side epoch flags (k_pg_barrier, the default when
+    # every member has its own GPU) forced onto members that share this GPU: the frames
+    # (graph capture, replay, op-level calls) are bit-identical to the stream-edge
+    # barriers and within the frame tolerance of the reference
+    plan = gpu.raw_plan(128, 8)
+    plan.newton_steps, plan.cg_iter_budget = 7, 50
+    inp = phantom_frame_inputs(ref, plan, K=13, U=5)
+    init = gpu.initial_estimate(plan)
+    x = random_estimate(plan, 5)
+    outs = {}
+    for mode in ("events", "flags"):
+        monkeypatch.setenv("RTN_GROUP_BARRIER", mode)
+        with gpu.Context(plan, devices=_devices(gpu, A)) as ctx:
+            ctx.set_psf(inp["P"][0])
+            ctx.set_data(inp["z"][0])
+            f1 = ctx.reconstruct_frame(init)
+            f2 = ctx.reconstruct_frame(f1.est, f1.est)  # replay of the captured frame graph
+            ctx.make_step_cache(x)
+            op = ctx.apply_normal(random_estimate(plan, 6))
+            outs[mode] = (f1, f2, op)
+    for k in range(2):
+        assert np.array_equal(outs["flags"][k].image, outs["events"][k].image), k
+        assert np.array_equal(outs["flags"][k].est, outs["events"][k].est), k
+        assert outs["flags"][k].cg_per_step == outs["events"][k].cg_per_step
+    assert np.array_equal(outs["flags"][2], outs["events"][2])
+    img, _, per, _ = ref.reconstruct_frame(plan, inp["z"][0], inp["P"][0], init, A=min(A, 4))
+    assert outs["flags"][0].cg_per_step == per
+    assert rel_err(outs["flags"][0].image, img) < FRAME_TOL
+
+
 def test_group_fft_accounting(gpu, ref):
     # test_nlinv.cpp:370-389 counts logical transforms, whatever the decomposition
     plan = gpu.make_plan(16, 3)
