@@ -121,16 +121,30 @@ Registry& registry() {
     // Per-kernel factorisation preferences (measured, scripts/prof_kernels.py): the last
     // registration of a grid side is its default; a kernel may come from another
     // factorisation with the same lines per block (same k_rows2 channel grouping)
-    auto prefer_rows2 = [&](int G, int N1, int N2) {
-      Engine::Ops* dflt = nullptr;
+    auto alt_of = [&](int G, int N1, int N2, Engine::Ops*& dflt) -> const Engine::Ops* {
+      dflt = nullptr;
       const Engine::Ops* alt = nullptr;
       for (auto& o : reg->ops) {
         if (o.G == G) dflt = &o;
         if (o.G == G && o.N1 == N1 && o.N2 == N2) alt = &o;
       }
-      if (dflt && alt && dflt != alt && dflt->LPB == alt->LPB) dflt->rows2 = alt->rows2;
+      return (dflt && alt != dflt) ? alt : nullptr;
+    };
+    auto prefer_rows2 = [&](int G, int N1, int N2) {
+      Engine::Ops* dflt = nullptr;
+      const Engine::Ops* alt = alt_of(G, N1, N2, dflt);
+      if (alt && dflt->LPBR == alt->LPBR) dflt->rows2 = alt->rows2;
+    };
+    // a column pass from another factorisation (same lines per block; U / Y layouts do not
+    // depend on the factorisation): the 16 x 24 k_colA holds its 16-point first step in
+    // registers where the 24 x 16 one spills
+    auto prefer_colA = [&](int G, int N1, int N2) {
+      Engine::Ops* dflt = nullptr;
+      const Engine::Ops* alt = alt_of(G, N1, N2, dflt);
+      if (alt && dflt->LPB == alt->LPB) dflt->colA = alt->colA;
     };
     prefer_rows2(320, 20, 16);
+    prefer_colA(384, 16, 24);
     return reg;
   }();
   return *r;
@@ -259,7 +273,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), dev_(device) {
   dims_.off = plan.G / 2 - plan.Gc / 2;
   dims_.N = plan.N;
   dims_.invG = 1.0f / static_cast<float>(plan.G);
-  dims_.H = (plan.J + ops_->LPB - 1) / ops_->LPB;
+  dims_.H = (plan.J + ops_->LPBR - 1) / ops_->LPBR;
   dims_.grp = 0;
   dims_.count_rho = 1;
   D_ = plan.G * plan.G + plan.J * plan.Gc * plan.Gc;
@@ -342,6 +356,10 @@ void Engine::alloc() {
   const int max_grid = std::max({vec_grid_, plan_.J * ((plan_.G + ops_->LPB - 1) / ops_->LPB) + nbr_ + 8, 4 * 148});
   // grid_reduce<K> writes K doubles per block; K <= kMaxReduce
   check_cuda(cudaMalloc(&partials_, sizeof(double) * kMaxReduce * max_grid), "partials");
+  check_cuda(cudaMalloc(&dpart_w_, sizeof(double) * 7 * max_grid), "deferred partials");
+  dpart_c_[0] = dpart_w_ + 3 * max_grid;
+  dpart_c_[1] = dpart_w_ + 5 * max_grid;
+  if (const char* e = std::getenv("RTN_DEFER_RED")) defer_red_ = e[0] != '0';
   check_cuda(cudaMalloc(&st_, sizeof(DevState)), "state");
   check_cuda(cudaMemset(st_, 0, sizeof(DevState)), "state");
   check_cuda(cudaMallocHost(&st_host_, sizeof(DevState)), "state mirror");
@@ -402,7 +420,7 @@ void Engine::ensure_cr_capacity(int max_iter) {
 
 void Engine::sync() { check_cuda(cudaStreamSynchronize(s_), "stream sync"); }
 
-int Engine::line_batch() const { return ops_->LPB; }
+int Engine::line_batch() const { return ops_->LPBR; }
 
 void Engine::set_cluster(bool on) {
   on = on && cluster_supported();
@@ -469,10 +487,10 @@ void Engine::enq_step_begin(int m) {
 }
 
 void Engine::enq_decode(const float2* est) {
-  const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
-  const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB;
+  const int J = plan_.J, G = plan_.G, LPB = ops_->LPB, LPBR = ops_->LPBR;
+  const int tGc = (plan_.Gc + LPB - 1) / LPB, tGr = (G + LPBR - 1) / LPBR;
   ops_->colA(s_, J * tGc, dims_, winv_, twG_, est + static_cast<size_t>(G) * G, U_, 0, G, st_, 0);
-  ops_->rows1(s_, J * tG, dims_, R1_DECODE, twG_, U_, nullptr, nullptr, nullptr, nullptr, coils_, est, rhom_,
+  ops_->rows1(s_, J * tGr, dims_, R1_DECODE, twG_, U_, nullptr, nullptr, nullptr, nullptr, coils_, est, rhom_,
               st_, 0);
 }
 
@@ -513,7 +531,7 @@ __global__ void k_nop(const DevState* st) {
 
 void Engine::enq_apply_front(const float2* dx, int use_halt, bool skip_colA) {
   const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
-  const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
+  const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + ops_->LPBR - 1) / ops_->LPBR;
   if (!skip_colA) {
     ops_->colA(s_, J * tGc, dims_, winv_, twG_, dx + static_cast<size_t>(G) * G, U_, dims_.lo, dims_.L, st_,
                use_halt);
@@ -538,6 +556,7 @@ void Engine::enq_apply_back(const float2* dx, float2* out, int cw_mode, float al
   a.out = out;
   a.ap_prev = ap_prev;
   a.win_only_ok = win_only_ok_;
+  a.defer_out = defer_w_;
   const int nbw = J * tGc;
   for (int k = pass_reps("colsW"); k > 0; --k)
     ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, use_halt, gv_);
@@ -550,7 +569,7 @@ void Engine::enq_setup(const float2* x, const float2* reg, float alpha) {
 
 void Engine::enq_setup_front(const float2* x) {
   const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
-  const int tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
+  const int tG = (G + LPB - 1) / LPB, tL = (dims_.L + ops_->LPBR - 1) / ops_->LPBR;
   enq_decode(x);
   ops_->rows1(s_, J * tL, dims_, R1_SETUP, twG_, U_, coils_, rhom_, nullptr, V_, nullptr, nullptr, nullptr, st_, 0);
   ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, 0);
@@ -581,18 +600,40 @@ void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
     // budget-mode graphs: one fused recurrence kernel per iteration (k_cr_fused)
     // on the pass path the recurrence also runs the next application's W^-1 column pass
     const bool crA = fused_crA() && !use_cluster_;
+    // pass path, one device: k_colsW and every recurrence but the step's last leave their
+    // reductions to the next recurrence (DeferRed)
+    const bool defer = defer_red_ && !use_cluster_ && !dims_.grp;
+    const int nbw = plan_.J * ((plan_.Gc + ops_->LPB - 1) / ops_->LPB) + nbr_;
+    int prev_grid = 0;  // block count of the previous recurrence with deferred partials
+    auto red = [&](int it, bool last) {
+      DeferRed dr{};
+      if (!defer) return dr;
+      dr.w = dpart_w_;
+      dr.nw = nbw;
+      if (it > 0) {
+        dr.c = dpart_c_[(it - 1) & 1];
+        dr.nc = prev_grid;
+      }
+      dr.out = last ? nullptr : dpart_c_[it & 1];
+      return dr;
+    };
     win_only_ok_ = 1;
+    defer_w_ = defer ? dpart_w_ : nullptr;
     enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1, nullptr);
     for (int it = 0; it < cap; ++it) {
-      if (!crA || it + 1 == cap) {
-        enq_cr_fused(it, tol);
-        if (it + 1 < cap) enq_apply(r_, ar_, CW_OPALPHA, alpha, it + 1, 1, ap_);
+      const bool last = it + 1 == cap;
+      if (!crA || last) {
+        enq_cr_fused(it, tol, red(it, last));
+        prev_grid = vec_grid_;
+        if (!last) enq_apply(r_, ar_, CW_OPALPHA, alpha, it + 1, 1, ap_);
       } else {
-        enq_crA(it, tol);
+        enq_crA(it, tol, red(it, false));
+        prev_grid = crA_grid();
         enq_apply_front(r_, 1, true);
         enq_apply_back(r_, ar_, CW_OPALPHA, alpha, it + 1, 1, ap_);
       }
     }
+    defer_w_ = nullptr;
     win_only_ok_ = 0;
     return;
   }
@@ -630,19 +671,24 @@ void Engine::enq_image(const float2* est, float2* img, float scale, bool apply_s
            est, coils_, scale, apply_scale ? 1 : 0, img, st_);
 }
 
-void Engine::enq_cr_fused(int it, float tol) {
+void Engine::enq_cr_fused(int it, float tol, const DeferRed& dr) {
   const int rho_skip = (dims_.grp && !dims_.count_rho) ? plan_.G * plan_.G : 0;
   launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, static_cast<const float2*>(ar_),
-           partials_, st_, cr_, it, tol, rho_skip, dims_.grp, plan_.G);
+           partials_, st_, cr_, it, tol, rho_skip, dims_.grp, plan_.G, dr);
 }
 
 bool Engine::fused_crA() const { return fused_crA_ && fused_cr_ && ops_->crA != nullptr && !dims_.grp; }
 
-void Engine::enq_crA(int it, float tol) {
+int Engine::crA_grid() const {
   const int nbc = plan_.J * ((plan_.Gc + ops_->LPB - 1) / ops_->LPB);
   // rho part: the window's L^2 entries at four per thread (all G^2 when it is not window-only)
   const int nbr = std::max(1, std::min(vec_grid_, (dims_.L * dims_.L + 4 * kThreads - 1) / (4 * kThreads)));
-  ops_->crA(s_, nbc + nbr, nbc, dims_, xcg_, r_, p_, ap_, ar_, winv_, twG_, U_, partials_, st_, cr_, it, tol);
+  return nbc + nbr;
+}
+
+void Engine::enq_crA(int it, float tol, const DeferRed& dr) {
+  const int nbc = plan_.J * ((plan_.Gc + ops_->LPB - 1) / ops_->LPB);
+  ops_->crA(s_, crA_grid(), nbc, dims_, xcg_, r_, p_, ap_, ar_, winv_, twG_, U_, partials_, st_, cr_, it, tol, dr);
 }
 
 void Engine::join_group(int rank, const GroupView& gv, const GroupScal& gs) {
@@ -1038,8 +1084,27 @@ double Engine::time_kernel(const char* which, int reps) {
   const bool cold = w.size() > 5 && w.compare(w.size() - 5, 5, ":cold") == 0;
   if (cold) w.resize(w.size() - 5);
   const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
-  const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + LPB - 1) / LPB;
+  const int tGc = (plan_.Gc + LPB - 1) / LPB, tG = (G + LPB - 1) / LPB, tL = (dims_.L + ops_->LPBR - 1) / ops_->LPBR;
   check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
+  // the recurrences consume deferred partials as in the step (DeferRed): plausible totals
+  // (rar = |ar|^2 = |ap|^2 = |r|^2 = 1) so every timed launch runs the full update
+  const int nbw = J * tGc + nbr_;
+  DeferRed dr{};
+  if (defer_red_ && !dims_.grp) {
+    std::vector<double> hw(3 * static_cast<size_t>(nbw)), hc(2 * static_cast<size_t>(crA_grid()));
+    for (int b = 0; b < nbw; ++b) {
+      hw[3 * b] = hw[3 * b + 1] = 1.0 / nbw;
+      hw[3 * b + 2] = 0.0;
+    }
+    for (size_t b = 0; b < hc.size(); ++b) hc[b] = 2.0 / static_cast<double>(hc.size());
+    check_cuda(cudaMemcpyAsync(dpart_w_, hw.data(), sizeof(double) * hw.size(), cudaMemcpyHostToDevice, s_), "h2d");
+    check_cuda(cudaMemcpyAsync(dpart_c_[0], hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice, s_), "h2d");
+    check_cuda(cudaStreamSynchronize(s_), "sync");
+    dr.w = dpart_w_;
+    dr.nw = nbw;
+    dr.c = dpart_c_[0];
+    dr.nc = crA_grid();
+  }
   auto launch = [&] {
     if (w == "colsT") {
       ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, 0);
@@ -1054,17 +1119,20 @@ double Engine::time_kernel(const char* which, int reps) {
       a.dot_slot = -1;
       a.dx = r_;
       a.out = ar_;
-      const int nbw = J * tGc;
-      ops_->colsW(s_, nbw + nbr_, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, nbw, partials_, st_, cr_, 0, gv_);
+      // as in the CR solve: a scratch output, the partials deferred to the recurrence
+      a.defer_out = dr.w ? dpart_w_ : nullptr;
+      ops_->colsW(s_, nbw, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, J * tGc, partials_, st_, cr_, 0, gv_);
     } else if (w == "cr_xr") {
       launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, partials_, st_, cr_, 1, 0.f);
     } else if (w == "cr_fused") {
+      // a step's last recurrence: the deferred partials in, its own grid reduction out
       launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_,
-               static_cast<const float2*>(ar_), partials_, st_, cr_, 1, 0.f, 0, 0, plan_.G);
+               static_cast<const float2*>(ar_), partials_, st_, cr_, 1, 0.f, 0, 0, plan_.G, dr);
     } else if (w == "crA") {
-      const int nbc = J * tGc;
-      const int nbr = std::max(1, std::min(vec_grid_, (dims_.L * dims_.L + 4 * kThreads - 1) / (4 * kThreads)));
-      ops_->crA(s_, nbc + nbr, nbc, dims_, xcg_, r_, p_, ap_, ar_, winv_, twG_, U_, partials_, st_, cr_, 1, 0.f);
+      DeferRed d2 = dr;
+      if (d2.w) d2.out = dpart_c_[1];
+      ops_->crA(s_, crA_grid(), J * tGc, dims_, xcg_, r_, p_, ap_, ar_, winv_, twG_, U_, partials_, st_, cr_, 1, 0.f,
+                d2);
     } else if (w == "cr_pap") {
       launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, p_, ap_, r_, ar_, partials_, st_, cr_, 1);
     } else if (w == "colA") {

@@ -175,7 +175,7 @@ class Engine : public FrameWorker {
   void set_cluster(bool on);
   bool cluster_supported() const { return RC_ != nullptr; }
   bool fused_crA() const;  // budget-mode CR solves use k_crA on the five-kernel path
-  int line_batch() const;  // lines per block of the pass kernels (channel-group size of k_rows2)
+  int line_batch() const;  // lines per block of the row passes (channel-group size of k_rows2)
 
   float2* x_dev() { return x_; }
   float2* reg_dev() { return reg_; }
@@ -217,8 +217,9 @@ class Engine : public FrameWorker {
   // group-member kernels (group.cu)
   void join_group(int rank, const GroupView& gv, const GroupScal& gs);
   void enq_grp_fin(int setup, int op_slot, int cr_slot, float tol);
-  void enq_cr_fused(int it, float tol);
-  void enq_crA(int it, float tol);
+  void enq_cr_fused(int it, float tol, const DeferRed& dr = DeferRed{});
+  void enq_crA(int it, float tol, const DeferRed& dr);
+  int crA_grid() const;
   void enq_axpy1();
   void enq_state_reset();
   void enq_z_scan();  // st->z_out for the data now in z_ (stream ordered)
@@ -263,6 +264,12 @@ class Engine : public FrameWorker {
   float2* gbuf_ = nullptr;
   float2* img_ = nullptr;
   double* partials_ = nullptr;
+  // deferred reductions of the budget-mode CR solve (DeferRed): k_colsW's partials (3 per
+  // block) and the recurrences' (2 per block, by iteration parity)
+  double* dpart_w_ = nullptr;
+  double* dpart_c_[2] = {nullptr, nullptr};
+  double* defer_w_ = nullptr;  // set while enqueueing: k_colsW writes deferred partials here
+  bool defer_red_ = true;      // RTN_DEFER_RED=0: the grid reductions with last-block tails
   DevState* st_ = nullptr;
   DevState* st_host_ = nullptr;  // pinned mirror
   double* cr_buf_ = nullptr;

@@ -344,14 +344,17 @@ __device__ __forceinline__ void dft_m(float2 (&x)[N]) {
 // contiguous in memory), COLS tiles put the line fastest (lines are adjacent
 // columns), so every global access of both passes is coalesced.
 // ---------------------------------------------------------------------------------
-template <int N1_, int N2_, int LPB_>
+// RS_ (row geometries only): thread slots per row line, a power of two >= NMAX dividing 32,
+// so a line whose NMAX does not divide 32 (20, 24, ...) still lives in one warp; 0 = NMAX
+template <int N1_, int N2_, int LPB_, int RS_ = 0>
 struct LineGeom {
   static constexpr int N1 = N1_;
   static constexpr int N2 = N2_;
   static constexpr int G = N1 * N2;
   static constexpr int LPB = LPB_;
   static constexpr int NMAX = N1 > N2 ? N1 : N2;
-  static constexpr int NT = LPB * NMAX;
+  static constexpr int RS = RS_ ? RS_ : NMAX;
+  static constexpr int NT = LPB * RS;
   static constexpr int LS0 = G + G / N2;
   static constexpr int LS = (LS0 % 2 == 1) ? LS0 : LS0 + 1;
   static constexpr int SMEM_FLOAT2 = LPB * LS;

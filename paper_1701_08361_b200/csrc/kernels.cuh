@@ -82,6 +82,19 @@ struct GroupFlags {
   const int* flag[kMaxGroup];
 };
 
+// Deferred grid reductions of the budget-mode CR solve (pass path, one device): the
+// producer (k_colsW's operator application, a k_crA / k_cr_fused recurrence that is not
+// the step's last) writes one partial per block and exits; the next consumer in stream
+// order (k_crA / k_cr_fused) forms the totals in every block, in one fixed order, so
+// every block gets bit-identical values and the producer has no ticket or last-block tail.
+struct DeferRed {
+  const double* w;  // k_colsW partials {Re<dx,out>, |out|^2, Re<ap_prev,out>}, 3 per block
+  int nw;           // their block count (0: the dots come from CrScalars as before)
+  const double* c;  // the previous recurrence's partials {|ap|^2, |r|^2}, 2 per block
+  int nc;           // their block count (0: none; iteration it-1's tail already ran)
+  double* out;      // this recurrence's partials, 2 per block (nullptr: grid reduction + tail)
+};
+
 // CR scalars of the current step: rar[k] = <r, A r> after apply k, ap2[k] = |ap|^2
 // after update k, rn[k] = |r| after iteration k (cg_solve nlinv.cpp:179-234).
 struct CrScalars {

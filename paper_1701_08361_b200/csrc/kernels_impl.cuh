@@ -133,6 +133,42 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
   return true;
 }
 
+// one partial of K doubles per block, in the fixed order of grid_reduce (warp sums, then
+// the warps in order), written to out[blockIdx.x * K + k]: the producer half of a
+// deferred reduction (DeferRed)
+template <int K>
+__device__ void block_partial(double (&v)[K], double* out) {
+  __shared__ double red[K][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double s = warp_sum(v[k]);
+    if (lane == 0) red[k][warp] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double s = 0;
+    for (int w = 0; w < nw; ++w) s += red[threadIdx.x][w];
+    out[blockIdx.x * K + threadIdx.x] = s;
+  }
+}
+
+// the consumer half, one warp: lane l sums blocks l, l + 32, ... in order, then the
+// warp tree; every lane gets the totals. Identical in every block of the consumer.
+template <int K>
+__device__ __forceinline__ void warp_totals(const double* part, int nb, double (&tot)[K]) {
+  const int lane = threadIdx.x & 31;
+  double s[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) s[k] = 0.0;
+  for (int b = lane; b < nb; b += 32) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) s[k] += __ldcg(part + b * K + k);
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) tot[k] = __shfl_sync(0xffffffffu, warp_sum(s[k]), 0);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------------
@@ -148,10 +184,11 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
 #define RTNB_MINB 3
 #endif
 #define RTNB_PASS_BOUNDS __launch_bounds__(Geo::NT, (RTNB_MINB * 256 + Geo::NT - 1) / Geo::NT)
-// per-kernel overrides: the column passes at the coil resolution and k_rows2 fit 64
-// registers without spills (ptxas -v), k_rows1 / k_colsT need the 80 of MINB 3
+// per-kernel override for the column passes at the coil resolution and k_rows2: 3 (80
+// registers at 256 threads) measured +4.5 % at C3 T = 3, +3 % at C2 over 4 (64 registers:
+// k_colsW spilled 40 B)
 #ifndef RTNB_MINB_LIGHT
-#define RTNB_MINB_LIGHT 4
+#define RTNB_MINB_LIGHT 3
 #endif
 #define RTNB_PASS_BOUNDS_LIGHT __launch_bounds__(Geo::NT, (RTNB_MINB_LIGHT * 256 + Geo::NT - 1) / Geo::NT)
 // per-kernel residency targets (256-thread blocks per SM) of the heavy passes
@@ -164,7 +201,7 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
 #define RTNB_BOUNDS_N(M) __launch_bounds__(Geo::NT, ((M) * 256 + Geo::NT - 1) / Geo::NT)
 
 template <class Geo, bool COLS>
-constexpr int kRowStride = (!COLS && 32 % Geo::NMAX == 0) ? Geo::NMAX : 0;
+constexpr int kRowStride = (!COLS && 32 % Geo::RS == 0) ? Geo::RS : 0;
 
 #define RTNB_TILE_SETUP(COLS_)                                  \
   extern __shared__ float2 A[];                                 \
@@ -177,8 +214,9 @@ constexpr int kRowStride = (!COLS && 32 % Geo::NMAX == 0) ? Geo::NMAX : 0;
   (void)LO;                                                     \
   (void)LW
 
-// Barrier between the steps of a row-pass transform. A row line owns the same NMAX
-// consecutive thread slots in both steps (kRowStride); when NMAX divides 32 every line stays
+// Barrier between the steps of a row-pass transform. A row line owns the same RS
+// consecutive thread slots in both steps (kRowStride; RS = NMAX, or NMAX rounded up to a
+// power of two for the 20- and 24-point geometries); when RS divides 32 every line stays
 // inside one warp, so the exchange needs only a warp barrier and the warps of a block run
 // their lines independently. Column passes spread a line over the block.
 template <bool WARP>
@@ -191,7 +229,7 @@ __device__ __forceinline__ void step_sync() {
 }
 template <class Geo>
 __device__ __forceinline__ void row_line_sync() {
-  if constexpr (32 % Geo::NMAX == 0) {
+  if constexpr (32 % Geo::RS == 0) {
     __syncwarp();
   } else {
     __syncthreads();
@@ -451,6 +489,8 @@ struct ColsWArgs {
   float2* out2;       // SETUP: p (= r)
   float2* out3;       // SETUP: x_cg (zeroed)
   const float2* ap_prev;  // fused CR: also reduce |out|^2 and Re<ap_prev, out> (nullable)
+  double* defer_out;      // fused CR, one device: per-block partials {acc0, aa, pa} for the
+                          // next recurrence (DeferRed) instead of the grid reduction
   int win_only_ok;        // fused CR: rho entries outside the window may be skipped when the
                           // step's setup left them exactly zero (see rho_window_only)
 };
@@ -587,16 +627,16 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
       }
     }
   } else {
-    // 320/384-thread lines (block barriers): the usual step order spills less
-    __syncthreads();
+    // 20- and 24-point lines: the usual step order spills less
+    row_line_sync<Geo>();
     if (a2) put_natural<Geo>(A, i2.l, i2.k, u);
-    __syncthreads();
+    row_line_sync<Geo>();
     if (a1) {
       get_step1<Geo>(A, i1.l, i1.k, v);
       fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
       park_step1<Geo>(A, i1.l, i1.k, v);
     }
-    __syncthreads();
+    row_line_sync<Geo>();
     if (a2) {
       if (d.Gc * 4 == G) {  // pruned: only the coil band is kept
         fft_step2<Geo, -1, Geo::GC_K2>(A, i2.l, i2.k, u);
@@ -799,6 +839,11 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
     }
     if (a.mode == CW_SETUP && __syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&st->rho_out_nz, 1);
   }
+  if (a.defer_out) {
+    double dv[3] = {acc0, aa, pa};
+    block_partial<3>(dv, a.defer_out);
+    return;
+  }
   double vv[4] = {acc0, acc1, aa, pa}, tot[4];
   if (grid_reduce<4>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
     const double total = tot[0];
@@ -870,6 +915,104 @@ __device__ __forceinline__ bool cr_coef(DevState* st, const CrScalars& cr, int i
   return true;
 }
 
+// Entry of a fused recurrence kernel, all threads of the block: the frame / CR state
+// checks, the totals of the deferred reductions (DeferRed) -- the previous iteration's
+// tail (|ap|^2 for the denominator, |r|, the iteration count and the tolerance stop,
+// as cr_fused_tail) and this iteration's dots -- then the step coefficients (cr_coef).
+// Warp 0 loads and sums the partials, thread 0 decides (block 0 records), the block
+// reads the decision from shared memory. Returns false when the iteration must not run.
+__device__ inline bool cr_begin(DevState* st, const CrScalars& cr, int it, float tol, const DeferRed& dr, CrCoef& c) {
+  if (!dr.nw && !dr.nc) {
+    if (st->status || st->cr_halt) return false;
+    return cr_coef(st, cr, it, tol, c);
+  }
+  __shared__ double s_c[2];
+  __shared__ int s_ok;
+  if (threadIdx.x < 32) {
+    double wt[3] = {0.0, 0.0, 0.0}, ct[2] = {0.0, 0.0};
+    const int status = st->status, halt = st->cr_halt;
+    const double rar_old = it > 0 ? cr.rar[it - 1] : 0.0;
+    const double rhs2 = tol > 0.0f ? st->steps[st->cur_step].rhs_nrm2 : 0.0;
+    if (dr.nw) warp_totals<3>(dr.w, dr.nw, wt);
+    if (dr.nc) warp_totals<2>(dr.c, dr.nc, ct);
+    if (threadIdx.x == 0) {
+      const bool rec = blockIdx.x == 0;
+      int ok = !(status || halt);
+      double ap2_prev = 0.0;
+      if (ok && dr.nc) {
+        // iteration it-1's tail (cr_fused_tail, nlinv.cpp:205-220)
+        ap2_prev = ct[0];
+        const double rn = sqrt(ct[1]);
+        if (rec) {
+          cr.ap2[it - 1] = ap2_prev;
+          cr.rn[it] = rn;
+        }
+        if (!isfinite(rn)) {
+          if (rec) {
+            st->status = ST_SOLVER;
+            st->cr_halt = 1;
+          }
+          ok = 0;
+        } else {
+          if (rec) st->steps[st->cur_step].iters = it;
+          if (tol > 0.0f && (rn == 0.0 || rn <= (double)tol * sqrt(rhs2))) {
+            if (rec) st->cr_halt = 1;
+            ok = 0;
+          }
+        }
+      } else if (ok && it > 0) {
+        ap2_prev = cr.ap2[it - 1];
+      }
+      double a = 0.0, b = 0.0;
+      if (ok) {
+        double rar_new, saa, spa;
+        if (dr.nw) {
+          rar_new = wt[0];
+          saa = wt[1];
+          spa = wt[2];
+          if (rec) {
+            cr.rar[it] = rar_new;
+            cr.saa[it] = saa;
+            cr.spa[it] = spa;
+          }
+        } else {
+          rar_new = cr.rar[it];
+          saa = cr.saa[it];
+          spa = cr.spa[it];
+        }
+        // cr_coef with the totals in registers
+        double denom = saa;
+        if (it > 0) {
+          b = (rar_old != 0.0) ? rar_new / rar_old : 0.0;
+          denom = b * b * ap2_prev + 2.0 * b * spa + saa;
+        }
+        if (!isfinite(denom) || !isfinite(rar_new)) {
+          if (rec) {
+            st->status = ST_SOLVER;
+            st->cr_halt = 1;
+          }
+          ok = 0;
+        } else if (denom <= 0.0 && tol > 0.0f) {
+          if (rec) st->cr_halt = 1;
+          ok = 0;
+        } else {
+          ok = denom > 0.0 ? 2 : 1;  // 2: the update runs (upd)
+          a = denom > 0.0 ? rar_new / denom : 0.0;
+        }
+      }
+      s_c[0] = b;
+      s_c[1] = a;
+      s_ok = ok;
+    }
+  }
+  __syncthreads();
+  if (!s_ok) return false;
+  c.b = s_c[0];
+  c.a = s_c[1];
+  c.upd = s_ok == 2;
+  return true;
+}
+
 // the single-device epilogue of the fused recurrence (last block): |ap|^2 for the next
 // iteration's denominator, |r|, iteration count, tolerance stop (nlinv.cpp:205-220)
 __device__ __forceinline__ void cr_fused_tail(DevState* st, const CrScalars& cr, int it, float tol,
@@ -913,24 +1056,46 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_CRA) k_crA(Dims d, float2* __restrict__ 
                                        float2* __restrict__ p, float2* __restrict__ ap,
                                        const float2* __restrict__ ar, const float* __restrict__ winv,
                                        const float4* __restrict__ twG, float2* __restrict__ U, int nbc,
-                                       double* partials, DevState* st, CrScalars cr, int it, float tol) {
+                                       double* partials, DevState* st, CrScalars cr, int it, float tol,
+                                       DeferRed dr) {
   pdl_enter();
-  if (st->status || st->cr_halt) return;
-  CrCoef c;
-  if (!cr_coef(st, cr, it, tol, c)) return;
-  const float bf = (float)c.b, af = (float)c.a, naf = (float)(-c.a);
-  double acc_ap = 0.0, acc_r = 0.0;
   extern __shared__ float2 A[];
   constexpr int G = Geo::G, N1 = Geo::N1, N2 = Geo::N2, LO = G / 4, LW = G / 2;
   const int G2 = G * G;
-  if ((int)blockIdx.x < nbc) {
-    const Item<Geo, true> i1(threadIdx.x, N2), i2(threadIdx.x, N1);
-    const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
-    const int j = blockIdx.x / tiles;
-    const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
-    const int nl = min(Geo::LPB, d.Gc - q0);
-    const size_t cbase = (size_t)G2 + (size_t)j * d.Gc * d.Gc;
-    if (i1.on && i1.l < nl) {
+  // coil blocks: the band's CR operands do not depend on the step coefficients, so their
+  // loads are issued before the coefficients are formed (overlapping cr_begin's reads of
+  // the deferred partials)
+  constexpr uint32_t BAND = Geo::GC_N1;
+  constexpr bool kBand = BAND != Geo::ALL_N1;
+  constexpr int B0 = kBand ? __builtin_ctz(BAND) : 0, BN = kBand ? __builtin_popcount(BAND) : 1;
+  const Item<Geo, true> i1(threadIdx.x, N2), i2(threadIdx.x, N1);
+  const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
+  const int j = blockIdx.x / tiles;
+  const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
+  const int nl = min(Geo::LPB, d.Gc - q0);
+  const size_t cbase = (size_t)G2 + (size_t)j * d.Gc * d.Gc;
+  const bool colblk = (int)blockIdx.x < nbc;
+  const bool act1 = colblk && i1.on && i1.l < nl;
+  const bool band = kBand && d.Gc * 4 == G;
+  float2 pv[BN], apv[BN], rv[BN], arv[BN], xv[BN];
+  if (band && act1) {
+    const int q = q0 + i1.l;
+#pragma unroll
+    for (int b = 0; b < BN; ++b) {
+      const size_t e = cbase + (size_t)(N2 * (B0 + b) + i1.k - d.off) * d.Gc + q;
+      pv[b] = p[e];
+      apv[b] = ap[e];
+      rv[b] = r[e];
+      arv[b] = ar[e];
+      xv[b] = x[e];
+    }
+  }
+  CrCoef c;
+  if (!cr_begin(st, cr, it, tol, dr, c)) return;
+  const float bf = (float)c.b, af = (float)c.a, naf = (float)(-c.a);
+  double acc_ap = 0.0, acc_r = 0.0;
+  if (colblk) {
+    if (act1) {
       const int q = q0 + i1.l;
       float2 v[N1];
 #pragma unroll
@@ -953,23 +1118,11 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_CRA) k_crA(Dims d, float2* __restrict__ 
         const float w = winv[i * d.Gc + q];
         v[n1] = flip(make_float2(nr.x * w, nr.y * w), t);  // chat * winv.real() (nlinv.cpp:121)
       };
-      constexpr uint32_t BAND = Geo::GC_N1;
-      if (BAND != Geo::ALL_N1 && d.Gc * 4 == G) {
-        // the coil band's step-1 slots are compile-time: every load issued up front
-        constexpr int B0 = __builtin_ctz(BAND), BN = __builtin_popcount(BAND);
-        float2 pv[BN], apv[BN], rv[BN], arv[BN], xv[BN];
-#pragma unroll
-        for (int b = 0; b < BN; ++b) {
-          const size_t e = cbase + (size_t)(N2 * (B0 + b) + i1.k - d.off) * d.Gc + q;
-          pv[b] = p[e];
-          apv[b] = ap[e];
-          rv[b] = r[e];
-          arv[b] = ar[e];
-          xv[b] = c.upd ? x[e] : make_float2(0.f, 0.f);
-        }
+      if (band) {
+        // the coil band's step-1 slots are compile-time, their operands already loaded
 #pragma unroll
         for (int b = 0; b < BN; ++b) entry(B0 + b, pv[b], apv[b], rv[b], arv[b], xv[b]);
-        fft_step1<Geo, +1, BAND>(v, i1.k, twG);
+        fft_step1<Geo, +1, kBand ? BAND : Geo::ALL_N1>(v, i1.k, twG);
       } else {
 #pragma unroll
         for (int n1 = 0; n1 < N1; ++n1) {
@@ -1036,7 +1189,11 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_CRA) k_crA(Dims d, float2* __restrict__ 
     }
   }
   double vv[2] = {acc_ap, acc_r}, tot[2];
-  if (grid_reduce<2>(vv, partials, &st->counter, tot) && threadIdx.x == 0) cr_fused_tail(st, cr, it, tol, tot[0], tot[1]);
+  if (dr.out) {
+    block_partial<2>(vv, dr.out);  // the tail runs in the next recurrence (cr_begin)
+  } else if (grid_reduce<2>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
+    cr_fused_tail(st, cr, it, tol, tot[0], tot[1]);
+  }
 }
 
 #ifndef RTNB_PASS_ONLY  // non-template kernels: compiled once (engine.cu)
@@ -1166,11 +1323,10 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
                                                        float2* __restrict__ p, float2* __restrict__ ap,
                                                        const float2* __restrict__ ar, double* partials,
                                                        DevState* st, CrScalars cr, int it, float tol,
-                                                       int rho_skip, int grp, int G) {
+                                                       int rho_skip, int grp, int G, DeferRed dr) {
   pdl_enter();
-  if (st->status || st->cr_halt) return;
   CrCoef c;
-  if (!cr_coef(st, cr, it, tol, c)) return;
+  if (!cr_begin(st, cr, it, tol, dr, c)) return;
   const float bf = (float)c.b, af = (float)c.a, naf = (float)(-c.a);
   double acc_ap = 0.0, acc_r = 0.0;
   // rho entries outside the window are exactly zero in every vector: skip them
@@ -1217,6 +1373,10 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
     }
   }
   double v[2] = {acc_ap, acc_r}, tot[2];
+  if (dr.out) {
+    block_partial<2>(v, dr.out);  // the tail runs in the next recurrence (cr_begin)
+    return;
+  }
   if (grid_reduce<2>(v, partials, &st->counter, tot) && threadIdx.x == 0) {
     if (grp) {
       cr.pcr[2 * it + 0] = tot[0];

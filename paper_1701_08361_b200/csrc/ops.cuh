@@ -15,7 +15,9 @@
 namespace rtnb {
 
 struct Engine::Ops {
-  int G = 0, N1 = 0, N2 = 0, LPB = 0, NT = 0;
+  // LPB / NT: lines and threads per block of the column passes; LPBR: lines per block of
+  // the row passes (k_rows1, k_rows2: fewer, wider-strided lines when NMAX does not divide 32)
+  int G = 0, N1 = 0, N2 = 0, LPB = 0, NT = 0, LPBR = 0;
   size_t smem = 0;
   void (*colA)(cudaStream_t, int, Dims, const float*, const float4*, const float2*, float2*, int, int,
                const DevState*, int) = nullptr;
@@ -30,7 +32,8 @@ struct Engine::Ops {
   void (*fft)(cudaStream_t, int, int, float2*, int, int, const float4*, float) = nullptr;
   // CR recurrence + the next application's W^-1 column pass (k_crA)
   void (*crA)(cudaStream_t, int grid, int nbc, Dims, float2*, float2*, float2*, float2*, const float2*,
-              const float*, const float4*, float2*, double*, DevState*, CrScalars, int, float) = nullptr;
+              const float*, const float4*, float2*, double*, DevState*, CrScalars, int, float,
+              const DeferRed&) = nullptr;
   // whole application per channel in one thread-block cluster (kernels_cluster.cuh);
   // nullptr where not instantiated (grid, tail, CTA count per channel)
   void (*apply_cluster)(cudaStream_t, int J, Dims, ColsWArgs, const float*, const float4*, const float2*,
@@ -83,8 +86,17 @@ struct Inst {
   using Geo = LineGeom<N1, N2, kLpb>;
   static constexpr size_t kSmem = sizeof(float2) * Geo::SMEM_FLOAT2;
   static constexpr int kNT = Geo::NT;
-  // row pass 2: one window row x one group of kLpb channels (+ the channel terms)
-  static constexpr size_t kSmem2 = sizeof(float2) * (Geo::SMEM_FLOAT2 + kLpb * (N1 * N2 / 2));
+  // row passes: a line owns RS thread slots, NMAX rounded up to a power of two when it
+  // does not divide 32 (every line inside one warp: warp barriers between the transform
+  // steps), with at most 256 threads per block
+  static constexpr int kNMax = N1 > N2 ? N1 : N2;
+  static constexpr int kRS = (32 % kNMax == 0) ? kNMax : (kNMax <= 8 ? 8 : kNMax <= 16 ? 16 : 32);
+  static constexpr int kLpbR = (32 % kNMax == 0) ? kLpb : (kLpb < 256 / kRS ? kLpb : 256 / kRS);
+  using GeoR = LineGeom<N1, N2, kLpbR, (32 % kNMax == 0) ? 0 : kRS>;
+  static constexpr size_t kSmemR = sizeof(float2) * GeoR::SMEM_FLOAT2;
+  static constexpr int kNTR = GeoR::NT;
+  // row pass 2: one window row x one group of kLpbR channels (+ the channel terms)
+  static constexpr size_t kSmem2 = sizeof(float2) * (GeoR::SMEM_FLOAT2 + kLpbR * (N1 * N2 / 2));
 
   static void set_attrs() {
     // c_small_tw is a per-translation-unit __constant__ (no relocatable device code):
@@ -92,9 +104,11 @@ struct Inst {
     upload_small_twiddles();
     const int s = static_cast<int>(kSmem);
     check_cuda(cudaFuncSetAttribute(k_colA<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colA");
-    check_cuda(cudaFuncSetAttribute(k_rows1<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr rows1");
+    check_cuda(cudaFuncSetAttribute(k_rows1<GeoR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemR)),
+               "attr rows1");
     check_cuda(cudaFuncSetAttribute(k_colsT<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsT");
-    check_cuda(cudaFuncSetAttribute(k_rows2<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    check_cuda(cudaFuncSetAttribute(k_rows2<GeoR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmem2)),
                "attr rows2");
     check_cuda(cudaFuncSetAttribute(k_colsW<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsW");
@@ -119,6 +133,7 @@ Engine::Ops Inst<N1, N2>::make() {
   o.N1 = N1;
   o.N2 = N2;
   o.LPB = Geo::LPB;
+  o.LPBR = GeoR::LPB;
   o.smem = kSmem;
   o.NT = kNT;
   o.colA = [](cudaStream_t s, int grid, Dims d, const float* winv, const float4* tw, const float2* chat,
@@ -128,7 +143,7 @@ Engine::Ops Inst<N1, N2>::make() {
   o.rows1 = [](cudaStream_t s, int grid, Dims d, int mode, const float4* tw, const float2* U,
                const float2* coils, const float2* rhom, const float2* drho, float2* V, float2* coils_out,
                const float2* rho_src, float2* rhom_out, const DevState* st, int h) {
-    launch_k(k_rows1<Geo>, grid, kNT, kSmem, s, d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
+    launch_k(k_rows1<GeoR>, grid, kNTR, kSmemR, s, d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
              rhom_out, st, h);
   };
   o.colsT = [](cudaStream_t s, int grid, Dims d, const float4* tw, const float2* P, float2* V,
@@ -138,7 +153,7 @@ Engine::Ops Inst<N1, N2>::make() {
   o.rows2 = [](cudaStream_t s, int grid, Dims d, int setup, const float4* tw, const float2* V,
                const float2* coils, const float2* rhom, const float2* z, float2* Y, double2* RP,
                double* partials, DevState* st, int h) {
-    launch_k(k_rows2<Geo>, grid, kNT, kSmem2, s, d, setup, tw, V, coils, rhom, z, Y, RP, partials, st, h);
+    launch_k(k_rows2<GeoR>, grid, kNTR, kSmem2, s, d, setup, tw, V, coils, rhom, z, Y, RP, partials, st, h);
   };
   o.colsW = [](cudaStream_t s, int grid, Dims d, ColsWArgs a, const float* winv, const float4* tw,
                const float2* Y, const double2* RP, const float2* coils, const float2* z, int nbw,
@@ -147,8 +162,8 @@ Engine::Ops Inst<N1, N2>::make() {
   };
   o.crA = [](cudaStream_t s, int grid, int nbc, Dims d, float2* x, float2* r, float2* p, float2* ap,
              const float2* ar, const float* winv, const float4* tw, float2* U, double* partials, DevState* st,
-             CrScalars cr, int it, float tol) {
-    launch_k(k_crA<Geo>, grid, kNT, kSmem, s, d, x, r, p, ap, ar, winv, tw, U, nbc, partials, st, cr, it, tol);
+             CrScalars cr, int it, float tol, const DeferRed& dr) {
+    launch_k(k_crA<Geo>, grid, kNT, kSmem, s, d, x, r, p, ap, ar, winv, tw, U, nbc, partials, st, cr, it, tol, dr);
   };
   o.fft = [](cudaStream_t s, int grid, int sign, float2* data, int batch, int axis, const float4* tw,
              float scale) {
