@@ -144,7 +144,7 @@ Registry& registry() {
       if (alt && dflt->LPB == alt->LPB) dflt->colA = alt->colA;
     };
     prefer_rows2(320, 20, 16);
-    prefer_colA(384, 16, 24);
+    prefer_colA(384, 16, 24);  // spill-free, neutral at C5 (k_crA from 16 x 24 there: -1.5 %)
     return reg;
   }();
   return *r;
@@ -281,7 +281,7 @@ Engine::Engine(const Plan& plan, int device) : plan_(plan), dev_(device) {
   if (const char* e = std::getenv("RTN_FUSED_CR")) fused_cr_ = e[0] != '0';
   // k_crA by measurement: +4 % at C3 and C4 (16 x 16); the 24-point step-1 geometries
   // (C5's 24 x 16) hold too many CR operands with their DFT and lose 2 %
-  fused_crA_ = ops_->N1 <= 16;
+  fused_crA_ = ops_->crA_N1 <= 16;
   if (const char* e = std::getenv("RTN_CRA")) fused_crA_ = e[0] != '0';
   alloc();
 }
@@ -486,11 +486,14 @@ void Engine::enq_step_begin(int m) {
   launch_k(k_step_begin, 1, 32, 0, s_, st_, m);
 }
 
-void Engine::enq_decode(const float2* est) {
+void Engine::enq_decode(const float2* est, bool full) {
   const int J = plan_.J, G = plan_.G, LPB = ops_->LPB, LPBR = ops_->LPBR;
   const int tGc = (plan_.Gc + LPB - 1) / LPB, tGr = (G + LPBR - 1) / LPBR;
-  ops_->colA(s_, J * tGc, dims_, winv_, twG_, est + static_cast<size_t>(G) * G, U_, 0, G, st_, 0);
-  ops_->rows1(s_, J * tGr, dims_, R1_DECODE, twG_, U_, nullptr, nullptr, nullptr, nullptr, coils_, est, rhom_,
+  // nr = -1 / R1_DECODE_WIN: all G rows and columns when st->z_out, else the window only
+  // (every in-frame consumer of the coils reads them on the window unless the data has
+  // samples outside it: k_colsW's / k_rho_out's setup data term)
+  ops_->colA(s_, J * tGc, dims_, winv_, twG_, est + static_cast<size_t>(G) * G, U_, 0, full ? G : -1, st_, 0);
+  ops_->rows1(s_, J * tGr, dims_, full ? R1_DECODE : R1_DECODE_WIN, twG_, U_, nullptr, nullptr, nullptr, nullptr, coils_, est, rhom_,
               st_, 0);
 }
 
@@ -783,7 +786,7 @@ void Engine::toeplitz_apply(float* x) {
 void Engine::make_step_cache(const float* x, float* rho_out, float* coils_out) {
   check_cuda(cudaMemcpyAsync(est_scratch_[2], x, sizeof(float2) * D_, cudaMemcpyHostToDevice, s_), "h2d");
   check_cuda(cudaMemsetAsync(st_, 0, sizeof(int) * 4, s_), "state reset");
-  enq_decode(est_scratch_[2]);
+  enq_decode(est_scratch_[2], true);
   fft_book(fft_current_ctx(), static_cast<uint64_t>(plan_.J));
   const size_t G2 = static_cast<size_t>(plan_.G) * plan_.G;
   if (rho_out) check_cuda(cudaMemcpyAsync(rho_out, rhom_, sizeof(float2) * G2, cudaMemcpyDeviceToHost, s_), "d2h");

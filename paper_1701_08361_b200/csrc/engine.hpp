@@ -201,7 +201,9 @@ class Engine : public FrameWorker {
   void alloc();
   void ensure_cr_capacity(int max_iter);
   void enq_step_begin(int m);
-  void enq_decode(const float2* est);
+  // full: every coil entry (make_step_cache); else the window only when the frame's data is
+  // window-masked (st->z_out == 0, decided on the device)
+  void enq_decode(const float2* est, bool full = false);
   void enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
                  const float2* ap_prev = nullptr);
   // the two halves of an application / a Newton-step setup: everything up to the

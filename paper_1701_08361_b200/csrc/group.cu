@@ -474,7 +474,7 @@ void Group::make_step_cache(const float* x) {
   fork();
   each([&](int, Engine& e) {
     e.enq_state_reset();
-    e.enq_decode(e.x_);
+    e.enq_decode(e.x_, true);
   });
   join();
   read_state();

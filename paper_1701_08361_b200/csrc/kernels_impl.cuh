@@ -246,6 +246,10 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colA(Dims d, const float* __restrict__ 
   pdl_enter();
   if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(true);
+  if (nr < 0) {  // decode: every row when the data has samples outside the window
+    r0 = st->z_out ? 0 : LO;
+    nr = st->z_out ? G : LW;
+  }
   const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
   const int j = blockIdx.x / tiles;
   const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
@@ -289,7 +293,9 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colA(Dims d, const float* __restrict__ 
   }
 }
 
-enum Rows1Mode : int { R1_DECODE = 0, R1_OP = 1, R1_SETUP = 2 };
+// R1_DECODE_WIN: R1_DECODE on the window rows and columns only, unless the frame's data
+// has samples outside the window (st->z_out), when it is R1_DECODE
+enum Rows1Mode : int { R1_DECODE = 0, R1_OP = 1, R1_SETUP = 2, R1_DECODE_WIN = 3 };
 
 // Row pass 1.
 //  DECODE: rows 0..G-1 of U_j -> inverse row FFT -> coils_j (full G x G, scaled 1/G);
@@ -297,7 +303,7 @@ enum Rows1Mode : int { R1_DECODE = 0, R1_OP = 1, R1_SETUP = 2 };
 //  OP:     window rows: W^-1 row pass of U_j, t = c_j*drho + rho*a on the window,
 //          forward row FFT -> V_j (L x G).
 //  SETUP:  window rows: t = rho*c_j (nlinv.cpp:252) -> forward row FFT -> V_j.
-template <class Geo>
+template <class Geo, bool DEC = false>
 __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const float4* __restrict__ twG,
                                                    const float2* __restrict__ U,
                                                    const float2* __restrict__ coils,
@@ -310,6 +316,14 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const f
   pdl_enter();
   if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(false);
+  // DEC: the decode instantiation (R1_DECODE / R1_DECODE_WIN), else R1_OP / R1_SETUP
+  bool wdec = false;
+  if constexpr (DEC) {
+    wdec = mode == R1_DECODE_WIN && !st->z_out;
+    mode = R1_DECODE;
+  } else {
+    if (mode == R1_DECODE || mode == R1_DECODE_WIN) return;
+  }
   const int nrows = (mode == R1_DECODE) ? G : LW;
   const int row0 = (mode == R1_DECODE) ? 0 : LO;
   const int tiles = (nrows + Geo::LPB - 1) / Geo::LPB;
@@ -318,8 +332,10 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const f
   const int nl = min(Geo::LPB, nrows - rl0);
   const float2* Uj = U + (size_t)j * G * d.Gc;
   const float2* cj = coils + (size_t)j * G * G;
-  const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
+  if (wdec && (rl0 + nl <= LO || rl0 >= LO + LW)) return;  // a block of rows outside the window
   const int r1 = row0 + rl0 + i1.l, r2 = row0 + rl0 + i2.l;
+  const bool a1 = i1.on && i1.l < nl && !(wdec && (r1 < LO || r1 >= LO + LW));
+  const bool a2 = i2.on && i2.l < nl && !(wdec && (r2 < LO || r2 >= LO + LW));
   float2 v[N1];
   if (mode != R1_SETUP) {
     if (a1) {
@@ -339,16 +355,17 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const f
     row_line_sync<Geo>();
     float2 u[N2];
     if (a2) {
-      if (mode == R1_DECODE) {
+      if (DEC && !wdec) {
         fft_step2<Geo, +1>(A, i2.l, i2.k, u);
       } else {
         fft_step2<Geo, +1, Geo::WIN_K2>(A, i2.l, i2.k, u);
       }
-      if (mode == R1_DECODE) {
+      if constexpr (DEC) {
         float2* out = coils_out + (size_t)j * G * G + (size_t)r2 * G;
 #pragma unroll
         for (int k2 = 0; k2 < N2; ++k2) {
           const int p = i2.k + N1 * k2;
+          if (wdec && (p < LO || p >= LO + LW)) continue;
           out[p] = cscale(flip(u[k2], p), d.invG);
           if (j == 0) {
             const float2 x = rho_src[(size_t)r2 * G + p];
@@ -372,7 +389,7 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const f
         }
       }
     }
-    if (mode == R1_DECODE) return;  // uniform across the block: no barrier follows
+    if constexpr (DEC) return;  // uniform across the block: no barrier follows
     // OP: the forward Toeplitz row transform in the reverse step order (inner DFTs over
     // the window k2 on the registers, one exchange, outer DFT over k1)
     if (a2) inv_inner<Geo, -1, Geo::WIN_K2>(A, i2.l, i2.k, u, twG);

@@ -12,12 +12,17 @@
 #include "kernels_impl.cuh"
 #include "kernels_cluster.cuh"
 
+#ifndef RTNB_LPB_WIDE
+#define RTNB_LPB_WIDE 16
+#endif
+
 namespace rtnb {
 
 struct Engine::Ops {
   // LPB / NT: lines and threads per block of the column passes; LPBR: lines per block of
   // the row passes (k_rows1, k_rows2: fewer, wider-strided lines when NMAX does not divide 32)
   int G = 0, N1 = 0, N2 = 0, LPB = 0, NT = 0, LPBR = 0;
+  int crA_N1 = 0;  // first-step length of the k_crA instantiation (it may come from another factorisation)
   size_t smem = 0;
   void (*colA)(cudaStream_t, int, Dims, const float*, const float4*, const float2*, float2*, int, int,
                const DevState*, int) = nullptr;
@@ -81,8 +86,10 @@ inline void upload_small_twiddles() {
 
 template <int N1, int N2>
 struct Inst {
-  // 16 lines per block, 32 when that keeps the block a whole number of warps
-  static constexpr int kLpb = ((16 * (N1 > N2 ? N1 : N2)) % 32 == 0) ? 16 : 32;
+  // 16 lines per block, 32 when that keeps the block a whole number of warps; the 20- and
+  // 24-point geometries take RTNB_LPB_WIDE (column passes of 320 / 384 or 160 / 192 threads)
+  static constexpr int kLpb = ((N1 > N2 ? N1 : N2) >= 20) ? RTNB_LPB_WIDE
+                              : ((16 * (N1 > N2 ? N1 : N2)) % 32 == 0) ? 16 : 32;
   using Geo = LineGeom<N1, N2, kLpb>;
   static constexpr size_t kSmem = sizeof(float2) * Geo::SMEM_FLOAT2;
   static constexpr int kNT = Geo::NT;
@@ -107,6 +114,9 @@ struct Inst {
     check_cuda(cudaFuncSetAttribute(k_rows1<GeoR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmemR)),
                "attr rows1");
+    check_cuda(cudaFuncSetAttribute(k_rows1<GeoR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemR)),
+               "attr rows1 decode");
     check_cuda(cudaFuncSetAttribute(k_colsT<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsT");
     check_cuda(cudaFuncSetAttribute(k_rows2<GeoR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmem2)),
@@ -134,6 +144,7 @@ Engine::Ops Inst<N1, N2>::make() {
   o.N2 = N2;
   o.LPB = Geo::LPB;
   o.LPBR = GeoR::LPB;
+  o.crA_N1 = N1;
   o.smem = kSmem;
   o.NT = kNT;
   o.colA = [](cudaStream_t s, int grid, Dims d, const float* winv, const float4* tw, const float2* chat,
@@ -143,7 +154,8 @@ Engine::Ops Inst<N1, N2>::make() {
   o.rows1 = [](cudaStream_t s, int grid, Dims d, int mode, const float4* tw, const float2* U,
                const float2* coils, const float2* rhom, const float2* drho, float2* V, float2* coils_out,
                const float2* rho_src, float2* rhom_out, const DevState* st, int h) {
-    launch_k(k_rows1<GeoR>, grid, kNTR, kSmemR, s, d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
+    launch_k((mode == R1_DECODE || mode == R1_DECODE_WIN) ? k_rows1<GeoR, true> : k_rows1<GeoR, false>, grid,
+             kNTR, kSmemR, s, d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
              rhom_out, st, h);
   };
   o.colsT = [](cudaStream_t s, int grid, Dims d, const float4* tw, const float2* P, float2* V,
