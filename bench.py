@@ -560,7 +560,7 @@ def single_series_multi_gpu(pb, plan, frames, P, U, sched, ngpu, cfg, W, S, with
         span_ms = s.last_span_ms()
     lat = [float(v) for v in out["gpu_ms"]]
     head = {"T": T, "A": A, "span_ms": span_ms, "lat": lat, "clocks": clk.summary(), "decompositions": res,
-            "cg_iters": list(out["cg_iters"])}
+            "cg_iters": [int(v) for v in out["cg_iters"]]}
     s.close()
     if with_e2e:
         head["e2e"] = e2e_raw(pb, lambda n: pb.Series(pb.Context(plan, device=0), n, U, devices=devices), plan, o,
@@ -693,6 +693,8 @@ def main():
         series.run(opts_for(T, A), first=W, count=NTUNE, want_images=False)  # warm the selected config
     else:
         T, A = int(args.T), int(args.A)
+        # graph capture on every worker of the requested configuration, outside the timed region
+        series.run(opts_for(T, A), first=0, count=min(F, max(W, 2 * T)), want_images=False)
     opts = opts_for(T, A)
     barrier(world, local)
     with ClockSampler(local) as clk:

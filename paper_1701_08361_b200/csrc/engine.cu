@@ -497,20 +497,41 @@ void Engine::enq_decode(const float2* est, bool full) {
               st_, 0);
 }
 
+// the cluster-fused application's two halves: one 8-CTA cluster per channel (W^-1 ..
+// W^-H, the coil part of out and its dots, the channel terms rc_j), then the channel sum
+// of out.rho with the CR "+alpha p" and the dots (a channel group puts its all-member
+// barrier between them: k_rho_sum reads every member's rc_j)
+ColsWArgs Engine::cluster_args(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot,
+                               const float2* ap_prev) const {
+  ColsWArgs a{};
+  a.mode = cw_mode;
+  a.alpha = alpha;
+  a.dot_slot = dot_slot;
+  a.dx = dx;
+  a.out = out;
+  a.ap_prev = ap_prev;
+  a.win_only_ok = win_only_ok_;
+  return a;
+}
+
+void Engine::enq_cluster_front(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
+                               const float2* ap_prev) {
+  const ColsWArgs a = cluster_args(dx, out, cw_mode, alpha, dot_slot, ap_prev);
+  ops_->apply_cluster(s_, plan_.J, dims_, a, winv_, twG_, coils_, rhom_, P_, RC_, kpart_, st_, use_halt);
+}
+
+void Engine::enq_rho_sum(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
+                         const float2* ap_prev) {
+  const ColsWArgs a = cluster_args(dx, out, cw_mode, alpha, dot_slot, ap_prev);
+  launch_k(k_rho_sum, rho_grid_, kThreads, 0, s_, dims_, a, static_cast<const float2*>(RC_),
+           static_cast<const double*>(kpart_), plan_.J * ops_->cluster_ctas, partials_, st_, cr_, use_halt, gv_);
+}
+
 void Engine::enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
                        const float2* ap_prev) {
-  if (use_cluster_ && !dims_.grp && cw_mode != CW_SETUP) {
-    ColsWArgs a{};
-    a.mode = cw_mode;
-    a.alpha = alpha;
-    a.dot_slot = dot_slot;
-    a.dx = dx;
-    a.out = out;
-    a.ap_prev = ap_prev;
-    a.win_only_ok = win_only_ok_;
-    ops_->apply_cluster(s_, plan_.J, dims_, a, winv_, twG_, coils_, rhom_, P_, RC_, kpart_, st_, use_halt);
-    launch_k(k_rho_sum, rho_grid_, kThreads, 0, s_, dims_, a, static_cast<const float2*>(RC_),
-             static_cast<const double*>(kpart_), plan_.J * ops_->cluster_ctas, partials_, st_, cr_, use_halt);
+  if (use_cluster_ && cw_mode != CW_SETUP) {
+    enq_cluster_front(dx, out, cw_mode, alpha, dot_slot, use_halt, ap_prev);
+    enq_rho_sum(dx, out, cw_mode, alpha, dot_slot, use_halt, ap_prev);
     return;
   }
   enq_apply_front(dx, use_halt);

@@ -97,9 +97,12 @@ class FrameWorker {
   virtual void frame_run_sync(const RegFn& reg, float2* img_dst, float image_scale, bool apply_scale,
                               FrameStats* stats) = 0;
   virtual void sync() = 0;
+  // cluster-fused applications for the CR solve (latency mode), where supported
+  virtual void set_cluster(bool on) = 0;
 };
 
 class Group;
+struct ColsWArgs;  // kernels_impl.cuh
 
 class Engine : public FrameWorker {
  public:
@@ -172,7 +175,7 @@ class Engine : public FrameWorker {
   // latency mode: every non-setup application as one thread-block cluster per channel
   // (kernels_cluster.cuh) where the geometry supports it; throughput mode (several
   // frames in flight): the five-kernel passes, which share the SMs better
-  void set_cluster(bool on);
+  void set_cluster(bool on) override;
   bool cluster_supported() const { return RC_ != nullptr; }
   bool fused_crA() const;  // budget-mode CR solves use k_crA on the five-kernel path
   int line_batch() const;  // lines per block of the row passes (channel-group size of k_rows2)
@@ -213,6 +216,13 @@ class Engine : public FrameWorker {
   void enq_apply_front(const float2* dx, int use_halt, bool skip_colA = false);
   void enq_apply_back(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
                       const float2* ap_prev);
+  // the cluster-fused application's halves (use_cluster_): clusters, then k_rho_sum
+  ColsWArgs cluster_args(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot,
+                         const float2* ap_prev) const;
+  void enq_cluster_front(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
+                         const float2* ap_prev);
+  void enq_rho_sum(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
+                   const float2* ap_prev);
   void enq_setup_front(const float2* x);
   void enq_setup_back(const float2* x, const float2* reg, float alpha);
   void enq_setup(const float2* x, const float2* reg, float alpha);

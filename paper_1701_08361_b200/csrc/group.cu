@@ -56,6 +56,9 @@ Group::Group(const Plan& plan, const std::vector<int>& devices, int a_cap) : pla
     gv.h[d] = e.dims_.H;
     gv.rp[d] = e.RP_;
     gv.rpo[d] = e.RPO_;
+    gv.rc[d] = e.RC_;
+    gv.jb[d] = blocks_[static_cast<size_t>(d)].first;
+    gv.jb[d + 1] = blocks_[static_cast<size_t>(d)].second;
     gs.st[d] = e.st_;
     gs.pcw[d] = e.cr_.pcw;
     gs.pcr[d] = e.cr_.pcr;
@@ -81,7 +84,10 @@ Group::Group(const Plan& plan, const std::vector<int>& devices, int a_cap) : pla
     flag_barrier_ = std::adjacent_find(dv.begin(), dv.end()) == dv.end();
     if (const char* e = std::getenv("RTN_GROUP_BARRIER")) flag_barrier_ = std::strcmp(e, "flags") == 0;
   }
-  for (int d = 0; d < A_; ++d) mem_[static_cast<size_t>(d)]->join_group(d, gv, gs);
+  for (int d = 0; d < A_; ++d) {
+    mem_[static_cast<size_t>(d)]->join_group(d, gv, gs);
+    mem_[static_cast<size_t>(d)]->set_cluster(false);  // the five passes unless set_cluster(true)
+  }
   check_cuda(cudaSetDevice(mem_[0]->dev_), "set device");
   check_cuda(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   check_cuda(cudaMalloc(&h_stage_, sizeof(float2) * std::max<size_t>(static_cast<size_t>(D_), 1)), "stage");
@@ -150,6 +156,26 @@ void Group::barrier() {
       if (o != d) check_cuda(cudaStreamWaitEvent(e.s_, ev_[static_cast<size_t>(o)], 0), "barrier wait");
     }
   });
+}
+
+void Group::set_cluster(bool on) {
+  bool all = true;
+  for (auto& m : mem_) all = all && m->cluster_supported();
+  on = on && all;
+  if (on == mem_[0]->use_cluster_) return;
+  sync();
+  // captured graphs embed the kernel choice
+  for (auto& g : step_graph_) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
+  }
+  if (frame_graph_) cudaGraphExecDestroy(frame_graph_);
+  frame_graph_ = nullptr;
+  DeviceRestore restore;
+  for (auto& m : mem_) {
+    check_cuda(cudaSetDevice(m->dev_), "set device");
+    m->set_cluster(on);
+  }
 }
 
 void Group::sync() {
@@ -240,10 +266,18 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
   if (run_cr) {
     // the fused recurrence handles every CR vector, so the window-only skip is exact
     each([&](int, Engine& e) { e.win_only_ok_ = 1; });
+    const bool cl = mem_[0]->use_cluster_;
     for (int it = 0; it < cap; ++it) {
-      each([&](int, Engine& e) { e.enq_apply_front(e.r_, 1); });
-      barrier();
-      each([&](int, Engine& e) { e.enq_apply_back(e.r_, e.ar_, CW_OPALPHA, alpha, it, 1, it > 0 ? e.ap_ : nullptr); });
+      if (cl) {
+        // one cluster per own channel, then out.rho over every member's channel terms
+        each([&](int, Engine& e) { e.enq_cluster_front(e.r_, e.ar_, CW_OPALPHA, alpha, it, 1, it > 0 ? e.ap_ : nullptr); });
+        barrier();
+        each([&](int, Engine& e) { e.enq_rho_sum(e.r_, e.ar_, CW_OPALPHA, alpha, it, 1, it > 0 ? e.ap_ : nullptr); });
+      } else {
+        each([&](int, Engine& e) { e.enq_apply_front(e.r_, 1); });
+        barrier();
+        each([&](int, Engine& e) { e.enq_apply_back(e.r_, e.ar_, CW_OPALPHA, alpha, it, 1, it > 0 ? e.ap_ : nullptr); });
+      }
       barrier();
       each([&](int, Engine& e) {
         e.enq_grp_fin(0, it, sync_each ? -1 : it - 1, tol);

@@ -57,6 +57,9 @@ class Group : public FrameWorker {
   void frame_run_sync(const RegFn& reg, float2* img_dst, float image_scale, bool apply_scale,
                       FrameStats* stats) override;
   void sync() override;
+  // members run the cluster-fused applications (one cluster per own channel), then
+  // k_rho_sum over every member's channel terms after an all-member barrier
+  void set_cluster(bool on) override;
   void set_use_graphs(bool on) { use_graphs_ = on; }
 
   // host in / host out (parity boundary)

@@ -32,6 +32,10 @@ struct GroupView {
   int h[kMaxGroup];                 // k_rows2 channel groups of each member
   const double2* rp[kMaxGroup];     // window channel-sum partials (H_d x L x L)
   const double2* rpo[kMaxGroup];    // SETUP: out-of-window partials sum_j conj(c_j) z_j (G x G)
+  // cluster-fused applications (k_rho_sum): every member's channel terms rc_j (J_d x L x L)
+  // and its first channel, so out.rho sums all channels in the single-device order
+  const float2* rc[kMaxGroup];
+  int jb[kMaxGroup + 1];            // member d owns channels [jb[d], jb[d+1])
 };
 
 // k_colsW epilogue modes: plain application, application + alpha*dx (CR), Newton setup

@@ -432,9 +432,13 @@ __global__ void __launch_bounds__(Geo::NT, 2)
 // in flight), the 8 warp partials are added in warp order in shared memory. Warp 0
 // loads the finish operands (dx, ap_prev) before the channel sums land.
 constexpr int kRhoTile = 32;
+// Channel decomposition (d.grp): every member runs this kernel after an all-member barrier;
+// out.rho reads each channel's term from its owner's RC (peer memory) in the single-device
+// channel order, the rho part of the dots is counted on one member, the coil part from the
+// member's own cluster partials, and the member's dot partials go to cr.pcw for k_grp_fin.
 __global__ void __launch_bounds__(kThreads) k_rho_sum(Dims d, ColsWArgs a, const float2* __restrict__ RC,
                                                       const double* __restrict__ kpart, int nk, double* partials,
-                                                      DevState* st, CrScalars cr, int use_halt) {
+                                                      DevState* st, CrScalars cr, int use_halt, GroupView gv) {
   pdl_enter();
   if (st->status || (use_halt && st->cr_halt)) return;
   __shared__ double2 part[kThreads / 32][kRhoTile];
@@ -469,14 +473,24 @@ __global__ void __launch_bounds__(kThreads) k_rho_sum(Dims d, ColsWArgs a, const
     }
     double sx = 0.0, sy = 0.0;
     if (e >= 0 && in_win(d, r, c)) {
-      const float2* src = RC + (size_t)(r - d.lo) * L + (c - d.lo);
+      const size_t w = (size_t)(r - d.lo) * L + (c - d.lo);
+      const float2* src = RC + w;
+      const int Jt = d.grp ? gv.jb[gv.A] : d.J;
       constexpr int kB = 4;
-      for (int j0 = warp; j0 < d.J; j0 += kB * nw) {
+      for (int j0 = warp; j0 < Jt; j0 += kB * nw) {
         float2 t[kB];
 #pragma unroll
         for (int q = 0; q < kB; ++q) {
           const int jj = j0 + q * nw;
-          t[q] = jj < d.J ? __ldcg(src + (size_t)jj * L * L) : make_float2(0.f, 0.f);
+          if (jj >= Jt) {
+            t[q] = make_float2(0.f, 0.f);
+          } else if (d.grp) {
+            int m = 0;
+            while (jj >= gv.jb[m + 1]) ++m;
+            t[q] = __ldcg(gv.rc[m] + (size_t)(jj - gv.jb[m]) * L * L + w);
+          } else {
+            t[q] = __ldcg(src + (size_t)jj * L * L);
+          }
         }
 #pragma unroll
         for (int q = 0; q < kB; ++q) {
@@ -493,12 +507,27 @@ __global__ void __launch_bounds__(kThreads) k_rho_sum(Dims d, ColsWArgs a, const
         tx += part[w][lane].x;
         ty += part[w][lane].y;
       }
-      finish_op(a, (size_t)e, make_float2((float)tx, (float)ty), pdx, pap, acc, aa, pa);
+      if (d.count_rho) {
+        finish_op(a, (size_t)e, make_float2((float)tx, (float)ty), pdx, pap, acc, aa, pa);
+      } else {  // the replicated rho part of the dots is counted on member 0 only
+        double z0 = 0.0, z1 = 0.0, z2 = 0.0;
+        finish_op(a, (size_t)e, make_float2((float)tx, (float)ty), pdx, pap, z0, z1, z2);
+      }
     }
     __syncthreads();
   }
   double vv[3] = {acc, aa, pa}, tot[3];
   if (grid_reduce<3>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
+    if (d.grp) {  // member partials; k_grp_fin forms the totals in member order
+      if (a.dot_slot >= 0) {
+        cr.pcw[3 * a.dot_slot + 0] = tot[0];
+        cr.pcw[3 * a.dot_slot + 1] = tot[1];
+        cr.pcw[3 * a.dot_slot + 2] = tot[2];
+      } else {
+        st->scal[0] = tot[0];
+      }
+      return;
+    }
     if (a.dot_slot >= 0) {
       cr.rar[a.dot_slot] = tot[0];
       cr.saa[a.dot_slot] = tot[1];

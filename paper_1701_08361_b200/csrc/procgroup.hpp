@@ -61,6 +61,7 @@ class ProcGroup : public FrameWorker {
   void frame_run_sync(const RegFn& reg, float2* img_dst, float image_scale, bool apply_scale,
                       FrameStats* stats) override;
   void sync() override;
+  void set_cluster(bool) override {}  // the IPC members run the five passes
 
   // host in / host out: full-layout buffers on every member (each uses its block)
   void set_psf(const float* P);

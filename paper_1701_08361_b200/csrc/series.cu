@@ -505,6 +505,8 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   if (A_ == 1) {
     eng0_.set_cluster(cl);
     for (auto& ex : extra_) ex->set_cluster(cl);
+  } else {
+    for (int t = 0; t < T; ++t) worker(t).set_cluster(cl);
   }
   check_cuda(cudaEventRecord(span0_, copy_), "span event");
   for (int t = 0; t < T; ++t) check_cuda(cudaStreamWaitEvent(worker(t).stream(), span0_, 0), "span wait");

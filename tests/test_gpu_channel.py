@@ -175,6 +175,31 @@ def test_channel_decomposed_plain_series_matches_reference(gpu, ref):
     assert list(got["cg_iters"]) == list(want["cg_iters"])
 
 
+@pytest.mark.parametrize("A", [2, 4])
+def test_group_cluster_applications_match_reference(gpu, ref, A):
+    # latency mode on a channel group: each member runs one thread-block cluster per own
+    # channel, then k_rho_sum forms out.rho over every member's channel terms (peer reads,
+    # in the single-device channel order) after an all-member barrier
+    plan = gpu.raw_plan(128, 8)
+    plan.newton_steps, plan.cg_iter_budget = 7, 50
+    with gpu.Context(plan) as probe:
+        if not probe.cluster_supported():
+            pytest.skip("no cluster-fused application for this grid")
+    samples, angles, z, P, idx = _series_inputs(ref, plan, F=3, K=13, U=3)
+    want = ref.reconstruct_series(plan, samples, angles, plain=True, A=min(A, 4))
+    got = {}
+    for cl in (1, 0):
+        out = _series(gpu, plan, z, P, idx, gpu.SeriesOptions(plain=True, A=A, cluster=cl))
+        got[cl] = out
+        for n in range(3):
+            assert rel_err(out["images"][n], want["images"][n]) < FRAME_TOL, (cl, n)
+            assert out["audit"][n].workers == A
+        assert list(out["cg_iters"]) == list(want["cg_iters"])
+    # the two application paths differ only in FP32 rounding of the fused passes
+    for n in range(3):
+        assert rel_err(got[1]["images"][n], got[0]["images"][n]) < 1e-5, n
+
+
 @pytest.mark.parametrize("T,A", [(2, 2), (4, 2), (2, 3)])
 def test_hybrid_temporal_channel_series_replays_exactly(gpu, ref, T, A):
     # hybrid T x A split: T frame workers, each a channel group of A members; every
