@@ -232,6 +232,13 @@ class Engine : public FrameWorker {
   void enq_cr_fused(int it, float tol, const DeferRed& dr = DeferRed{});
   void enq_crA(int it, float tol, const DeferRed& dr);
   int crA_grid() const;
+  // a group member's recurrence forming the member-order totals itself (DeferRed::grp)
+  DeferRed group_red() const {
+    DeferRed d{};
+    d.grp = 1;
+    d.gs = gs_;
+    return d;
+  }
   void enq_axpy1();
   void enq_state_reset();
   void enq_z_scan();  // st->z_out for the data now in z_ (stream ordered)

@@ -280,8 +280,12 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
       }
       barrier();
       each([&](int, Engine& e) {
-        e.enq_grp_fin(0, it, sync_each ? -1 : it - 1, tol);
-        e.enq_cr_fused(it, tol);
+        if (sync_each) {
+          e.enq_grp_fin(0, it, -1, tol);
+          e.enq_cr_fused(it, tol);
+        } else {
+          e.enq_cr_fused(it, tol, e.group_red());  // k_grp_fin's sums inside the recurrence
+        }
       });
       if (sync_each) {
         barrier();

@@ -97,6 +97,10 @@ struct DeferRed {
   const double* c;  // the previous recurrence's partials {|ap|^2, |r|^2}, 2 per block
   int nc;           // their block count (0: none; iteration it-1's tail already ran)
   double* out;      // this recurrence's partials, 2 per block (nullptr: grid reduction + tail)
+  // channel group, budget mode: the member partials of the application's dots (pcw) and of
+  // the previous recurrence (pcr) summed in member order here, in place of k_grp_fin
+  int grp;
+  GroupScal gs;
 };
 
 // CR scalars of the current step: rar[k] = <r, A r> after apply k, ap2[k] = |ap|^2

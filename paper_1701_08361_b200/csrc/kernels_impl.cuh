@@ -932,6 +932,13 @@ __device__ __forceinline__ bool cr_coef(DevState* st, const CrScalars& cr, int i
   return true;
 }
 
+// member-order sum of one scalar partial over a channel group's members
+__device__ __forceinline__ double grp_sum(const GroupScal& g, const double* const* base, int idx) {
+  double t = 0.0;
+  for (int m = 0; m < g.A; ++m) t += __ldcg(base[m] + idx);
+  return t;
+}
+
 // Entry of a fused recurrence kernel, all threads of the block: the frame / CR state
 // checks, the totals of the deferred reductions (DeferRed) -- the previous iteration's
 // tail (|ap|^2 for the denominator, |r|, the iteration count and the tolerance stop,
@@ -939,6 +946,79 @@ __device__ __forceinline__ bool cr_coef(DevState* st, const CrScalars& cr, int i
 // Warp 0 loads and sums the partials, thread 0 decides (block 0 records), the block
 // reads the decision from shared memory. Returns false when the iteration must not run.
 __device__ inline bool cr_begin(DevState* st, const CrScalars& cr, int it, float tol, const DeferRed& dr, CrCoef& c) {
+  if (dr.grp) {
+    // channel group: k_grp_fin's member-order totals and decisions (the previous
+    // iteration's tail, this application's dots), then the step coefficients; every block
+    // of every member sums the same member partials in the same order
+    __shared__ double g_c[2];
+    __shared__ int g_ok;
+    if (threadIdx.x == 0) {
+      int ok = !(st->status || st->cr_halt);
+      const bool rec = blockIdx.x == 0;
+      double ap2 = 0.0, rar_old = 0.0;
+      if (ok && it > 0) {
+        rar_old = cr.rar[it - 1];
+        ap2 = grp_sum(dr.gs, dr.gs.pcr, 2 * (it - 1));
+        const double rn = sqrt(grp_sum(dr.gs, dr.gs.pcr, 2 * (it - 1) + 1));
+        if (rec) {
+          cr.ap2[it - 1] = ap2;
+          cr.rn[it] = rn;
+        }
+        if (!isfinite(rn)) {
+          if (rec) {
+            st->status = ST_SOLVER;
+            st->cr_halt = 1;
+          }
+          ok = 0;
+        } else {
+          StepRec& s = st->steps[st->cur_step];
+          if (rec) s.iters = it;
+          if (tol > 0.0f && (rn == 0.0 || rn <= (double)tol * sqrt(s.rhs_nrm2))) {
+            if (rec) st->cr_halt = 1;
+            ok = 0;
+          }
+        }
+      }
+      double a = 0.0, b = 0.0;
+      if (ok) {
+        const double rar = grp_sum(dr.gs, dr.gs.pcw, 3 * it + 0);
+        const double saa = grp_sum(dr.gs, dr.gs.pcw, 3 * it + 1);
+        const double spa = grp_sum(dr.gs, dr.gs.pcw, 3 * it + 2);
+        if (rec) {
+          cr.rar[it] = rar;
+          cr.saa[it] = saa;
+          cr.spa[it] = spa;
+        }
+        double denom = saa;
+        if (it > 0) {
+          b = (rar_old != 0.0) ? rar / rar_old : 0.0;
+          denom = b * b * ap2 + 2.0 * b * spa + saa;
+        }
+        if (!isfinite(denom) || !isfinite(rar)) {
+          if (rec) {
+            st->status = ST_SOLVER;
+            st->cr_halt = 1;
+          }
+          ok = 0;
+        } else if (denom <= 0.0 && tol > 0.0f) {
+          if (rec) st->cr_halt = 1;
+          ok = 0;
+        } else {
+          ok = denom > 0.0 ? 2 : 1;
+          a = denom > 0.0 ? rar / denom : 0.0;
+        }
+      }
+      g_c[0] = b;
+      g_c[1] = a;
+      g_ok = ok;
+    }
+    __syncthreads();
+    if (!g_ok) return false;
+    c.b = g_c[0];
+    c.a = g_c[1];
+    c.upd = g_ok == 2;
+    return true;
+  }
   if (!dr.nw && !dr.nc) {
     if (st->status || st->cr_halt) return false;
     return cr_coef(st, cr, it, tol, c);
@@ -1443,11 +1523,6 @@ __global__ void __launch_bounds__(kThreads) k_rho_out(Dims d, const float2* __re
   if (grid_reduce<1>(vv, partials, &st->counter, tot) && threadIdx.x == 0) st->gp[1] = tot[0];
 }
 
-__device__ __forceinline__ double grp_sum(const GroupScal& g, const double* const* base, int idx) {
-  double t = 0.0;
-  for (int m = 0; m < g.A; ++m) t += __ldcg(base[m] + idx);
-  return t;
-}
 
 // Group totals and the decisions that depend on them.
 //  setup:       |rhs|^2, resid_out, resid_win of the step; cg_solve entry checks

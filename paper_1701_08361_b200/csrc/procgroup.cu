@@ -172,8 +172,12 @@ void ProcGroup::enq_newton_step(int m, float tol, int cap, bool sync_each) {
       barrier();
       e.enq_apply_back(e.r_, e.ar_, CW_OPALPHA, alpha, it, 1, it > 0 ? e.ap_ : nullptr);
       barrier();
-      e.enq_grp_fin(0, it, sync_each ? -1 : it - 1, tol);
-      e.enq_cr_fused(it, tol);
+      if (sync_each) {
+        e.enq_grp_fin(0, it, -1, tol);
+        e.enq_cr_fused(it, tol);
+      } else {
+        e.enq_cr_fused(it, tol, e.group_red());  // k_grp_fin's sums inside the recurrence
+      }
       if (sync_each) {
         barrier();
         e.enq_grp_fin(0, -1, it, tol);
