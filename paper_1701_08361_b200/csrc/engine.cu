@@ -1,6 +1,8 @@
 // Engine: device buffers, size dispatch and kernel sequencing for one plan.
 #include "engine.hpp"
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cstddef>
@@ -110,6 +112,27 @@ struct Registry {
   std::vector<std::pair<std::pair<int, int>, float4*>> twG;  // (device, G) -> table
   std::vector<std::pair<std::pair<int, int>, double2*>> twD;  // (device, n*sign) -> direct table
 };
+
+// TMA descriptor of a G x G complex64 array (8-byte elements, row pitch 8G) read in boxes
+// of lpb columns x rows rows (k_colsT's P tiles). cuTensorMapEncodeTiled comes from the
+// driver through the runtime's entry-point query (no link against libcuda).
+void encode_psf_map(CUtensorMap* map, const float2* P, int G, int lpb, int rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    check_cuda(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q), "tensor map entry");
+    if (!fn || q != cudaDriverEntryPointSuccess) fail(5, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  const cuuint64_t dim[2] = {static_cast<cuuint64_t>(G), static_cast<cuuint64_t>(G)};
+  const cuuint64_t stride[1] = {static_cast<cuuint64_t>(G) * sizeof(float2)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(lpb), static_cast<cuuint32_t>(rows)};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<float2*>(P), dim, stride, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(5, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
 
 Registry& registry() {
   static Registry* r = [] {
@@ -356,6 +379,7 @@ void Engine::alloc() {
   const int max_grid = std::max({vec_grid_, plan_.J * ((plan_.G + ops_->LPB - 1) / ops_->LPB) + nbr_ + 8, 4 * 148});
   // grid_reduce<K> writes K doubles per block; K <= kMaxReduce
   check_cuda(cudaMalloc(&partials_, sizeof(double) * kMaxReduce * max_grid), "partials");
+  if (ops_->colsT_box_rows > 0) encode_psf_map(&tmP_, P_, plan_.G, ops_->LPB, ops_->colsT_box_rows);
   check_cuda(cudaMalloc(&dpart_w_, sizeof(double) * 7 * max_grid), "deferred partials");
   dpart_c_[0] = dpart_w_ + 3 * max_grid;
   dpart_c_[1] = dpart_w_ + 5 * max_grid;
@@ -563,7 +587,7 @@ void Engine::enq_apply_front(const float2* dx, int use_halt, bool skip_colA) {
   if (pass_reps("nop") == 2) launch_k(k_nop, 1, 32, 0, s_, static_cast<const DevState*>(st_));
   for (int k = pass_reps("rows1"); k > 0; --k)
     ops_->rows1(s_, J * tL, dims_, R1_OP, twG_, U_, coils_, rhom_, dx, V_, nullptr, nullptr, nullptr, st_, use_halt);
-  for (int k = pass_reps("colsT"); k > 0; --k) ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, use_halt);
+  for (int k = pass_reps("colsT"); k > 0; --k) ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, use_halt, &tmP_);
   for (int k = pass_reps("rows2"); k > 0; --k)
     ops_->rows2(s_, dims_.L * dims_.H, dims_, 0, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, use_halt);
 }
@@ -596,7 +620,7 @@ void Engine::enq_setup_front(const float2* x) {
   const int tG = (G + LPB - 1) / LPB, tL = (dims_.L + ops_->LPBR - 1) / ops_->LPBR;
   enq_decode(x);
   ops_->rows1(s_, J * tL, dims_, R1_SETUP, twG_, U_, coils_, rhom_, nullptr, V_, nullptr, nullptr, nullptr, st_, 0);
-  ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, 0);
+  ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, 0, &tmP_);
   ops_->rows2(s_, dims_.L * dims_.H, dims_, 1, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, 0);
   if (dims_.grp) launch_k(k_rho_out, nbr_, kThreads, 0, s_, dims_, coils_, z_, RPO_, partials_, st_);
 }
@@ -1131,7 +1155,7 @@ double Engine::time_kernel(const char* which, int reps) {
   }
   auto launch = [&] {
     if (w == "colsT") {
-      ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, 0);
+      ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, 0, &tmP_);
     } else if (w == "rows1") {
       ops_->rows1(s_, J * tL, dims_, R1_OP, twG_, U_, coils_, rhom_, r_, V_, nullptr, nullptr, nullptr, st_, 0);
     } else if (w == "rows2") {

@@ -3,6 +3,7 @@
 // (capi.cpp) and the C++ drop-in over it (compat/rtnlinv_compat.cpp) are thin layers.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -283,6 +284,7 @@ class Engine : public FrameWorker {
   float2* gbuf_ = nullptr;
   float2* img_ = nullptr;
   double* partials_ = nullptr;
+  CUtensorMap tmP_{};  // TMA descriptor of P_ for k_colsT's P tiles
   // deferred reductions of the budget-mode CR solve (DeferRed): k_colsW's partials (3 per
   // block) and the recurrences' (2 per block, by iteration parity)
   double* dpart_w_ = nullptr;

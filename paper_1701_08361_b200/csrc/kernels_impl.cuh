@@ -25,6 +25,7 @@
 // device-resident FP64 scalars.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (the k_colsT P tile)
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -436,12 +437,66 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const f
   }
 }
 
+// Bulk asynchronous copies (sm_90+ copy engine: cp.async.bulk with mbarrier completion).
+// Used to stage a block's P columns in shared memory at kernel entry, without registers,
+// while the forward column transform runs.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// 2D tensor tile (TMA, cp.async.bulk.tensor) into shared memory, completion on an mbarrier
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// RTNB_COLST_TMAP=1: k_colsT stages its LPB P columns (G rows x LPB x 8 bytes) behind the
+// FFT tile with TMA (tensor map over P: 8-byte elements, boxes of LPB columns x up to 256
+// rows), issued at kernel entry and waited for just before the k-space multiply. Measured
+// (profiles/r02/ab_colsT_tma.txt): k_colsT 9.7 -> 10.1 us, C3 T = 3 -2.6 %, C5 -10 % (the
+// 32-48 KB tile per block costs co-residency with the other frames' passes); one bulk copy
+// per P row instead of the tensor map: 21 us. Off by default; the direct L2 loads win.
+#ifndef RTNB_COLST_TMAP
+#define RTNB_COLST_TMAP 0
+#endif
+template <class Geo>
+constexpr bool kColsTTmaP = RTNB_COLST_TMAP && Geo::G % Geo::LPB == 0 && (Geo::LPB * 8) % 16 == 0;
+template <class Geo>
+constexpr int kColsTBoxRows = Geo::G <= 256 ? Geo::G : Geo::G / 2;
+template <class Geo>
+constexpr size_t colsT_smem_bytes() {
+  // the FFT tile, 128 bytes of alignment slack, the P tile, the mbarrier
+  return sizeof(float2) * Geo::SMEM_FLOAT2 + (kColsTTmaP<Geo> ? 128 + sizeof(float2) * Geo::G * Geo::LPB + 16 : 0);
+}
+
 // Toeplitz column pass: forward column FFT of the window rows of V_j, * P/G, inverse
 // column FFT, keep the window rows (in place in V_j). Lines: (j, column q).
 template <class Geo>
 __global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
                                                    const float2* __restrict__ P, float2* __restrict__ V,
-                                                   const DevState* st, int use_halt) {
+                                                   const DevState* st, int use_halt,
+                                                   const __grid_constant__ CUtensorMap tmP) {
   pdl_enter();
   if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(true);
@@ -449,6 +504,23 @@ __global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
   const int j = blockIdx.x / tiles;
   const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
   const int nl = min(Geo::LPB, G - q0);
+  // the block's P columns: G rows of LPB contiguous entries (a 128-byte aligned tile after
+  // the FFT tile), loaded by TMA now and waited for just before the k-space multiply
+  float2* Ps = A + Geo::SMEM_FLOAT2;
+  if constexpr (kColsTTmaP<Geo>) {
+    const uint32_t base = smem_u32(Ps);
+    Ps += ((base + 127u) & ~127u) - base >> 3;
+  }
+  uint64_t* pbar = reinterpret_cast<uint64_t*>(Ps + G * Geo::LPB);
+  if constexpr (kColsTTmaP<Geo>) {
+    if (threadIdx.x == 0) {
+      mbar_init(pbar, 1);
+      mbar_expect_tx(pbar, (uint32_t)(sizeof(float2) * G * Geo::LPB));
+      constexpr int R = kColsTBoxRows<Geo>;
+#pragma unroll
+      for (int r0 = 0; r0 < G; r0 += R) tma_load_2d(Ps + r0 * Geo::LPB, &tmP, q0, r0, pbar);
+    }
+  }
   const bool a1 = i1.on && i1.l < nl, a2 = i2.on && i2.l < nl;
   float2* Vj = V + (size_t)j * LW * G;
   float2 v[N1];
@@ -464,15 +536,25 @@ __global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
   }
   __syncthreads();
   float2 u[N2];
+  if constexpr (kColsTTmaP<Geo>) mbar_wait(pbar, 0);
   if (a2) {
     fft_step2<Geo, -1>(A, i2.l, i2.k, u);
     // k-space multiply; the forward pass's output flip cancels the inverse pass's
     // input flip
-    const float2* Pc = P + q0 + i2.l;
+    if constexpr (kColsTTmaP<Geo>) {
+      const float2* Pc = Ps + i2.l;
 #pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) {
-      const int p = i2.k + N1 * k2;
-      u[k2] = cscale(cmul(u[k2], Pc[(size_t)p * G]), d.invG);
+      for (int k2 = 0; k2 < N2; ++k2) {
+        const int p = i2.k + N1 * k2;
+        u[k2] = cscale(cmul(u[k2], Pc[p * Geo::LPB]), d.invG);
+      }
+    } else {
+      const float2* Pc = P + q0 + i2.l;
+#pragma unroll
+      for (int k2 = 0; k2 < N2; ++k2) {
+        const int p = i2.k + N1 * k2;
+        u[k2] = cscale(cmul(u[k2], Pc[(size_t)p * G]), d.invG);
+      }
     }
     // the inverse transform in the reverse step order: its N2-point DFTs over k2 act on
     // this thread's registers, so no reordering exchange is needed

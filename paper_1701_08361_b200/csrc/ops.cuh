@@ -19,6 +19,8 @@
 namespace rtnb {
 
 struct Engine::Ops {
+  // the k_colsT P-tile tensor map's box (kColsTTmaP): LPB columns x colsT_box_rows rows
+  int colsT_box_rows = 0;
   // LPB / NT: lines and threads per block of the column passes; LPBR: lines per block of
   // the row passes (k_rows1, k_rows2: fewer, wider-strided lines when NMAX does not divide 32)
   int G = 0, N1 = 0, N2 = 0, LPB = 0, NT = 0, LPBR = 0;
@@ -28,7 +30,8 @@ struct Engine::Ops {
                const DevState*, int) = nullptr;
   void (*rows1)(cudaStream_t, int, Dims, int, const float4*, const float2*, const float2*, const float2*,
                 const float2*, float2*, float2*, const float2*, float2*, const DevState*, int) = nullptr;
-  void (*colsT)(cudaStream_t, int, Dims, const float4*, const float2*, float2*, const DevState*, int) = nullptr;
+  void (*colsT)(cudaStream_t, int, Dims, const float4*, const float2*, float2*, const DevState*, int,
+                const CUtensorMap*) = nullptr;
   void (*rows2)(cudaStream_t, int, Dims, int, const float4*, const float2*, const float2*,
                 const float2*, const float2*, float2*, double2*, double*, DevState*, int) = nullptr;
   void (*colsW)(cudaStream_t, int, Dims, ColsWArgs, const float*, const float4*, const float2*,
@@ -117,7 +120,9 @@ struct Inst {
     check_cuda(cudaFuncSetAttribute(k_rows1<GeoR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmemR)),
                "attr rows1 decode");
-    check_cuda(cudaFuncSetAttribute(k_colsT<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize, s), "attr colsT");
+    check_cuda(cudaFuncSetAttribute(k_colsT<Geo>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(colsT_smem_bytes<Geo>())),
+               "attr colsT");
     check_cuda(cudaFuncSetAttribute(k_rows2<GeoR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmem2)),
                "attr rows2");
@@ -145,6 +150,7 @@ Engine::Ops Inst<N1, N2>::make() {
   o.LPB = Geo::LPB;
   o.LPBR = GeoR::LPB;
   o.crA_N1 = N1;
+  o.colsT_box_rows = kColsTTmaP<Geo> ? kColsTBoxRows<Geo> : 0;
   o.smem = kSmem;
   o.NT = kNT;
   o.colA = [](cudaStream_t s, int grid, Dims d, const float* winv, const float4* tw, const float2* chat,
@@ -159,8 +165,8 @@ Engine::Ops Inst<N1, N2>::make() {
              rhom_out, st, h);
   };
   o.colsT = [](cudaStream_t s, int grid, Dims d, const float4* tw, const float2* P, float2* V,
-               const DevState* st, int h) {
-    launch_k(k_colsT<Geo>, grid, kNT, kSmem, s, d, tw, P, V, st, h);
+               const DevState* st, int h, const CUtensorMap* tmP) {
+    launch_k(k_colsT<Geo>, grid, kNT, colsT_smem_bytes<Geo>(), s, d, tw, P, V, st, h, *tmP);
   };
   o.rows2 = [](cudaStream_t s, int grid, Dims d, int setup, const float4* tw, const float2* V,
                const float2* coils, const float2* rhom, const float2* z, float2* Y, double2* RP,
