@@ -246,6 +246,25 @@ def launches_per_frame(caps, M, cra=False):
     return n + 3
 
 
+class profiled_step:
+    """RTN_PROFILE_STEP=1: cudaProfilerStart/Stop around the timed step, so
+    `ncu --profile-from-start off --metrics gpu__time_duration.sum ...` lists exactly the
+    timed frames' kernels (a no-op otherwise)"""
+
+    def __enter__(self):
+        self.rt = None
+        if os.environ.get("RTN_PROFILE_STEP") == "1":
+            import ctypes
+            self.rt = ctypes.CDLL("libcudart.so.12")
+            self.rt.cudaProfilerStart()
+        return self
+
+    def __exit__(self, *exc):
+        if self.rt is not None:
+            self.rt.cudaProfilerStop()
+        return False
+
+
 def launches_per_frame_group(caps, M, A):
     """kernels one frame launches on a channel group of A members (group.cu enqueue order,
     all members): per step and member 1 step_begin + 2 decode + 3 setup passes + 1
@@ -697,7 +716,7 @@ def main():
         series.run(opts_for(T, A), first=0, count=min(F, max(W, 2 * T)), want_images=False)
     opts = opts_for(T, A)
     barrier(world, local)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk, profiled_step():
         out = series.run(opts, first=W + NTUNE, count=S, want_images=False)
         span_ms = series.last_span_ms()
     barrier(world, local)

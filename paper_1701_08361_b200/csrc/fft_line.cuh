@@ -345,8 +345,10 @@ __device__ __forceinline__ void dft_m(float2 (&x)[N]) {
 // columns), so every global access of both passes is coalesced.
 // ---------------------------------------------------------------------------------
 // RS_ (row geometries only): thread slots per row line, a power of two >= NMAX dividing 32,
-// so a line whose NMAX does not divide 32 (20, 24, ...) still lives in one warp; 0 = NMAX
-template <int N1_, int N2_, int LPB_, int RS_ = 0>
+// so a line whose NMAX does not divide 32 (20, 24, ...) still lives in one warp; 0 = NMAX.
+// RG_ (row geometries only): lines of NMAX slots synchronise in groups of RG_ threads
+// (lcm(NMAX, 32): whole warps holding whole lines) on named barriers; 0 = none.
+template <int N1_, int N2_, int LPB_, int RS_ = 0, int RG_ = 0>
 struct LineGeom {
   static constexpr int N1 = N1_;
   static constexpr int N2 = N2_;
@@ -354,6 +356,7 @@ struct LineGeom {
   static constexpr int LPB = LPB_;
   static constexpr int NMAX = N1 > N2 ? N1 : N2;
   static constexpr int RS = RS_ ? RS_ : NMAX;
+  static constexpr int RG = RG_;
   static constexpr int NT = LPB * RS;
   static constexpr int LS0 = G + G / N2;
   static constexpr int LS = (LS0 % 2 == 1) ? LS0 : LS0 + 1;

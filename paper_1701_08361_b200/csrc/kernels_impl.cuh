@@ -184,14 +184,21 @@ __device__ __forceinline__ void warp_totals(const double* part, int nb, double (
 #ifndef RTNB_MINB
 #define RTNB_MINB 3
 #endif
-#define RTNB_PASS_BOUNDS __launch_bounds__(Geo::NT, (RTNB_MINB * 256 + Geo::NT - 1) / Geo::NT)
+// resident blocks for a target of M 256-thread blocks per SM: rounded up (the default), or
+// down (RTNB_BOUNDS_FLOOR=1: 320-thread blocks get 2 blocks and 96 registers, not 3 and 64)
+#ifndef RTNB_BOUNDS_FLOOR
+#define RTNB_BOUNDS_FLOOR 0
+#endif
+#define RTNB_BLOCKS_FOR(M) (RTNB_BOUNDS_FLOOR ? ((M) * 256 / Geo::NT > 0 ? (M) * 256 / Geo::NT : 1) \
+                                              : ((M) * 256 + Geo::NT - 1) / Geo::NT)
+#define RTNB_PASS_BOUNDS __launch_bounds__(Geo::NT, RTNB_BLOCKS_FOR(RTNB_MINB))
 // per-kernel override for the column passes at the coil resolution and k_rows2: 3 (80
 // registers at 256 threads) measured +4.5 % at C3 T = 3, +3 % at C2 over 4 (64 registers:
 // k_colsW spilled 40 B)
 #ifndef RTNB_MINB_LIGHT
 #define RTNB_MINB_LIGHT 3
 #endif
-#define RTNB_PASS_BOUNDS_LIGHT __launch_bounds__(Geo::NT, (RTNB_MINB_LIGHT * 256 + Geo::NT - 1) / Geo::NT)
+#define RTNB_PASS_BOUNDS_LIGHT __launch_bounds__(Geo::NT, RTNB_BLOCKS_FOR(RTNB_MINB_LIGHT))
 // per-kernel residency targets (256-thread blocks per SM) of the heavy passes
 #ifndef RTNB_MINB_ROWS1
 #define RTNB_MINB_ROWS1 RTNB_MINB
@@ -199,10 +206,10 @@ __device__ __forceinline__ void warp_totals(const double* part, int nb, double (
 #ifndef RTNB_MINB_CRA
 #define RTNB_MINB_CRA RTNB_MINB
 #endif
-#define RTNB_BOUNDS_N(M) __launch_bounds__(Geo::NT, ((M) * 256 + Geo::NT - 1) / Geo::NT)
+#define RTNB_BOUNDS_N(M) __launch_bounds__(Geo::NT, RTNB_BLOCKS_FOR(M))
 
 template <class Geo, bool COLS>
-constexpr int kRowStride = (!COLS && 32 % Geo::RS == 0) ? Geo::RS : 0;
+constexpr int kRowStride = (!COLS && (32 % Geo::RS == 0 || Geo::RG)) ? Geo::RS : 0;
 
 #define RTNB_TILE_SETUP(COLS_)                                  \
   extern __shared__ float2 A[];                                 \
@@ -232,6 +239,10 @@ template <class Geo>
 __device__ __forceinline__ void row_line_sync() {
   if constexpr (32 % Geo::RS == 0) {
     __syncwarp();
+  } else if constexpr (Geo::RG > 0) {
+    // the lines of this thread's group of RG threads (whole warps, whole lines): named
+    // barrier 1 + group index (0 is __syncthreads')
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)threadIdx.x / Geo::RG), "r"(Geo::RG) : "memory");
   } else {
     __syncthreads();
   }

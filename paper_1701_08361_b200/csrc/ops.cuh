@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cmath>
+#include <numeric>
 #include <cstdlib>
 #include <utility>
 #include <vector>
@@ -14,6 +15,9 @@
 
 #ifndef RTNB_LPB_WIDE
 #define RTNB_LPB_WIDE 16
+#endif
+#ifndef RTNB_ROW_NAMED
+#define RTNB_ROW_NAMED 0
 #endif
 
 namespace rtnb {
@@ -101,8 +105,13 @@ struct Inst {
   // steps), with at most 256 threads per block
   static constexpr int kNMax = N1 > N2 ? N1 : N2;
   static constexpr int kRS = (32 % kNMax == 0) ? kNMax : (kNMax <= 8 ? 8 : kNMax <= 16 ? 16 : 32);
-  static constexpr int kLpbR = (32 % kNMax == 0) ? kLpb : (kLpb < 256 / kRS ? kLpb : 256 / kRS);
-  using GeoR = LineGeom<N1, N2, kLpbR, (32 % kNMax == 0) ? 0 : kRS>;
+  // RTNB_ROW_NAMED=1: the 24-point lines keep NMAX slots and synchronise on named barriers
+  // over lcm(NMAX, 32) threads (no idle lanes); measured C5 -16 % against the default RS
+  // power-of-two slots (idle lanes, warp barriers): profiles/r02/ab_rows_named.txt
+  static constexpr int kRG = (kNMax == 24 && RTNB_ROW_NAMED) ? std::lcm(kNMax, 32) : 0;
+  static constexpr bool kNamed = kRG > 0 && (kLpb * kNMax) % kRG == 0 && (kLpb * kNMax) / kRG <= 15;
+  static constexpr int kLpbR = (32 % kNMax == 0 || kNamed) ? kLpb : (kLpb < 256 / kRS ? kLpb : 256 / kRS);
+  using GeoR = LineGeom<N1, N2, kLpbR, (32 % kNMax == 0 || kNamed) ? 0 : kRS, kNamed ? kRG : 0>;
   static constexpr size_t kSmemR = sizeof(float2) * GeoR::SMEM_FLOAT2;
   static constexpr int kNTR = GeoR::NT;
   // row pass 2: one window row x one group of kLpbR channels (+ the channel terms)

@@ -10,7 +10,7 @@ if [ -z "$SKIP_TESTS" ]; then
   timeout 1500 python -m pytest tests -m gpu -x -q > $O/${TAG}_pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/${TAG}_pytest_gpu.log
 fi
 timeout 600 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 1500 -c 1200 --csv \
+RTN_PROFILE_STEP=1 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $O/${TAG}_launches.csv python bench.py --T 3 --steps 4 --warmup 3 --no-e2e --no-cpu-baseline --no-check > $O/${TAG}_launches.log 2>&1
 REPS=2 timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none \
   -o $O/${TAG}_full -f python scripts/prof_kernels.py c3 colA rows1 colsT rows2 colsW cr_fused crA > $O/${TAG}_full.log 2>&1

@@ -7,7 +7,7 @@ timeout 600 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 for c in c1 c2 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --no-check 2>>$O/${TAG}_configs.err; done > $O/${TAG}_configs.jsonl
 timeout 600 python bench.py --config c4 --T 8 --sched 5,8 --no-cpu-baseline 2>>$O/${TAG}_configs.err > $O/${TAG}_c4_t8.json
 timeout 600 python scripts/decomp_bench_check.py c3 2 > $O/${TAG}_single_series_2dev.json 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 1500 -c 1200 --csv \
+RTN_PROFILE_STEP=1 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $O/${TAG}_launches.csv python bench.py --T 3 --steps 4 --warmup 3 --no-e2e --no-cpu-baseline --no-check > $O/${TAG}_launches.log 2>&1
 REPS=2 timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none \
   -o $O/${TAG}_full -f python scripts/prof_kernels.py c3 colA rows1 colsT rows2 colsW cr_fused crA > $O/${TAG}_full.log 2>&1
