@@ -235,12 +235,13 @@ def profile_traffic(kernel, cfg):
 
 def launches_per_frame(caps, M, cra=False):
     """kernels one frame launches (engine.cu enqueue order, fused CR): per step 1
-    step_begin + 2 decode + 4 setup passes + cap x (5 apply passes + 1 fused CR
-    recurrence) + 1 axpy; then 2 decode + 1 image. With k_crA every recurrence but a
-    step's last also runs the next application's W^-1 column pass (one launch fewer)"""
+    step_begin + 2 decode (k_colA, k_rows1 decode fused with the setup's first row pass) +
+    3 setup passes + cap x (5 apply passes + 1 fused CR recurrence) + 1 axpy; then 2
+    decode + 1 image. With k_crA every recurrence but a step's last also runs the next
+    application's W^-1 column pass (one launch fewer)"""
     n = 0
     for m in range(M):
-        n += 1 + 2 + 4 + 6 * caps[m] + 1
+        n += 1 + 2 + 3 + 6 * caps[m] + 1
         if cra and caps[m] > 1:
             n -= caps[m] - 1
     return n + 3
@@ -265,14 +266,17 @@ class profiled_step:
         return False
 
 
-def launches_per_frame_group(caps, M, A):
+def launches_per_frame_group(caps, M, A, cluster=False):
     """kernels one frame launches on a channel group of A members (group.cu enqueue order,
-    all members): per step and member 1 step_begin + 2 decode + 3 setup passes + 1
-    k_rho_out + 1 k_colsW + 1 k_grp_fin + cap x (5 apply passes + k_grp_fin + k_cr_fused)
-    + 1 closing k_grp_fin + 1 axpy; then per member 2 decode + 1 k_coil_ss, + 1 k_image_grp"""
+    all members, budget mode): per step and member 1 step_begin + 2 decode (+ the setup's
+    first row pass) + 2 setup passes + 1 k_rho_out + 1 k_colsW + 1 k_grp_fin + cap x (the
+    application: 5 passes, or a cluster kernel + k_rho_sum, + k_cr_fused forming the group
+    totals) + 1 closing k_grp_fin + 1 axpy; then per member 2 decode + 1 k_coil_ss, + 1
+    k_image_grp"""
+    per_it = 3 if cluster else 6
     n = 0
     for m in range(M):
-        n += A * (1 + 2 + 3 + 1 + 1 + 1 + 7 * caps[m] + (1 if caps[m] else 0) + 1)
+        n += A * (1 + 2 + 2 + 1 + 1 + 1 + per_it * caps[m] + (1 if caps[m] else 0) + 1)
     return n + 3 * A + 1
 
 
@@ -848,7 +852,7 @@ def main():
                 "latency_ms_min_max": [min(single["lat"]), max(single["lat"])],
                 "e2e": single.get("e2e"), "clocks": single["clocks"],
                 "gpu_launches": (launches_per_frame(caps, M, ctx.fused_cra() and Ts > 1) if As == 1
-                                 else launches_per_frame_group(caps, M, As)) * S,
+                                 else launches_per_frame_group(caps, M, As, cluster=Ts == 1)) * S,
                 "decompositions": dict(single["decompositions"], channel_processes=single.get("channel_processes")),
             })
             line["config"].update({"frames_in_flight": Ts, "channel_group": As,

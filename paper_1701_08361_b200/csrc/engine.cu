@@ -510,14 +510,15 @@ void Engine::enq_step_begin(int m) {
   launch_k(k_step_begin, 1, 32, 0, s_, st_, m);
 }
 
-void Engine::enq_decode(const float2* est, bool full) {
+void Engine::enq_decode(const float2* est, bool full, bool setup) {
   const int J = plan_.J, G = plan_.G, LPB = ops_->LPB, LPBR = ops_->LPBR;
   const int tGc = (plan_.Gc + LPB - 1) / LPB, tGr = (G + LPBR - 1) / LPBR;
   // nr = -1 / R1_DECODE_WIN: all G rows and columns when st->z_out, else the window only
   // (every in-frame consumer of the coils reads them on the window unless the data has
   // samples outside it: k_colsW's / k_rho_out's setup data term)
   ops_->colA(s_, J * tGc, dims_, winv_, twG_, est + static_cast<size_t>(G) * G, U_, 0, full ? G : -1, st_, 0);
-  ops_->rows1(s_, J * tGr, dims_, full ? R1_DECODE : R1_DECODE_WIN, twG_, U_, nullptr, nullptr, nullptr, nullptr, coils_, est, rhom_,
+  ops_->rows1(s_, J * tGr, dims_, full ? R1_DECODE : setup ? R1_DECODE_SETUP : R1_DECODE_WIN, twG_, U_, nullptr,
+              nullptr, nullptr, V_, coils_, est, rhom_,
               st_, 0);
 }
 
@@ -617,9 +618,9 @@ void Engine::enq_setup(const float2* x, const float2* reg, float alpha) {
 
 void Engine::enq_setup_front(const float2* x) {
   const int J = plan_.J, G = plan_.G, LPB = ops_->LPB;
-  const int tG = (G + LPB - 1) / LPB, tL = (dims_.L + ops_->LPBR - 1) / ops_->LPBR;
-  enq_decode(x);
-  ops_->rows1(s_, J * tL, dims_, R1_SETUP, twG_, U_, coils_, rhom_, nullptr, V_, nullptr, nullptr, nullptr, st_, 0);
+  const int tG = (G + LPB - 1) / LPB;
+  // the step's decode and the setup's first row pass in one launch (R1_DECODE_SETUP)
+  enq_decode(x, false, true);
   ops_->colsT(s_, J * tG, dims_, twG_, P_, V_, st_, 0, &tmP_);
   ops_->rows2(s_, dims_.L * dims_.H, dims_, 1, twG_, V_, coils_, rhom_, z_, Y_, RP_, partials_, st_, 0);
   if (dims_.grp) launch_k(k_rho_out, nbr_, kThreads, 0, s_, dims_, coils_, z_, RPO_, partials_, st_);

@@ -207,7 +207,8 @@ class Engine : public FrameWorker {
   void enq_step_begin(int m);
   // full: every coil entry (make_step_cache); else the window only when the frame's data is
   // window-masked (st->z_out == 0, decided on the device)
-  void enq_decode(const float2* est, bool full = false);
+  // setup: also the Newton setup's first row pass (e = rho c_j -> V) on the window rows
+  void enq_decode(const float2* est, bool full = false, bool setup = false);
   void enq_apply(const float2* dx, float2* out, int cw_mode, float alpha, int dot_slot, int use_halt,
                  const float2* ap_prev = nullptr);
   // the two halves of an application / a Newton-step setup: everything up to the

@@ -184,10 +184,11 @@ __device__ __forceinline__ void warp_totals(const double* part, int nb, double (
 #ifndef RTNB_MINB
 #define RTNB_MINB 3
 #endif
-// resident blocks for a target of M 256-thread blocks per SM: rounded up (the default), or
-// down (RTNB_BOUNDS_FLOOR=1: 320-thread blocks get 2 blocks and 96 registers, not 3 and 64)
+// resident blocks for a target of M 256-thread blocks per SM, rounded down: 320-thread
+// blocks (G = 320) get 2 blocks and 96 registers, spill-free, instead of 3 and 64 with
+// spills (C2 +5 %, profiles/r02/ab_bounds_floor.txt); RTNB_BOUNDS_FLOOR=0 rounds up
 #ifndef RTNB_BOUNDS_FLOOR
-#define RTNB_BOUNDS_FLOOR 0
+#define RTNB_BOUNDS_FLOOR 1
 #endif
 #define RTNB_BLOCKS_FOR(M) (RTNB_BOUNDS_FLOOR ? ((M) * 256 / Geo::NT > 0 ? (M) * 256 / Geo::NT : 1) \
                                               : ((M) * 256 + Geo::NT - 1) / Geo::NT)
@@ -307,7 +308,9 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colA(Dims d, const float* __restrict__ 
 
 // R1_DECODE_WIN: R1_DECODE on the window rows and columns only, unless the frame's data
 // has samples outside the window (st->z_out), when it is R1_DECODE
-enum Rows1Mode : int { R1_DECODE = 0, R1_OP = 1, R1_SETUP = 2, R1_DECODE_WIN = 3 };
+// R1_DECODE_SETUP: R1_DECODE_WIN and, on the window rows, R1_SETUP from the coil rows just
+// decoded (the Newton step's decode and its setup's first pass in one launch)
+enum Rows1Mode : int { R1_DECODE = 0, R1_OP = 1, R1_SETUP = 2, R1_DECODE_WIN = 3, R1_DECODE_SETUP = 4 };
 
 // Row pass 1.
 //  DECODE: rows 0..G-1 of U_j -> inverse row FFT -> coils_j (full G x G, scaled 1/G);
@@ -329,12 +332,13 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const f
   if (st->status || (use_halt && st->cr_halt)) return;
   RTNB_TILE_SETUP(false);
   // DEC: the decode instantiation (R1_DECODE / R1_DECODE_WIN), else R1_OP / R1_SETUP
-  bool wdec = false;
+  bool wdec = false, fset = false;
   if constexpr (DEC) {
-    wdec = mode == R1_DECODE_WIN && !st->z_out;
+    fset = mode == R1_DECODE_SETUP;
+    wdec = (mode == R1_DECODE_WIN || fset) && !st->z_out;
     mode = R1_DECODE;
   } else {
-    if (mode == R1_DECODE || mode == R1_DECODE_WIN) return;
+    if (mode == R1_DECODE || mode == R1_DECODE_WIN || mode == R1_DECODE_SETUP) return;
   }
   const int nrows = (mode == R1_DECODE) ? G : LW;
   const int row0 = (mode == R1_DECODE) ? 0 : LO;
@@ -374,15 +378,21 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const f
       }
       if constexpr (DEC) {
         float2* out = coils_out + (size_t)j * G * G + (size_t)r2 * G;
+        const bool wrow = r2 >= LO && r2 < LO + LW;
 #pragma unroll
         for (int k2 = 0; k2 < N2; ++k2) {
           const int p = i2.k + N1 * k2;
-          if (wdec && (p < LO || p >= LO + LW)) continue;
-          out[p] = cscale(flip(u[k2], p), d.invG);
-          if (j == 0) {
+          float2 w = make_float2(0.f, 0.f);
+          if (!(wdec && (p < LO || p >= LO + LW))) {
+            const float2 c = cscale(flip(u[k2], p), d.invG);
+            out[p] = c;
             const float2 x = rho_src[(size_t)r2 * G + p];
-            rhom_out[(size_t)r2 * G + p] = in_win_c<G>(r2, p) ? x : make_float2(0.f, 0.f);
+            const bool win = in_win_c<G>(r2, p);
+            if (j == 0) rhom_out[(size_t)r2 * G + p] = win ? x : make_float2(0.f, 0.f);
+            // the setup's e = rho * c_j on the window (nlinv.cpp:252), as k_rows1 R1_SETUP
+            if (fset && win) w = flip(cmul_rn(x, c), p);
           }
+          if (fset) u[k2] = wrow ? w : make_float2(0.f, 0.f);
         }
       } else {
 #pragma unroll
@@ -401,7 +411,25 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const f
         }
       }
     }
-    if constexpr (DEC) return;  // uniform across the block: no barrier follows
+    if constexpr (DEC) {
+      if (!fset) return;  // uniform across the block: no barrier follows
+      // R1_DECODE_SETUP: the forward Toeplitz row transform of e on the window rows, in
+      // the reverse step order (as R1_OP), into V
+      const bool w2 = a2 && r2 >= LO && r2 < LO + LW, w1 = a1 && r1 >= LO && r1 < LO + LW;
+      if (w2) inv_inner<Geo, -1, Geo::WIN_K2>(A, i2.l, i2.k, u, twG);
+      row_line_sync<Geo>();
+      if (w1) {
+        get_step1<Geo>(A, i1.l, i1.k, v);
+        dft_m<N1, -1, Geo::ALL_N1, Geo::ALL_N1>(v);
+        float2* Vr = V + (size_t)j * LW * G + (size_t)(r1 - LO) * G;
+#pragma unroll
+        for (int n1 = 0; n1 < N1; ++n1) {
+          const int t = N2 * n1 + i1.k;
+          Vr[t] = flip(v[n1], t);
+        }
+      }
+      return;
+    }
     // OP: the forward Toeplitz row transform in the reverse step order (inner DFTs over
     // the window k2 on the registers, one exchange, outer DFT over k1)
     if (a2) inv_inner<Geo, -1, Geo::WIN_K2>(A, i2.l, i2.k, u, twG);

@@ -169,7 +169,9 @@ Engine::Ops Inst<N1, N2>::make() {
   o.rows1 = [](cudaStream_t s, int grid, Dims d, int mode, const float4* tw, const float2* U,
                const float2* coils, const float2* rhom, const float2* drho, float2* V, float2* coils_out,
                const float2* rho_src, float2* rhom_out, const DevState* st, int h) {
-    launch_k((mode == R1_DECODE || mode == R1_DECODE_WIN) ? k_rows1<GeoR, true> : k_rows1<GeoR, false>, grid,
+    launch_k((mode == R1_DECODE || mode == R1_DECODE_WIN || mode == R1_DECODE_SETUP) ? k_rows1<GeoR, true>
+                                                                                    : k_rows1<GeoR, false>,
+             grid,
              kNTR, kSmemR, s, d, mode, tw, U, coils, rhom, drho, V, coils_out, rho_src,
              rhom_out, st, h);
   };
