@@ -536,6 +536,7 @@ ColsWArgs Engine::cluster_args(const float2* dx, float2* out, int cw_mode, float
   a.out = out;
   a.ap_prev = ap_prev;
   a.win_only_ok = win_only_ok_;
+  a.defer_out = defer_w_;
   return a;
 }
 
@@ -727,6 +728,10 @@ void Engine::enq_cr_fused(int it, float tol, const DeferRed& dr) {
 }
 
 bool Engine::fused_crA() const { return fused_crA_ && fused_cr_ && ops_->crA != nullptr && !dims_.grp; }
+
+int Engine::back_grid() const {
+  return use_cluster_ ? rho_grid_ : plan_.J * ((plan_.Gc + ops_->LPB - 1) / ops_->LPB) + nbr_;
+}
 
 int Engine::crA_grid() const {
   const int nbc = plan_.J * ((plan_.Gc + ops_->LPB - 1) / ops_->LPB);

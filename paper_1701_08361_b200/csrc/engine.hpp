@@ -241,6 +241,8 @@ class Engine : public FrameWorker {
     d.gs = gs_;
     return d;
   }
+  // blocks of this member's back half (k_rho_sum on the cluster path, else k_colsW)
+  int back_grid() const;
   void enq_axpy1();
   void enq_state_reset();
   void enq_z_scan();  // st->z_out for the data now in z_ (stream ordered)

@@ -266,6 +266,19 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
   if (run_cr) {
     // the fused recurrence handles every CR vector, so the window-only skip is exact
     each([&](int, Engine& e) { e.win_only_ok_ = 1; });
+    // budget mode: the back halves leave per-block dot partials, which every member's
+    // recurrence sums member by member (DeferRed::grp = 2), in place of their grid
+    // reductions and k_grp_fin
+    DeferRed gdr = mem_[0]->group_red();
+    if (!sync_each) {
+      gdr.grp = 2;
+      for (int d = 0; d < A_; ++d) {
+        Engine& m = *mem_[static_cast<size_t>(d)];
+        gdr.gw[d] = m.dpart_w_;
+        gdr.gnw[d] = m.back_grid();
+      }
+      each([&](int, Engine& e) { e.defer_w_ = e.dpart_w_; });
+    }
     const bool cl = mem_[0]->use_cluster_;
     for (int it = 0; it < cap; ++it) {
       if (cl) {
@@ -284,7 +297,9 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
           e.enq_grp_fin(0, it, -1, tol);
           e.enq_cr_fused(it, tol);
         } else {
-          e.enq_cr_fused(it, tol, e.group_red());  // k_grp_fin's sums inside the recurrence
+          DeferRed dr = gdr;  // k_grp_fin's sums inside the recurrence
+          dr.gs = e.gs_;
+          e.enq_cr_fused(it, tol, dr);
         }
       });
       if (sync_each) {
@@ -298,7 +313,10 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
       barrier();
       each([&](int, Engine& e) { e.enq_grp_fin(0, -1, cap - 1, tol); });
     }
-    each([&](int, Engine& e) { e.win_only_ok_ = 0; });
+    each([&](int, Engine& e) {
+      e.win_only_ok_ = 0;
+      e.defer_w_ = nullptr;
+    });
   } else {
     // no CR iteration follows: a lagging member may still be reading this step's setup
     // partials in its k_grp_fin when the next step's setup_front overwrites them

@@ -99,8 +99,11 @@ struct DeferRed {
   double* out;      // this recurrence's partials, 2 per block (nullptr: grid reduction + tail)
   // channel group, budget mode: the member partials of the application's dots (pcw) and of
   // the previous recurrence (pcr) summed in member order here, in place of k_grp_fin
-  int grp;
+  int grp;         // 1: dots from the members' grid-reduced partials (pcw); 2: from every
+                   // member's per-block partials gw[m] (gnw[m] blocks), member by member
   GroupScal gs;
+  const double* gw[kMaxGroup];
+  int gnw[kMaxGroup];
 };
 
 // CR scalars of the current step: rar[k] = <r, A r> after apply k, ap2[k] = |ap|^2

@@ -517,6 +517,10 @@ __global__ void __launch_bounds__(kThreads) k_rho_sum(Dims d, ColsWArgs a, const
     __syncthreads();
   }
   double vv[3] = {acc, aa, pa}, tot[3];
+  if (a.defer_out) {  // per-block partials for the recurrence (DeferRed)
+    block_partial<3>(vv, a.defer_out);
+    return;
+  }
   if (grid_reduce<3>(vv, partials, &st->counter, tot) && threadIdx.x == 0) {
     if (d.grp) {  // member partials; k_grp_fin forms the totals in member order
       if (a.dot_slot >= 0) {

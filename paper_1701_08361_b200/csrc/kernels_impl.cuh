@@ -1073,6 +1073,18 @@ __device__ inline bool cr_begin(DevState* st, const CrScalars& cr, int it, float
     // of every member sums the same member partials in the same order
     __shared__ double g_c[2];
     __shared__ int g_ok;
+    double wt[3] = {0.0, 0.0, 0.0};
+    if (dr.grp == 2 && threadIdx.x < 32) {
+      // every member's per-block dot partials: each member's blocks in order (warp_totals),
+      // then the members in order
+      for (int m = 0; m < dr.gs.A; ++m) {
+        double t[3];
+        warp_totals<3>(dr.gw[m], dr.gnw[m], t);
+        wt[0] += t[0];
+        wt[1] += t[1];
+        wt[2] += t[2];
+      }
+    }
     if (threadIdx.x == 0) {
       int ok = !(st->status || st->cr_halt);
       const bool rec = blockIdx.x == 0;
@@ -1102,9 +1114,9 @@ __device__ inline bool cr_begin(DevState* st, const CrScalars& cr, int it, float
       }
       double a = 0.0, b = 0.0;
       if (ok) {
-        const double rar = grp_sum(dr.gs, dr.gs.pcw, 3 * it + 0);
-        const double saa = grp_sum(dr.gs, dr.gs.pcw, 3 * it + 1);
-        const double spa = grp_sum(dr.gs, dr.gs.pcw, 3 * it + 2);
+        const double rar = dr.grp == 2 ? wt[0] : grp_sum(dr.gs, dr.gs.pcw, 3 * it + 0);
+        const double saa = dr.grp == 2 ? wt[1] : grp_sum(dr.gs, dr.gs.pcw, 3 * it + 1);
+        const double spa = dr.grp == 2 ? wt[2] : grp_sum(dr.gs, dr.gs.pcw, 3 * it + 2);
         if (rec) {
           cr.rar[it] = rar;
           cr.saa[it] = saa;

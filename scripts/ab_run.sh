@@ -1,12 +1,9 @@
 #!/bin/bash
-# full GPU suite, then same-box A/B: base (previous commit) vs the working tree
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/ab11_tests.log 2>&1; echo "exit $?" >> gpurun_out/ab11_tests.log
+# C5 knobs: vector-recurrence grid and rho blocks; C3 vector grid
 for round in 1 2; do
-  for lib in base new; do
-    if [ $lib = new ]; then export RTN_LIB=$PWD/paper_1701_08361_b200/librtnlinv_b200.so; else export RTN_LIB=$PWD/build_var/lib_$lib.so; fi
-    for c in c3 c4 c1; do timeout 120 python scripts/decomp_probe.py $c 3x1 | sed "s/^/$lib $c /"; done
-    for c in c5 c2; do timeout 120 python scripts/decomp_probe.py $c 2x1 | sed "s/^/$lib $c /"; done
-    timeout 120 python scripts/decomp_probe.py c3 1x1 | sed "s/^/$lib c3-latency /"
-    RTN_CLUSTER=0 timeout 120 python scripts/decomp_probe.py c3 1x1 | sed "s/^/$lib c3-passes /"
-  done
-done > gpurun_out/ab11.txt 2>&1
+  timeout 120 python scripts/decomp_probe.py c5 2x1 | sed "s/^/c5 default /"
+  for v in 444 592; do RTN_VEC_BLOCKS=$v timeout 120 python scripts/decomp_probe.py c5 2x1 | sed "s/^/c5 vec$v /"; done
+  for r in 72 144; do RTN_RHO_BLOCKS=$r timeout 120 python scripts/decomp_probe.py c5 2x1 | sed "s/^/c5 rho$r /"; done
+  RTN_CRA=1 timeout 120 python scripts/decomp_probe.py c5 2x1 | sed "s/^/c5 crA /"
+  for v in 148 444; do RTN_VEC_BLOCKS=$v timeout 120 python scripts/decomp_probe.py c3 3x1 | sed "s/^/c3 vec$v /"; done
+done > gpurun_out/ab12.txt 2>&1

@@ -194,3 +194,27 @@ def test_c1_large_cr_budget_matches_the_reference(gpu, ref):
     assert fr.cg_per_step == per
     assert rel_err(fr.image, img) < FRAME_TOL
     assert rel_err(fr.est, est) < FRAME_TOL
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c1"])
+def test_deferred_cr_reductions_match_grid_reductions(gpu, monkeypatch, cfg):
+    # the budget-mode CR solve with deferred reductions (k_colsW and every recurrence but a
+    # step's last leave per-block partials; the next recurrence forms the totals and takes
+    # the previous iteration's decisions) against the grid reductions with last-block tails
+    # (RTN_DEFER_RED=0): same iteration counts, frames equal to FP64 summation order
+    G, J, K, U, _ = bench.CONFIGS[cfg]
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("RTN_DEFER_RED", mode)
+        plan = _plan(gpu, G, J)
+        # a plain chain on the five-kernel passes (deterministic sources; the cluster path
+        # keeps its own reductions)
+        ctx, s, z, P, idx, scale, out = _bench_series(gpu, plan, 6, gpu.SeriesOptions(plain=True, cluster=0))
+        outs[mode] = (out, [s.estimate(n) for n in range(6)])
+        s.close()
+        ctx.close()
+    a, b = outs["1"], outs["0"]
+    assert list(a[0]["cg_iters"]) == list(b[0]["cg_iters"])
+    for n in range(6):
+        assert rel_err(a[0]["images"][n], b[0]["images"][n]) < 1e-5, n
+        assert rel_err(a[1][n], b[1][n]) < 1e-5, n
