@@ -89,11 +89,27 @@ Series::Series(Engine& primary, int frames, int n_psf, std::vector<int> devices)
   }
   check_cuda(cudaMemcpy(unity_, u.data(), sizeof(float2) * D_, cudaMemcpyHostToDevice), "unity upload");
   if (const char* e = std::getenv("RTN_STEP_SYNC")) step_sync_ = e[0] == '1';
+  if (const char* e = std::getenv("RTN_PRE_LANES")) force_lanes_ = e[0] == '1';
   psf_idx_.resize(static_cast<size_t>(F_));
   for (int n = 0; n < F_; ++n) psf_idx_[static_cast<size_t>(n)] = n % n_psf_;
 }
 
+Series::PreLane::~PreLane() {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(dev);
+  if (copy) cudaStreamSynchronize(copy);
+  pre.reset();
+  for (void* b : {static_cast<void*>(raw), static_cast<void*>(raw_c), static_cast<void*>(z), static_cast<void*>(psf),
+                  static_cast<void*>(nsq)}) {
+    if (b) cudaFree(b);
+  }
+  if (copy) cudaStreamDestroy(copy);
+  cudaSetDevice(cur);
+}
+
 Series::~Series() {
+  lanes_.clear();
   cudaSetDevice(eng0_.device());
   if (copy_) cudaStreamSynchronize(copy_);
   pre_.reset();
@@ -214,7 +230,11 @@ void Series::run_frame(int t, int g, const SeriesOptions& o, SeriesFrameOut& out
 
   if (ready) check_cuda(cudaStreamWaitEvent(s, ready, 0), "wait frame upload");
   check_cuda(cudaSetDevice(e.device()), "set device");
-  e.load_frame(z_ + zsz_ * g, psf_ + psz_ * psf_idx_[static_cast<size_t>(g)]);
+  // the frame's gridded data and PSF: the store, or the lane that ran its pre stage
+  const size_t kr = static_cast<size_t>(g - run_first_);
+  const float2* zl = kr < zsrc_.size() ? zsrc_[kr] : nullptr;
+  const float2* pl = kr < psrc_.size() ? psrc_[kr] : nullptr;
+  e.load_frame(zl ? zl : z_ + zsz_ * g, pl ? pl : psf_ + psz_ * psf_idx_[static_cast<size_t>(g)]);
   e.load_x(init);
   cudaEvent_t ev0, ev1;
   check_cuda(cudaEventCreate(&ev0), "event");
@@ -389,84 +409,152 @@ void Series::post(int first, int count, int mode, float* out) {
   check_cuda(e2, "post sync");
 }
 
+Series::PreLane* Series::lane_for(int t) {
+  if (t == 0) return nullptr;  // worker 0 is the store's engine
+  const int dev = worker(t).device();
+  if (dev == eng0_.device() && !force_lanes_) return nullptr;
+  if (lanes_.size() <= static_cast<size_t>(t)) lanes_.resize(static_cast<size_t>(t) + 1);
+  auto& l = lanes_[static_cast<size_t>(t)];
+  if (!l || l->dev != dev) {
+    l = std::make_unique<PreLane>();
+    l->dev = dev;
+    check_cuda(cudaSetDevice(dev), "set device");
+    check_cuda(cudaStreamCreateWithFlags(&l->copy, cudaStreamNonBlocking), "lane stream");
+    l->pre = std::make_unique<Preproc>(eng0_.plan(), dev);
+    check_cuda(cudaMalloc(&l->psf, sizeof(float2) * psz_ * n_psf_), "lane psf");
+    check_cuda(cudaMalloc(&l->nsq, sizeof(double)), "lane nsq");
+    check_cuda(cudaSetDevice(eng0_.device()), "set device");
+  }
+  return l.get();
+}
+
 void Series::produce_frames(const SeriesOptions& o, int first, int count, const float* z_host,
                             const RawInput* raw, std::vector<cudaEvent_t>& ready) {
   NvtxRange range(raw ? "pre stage (raw acquisitions)" : "frame upload");
   const Plan& p = eng0_.plan();
   const size_t nsamp = raw ? static_cast<size_t>(raw->K) * raw->S : 0;
+  const int T = o.plain ? 1 : std::min(o.T, count);
+  const int Jp = raw && raw->cmat ? raw->Jp : p.J;
+  // where frame k's pre stage runs: the store's copy stream (worker 0 and same-device
+  // workers), or the lane of the worker that reconstructs it (k mod T) on its own device
+  struct View {
+    int dev;
+    cudaStream_t s;
+    Preproc* pre;
+    float2* raw;       // this frame's raw staging
+    float2* raw_c;     // compression: matrix, then per-frame compressed samples
+    float2* z;         // gridded frame destination
+    float2* psf;       // PSF slots
+    std::vector<uint64_t>* keys;
+    double* nsq;
+    PreLane* lane;
+  };
+  zsrc_.assign(static_cast<size_t>(count), nullptr);
+  psrc_.assign(static_cast<size_t>(count), nullptr);
+  std::vector<PreLane*> lane_of(static_cast<size_t>(T), nullptr);
   if (raw) {
     if (!raw->samples || !raw->angles || raw->K < 1 || raw->S < 1) fail(2, "reconstruct_series: empty raw input");
-    const int Jp = raw->cmat ? raw->Jp : p.J;
     if (raw->cmat && Jp < p.J) fail(2, "reconstruct_series: fewer physical than virtual channels");
     if (!pre_) pre_ = std::make_unique<Preproc>(p, eng0_.device());
     const size_t need = static_cast<size_t>(count) * Jp * nsamp;
-    if (need > raw_cap_) {
-      if (raw_) cudaFree(raw_);
-      check_cuda(cudaMalloc(&raw_, sizeof(float2) * need), "raw staging");
-      raw_cap_ = need;
-    }
+    const size_t needc = raw->cmat ? static_cast<size_t>(p.J) * nsamp * count + static_cast<size_t>(p.J) * Jp : 0;
+    auto grow = [](float2*& b, size_t& cap, size_t n, const char* what) {
+      if (n <= cap) return;
+      if (b) cudaFree(b);
+      check_cuda(cudaMalloc(&b, sizeof(float2) * n), what);
+      cap = n;
+    };
+    grow(raw_, raw_cap_, need, "raw staging");
     if (raw->cmat) {
-      const size_t needc = static_cast<size_t>(p.J) * nsamp * count + static_cast<size_t>(p.J) * Jp;
-      if (needc > raw_c_cap_) {
-        if (raw_c_) cudaFree(raw_c_);
-        check_cuda(cudaMalloc(&raw_c_, sizeof(float2) * needc), "compression staging");
-        raw_c_cap_ = needc;
-      }
+      grow(raw_c_, raw_c_cap_, needc, "compression staging");
       check_cuda(cudaMemcpyAsync(raw_c_, raw->cmat, sizeof(float2) * p.J * Jp, cudaMemcpyHostToDevice, copy_),
                  "compression matrix");
     }
+    for (int t = 1; t < T; ++t) {
+      PreLane* l = lane_for(t);
+      lane_of[static_cast<size_t>(t)] = l;
+      if (!l) continue;
+      check_cuda(cudaSetDevice(l->dev), "set device");
+      const size_t nk = static_cast<size_t>((count + T - 1) / T);  // frames of this worker
+      grow(l->raw, l->raw_cap, nk * Jp * nsamp, "lane raw staging");
+      grow(l->z, l->z_cap, nk * zsz_, "lane frames");
+      check_cuda(cudaStreamWaitEvent(l->copy, span0_, 0), "lane span wait");
+      if (raw->cmat) {
+        grow(l->raw_c, l->raw_c_cap, static_cast<size_t>(p.J) * nsamp * nk + static_cast<size_t>(p.J) * Jp,
+             "lane compression staging");
+        check_cuda(cudaMemcpyAsync(l->raw_c, raw->cmat, sizeof(float2) * p.J * Jp, cudaMemcpyHostToDevice, l->copy),
+                   "compression matrix");
+      }
+      check_cuda(cudaSetDevice(eng0_.device()), "set device");
+    }
   }
-  // frame k of the call into store slot first + k, on the copy stream
-  auto produce = [&](int k) {
+  auto view_of = [&](int k) {
     const int n = first + k;
-    float2* zn = z_ + zsz_ * n;
+    PreLane* l = raw ? lane_of[static_cast<size_t>(k % T)] : nullptr;
+    if (!l) {
+      return View{eng0_.device(), copy_, pre_.get(), raw ? raw_ + static_cast<size_t>(k) * Jp * nsamp : nullptr,
+                  raw_c_, z_ + zsz_ * n, psf_, &psf_keys_, nsq_, nullptr};
+    }
+    const size_t slot = static_cast<size_t>(k / T);
+    return View{l->dev, l->copy, l->pre.get(), l->raw + slot * Jp * nsamp, l->raw_c, l->z + zsz_ * slot, l->psf,
+                &l->keys, l->nsq, l};
+  };
+  // frame k of the call: H2D, compression, gridding and its PSF on the view's stream
+  auto produce = [&](int k, const View& v) {
     if (!raw) {
-      check_cuda(cudaMemcpyAsync(zn, z_host + 2 * zsz_ * k, sizeof(float2) * zsz_, cudaMemcpyHostToDevice, copy_),
+      check_cuda(cudaMemcpyAsync(v.z, z_host + 2 * zsz_ * k, sizeof(float2) * zsz_, cudaMemcpyHostToDevice, v.s),
                  "frame upload");
       return;
     }
-    const int Jp = raw->cmat ? raw->Jp : p.J;
-    float2* smp = raw_ + static_cast<size_t>(k) * Jp * nsamp;
+    float2* smp = v.raw;
     check_cuda(cudaMemcpyAsync(smp, raw->samples + 2 * static_cast<size_t>(k) * Jp * nsamp,
-                               sizeof(float2) * Jp * nsamp, cudaMemcpyHostToDevice, copy_),
+                               sizeof(float2) * Jp * nsamp, cudaMemcpyHostToDevice, v.s),
                "raw upload");
     if (raw->cmat) {
-      float2* cs = raw_c_ + static_cast<size_t>(p.J) * Jp + static_cast<size_t>(k) * p.J * nsamp;
-      pre_->apply_compression(raw_c_, p.J, Jp, smp, static_cast<int>(nsamp), cs, copy_);
+      const size_t slot = v.lane ? static_cast<size_t>(k / T) : static_cast<size_t>(k);
+      float2* cs = v.raw_c + static_cast<size_t>(p.J) * Jp + slot * p.J * nsamp;
+      v.pre->apply_compression(v.raw_c, p.J, Jp, smp, static_cast<int>(nsamp), cs, v.s);
       smp = cs;
     }
     const double* ang = raw->angles + static_cast<size_t>(k) * raw->K;
-    pre_->grid_adjoint(smp, p.J, ang, raw->K, raw->S, raw->delay, zn, copy_);
-    // PsfCache::get (preproc.cpp:315-332): one PSF per distinct angle set
+    v.pre->grid_adjoint(smp, p.J, ang, raw->K, raw->S, raw->delay, v.z, v.s);
+    // PsfCache::get (preproc.cpp:315-332): one PSF per distinct angle set (per lane)
     const uint64_t key = psf_angle_key(ang, raw->K, raw->S, p.G);
+    std::vector<uint64_t>& keys = *v.keys;
     int slot = -1;
-    for (size_t i = 0; i < psf_keys_.size(); ++i) {
-      if (psf_keys_[i] == key) slot = static_cast<int>(i);
+    for (size_t i = 0; i < keys.size(); ++i) {
+      if (keys[i] == key) slot = static_cast<int>(i);
     }
     if (slot < 0) {
-      if (static_cast<int>(psf_keys_.size()) >= n_psf_) {
+      if (static_cast<int>(keys.size()) >= n_psf_) {
         fail(2, "reconstruct_series: more distinct spoke-angle sets than PSF slots");
       }
-      slot = static_cast<int>(psf_keys_.size());
-      pre_->build_psf(ang, raw->K, raw->S, psf_ + psz_ * slot, copy_);
-      psf_keys_.push_back(key);
+      slot = static_cast<int>(keys.size());
+      v.pre->build_psf(ang, raw->K, raw->S, v.psf + psz_ * slot, v.s);
+      keys.push_back(key);
     }
-    psf_idx_[static_cast<size_t>(n)] = slot;
+    if (v.lane) {
+      zsrc_[static_cast<size_t>(k)] = v.z;
+      psrc_[static_cast<size_t>(k)] = v.psf + psz_ * slot;
+    } else {
+      psf_idx_[static_cast<size_t>(first + k)] = slot;
+    }
   };
   ready.resize(static_cast<size_t>(count));
-  check_cuda(cudaSetDevice(eng0_.device()), "set device");
   if (first == 0) normalized_ = false;
   for (int k = 0; k < count; ++k) {
     const int g = first + k, sl = g % Sl_;
-    produce(k);
+    const View v = view_of(k);
+    check_cuda(cudaSetDevice(v.dev), "set device");
+    produce(k, v);
     if (g < Sl_) {
       // frame 0 of slice sl arrived: it sets the slice's scale (pipeline.cpp:429-434)
       double sc = 1.0;
       if (o.normalize) {
-        k_nrm2_frame<<<1, 256, 0, copy_>>>(z_ + zsz_ * g, static_cast<long long>(zsz_), nsq_);
+        k_nrm2_frame<<<1, 256, 0, v.s>>>(v.z, static_cast<long long>(zsz_), v.nsq);
         double nsq = 0;
-        check_cuda(cudaMemcpyAsync(&nsq, nsq_, sizeof(double), cudaMemcpyDeviceToHost, copy_), "nsq");
-        check_cuda(cudaStreamSynchronize(copy_), "nsq");
+        check_cuda(cudaMemcpyAsync(&nsq, v.nsq, sizeof(double), cudaMemcpyDeviceToHost, v.s), "nsq");
+        check_cuda(cudaStreamSynchronize(v.s), "nsq");
         sc = nsq > 0 ? 100.0 / std::sqrt(nsq) : 1.0;
       }
       slice_scale_[static_cast<size_t>(sl)] = sc;
@@ -474,12 +562,12 @@ void Series::produce_frames(const SeriesOptions& o, int first, int count, const 
     }
     const double sc = slice_scale_[static_cast<size_t>(sl)];
     if (o.normalize && sc != 1.0) {
-      k_scale_frames<<<148 * 2, 256, 0, copy_>>>(z_ + zsz_ * g, static_cast<long long>(zsz_),
-                                                 static_cast<float>(sc));
+      k_scale_frames<<<148 * 2, 256, 0, v.s>>>(v.z, static_cast<long long>(zsz_), static_cast<float>(sc));
     }
     check_cuda(cudaEventCreateWithFlags(&ready[static_cast<size_t>(k)], cudaEventDisableTiming), "event");
-    check_cuda(cudaEventRecord(ready[static_cast<size_t>(k)], copy_), "event");
+    check_cuda(cudaEventRecord(ready[static_cast<size_t>(k)], v.s), "event");
   }
+  check_cuda(cudaSetDevice(eng0_.device()), "set device");
   normalized_ = true;
 }
 
@@ -514,6 +602,8 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   // end-to-end path: frames produced on the copy stream (H2D, or raw samples through
   // the device pre stage), normalised on arrival
   std::vector<cudaEvent_t> ready;
+  zsrc_.clear();
+  psrc_.clear();
   if (z_host || raw) {
     produce_frames(o, first, count, z_host, raw, ready);
   } else if (o.normalize) {

@@ -123,6 +123,33 @@ class Series {
   size_t raw_c_cap_ = 0;
   void produce_frames(const SeriesOptions& o, int first, int count, const float* z_host, const RawInput* raw,
                       std::vector<cudaEvent_t>& ready);
+  // The raw-input pre stage of the frames a worker on another device reconstructs runs on
+  // that device (its own copy stream, Preproc, staging, PSF cache and gridded frames), so
+  // the H2D copies and gridding of a multi-GPU series are spread over the GPUs and the
+  // worker reads its frame locally. RTN_PRE_LANES=1 also gives same-device workers t >= 1
+  // their own lanes (tests exercise the lane path on one GPU).
+  struct PreLane {
+    int dev = 0;
+    cudaStream_t copy = nullptr;
+    std::unique_ptr<Preproc> pre;
+    float2* raw = nullptr;
+    size_t raw_cap = 0;
+    float2* raw_c = nullptr;
+    size_t raw_c_cap = 0;
+    float2* z = nullptr;       // gridded frames of the current call (count slots)
+    size_t z_cap = 0;
+    float2* psf = nullptr;     // this lane's PSF cache (n_psf slots)
+    std::vector<uint64_t> keys;
+    double* nsq = nullptr;
+    PreLane() = default;
+    PreLane(const PreLane&) = delete;
+    PreLane& operator=(const PreLane&) = delete;
+    ~PreLane();
+  };
+  PreLane* lane_for(int t);
+  std::vector<std::unique_ptr<PreLane>> lanes_;
+  bool force_lanes_ = false;
+  std::vector<const float2*> zsrc_, psrc_;  // per frame of the current run (nullptr: the store)
   std::vector<int> devices_;
   int F_ = 0, n_psf_ = 0, D_ = 0;
   size_t zsz_ = 0, psz_ = 0, isz_ = 0;

@@ -1,9 +1,8 @@
 #!/bin/bash
-# C5 knobs: vector-recurrence grid and rho blocks; C3 vector grid
+# per-worker pre-stage lanes: series tests (lanes forced and not), e2e probe at C3 T=3 with and without lanes
+timeout 900 python -m pytest tests/test_gpu_series.py tests/test_gpu_preproc.py -x -q > gpurun_out/ab14_tests.log 2>&1; echo "exit $?" >> gpurun_out/ab14_tests.log
 for round in 1 2; do
-  timeout 120 python scripts/decomp_probe.py c5 2x1 | sed "s/^/c5 default /"
-  for v in 444 592; do RTN_VEC_BLOCKS=$v timeout 120 python scripts/decomp_probe.py c5 2x1 | sed "s/^/c5 vec$v /"; done
-  for r in 72 144; do RTN_RHO_BLOCKS=$r timeout 120 python scripts/decomp_probe.py c5 2x1 | sed "s/^/c5 rho$r /"; done
-  RTN_CRA=1 timeout 120 python scripts/decomp_probe.py c5 2x1 | sed "s/^/c5 crA /"
-  for v in 148 444; do RTN_VEC_BLOCKS=$v timeout 120 python scripts/decomp_probe.py c3 3x1 | sed "s/^/c3 vec$v /"; done
-done > gpurun_out/ab12.txt 2>&1
+  for l in 0 1; do RTN_PRE_LANES=$l timeout 300 python bench.py --steps 20 --no-cpu-baseline --no-check 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('lanes$l', round(d['value'],1), 'e2e', round(d['e2e']['value'],1))"; done
+done > gpurun_out/ab14.txt 2>&1

@@ -401,9 +401,13 @@ def test_interleaved_slices_equal_independent_series_bit_for_bit(gpu, ref):
     assert [a.frame for a in out["audit"]] == [g // Sl for g in range(F * Sl)]
 
 
-def test_interleaved_slices_with_frames_in_flight_replay_per_slice(gpu, ref):
+@pytest.mark.parametrize("lanes", ["0", "1"])
+def test_interleaved_slices_with_frames_in_flight_replay_per_slice(gpu, ref, lanes, monkeypatch):
     """T = 3 workers over 2 interleaved slices with a short strict prefix: every slice
-    keeps the ordering contract on its own chain and replays through the reference"""
+    keeps the ordering contract on its own chain and replays through the reference.
+    lanes = 1: workers 1 and 2 run the pre stage of their own frames (RTN_PRE_LANES, the
+    multi-GPU layout) and normalise the slices whose first frame they receive"""
+    monkeypatch.setenv("RTN_PRE_LANES", lanes)
     plan = _small_plan(gpu, 16, 3, 3, 6)
     Sl, F, U = 2, 6, 3
     per, samples, angles = _slice_inputs(ref, plan, Sl, F, 5, U, [31, 32])
@@ -434,3 +438,26 @@ def test_interleaved_slices_with_frames_in_flight_replay_per_slice(gpu, ref):
             ests[n] = est
             assert rel_err(out["images"][n * Sl + sl], img * np.float32(1.0 / scale)) < FRAME_TOL, (sl, n)
             assert rel_err(s.estimate(n * Sl + sl), est) < FRAME_TOL, (sl, n)
+
+
+def test_pre_stage_lanes_equal_the_store_path(gpu, ref, monkeypatch):
+    # the raw-input pre stage on per-worker lanes (own stream, Preproc, staging, PSF cache,
+    # gridded frames; the multi-GPU layout, forced on one GPU) against the store's single
+    # copy stream: with compression, T = 3 workers and a fully sequential schedule the
+    # frames are bit-identical
+    plan = gpu.make_plan(24, 4)
+    plan.newton_steps, plan.cg_iter_budget = 5, 20
+    F, U, Jp = 7, 3, 8
+    samples, angles = ref.phantom_series(Jp, F, 11, U, plan.N, 1e-3, 37)
+    m, _ = ref.calibrate_compression(samples[:2], angles[:2], plan.J)
+    outs = {}
+    for lanes in ("0", "1"):
+        monkeypatch.setenv("RTN_PRE_LANES", lanes)
+        s = gpu.Series(gpu.Context(plan), F, U)
+        outs[lanes] = s.run(gpu.SeriesOptions(T=3, sched=gpu.TemporalSchedule(F, 1)),
+                            raw=dict(samples=samples, angles=angles, cmat=m))
+        outs[lanes]["scale"] = s.slice_scale(0)
+    assert list(outs["0"]["cg_iters"]) == list(outs["1"]["cg_iters"])
+    assert outs["0"]["scale"] == outs["1"]["scale"]
+    for n in range(F):
+        assert np.array_equal(outs["0"]["images"][n], outs["1"]["images"][n]), n
