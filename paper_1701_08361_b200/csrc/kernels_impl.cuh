@@ -257,20 +257,20 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colA(Dims d, const float* __restrict__ 
                                                   const float2* __restrict__ chat, float2* __restrict__ U,
                                                   int r0, int nr, const DevState* st, int use_halt) {
   pdl_enter();
-  if (st->status || (use_halt && st->cr_halt)) return;
+  // the state flags load with the first operands (their L2 round trips overlap); the
+  // kernel returns, before writing anything, once they are in
+  const int halt = st->status | (use_halt ? st->cr_halt : 0);
+  const int zo = nr < 0 ? st->z_out : 0;
   RTNB_TILE_SETUP(true);
-  if (nr < 0) {  // decode: every row when the data has samples outside the window
-    r0 = st->z_out ? 0 : LO;
-    nr = st->z_out ? G : LW;
-  }
   const int tiles = (d.Gc + Geo::LPB - 1) / Geo::LPB;
   const int j = blockIdx.x / tiles;
   const int q0 = (blockIdx.x - j * tiles) * Geo::LPB;
   const int nl = min(Geo::LPB, d.Gc - q0);
   const float2* src = chat + (size_t)j * d.Gc * d.Gc;
-  if (i1.on && i1.l < nl) {
+  const bool a1 = i1.on && i1.l < nl;
+  float2 v[N1];
+  if (a1) {
     const int q = q0 + i1.l;
-    float2 v[N1];
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) {
       const int t = N2 * n1 + i1.k;
@@ -282,6 +282,13 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colA(Dims d, const float* __restrict__ 
         v[n1] = flip(make_float2(c.x * w, c.y * w), t);  // chat * winv.real() (nlinv.cpp:121)
       }
     }
+  }
+  if (halt) return;
+  if (nr < 0) {  // decode: every row when the data has samples outside the window
+    r0 = zo ? 0 : LO;
+    nr = zo ? G : LW;
+  }
+  if (a1) {
     if (d.Gc * 4 == G) {  // pruned: only the coil band can be nonzero
       fft_step1<Geo, +1, Geo::GC_N1>(v, i1.k, twG);
     } else {
@@ -329,7 +336,10 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const f
                                                    float2* __restrict__ rhom_out, const DevState* st,
                                                    int use_halt) {
   pdl_enter();
-  if (st->status || (use_halt && st->cr_halt)) return;
+  // the state flags load with the first operands (the decode needs them first: its rows
+  // depend on st->z_out)
+  const int halt = st->status | (use_halt ? st->cr_halt : 0);
+  if (DEC && halt) return;
   RTNB_TILE_SETUP(false);
   // DEC: the decode instantiation (R1_DECODE / R1_DECODE_WIN), else R1_OP / R1_SETUP
   bool wdec = false, fset = false;
@@ -361,6 +371,9 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const f
         const int qk = t - d.off;
         v[n1] = (qk >= 0 && qk < d.Gc) ? flip(Uj[(size_t)r1 * d.Gc + qk], t) : make_float2(0.f, 0.f);
       }
+    }
+    if (!DEC && halt) return;
+    if (a1) {
       if (d.Gc * 4 == G) {  // pruned: only the coil band can be nonzero
         fft_step1<Geo, +1, Geo::GC_N1>(v, i1.k, twG);
       } else {
@@ -458,6 +471,7 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_ROWS1) k_rows1(Dims d, int mode, const f
         }
       }
     }
+    if (halt) return;
     if (a1) {
       fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
       park_step1<Geo>(A, i1.l, i1.k, v);
@@ -537,7 +551,7 @@ __global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
                                                    const DevState* st, int use_halt,
                                                    const __grid_constant__ CUtensorMap tmP) {
   pdl_enter();
-  if (st->status || (use_halt && st->cr_halt)) return;
+  const int halt = st->status | (use_halt ? st->cr_halt : 0);  // consumed after the first loads
   RTNB_TILE_SETUP(true);
   constexpr int tiles = (G + Geo::LPB - 1) / Geo::LPB;
   const int j = blockIdx.x / tiles;
@@ -552,7 +566,7 @@ __global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
   }
   uint64_t* pbar = reinterpret_cast<uint64_t*>(Ps + G * Geo::LPB);
   if constexpr (kColsTTmaP<Geo>) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !halt) {  // (a halted block must not leave copies in flight)
       mbar_init(pbar, 1);
       mbar_expect_tx(pbar, (uint32_t)(sizeof(float2) * G * Geo::LPB));
       constexpr int R = kColsTBoxRows<Geo>;
@@ -570,6 +584,9 @@ __global__ void RTNB_PASS_BOUNDS k_colsT(Dims d, const float4* __restrict__ twG,
       const int t = N2 * n1 + i1.k;
       v[n1] = (t >= LO && t < LO + LW) ? flip(col[(size_t)(t - LO) * G], t) : make_float2(0.f, 0.f);
     }
+  }
+  if (halt) return;
+  if (a1) {
     fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
   }
@@ -697,7 +714,7 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
                                                    double2* __restrict__ RP, double* partials, DevState* st,
                                                    int use_halt) {
   pdl_enter();
-  if (st->status || (use_halt && st->cr_halt)) return;
+  const int halt = st->status | (use_halt ? st->cr_halt : 0);  // consumed after the first loads
   RTNB_TILE_SETUP(false);
   constexpr int L = G / 2;
   float2* RCs = A + Geo::SMEM_FLOAT2;  // LPB x L channel terms of this row
@@ -716,6 +733,9 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_rows2(Dims d, int setup, const float4* 
       const int t = N2 * n1 + i1.k;
       v[n1] = flip(Vr[t], t);
     }
+  }
+  if (halt) return;
+  if (a1) {
     fft_step1<Geo, +1>(v, i1.k, twG);
     park_step1<Geo>(A, i1.l, i1.k, v);
   }
@@ -827,7 +847,7 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
                                                    double* partials, DevState* st, CrScalars cr,
                                                    int use_halt, GroupView gv) {
   pdl_enter();
-  if (st->status || (use_halt && st->cr_halt)) return;
+  const int halt = st->status | (use_halt ? st->cr_halt : 0);  // consumed after the first loads
   RTNB_TILE_SETUP(true);
   const int D0 = G * G;
   double acc0 = 0.0, acc1 = 0.0, aa = 0.0, pa = 0.0;
@@ -853,14 +873,17 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
         pap[kk] = a.ap_prev ? a.ap_prev[e] : make_float2(0.f, 0.f);
       }
     }
+    float2 v[N1];
     if (a1) {
       const float2* col = Y + (size_t)j * LW * d.Gc + q0 + i1.l;
-      float2 v[N1];
 #pragma unroll
       for (int n1 = 0; n1 < N1; ++n1) {
         const int t = N2 * n1 + i1.k;
         v[n1] = (t >= LO && t < LO + LW) ? flip(col[(size_t)(t - LO) * d.Gc], t) : make_float2(0.f, 0.f);
       }
+    }
+    if (halt) return;
+    if (a1) {
       fft_step1<Geo, -1, Geo::WIN_N1>(v, i1.k, twG);
       park_step1<Geo>(A, i1.l, i1.k, v);
     }
@@ -899,6 +922,7 @@ __global__ void RTNB_PASS_BOUNDS_LIGHT k_colsW(Dims d, ColsWArgs a, const float*
       }
     }
   } else {
+    if (halt) return;
     // window: the channel-group partials of k_rows2 added in group order. Outside the
     // window T is masked to zero (preproc.cpp:442), so out.rho there is only the SETUP
     // data term sum_j conj(c_j) z_j, in channel order in FP64

@@ -1,8 +1,13 @@
 #!/bin/bash
-# per-worker pre-stage lanes: series tests (lanes forced and not), e2e probe at C3 T=3 with and without lanes
-timeout 900 python -m pytest tests/test_gpu_series.py tests/test_gpu_preproc.py -x -q > gpurun_out/ab14_tests.log 2>&1; echo "exit $?" >> gpurun_out/ab14_tests.log
+# same-box A/B: base (previous commit) vs the working tree (state flags loaded with the first operands)
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/ab15_tests.log 2>&1; echo "exit $?" >> gpurun_out/ab15_tests.log
 for round in 1 2; do
-  for l in 0 1; do RTN_PRE_LANES=$l timeout 300 python bench.py --steps 20 --no-cpu-baseline --no-check 2>/dev/null | python -c "
-import json,sys
-d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('lanes$l', round(d['value'],1), 'e2e', round(d['e2e']['value'],1))"; done
-done > gpurun_out/ab14.txt 2>&1
+  for lib in base new; do
+    if [ $lib = new ]; then export RTN_LIB=$PWD/paper_1701_08361_b200/librtnlinv_b200.so; else export RTN_LIB=$PWD/build_var/lib_$lib.so; fi
+    for c in c3 c4 c1; do timeout 120 python scripts/decomp_probe.py $c 3x1 | sed "s/^/$lib $c /"; done
+    for c in c5 c2; do timeout 120 python scripts/decomp_probe.py $c 2x1 | sed "s/^/$lib $c /"; done
+    timeout 120 python scripts/decomp_probe.py c3 1x1 | sed "s/^/$lib c3-latency /"
+    RTN_CLUSTER=0 timeout 120 python scripts/decomp_probe.py c3 1x1 | sed "s/^/$lib c3-passes /"
+    REPS=50 timeout 120 python scripts/prof_kernels.py c3 colA rows1 colsT rows2 colsW | sed "s/^/$lib /"
+  done
+done > gpurun_out/ab15.txt 2>&1
