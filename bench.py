@@ -297,7 +297,20 @@ def dist_setup(n_gpus, backend=None):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
+        global _HOST_GROUP
+        _HOST_GROUP = dist.new_group(backend="gloo")
     return rank, world, local
+
+
+_HOST_GROUP = None
+
+
+def host_barrier(world):
+    """a barrier on the host (gloo over TCP): ranks that wait while rank 0 drives every GPU
+    must not leave an NCCL kernel spinning on their device meanwhile"""
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier(group=_HOST_GROUP)
 
 
 def _dist_device(local):
@@ -806,6 +819,7 @@ def main():
                                                  with_e2e=not args.no_e2e)
             except Exception as e:  # reported; the headline then stays the multi-slice figure
                 single = {"error": str(e)}
+        host_barrier(world)  # the other ranks wait on the host: their GPUs are rank 0's now
         barrier(world, local)
         # the same channel decomposition with one process per GPU: every rank is one
         # member (CUDA IPC views of the peers, device-side barriers), one chained frame

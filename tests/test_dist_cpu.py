@@ -40,6 +40,7 @@ def _worker(rank, world, port, q):
         r, w, local = bench.dist_setup(world, backend="gloo")
         assert (r, w) == (rank, world)
         bench.barrier(w, local)
+        bench.host_barrier(w)  # the N > 1 headline's host-side wait (gloo group)
         span = bench.max_over_ranks(10.0 * (rank + 1), w, local)
         value = bench.weak_scaling_value(w, 20, span)
 
