@@ -222,6 +222,16 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def step_traffic(cfg):
+    """whole-step DRAM bytes per frame from the committed app-range capture
+    (profiles/step_traffic.json, scripts/step_range.py), or None"""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "step_traffic.json")))[cfg]
+        return {k: d[k] for k in ("dram_bytes_per_frame", "l2_bytes_per_frame", "source", "how")}
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def profile_traffic(kernel, cfg):
     """dram bytes per launch of `kernel` from the committed ncu --set full summary"""
     try:
@@ -788,6 +798,7 @@ def main():
                 "cold": {"achieved": achieved_cold, "frac": achieved_cold / peak, "kernel_ms": kern[dom]["ms_cold"],
                          "how": "each launch timed alone after a 256 MiB write (L2 flushed)"},
                 "kernel_ms": kern[dom]["ms"], "algorithmic_bytes_per_launch": kern[dom]["bytes"],
+                "step_traffic": step_traffic(cfg),
                 "apply": {"ms": app_ms, "algorithmic_bytes": app_by,
                           "achieved_gbs": app_by / (app_ms / 1000.0) / 1e9},
                 "kernels": kern}
