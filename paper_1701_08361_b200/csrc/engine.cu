@@ -667,6 +667,15 @@ void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
       dr.out = last ? nullptr : dpart_c_[it & 1];
       return dr;
     };
+    // the enqueue-time modes are restored even if an enqueue throws (the op-level calls
+    // that follow must see plain grid reductions)
+    struct Restore {
+      Engine& e;
+      ~Restore() {
+        e.defer_w_ = nullptr;
+        e.win_only_ok_ = 0;
+      }
+    } restore{*this};
     win_only_ok_ = 1;
     defer_w_ = defer ? dpart_w_ : nullptr;
     enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1, nullptr);
@@ -683,8 +692,6 @@ void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
         enq_apply_back(r_, ar_, CW_OPALPHA, alpha, it + 1, 1, ap_);
       }
     }
-    defer_w_ = nullptr;
-    win_only_ok_ = 0;
     return;
   }
   enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1);

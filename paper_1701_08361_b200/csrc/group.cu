@@ -279,6 +279,16 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
       }
       each([&](int, Engine& e) { e.defer_w_ = e.dpart_w_; });
     }
+    // the enqueue-time modes are restored even if an enqueue throws
+    struct Restore {
+      std::vector<std::unique_ptr<Engine>>& m;
+      ~Restore() {
+        for (auto& e : m) {
+          e->win_only_ok_ = 0;
+          e->defer_w_ = nullptr;
+        }
+      }
+    } restore{mem_};
     const bool cl = mem_[0]->use_cluster_;
     for (int it = 0; it < cap; ++it) {
       if (cl) {
@@ -313,10 +323,7 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
       barrier();
       each([&](int, Engine& e) { e.enq_grp_fin(0, -1, cap - 1, tol); });
     }
-    each([&](int, Engine& e) {
-      e.win_only_ok_ = 0;
-      e.defer_w_ = nullptr;
-    });
+
   } else {
     // no CR iteration follows: a lagging member may still be reading this step's setup
     // partials in its k_grp_fin when the next step's setup_front overwrites them
