@@ -200,6 +200,47 @@ def test_group_cluster_applications_match_reference(gpu, ref, A):
         assert rel_err(got[1]["images"][n], got[0]["images"][n]) < 1e-5, n
 
 
+def test_group_cluster_applications_at_g256(gpu, ref):
+    # the C3/C4 instantiation (16 x 16, one 8-CTA cluster per channel) on a channel group:
+    # frames against the reference's WorkerGroup and against the group's five-kernel passes
+    plan = gpu.raw_plan(256, 8)
+    plan.newton_steps, plan.cg_iter_budget = 4, 16
+    with gpu.Context(plan) as probe:
+        if not probe.cluster_supported():
+            pytest.skip("no cluster-fused application for this grid")
+    samples, angles, z, P, idx = _series_inputs(ref, plan, F=2, K=15, U=2)
+    want = ref.reconstruct_series(plan, samples, angles, plain=True, A=2)
+    got = {}
+    for cl in (1, 0):
+        out = _series(gpu, plan, z, P, idx, gpu.SeriesOptions(plain=True, A=2, cluster=cl))
+        got[cl] = out
+        for n in range(2):
+            assert rel_err(out["images"][n], want["images"][n]) < FRAME_TOL, (cl, n)
+        assert list(out["cg_iters"]) == list(want["cg_iters"])
+    for n in range(2):
+        assert rel_err(got[1]["images"][n], got[0]["images"][n]) < 1e-5, n
+
+
+def test_group_workers_with_pre_stage_lanes(gpu, ref, monkeypatch):
+    # raw acquisitions on T = 2 channel-group workers (A = 2): worker 1's frames go through
+    # its own pre-stage lane (forced on one GPU) and its group splits them to its members;
+    # with a sequential schedule the frames equal the store path's bit for bit
+    plan = gpu.make_plan(24, 4)
+    plan.newton_steps, plan.cg_iter_budget = 4, 12
+    F, U = 5, 3
+    samples, angles = ref.phantom_series(plan.J, F, 11, U, plan.N, 1e-3, 41)
+    outs = {}
+    for lanes in ("0", "1"):
+        monkeypatch.setenv("RTN_PRE_LANES", lanes)
+        ctx = gpu.Context(plan)
+        s = gpu.Series(ctx, F, U, devices=_devices(gpu, 4))
+        outs[lanes] = s.run(gpu.SeriesOptions(T=2, A=2, sched=gpu.TemporalSchedule(F, 1)),
+                            raw=dict(samples=samples, angles=angles))
+    assert list(outs["0"]["cg_iters"]) == list(outs["1"]["cg_iters"])
+    for n in range(F):
+        assert np.array_equal(outs["0"]["images"][n], outs["1"]["images"][n]), n
+
+
 @pytest.mark.parametrize("T,A", [(2, 2), (4, 2), (2, 3)])
 def test_hybrid_temporal_channel_series_replays_exactly(gpu, ref, T, A):
     # hybrid T x A split: T frame workers, each a channel group of A members; every
