@@ -650,10 +650,11 @@ void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
     // budget-mode graphs: one fused recurrence kernel per iteration (k_cr_fused)
     // on the pass path the recurrence also runs the next application's W^-1 column pass
     const bool crA = fused_crA() && !use_cluster_;
-    // pass path, one device: k_colsW and every recurrence but the step's last leave their
-    // reductions to the next recurrence (DeferRed)
-    const bool defer = defer_red_ && !use_cluster_ && !dims_.grp;
-    const int nbw = plan_.J * ((plan_.Gc + ops_->LPB - 1) / ops_->LPB) + nbr_;
+    // one device: the application's back half (k_colsW, or k_rho_sum on the cluster path)
+    // and every recurrence but the step's last leave their reductions to the next
+    // recurrence (DeferRed)
+    const bool defer = defer_red_ && !dims_.grp;
+    const int nbw = back_grid();
     int prev_grid = 0;  // block count of the previous recurrence with deferred partials
     auto red = [&](int it, bool last) {
       DeferRed dr{};
