@@ -400,6 +400,7 @@ void Engine::alloc() {
     check_cuda(cudaMalloc(&kpart_, sizeof(double) * 3 * plan_.J * ops_->cluster_ctas), "cluster partials");
     // 32 window entries (x J channel terms) per block
     rho_grid_ = std::max(1, std::min(static_cast<int>((L * L + kRhoTile - 1) / kRhoTile), 4 * 148));
+    if (const char* e = std::getenv("RTN_RHO_SUM_BLOCKS")) rho_grid_ = std::max(1, std::atoi(e));
   }
   // alpha schedule and budget split are data independent (nlinv.cpp:295-313)
   float alpha = plan_.alpha0;
