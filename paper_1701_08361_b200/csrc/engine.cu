@@ -697,16 +697,16 @@ void Engine::enq_cr(float alpha, float tol, int cap, bool sync_each) {
     return;
   }
   enq_apply(r_, ar_, CW_OPALPHA, alpha, 0, 1);
-  launch_k(k_cr_prime, vec_grid_, kThreads, 0, s_, D_, ap_, ar_, partials_, st_, cr_);
+  launch_k(k_cr_prime, vec_grid_, kThreads, 0, s_, D_, ap_, ar_, partials_, st_, cr_, 0, 0);
   for (int it = 1; it <= cap; ++it) {
-    launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, partials_, st_, cr_, it, tol);
+    launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, partials_, st_, cr_, it, tol, 0, 0);
     if (it == cap) break;
     if (sync_each) {
       read_state();
       if (st_host_->status || st_host_->cr_halt) break;
     }
     enq_apply(r_, ar_, CW_OPALPHA, alpha, it, 1);
-    launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, p_, ap_, r_, ar_, partials_, st_, cr_, it);
+    launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, p_, ap_, r_, ar_, partials_, st_, cr_, it, 0, 0);
   }
 }
 
@@ -763,8 +763,21 @@ void Engine::join_group(int rank, const GroupView& gv, const GroupScal& gs) {
   gs_ = gs;
 }
 
-void Engine::enq_grp_fin(int setup, int op_slot, int cr_slot, float tol) {
-  launch_k(k_grp_fin, 1, 32, 0, s_, gs_, st_, cr_, setup, op_slot, cr_slot, tol);
+void Engine::enq_grp_fin(int setup, int op_slot, int cr_slot, float tol, int part) {
+  launch_k(k_grp_fin, 1, 32, 0, s_, gs_, st_, cr_, setup, op_slot, cr_slot, tol, part);
+}
+
+// a channel-group member's exact two-pass CR kernels (tolerance mode): member partials of
+// |ap|^2 and |r|^2, the replicated rho counted on member 0 (k_grp_fin forms the totals)
+void Engine::enq_cr_two_pass_grp(int kind, int it, float tol) {
+  const int rho_skip = dims_.count_rho ? 0 : plan_.G * plan_.G;
+  if (kind == 0) {
+    launch_k(k_cr_prime, vec_grid_, kThreads, 0, s_, D_, ap_, ar_, partials_, st_, cr_, 1, rho_skip);
+  } else if (kind == 1) {
+    launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, p_, ap_, r_, ar_, partials_, st_, cr_, it, 1, rho_skip);
+  } else {
+    launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, partials_, st_, cr_, it, tol, 1, rho_skip);
+  }
 }
 
 void Engine::enq_axpy1() { launch_k(k_axpy1, vec_grid_, kThreads, 0, s_, D_, x_, static_cast<const float2*>(xcg_), static_cast<const DevState*>(st_)); }
@@ -1186,7 +1199,7 @@ double Engine::time_kernel(const char* which, int reps) {
       a.defer_out = dr.w ? dpart_w_ : nullptr;
       ops_->colsW(s_, nbw, dims_, a, winv_, twG_, Y_, RP_, coils_, z_, J * tGc, partials_, st_, cr_, 0, gv_);
     } else if (w == "cr_xr") {
-      launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, partials_, st_, cr_, 1, 0.f);
+      launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, partials_, st_, cr_, 1, 0.f, 0, 0);
     } else if (w == "cr_fused") {
       // a step's last recurrence: the deferred partials in, its own grid reduction out
       launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_,
@@ -1197,7 +1210,7 @@ double Engine::time_kernel(const char* which, int reps) {
       ops_->crA(s_, crA_grid(), J * tGc, dims_, xcg_, r_, p_, ap_, ar_, winv_, twG_, U_, partials_, st_, cr_, 1, 0.f,
                 d2);
     } else if (w == "cr_pap") {
-      launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, p_, ap_, r_, ar_, partials_, st_, cr_, 1);
+      launch_k(k_cr_pap, vec_grid_, kThreads, 0, s_, D_, p_, ap_, r_, ar_, partials_, st_, cr_, 1, 0, 0);
     } else if (w == "colA") {
       ops_->colA(s_, J * tGc, dims_, winv_, twG_, r_ + static_cast<size_t>(G) * G, U_, dims_.lo, dims_.L, st_, 0);
     } else if (w == "apply") {

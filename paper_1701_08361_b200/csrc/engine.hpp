@@ -230,7 +230,9 @@ class Engine : public FrameWorker {
   void enq_setup(const float2* x, const float2* reg, float alpha);
   // group-member kernels (group.cu)
   void join_group(int rank, const GroupView& gv, const GroupScal& gs);
-  void enq_grp_fin(int setup, int op_slot, int cr_slot, float tol);
+  void enq_grp_fin(int setup, int op_slot, int cr_slot, float tol, int part = 0);
+  // kind 0: k_cr_prime, 1: k_cr_pap(it), 2: k_cr_xr(it), with member partials
+  void enq_cr_two_pass_grp(int kind, int it, float tol);
   void enq_cr_fused(int it, float tol, const DeferRed& dr = DeferRed{});
   void enq_crA(int it, float tol, const DeferRed& dr);
   int crA_grid() const;

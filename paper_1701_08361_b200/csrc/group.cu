@@ -264,8 +264,9 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
     run_cr = !mem_[0]->st_host_->cr_halt;
   }
   if (run_cr) {
-    // the fused recurrence handles every CR vector, so the window-only skip is exact
-    each([&](int, Engine& e) { e.win_only_ok_ = 1; });
+    // the fused recurrence handles every CR vector, so the window-only skip is exact (the
+    // tolerance mode's two-pass kernels read every entry of ar: no skip there)
+    each([&](int, Engine& e) { e.win_only_ok_ = sync_each ? 0 : 1; });
     // budget mode: the back halves leave per-block dot partials, which every member's
     // recurrence sums member by member (DeferRed::grp = 2), in place of their grid
     // reductions and k_grp_fin
@@ -302,21 +303,28 @@ void Group::enq_newton_step(int m, float tol, int cap, bool sync_each) {
         each([&](int, Engine& e) { e.enq_apply_back(e.r_, e.ar_, CW_OPALPHA, alpha, it, 1, it > 0 ? e.ap_ : nullptr); });
       }
       barrier();
-      each([&](int, Engine& e) {
-        if (sync_each) {
-          e.enq_grp_fin(0, it, -1, tol);
-          e.enq_cr_fused(it, tol);
-        } else {
+      if (sync_each) {
+        // tolerance mode: the reference's two-pass recurrence with the exact |ap|^2 of the
+        // rounded update (nlinv.cpp:204-230), member partials summed by k_grp_fin
+        each([&](int, Engine& e) {
+          e.enq_grp_fin(0, it, -1, tol);                       // <r, Ar>
+          e.enq_cr_two_pass_grp(it == 0 ? 0 : 1, it, tol);     // ap = ar, or p, ap update
+        });
+        barrier();
+        each([&](int, Engine& e) {
+          e.enq_grp_fin(0, -1, it, tol, 1);                    // |ap|^2
+          e.enq_cr_two_pass_grp(2, it + 1, tol);               // x, r update
+        });
+        barrier();
+        each([&](int, Engine& e) { e.enq_grp_fin(0, -1, it, tol, 2); });  // |r|, stop
+        read_state();
+        if (mem_[0]->st_host_->status || mem_[0]->st_host_->cr_halt) break;
+      } else {
+        each([&](int, Engine& e) {
           DeferRed dr = gdr;  // k_grp_fin's sums inside the recurrence
           dr.gs = e.gs_;
           e.enq_cr_fused(it, tol, dr);
-        }
-      });
-      if (sync_each) {
-        barrier();
-        each([&](int, Engine& e) { e.enq_grp_fin(0, -1, it, tol); });
-        read_state();
-        if (mem_[0]->st_host_->status || mem_[0]->st_host_->cr_halt) break;
+        });
       }
     }
     if (!sync_each) {

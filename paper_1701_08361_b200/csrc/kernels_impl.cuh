@@ -1473,26 +1473,37 @@ __global__ void k_step_begin(DevState* st, int m) {
 }
 
 // after the priming application: r_ar = <r, A r> is in rar[0]; ap = ar, ap2[0] = |ap|^2
+// Channel groups (grp != 0) run these with member partials: the norms skip the replicated
+// rho entries below rho_skip (counted on member 0 only) and go to cr.pcr (the k_cr_fused
+// layout: pcr[2k] = |ap|^2 after update k, pcr[2k+1] = |r|^2 after update k) for
+// k_grp_fin, which forms the totals in member order and takes the decisions.
 __global__ void __launch_bounds__(kThreads) k_cr_prime(int D, float2* __restrict__ ap,
                                                        const float2* __restrict__ ar, double* partials,
-                                                       DevState* st, CrScalars cr) {
+                                                       DevState* st, CrScalars cr, int grp, int rho_skip) {
   pdl_enter();
   if (st->status || st->cr_halt) return;
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
     const float2 v = ar[i];
     ap[i] = v;
-    acc += nrm2(v);
+    if (i >= rho_skip) acc += nrm2(v);
   }
   double v[1] = {acc}, tot[1];
-  if (grid_reduce<1>(v, partials, &st->counter, tot) && threadIdx.x == 0) cr.ap2[0] = tot[0];
+  if (grid_reduce<1>(v, partials, &st->counter, tot) && threadIdx.x == 0) {
+    if (grp) {
+      cr.pcr[0] = tot[0];
+    } else {
+      cr.ap2[0] = tot[0];
+    }
+  }
 }
 
 // iteration `it`, first half: a = r_ar / |ap|^2; x += a p; r -= a ap; rn[it] = |r|
 __global__ void __launch_bounds__(kThreads) k_cr_xr(int D, float2* __restrict__ x, float2* __restrict__ r,
                                                     const float2* __restrict__ p,
                                                     const float2* __restrict__ ap, double* partials,
-                                                    DevState* st, CrScalars cr, int it, float tol) {
+                                                    DevState* st, CrScalars cr, int it, float tol, int grp,
+                                                    int rho_skip) {
   pdl_enter();
   if (st->status || st->cr_halt) return;
   const double denom = cr.ap2[it - 1];
@@ -1519,10 +1530,14 @@ __global__ void __launch_bounds__(kThreads) k_cr_xr(int D, float2* __restrict__ 
       rv = axpy_rn(rv, naf, ap[i]);
       r[i] = rv;
     }
-    acc += nrm2(rv);
+    if (i >= rho_skip) acc += nrm2(rv);
   }
   double v[1] = {acc}, tot[1];
   if (grid_reduce<1>(v, partials, &st->counter, tot) && threadIdx.x == 0) {
+    if (grp) {  // member partial; k_grp_fin (part 2) forms rn[it] and decides
+      cr.pcr[2 * (it - 1) + 1] = tot[0];
+      return;
+    }
     const double rn = sqrt(tot[0]);
     cr.rn[it] = rn;
     StepRec& s = st->steps[st->cur_step];
@@ -1542,7 +1557,7 @@ __global__ void __launch_bounds__(kThreads) k_cr_xr(int D, float2* __restrict__ 
 __global__ void __launch_bounds__(kThreads) k_cr_pap(int D, float2* __restrict__ p, float2* __restrict__ ap,
                                                      const float2* __restrict__ r,
                                                      const float2* __restrict__ ar, double* partials,
-                                                     DevState* st, CrScalars cr, int it) {
+                                                     DevState* st, CrScalars cr, int it, int grp, int rho_skip) {
   pdl_enter();
   if (st->status || st->cr_halt) return;
   const double rar_new = cr.rar[it], rar_old = cr.rar[it - 1];
@@ -1558,10 +1573,16 @@ __global__ void __launch_bounds__(kThreads) k_cr_pap(int D, float2* __restrict__
     const float2 nap = make_float2(__fadd_rn(__fmul_rn(apv.x, bf), arv.x), __fadd_rn(__fmul_rn(apv.y, bf), arv.y));
     p[i] = np;
     ap[i] = nap;
-    acc += nrm2(nap);
+    if (i >= rho_skip) acc += nrm2(nap);
   }
   double v[1] = {acc}, tot[1];
-  if (grid_reduce<1>(v, partials, &st->counter, tot) && threadIdx.x == 0) cr.ap2[it] = tot[0];
+  if (grid_reduce<1>(v, partials, &st->counter, tot) && threadIdx.x == 0) {
+    if (grp) {
+      cr.pcr[2 * it] = tot[0];
+    } else {
+      cr.ap2[it] = tot[0];
+    }
+  }
 }
 
 // Fused CR recurrence for the budget-mode frame graphs: iteration `it` second half
@@ -1685,8 +1706,10 @@ __global__ void __launch_bounds__(kThreads) k_rho_out(Dims d, const float2* __re
 //  setup:       |rhs|^2, resid_out, resid_win of the step; cg_solve entry checks
 //  cr_slot >= 0: k_cr_fused(cr_slot): ap2[cr_slot], rn[cr_slot+1], iters, tolerance stop
 //  op_slot >= 0: colsW of application op_slot: rar, saa, spa
+//  part (cr_slot >= 0): 0 both halves (k_cr_fused), 1 only ap2[cr_slot] (after k_cr_pap /
+//               k_cr_prime), 2 only the |r| half (after k_cr_xr(cr_slot + 1))
 __global__ void k_grp_fin(GroupScal g, DevState* st, CrScalars cr, int setup, int op_slot, int cr_slot,
-                          float tol) {
+                          float tol, int part) {
   pdl_enter();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (st->status) return;
@@ -1712,8 +1735,8 @@ __global__ void k_grp_fin(GroupScal g, DevState* st, CrScalars cr, int setup, in
     return;
   }
   if (st->cr_halt) return;
-  if (cr_slot >= 0) {
-    cr.ap2[cr_slot] = grp_sum(g, g.pcr, 2 * cr_slot);
+  if (cr_slot >= 0 && part != 2) cr.ap2[cr_slot] = grp_sum(g, g.pcr, 2 * cr_slot);
+  if (cr_slot >= 0 && part != 1) {
     const double rn = sqrt(grp_sum(g, g.pcr, 2 * cr_slot + 1));
     cr.rn[cr_slot + 1] = rn;
     if (!isfinite(rn)) {

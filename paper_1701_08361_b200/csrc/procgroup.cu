@@ -166,23 +166,25 @@ void ProcGroup::enq_newton_step(int m, float tol, int cap, bool sync_each) {
     run_cr = !e.st_host_->cr_halt;
   }
   if (run_cr) {
-    e.win_only_ok_ = 1;
+    e.win_only_ok_ = sync_each ? 0 : 1;  // the two-pass kernels read every entry of ar
     for (int it = 0; it < cap; ++it) {
       e.enq_apply_front(e.r_, 1);
       barrier();
       e.enq_apply_back(e.r_, e.ar_, CW_OPALPHA, alpha, it, 1, it > 0 ? e.ap_ : nullptr);
       barrier();
       if (sync_each) {
+        // tolerance mode: the exact two-pass recurrence (as the in-process group)
         e.enq_grp_fin(0, it, -1, tol);
-        e.enq_cr_fused(it, tol);
-      } else {
-        e.enq_cr_fused(it, tol, e.group_red());  // k_grp_fin's sums inside the recurrence
-      }
-      if (sync_each) {
+        e.enq_cr_two_pass_grp(it == 0 ? 0 : 1, it, tol);
         barrier();
-        e.enq_grp_fin(0, -1, it, tol);
+        e.enq_grp_fin(0, -1, it, tol, 1);
+        e.enq_cr_two_pass_grp(2, it + 1, tol);
+        barrier();
+        e.enq_grp_fin(0, -1, it, tol, 2);
         read_state();
         if (e.st_host_->status || e.st_host_->cr_halt) break;
+      } else {
+        e.enq_cr_fused(it, tol, e.group_red());  // k_grp_fin's sums inside the recurrence
       }
     }
     if (!sync_each) {

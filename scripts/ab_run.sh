@@ -1,6 +1,4 @@
 #!/bin/bash
-# latency-mode knobs: k_rho_sum grid and the vector-recurrence grid at T = 1
-for round in 1 2; do
-  for r in 512 256 148; do RTN_RHO_SUM_BLOCKS=$r timeout 120 python scripts/decomp_probe.py c3 1x1 | sed "s/^/rhosum$r /"; done
-  for v in 148 296 444; do RTN_VEC_BLOCKS=$v timeout 120 python scripts/decomp_probe.py c3 1x1 | sed "s/^/vec$v /"; done
-done > gpurun_out/ab19.txt 2>&1
+# group tolerance mode (exact two-pass recurrence): channel and process-group tests, then the full suite
+timeout 900 python -m pytest tests/test_gpu_channel.py tests/test_gpu_procgroup.py -x -q > gpurun_out/ab20_tests.log 2>&1; echo "exit $?" >> gpurun_out/ab20_tests.log
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/ab20_all.log 2>&1; echo "exit $?" >> gpurun_out/ab20_all.log

@@ -48,15 +48,16 @@ def _member(rank, world, port, plan_args, z, P, q):
 
 
 @pytest.mark.timeout(900)
-def test_two_process_channel_group_matches_in_process_group_and_reference(gpu, ref):
+@pytest.mark.parametrize("budget", [6, 0])  # 0: tolerance mode (the exact two-pass recurrence)
+def test_two_process_channel_group_matches_in_process_group_and_reference(gpu, ref, budget):
     plan = gpu.make_plan(16, 3)
-    plan.newton_steps, plan.cg_iter_budget = 3, 6
+    plan.newton_steps, plan.cg_iter_budget = 3, budget
     inp = phantom_frame_inputs(ref, plan, K=7, U=1)
     z, P = inp["z"][0], inp["P"][0]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_member, args=(r, 2, port, (16, 3, 3, 6), z, P, q)) for r in range(2)]
+    procs = [ctx.Process(target=_member, args=(r, 2, port, (16, 3, 3, budget), z, P, q)) for r in range(2)]
     for p in procs:
         p.start()
     try:
