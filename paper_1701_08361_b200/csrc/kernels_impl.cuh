@@ -162,24 +162,9 @@ __device__ __forceinline__ void warp_totals(const double* part, int nb, double (
   double s[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) s[k] = 0.0;
-  // four blocks per lane in flight at a time (one L2 round trip per 128 blocks, not per
-  // 32), accumulated in the same ascending order
-  constexpr int kB = 4;
-  for (int b0 = lane; b0 < nb; b0 += 32 * kB) {
-    double t[kB][K];
+  for (int b = lane; b < nb; b += 32) {
 #pragma unroll
-    for (int u = 0; u < kB; ++u) {
-      const int b = b0 + 32 * u;
-#pragma unroll
-      for (int k = 0; k < K; ++k) t[u][k] = b < nb ? __ldcg(part + b * K + k) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < kB; ++u) {
-      if (b0 + 32 * u < nb) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) s[k] += t[u][k];
-      }
-    }
+    for (int k = 0; k < K; ++k) s[k] += __ldcg(part + b * K + k);
   }
 #pragma unroll
   for (int k = 0; k < K; ++k) tot[k] = __shfl_sync(0xffffffffu, warp_sum(s[k]), 0);
