@@ -168,6 +168,37 @@ Registry& registry() {
     };
     prefer_rows2(320, 20, 16);
     prefer_colA(384, 16, 24);  // spill-free, neutral at C5 (k_crA from 16 x 24 there: -1.5 %)
+    // measured per kernel (RTN_GEO_<G>_<kernel>, profiles/r02/ab_geo_per_kernel.txt):
+    // G = 320's k_colsW from 20 x 16 (C2 +6 %), G = 384's k_rows1 from 16 x 24 (C5 +0.9 %)
+    {
+      Engine::Ops* dflt = nullptr;
+      if (const Engine::Ops* alt = alt_of(320, 20, 16, dflt); alt && dflt->LPB == alt->LPB) dflt->colsW = alt->colsW;
+      if (const Engine::Ops* alt = alt_of(384, 16, 24, dflt); alt && dflt->LPBR == alt->LPBR) dflt->rows1 = alt->rows1;
+    }
+    // tuning: RTN_GEO_<G>_<kernel>=N1xN2 takes one pass kernel of the default geometry of G
+    // from another factorisation with the same lines per block
+    for (auto& o : reg->ops) {
+      for (const char* k : {"colA", "rows1", "colsT", "rows2", "colsW", "crA"}) {
+        const std::string var = "RTN_GEO_" + std::to_string(o.G) + "_" + k;
+        const char* e = std::getenv(var.c_str());
+        if (!e) continue;
+        int n1 = 0, n2 = 0;
+        if (std::sscanf(e, "%dx%d", &n1, &n2) != 2) continue;
+        Engine::Ops* dflt = nullptr;
+        const Engine::Ops* alt = alt_of(o.G, n1, n2, dflt);
+        if (!alt || dflt != &o) continue;
+        const std::string kk(k);
+        if (kk == "colA" && alt->LPB == o.LPB) o.colA = alt->colA;
+        if (kk == "colsT" && alt->LPB == o.LPB) o.colsT = alt->colsT;
+        if (kk == "colsW" && alt->LPB == o.LPB) o.colsW = alt->colsW;
+        if (kk == "crA" && alt->LPB == o.LPB) {
+          o.crA = alt->crA;
+          o.crA_N1 = alt->crA_N1;
+        }
+        if (kk == "rows1" && alt->LPBR == o.LPBR) o.rows1 = alt->rows1;
+        if (kk == "rows2" && alt->LPBR == o.LPBR) o.rows2 = alt->rows2;
+      }
+    }
     return reg;
   }();
   return *r;
