@@ -2,7 +2,7 @@
 # Round measurement: default bench line, every BASELINE config, C4 as configured (8 frames
 # in flight, t-k schedule), the N>1 headline path on this GPU, the launch list and one
 # ncu --set full summary of the C3 kernels. TAG names the outputs.
-TAG=${TAG:-r02v4}; O=gpurun_out; mkdir -p $O
+TAG=${TAG:-r02v5}; O=gpurun_out; mkdir -p $O
 timeout 600 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 for c in c1 c2 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --no-check 2>>$O/${TAG}_configs.err; done > $O/${TAG}_configs.jsonl
 timeout 600 python bench.py --config c4 --T 8 --sched 5,8 --no-cpu-baseline 2>>$O/${TAG}_configs.err > $O/${TAG}_c4_t8.json
