@@ -1,10 +1,10 @@
 #!/bin/bash
-# same-box A/B: k_crA with a 2-block residency target (128 registers, spill-free)
+# channel-chunked applications (RTN_CHUNKS): C5 and C3 throughput, parity at C5 chunked
+RTN_CHUNKS=2 timeout 900 python -m pytest tests/test_gpu_configs.py tests/test_gpu_ops.py -x -q -k "c5 or c3_bench or 384" > gpurun_out/ab25_tests.log 2>&1; echo "exit $?" >> gpurun_out/ab25_tests.log
 for round in 1 2; do
-  for lib in base cra2; do
-    export RTN_LIB=$PWD/build_var/lib_$lib.so
-    for c in c3 c4 c1; do timeout 120 python scripts/decomp_probe.py $c 3x1 | sed "s/^/$lib $c /"; done
-    timeout 120 python scripts/decomp_probe.py c2 3x1 | sed "s/^/$lib c2 /"
-    RTN_CLUSTER=0 timeout 120 python scripts/decomp_probe.py c3 1x1 | sed "s/^/$lib c3-passes /"
+  for ch in 1 2 4; do
+    RTN_CHUNKS=$ch timeout 120 python scripts/decomp_probe.py c5 2x1 1x1 | sed "s/^/chunks$ch c5 /"
+    RTN_CHUNKS=$ch timeout 120 python scripts/decomp_probe.py c3 3x1 | sed "s/^/chunks$ch c3 /"
+    RTN_CHUNKS=$ch timeout 120 python scripts/decomp_probe.py c2 3x1 | sed "s/^/chunks$ch c2 /"
   done
-done > gpurun_out/ab24.txt 2>&1
+done > gpurun_out/ab25.txt 2>&1
