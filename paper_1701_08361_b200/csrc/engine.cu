@@ -349,7 +349,7 @@ Engine::~Engine() {
   if (frame_graph_) cudaGraphExecDestroy(frame_graph_);
   void* bufs[] = {winv_, P_, z_, x_, xcg_, r_, p_, ap_, ar_, reg_, est_scratch_[0], est_scratch_[1],
                   est_scratch_[2], coils_, rhom_, U_, V_, Y_, RP_, gbuf_, img_, partials_, st_, cr_buf_,
-                  RPO_, SS_, RC_, kpart_};
+                  RPO_, SS_, RC_, kpart_, dpart_w_};
   for (void* b : bufs) {
     if (b) cudaFree(b);
   }
