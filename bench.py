@@ -258,13 +258,16 @@ def launches_per_frame(caps, M, cra=False):
 
 
 class profiled_step:
-    """RTN_PROFILE_STEP=1: cudaProfilerStart/Stop around the timed step, so
-    `ncu --profile-from-start off --metrics gpu__time_duration.sum ...` lists exactly the
-    timed frames' kernels (a no-op otherwise)"""
+    """RTN_PROFILE_STEP=1 (RTN_PROFILE_E2E=1 for the e2e run): cudaProfilerStart/Stop around
+    the timed step, so `ncu --profile-from-start off --metrics gpu__time_duration.sum ...`
+    lists exactly the timed frames' kernels (a no-op otherwise)"""
+
+    def __init__(self, var="RTN_PROFILE_STEP"):
+        self.var = var
 
     def __enter__(self):
         self.rt = None
-        if os.environ.get("RTN_PROFILE_STEP") == "1":
+        if os.environ.get(self.var) == "1":
             import ctypes
             self.rt = ctypes.CDLL("libcudart.so.12")
             self.rt.cudaProfilerStart()
@@ -543,9 +546,10 @@ def e2e_raw(pb, make_series, plan, opts, cfg, F, S, world, local):
     T0 += S
     raw_in = dict(samples_ptr=rt.data_ptr() + T0 * fb, S=Ssp, angles=ang[T0:T0 + S])
     barrier(world, local)
-    t0 = time.perf_counter()
-    rs.run(opts, first=T0, count=S, raw=raw_in, images_ptr=imt.data_ptr() + T0 * ib)
-    wall = time.perf_counter() - t0
+    with profiled_step("RTN_PROFILE_E2E"):
+        t0 = time.perf_counter()
+        rs.run(opts, first=T0, count=S, raw=raw_in, images_ptr=imt.data_ptr() + T0 * ib)
+        wall = time.perf_counter() - t0
     print(f"[bench] e2e wall {wall * 1e3:.1f} ms, device span {rs.last_span_ms():.1f} ms", file=sys.stderr,
           flush=True)
     barrier(world, local)

@@ -813,8 +813,9 @@ void Engine::enq_cr_two_pass_grp(int kind, int it, float tol) {
 
 void Engine::enq_axpy1() { launch_k(k_axpy1, vec_grid_, kThreads, 0, s_, D_, x_, static_cast<const float2*>(xcg_), static_cast<const DevState*>(st_)); }
 
-void Engine::enq_z_scan() {
+void Engine::enq_z_scan(bool masked) {
   check_cuda(cudaMemsetAsync(&st_->z_out, 0, sizeof(int), s_), "z scan reset");
+  if (masked) return;
   launch_k(k_z_outside, blocks_for(static_cast<long long>(plan_.J) * plan_.G * plan_.G, 148 * 4), kThreads, 0, s_,
            dims_, static_cast<const float2*>(z_), st_);
 }
@@ -837,10 +838,10 @@ void Engine::enq_image_grp(float2* img, float scale, bool apply_scale) {
 
 // ---- FrameWorker: full-layout device buffers in, stream ordered -----------------
 
-void Engine::load_frame(const float2* z, const float2* P) {
+void Engine::load_frame(const float2* z, const float2* P, bool masked) {
   check_cuda(cudaMemcpyAsync(z_, z, sizeof(float2) * plan_.J * plan_.G * plan_.G, cudaMemcpyDefault, s_), "z");
   check_cuda(cudaMemcpyAsync(P_, P, sizeof(float2) * plan_.G * plan_.G, cudaMemcpyDefault, s_), "psf");
-  enq_z_scan();
+  enq_z_scan(masked);
 }
 void Engine::load_x(const float2* src) {
   check_cuda(cudaMemcpyAsync(x_, src, sizeof(float2) * D_, cudaMemcpyDefault, s_), "x");

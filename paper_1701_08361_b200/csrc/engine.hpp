@@ -85,7 +85,9 @@ class FrameWorker {
   virtual cudaStream_t stream() const = 0;
   virtual int width() const { return 1; }  // channel-decomposition width A
   virtual bool budget_mode() const = 0;
-  virtual void load_frame(const float2* z, const float2* P) = 0;
+  // masked: the data is window-masked by construction (the device pre stage), so the
+  // outside-window scan is skipped (st->z_out = 0)
+  virtual void load_frame(const float2* z, const float2* P, bool masked = false) = 0;
   virtual void load_x(const float2* src) = 0;
   virtual void load_reg(const float2* src) = 0;
   virtual void store_x(float2* dst) = 0;
@@ -166,7 +168,7 @@ class Engine : public FrameWorker {
   void frame_run_sync(const RegFn& reg, float2* img_dst, float image_scale, bool apply_scale,
                       FrameStats* stats) override;
   bool budget_mode() const override { return plan_.cg_iter_budget > 0; }
-  void load_frame(const float2* z, const float2* P) override;
+  void load_frame(const float2* z, const float2* P, bool masked = false) override;
   void load_x(const float2* src) override;
   void load_reg(const float2* src) override;
   void store_x(float2* dst) override;
@@ -247,7 +249,7 @@ class Engine : public FrameWorker {
   int back_grid() const;
   void enq_axpy1();
   void enq_state_reset();
-  void enq_z_scan();  // st->z_out for the data now in z_ (stream ordered)
+  void enq_z_scan(bool masked = false);  // st->z_out for the data now in z_ (stream ordered)
   void enq_coil_ss();
   void enq_image_grp(float2* img, float scale, bool apply_scale);
   void enq_pg_barrier(int* own_flags, const GroupFlags& f);

@@ -211,7 +211,7 @@ void Group::split_copy(const float2* src, bool reg) {
   }
 }
 
-void Group::load_frame(const float2* z, const float2* P) {
+void Group::load_frame(const float2* z, const float2* P, bool masked) {
   const size_t G2 = static_cast<size_t>(plan_.G) * plan_.G;
   cudaStream_t s = mem_[0]->s_;
   check_cuda(cudaSetDevice(mem_[0]->dev_), "set device");
@@ -223,7 +223,7 @@ void Group::load_frame(const float2* z, const float2* P) {
   }
   // each member scans its own block on its stream, ordered after the copies
   fork();
-  each([&](int, Engine& e) { e.enq_z_scan(); });
+  each([&](int, Engine& e) { e.enq_z_scan(masked); });
   join();
 }
 

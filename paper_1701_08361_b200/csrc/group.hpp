@@ -44,7 +44,7 @@ class Group : public FrameWorker {
   Engine& member(int d) { return *mem_[static_cast<size_t>(d)]; }
 
   // FrameWorker (full-layout device sources / destinations)
-  void load_frame(const float2* z, const float2* P) override;
+  void load_frame(const float2* z, const float2* P, bool masked = false) override;
   void load_x(const float2* src) override;
   void load_reg(const float2* src) override;
   void store_x(float2* dst) override;

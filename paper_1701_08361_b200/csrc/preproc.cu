@@ -107,9 +107,11 @@ __global__ void __launch_bounds__(kPre) k_grid_gather(int J, int G, int n, const
   }
 }
 
-// z *= float(G) / deapodization, then mask_window (preproc.cpp:193-195)
+// z *= float(G) / deapodization, then mask_window (preproc.cpp:193-195); with apply_post,
+// then the series' normalisation z *= post (prep_series, nlinv.cpp:390-400) in the same
+// float multiply the separate scaling pass would do
 __global__ void __launch_bounds__(kPre) k_deapod_mask(int J, int G, const float* __restrict__ f,
-                                                      float2* __restrict__ z) {
+                                                      float2* __restrict__ z, int apply_post, float post) {
   const int L = G / 2, lo = (G - L) / 2;
   const long long G2 = static_cast<long long>(G) * G, total = J * G2;
   for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
@@ -121,6 +123,7 @@ __global__ void __launch_bounds__(kPre) k_deapod_mask(int J, int G, const float*
       const float2 x = z[t];
       v = make_float2(__fmul_rn(x.x, f[p]), __fmul_rn(x.y, f[p]));
     }
+    if (apply_post) v = make_float2(__fmul_rn(v.x, post), __fmul_rn(v.y, post));
     z[t] = v;
   }
 }
@@ -338,7 +341,7 @@ const Preproc::GridPlan& Preproc::grid_plan(const double* angles, int K, int S, 
 }
 
 void Preproc::grid_adjoint(const float2* samples, int J, const double* angles, int K, int S, double delay,
-                           float2* z_out, cudaStream_t s, bool spread_only) {
+                           float2* z_out, cudaStream_t s, bool spread_only, const float* post_scale) {
   if (J < 1 || K < 1 || S < 1) fail(2, "grid_adjoint: empty frame");
   const GridPlan& gp = grid_plan(angles, K, S, delay);
   const int G = plan_.G;
@@ -347,7 +350,8 @@ void Preproc::grid_adjoint(const float2* samples, int J, const double* angles, i
   check_cuda(cudaGetLastError(), "grid gather");
   if (spread_only) return;
   fft2_device(z_out, G, J, +1, s);  // fft::inverse per channel (preproc.cpp:193)
-  k_deapod_mask<<<grid_for(tot), kPre, 0, s>>>(J, G, deapod_, z_out);
+  k_deapod_mask<<<grid_for(tot), kPre, 0, s>>>(J, G, deapod_, z_out, post_scale ? 1 : 0,
+                                                post_scale ? *post_scale : 1.f);
   check_cuda(cudaGetLastError(), "deapodise");
   fft_book(fft_current_ctx(), static_cast<uint64_t>(J));
 }

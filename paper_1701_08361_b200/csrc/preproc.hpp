@@ -42,8 +42,9 @@ class Preproc {
   const Plan& plan() const { return plan_; }
 
   // device-side, stream ordered. samples: J x K x S complex64 (KSpaceFrame::samples)
+  // post_scale: the series normalisation applied in the deapodisation pass (nullptr: none)
   void grid_adjoint(const float2* samples, int J, const double* angles, int K, int S, double delay,
-                    float2* z_out, cudaStream_t s, bool spread_only = false);
+                    float2* z_out, cudaStream_t s, bool spread_only = false, const float* post_scale = nullptr);
   void build_psf(const double* angles, int K, int S, float2* P_out, cudaStream_t s);
   void build_psf_coords(const double* coords, const double* weights, int n, float2* P_out, cudaStream_t s);
   // out[jv][s] = sum_jp m[jv][jp] in[jp][s], FP64 accumulation (preproc.cpp:459-468)

@@ -105,13 +105,13 @@ void ProcGroup::read_state() { eng_->read_state(); }
 
 // ---- full-layout <-> member-layout copies -----------------------------------------------
 
-void ProcGroup::load_frame(const float2* z, const float2* P) {
+void ProcGroup::load_frame(const float2* z, const float2* P, bool masked) {
   Engine& e = *eng_;
   const size_t G2 = static_cast<size_t>(plan_.G) * plan_.G;
   const size_t j0 = static_cast<size_t>(block().first);
   check_cuda(cudaMemcpyAsync(e.z_, z + j0 * G2, sizeof(float2) * G2 * e.plan_.J, cudaMemcpyDefault, e.s_), "z");
   check_cuda(cudaMemcpyAsync(e.P_, P, sizeof(float2) * G2, cudaMemcpyDefault, e.s_), "psf");
-  e.enq_z_scan();
+  e.enq_z_scan(masked);
 }
 
 void ProcGroup::load_x(const float2* src) {

@@ -48,7 +48,7 @@ class ProcGroup : public FrameWorker {
   cudaStream_t stream() const override { return eng_->stream(); }
   int width() const override { return A_; }
   bool budget_mode() const override { return plan_.cg_iter_budget > 0; }
-  void load_frame(const float2* z, const float2* P) override;
+  void load_frame(const float2* z, const float2* P, bool masked = false) override;
   void load_x(const float2* src) override;
   void load_reg(const float2* src) override;
   void store_x(float2* dst) override;

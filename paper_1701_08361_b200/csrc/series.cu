@@ -234,7 +234,9 @@ void Series::run_frame(int t, int g, const SeriesOptions& o, SeriesFrameOut& out
   const size_t kr = static_cast<size_t>(g - run_first_);
   const float2* zl = kr < zsrc_.size() ? zsrc_[kr] : nullptr;
   const float2* pl = kr < psrc_.size() ? psrc_[kr] : nullptr;
-  e.load_frame(zl ? zl : z_ + zsz_ * g, pl ? pl : psf_ + psz_ * psf_idx_[static_cast<size_t>(g)]);
+  // frames the device pre stage gridded are window-masked by construction (mask_window,
+  // preproc.cpp:193-195): no outside-window scan
+  e.load_frame(zl ? zl : z_ + zsz_ * g, pl ? pl : psf_ + psz_ * psf_idx_[static_cast<size_t>(g)], raw_run_);
   e.load_x(init);
   cudaEvent_t ev0, ev1;
   check_cuda(cudaEventCreate(&ev0), "event");
@@ -500,7 +502,7 @@ void Series::produce_frames(const SeriesOptions& o, int first, int count, const 
                 &l->keys, l->nsq, l};
   };
   // frame k of the call: H2D, compression, gridding and its PSF on the view's stream
-  auto produce = [&](int k, const View& v) {
+  auto produce = [&](int k, const View& v, const float* post) {
     if (!raw) {
       check_cuda(cudaMemcpyAsync(v.z, z_host + 2 * zsz_ * k, sizeof(float2) * zsz_, cudaMemcpyHostToDevice, v.s),
                  "frame upload");
@@ -517,7 +519,7 @@ void Series::produce_frames(const SeriesOptions& o, int first, int count, const 
       smp = cs;
     }
     const double* ang = raw->angles + static_cast<size_t>(k) * raw->K;
-    v.pre->grid_adjoint(smp, p.J, ang, raw->K, raw->S, raw->delay, v.z, v.s);
+    v.pre->grid_adjoint(smp, p.J, ang, raw->K, raw->S, raw->delay, v.z, v.s, false, post);
     // PsfCache::get (preproc.cpp:315-332): one PSF per distinct angle set (per lane)
     const uint64_t key = psf_angle_key(ang, raw->K, raw->S, p.G);
     std::vector<uint64_t>& keys = *v.keys;
@@ -546,7 +548,11 @@ void Series::produce_frames(const SeriesOptions& o, int first, int count, const 
     const int g = first + k, sl = g % Sl_;
     const View v = view_of(k);
     check_cuda(cudaSetDevice(v.dev), "set device");
-    produce(k, v);
+    // a raw frame after its slice's first: the known normalisation is applied inside the
+    // gridding's deapodisation pass (the same float multiply, one pass over z fewer)
+    const float known = static_cast<float>(slice_scale_[static_cast<size_t>(sl)]);
+    const bool fold = raw && o.normalize && g >= Sl_ && slice_scale_[static_cast<size_t>(sl)] != 1.0;
+    produce(k, v, fold ? &known : nullptr);
     if (g < Sl_) {
       // frame 0 of slice sl arrived: it sets the slice's scale (pipeline.cpp:429-434)
       double sc = 1.0;
@@ -561,7 +567,7 @@ void Series::produce_frames(const SeriesOptions& o, int first, int count, const 
       if (sl == 0) scale_ = sc;
     }
     const double sc = slice_scale_[static_cast<size_t>(sl)];
-    if (o.normalize && sc != 1.0) {
+    if (o.normalize && sc != 1.0 && !fold) {
       k_scale_frames<<<148 * 2, 256, 0, v.s>>>(v.z, static_cast<long long>(zsz_), static_cast<float>(sc));
     }
     check_cuda(cudaEventCreateWithFlags(&ready[static_cast<size_t>(k)], cudaEventDisableTiming), "event");
@@ -604,6 +610,7 @@ void Series::run(const SeriesOptions& o, int first, int count, const float* z_ho
   std::vector<cudaEvent_t> ready;
   zsrc_.clear();
   psrc_.clear();
+  raw_run_ = raw != nullptr;
   if (z_host || raw) {
     produce_frames(o, first, count, z_host, raw, ready);
   } else if (o.normalize) {

@@ -150,6 +150,7 @@ class Series {
   std::vector<std::unique_ptr<PreLane>> lanes_;
   bool force_lanes_ = false;
   std::vector<const float2*> zsrc_, psrc_;  // per frame of the current run (nullptr: the store)
+  bool raw_run_ = false;  // the current run's frames came through the device pre stage
   std::vector<int> devices_;
   int F_ = 0, n_psf_ = 0, D_ = 0;
   size_t zsz_ = 0, psz_ = 0, isz_ = 0;
