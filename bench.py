@@ -871,8 +871,10 @@ def main():
                        "frames_in_flight": T, "channel_group": A,
                        "per_rank": "independent slice series (multi-slice acquisition), one per GPU"}
         line["multi_slice"] = multi_slice
-        if "error" in single:
+        if "error" in single:  # the headline falls back to the per-rank slice series
             line["single_series_error"] = single["error"]
+            line["scaling"] = "weak"
+            line["config"]["per_rank"] = "independent slice series (multi-slice)"
             line["decompositions"] = {"channel_processes": single.get("channel_processes")}
         else:
             Ts, As = single["T"], single["A"]
