@@ -1182,13 +1182,58 @@ __device__ inline bool cr_begin(DevState* st, const CrScalars& cr, int it, float
   }
   __shared__ double s_c[2];
   __shared__ int s_ok;
+  __shared__ double s_part[32][5];
+  // the state and scalars thread 0 decides with, loaded before the partials
+  int status = 0, halt = 0;
+  double rar_old = 0.0, rhs2 = 0.0;
+  if (threadIdx.x == 0) {
+    status = st->status;
+    halt = st->cr_halt;
+    rar_old = it > 0 ? cr.rar[it - 1] : 0.0;
+    rhs2 = tol > 0.0f ? st->steps[st->cur_step].rhs_nrm2 : 0.0;
+  }
+  {
+    // every thread of the block sums a stride of the partials (one round trip), the warps
+    // reduce, thread 0 adds the warp totals in warp order: the same totals in every block
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    {
+      double t[3] = {0.0, 0.0, 0.0};
+      for (int b = threadIdx.x; b < dr.nw; b += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) t[k] += __ldcg(dr.w + 3 * b + k);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double v = warp_sum(t[k]);
+        if (lane == 0) s_part[warp][k] = v;
+      }
+    }
+    {
+      double t[2] = {0.0, 0.0};
+      for (int b = threadIdx.x; b < dr.nc; b += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) t[k] += __ldcg(dr.c + 2 * b + k);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double v = warp_sum(t[k]);
+        if (lane == 0) s_part[warp][3 + k] = v;
+      }
+    }
+  }
+  __syncthreads();
   if (threadIdx.x < 32) {
     double wt[3] = {0.0, 0.0, 0.0}, ct[2] = {0.0, 0.0};
-    const int status = st->status, halt = st->cr_halt;
-    const double rar_old = it > 0 ? cr.rar[it - 1] : 0.0;
-    const double rhs2 = tol > 0.0f ? st->steps[st->cur_step].rhs_nrm2 : 0.0;
-    if (dr.nw) warp_totals<3>(dr.w, dr.nw, wt);
-    if (dr.nc) warp_totals<2>(dr.c, dr.nc, ct);
+    if (threadIdx.x == 0) {
+      const int nwarp = (blockDim.x + 31) >> 5;
+      for (int w = 0; w < nwarp; ++w) {
+        wt[0] += s_part[w][0];
+        wt[1] += s_part[w][1];
+        wt[2] += s_part[w][2];
+        ct[0] += s_part[w][3];
+        ct[1] += s_part[w][4];
+      }
+    }
     if (threadIdx.x == 0) {
       const bool rec = blockIdx.x == 0;
       int ok = !(status || halt);

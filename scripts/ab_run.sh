@@ -1,10 +1,10 @@
 #!/bin/bash
-# channel-chunked applications (RTN_CHUNKS): C5 and C3 throughput, parity at C5 chunked
-RTN_CHUNKS=2 timeout 900 python -m pytest tests/test_gpu_configs.py tests/test_gpu_ops.py -x -q -k "c5 or c3_bench or 384" > gpurun_out/ab25_tests.log 2>&1; echo "exit $?" >> gpurun_out/ab25_tests.log
-for round in 1 2; do
-  for ch in 1 2 4; do
-    RTN_CHUNKS=$ch timeout 120 python scripts/decomp_probe.py c5 2x1 1x1 | sed "s/^/chunks$ch c5 /"
-    RTN_CHUNKS=$ch timeout 120 python scripts/decomp_probe.py c3 3x1 | sed "s/^/chunks$ch c3 /"
-    RTN_CHUNKS=$ch timeout 120 python scripts/decomp_probe.py c2 3x1 | sed "s/^/chunks$ch c2 /"
+# block-wide deferred partial sums in cr_begin (bsum) vs warp-0 sums (base); parity of bsum
+timeout 900 python -m pytest tests/test_gpu_configs.py tests/test_gpu_ops.py tests/test_gpu_channel.py -x -q > gpurun_out/ab26_tests.log 2>&1; echo "exit $?" >> gpurun_out/ab26_tests.log
+for round in 1 2 3; do
+  for v in base bsum; do
+    RTN_LIB=build_var/lib_$v.so timeout 120 python scripts/decomp_probe.py c5 2x1 | sed "s/^/$v c5 /"
+    RTN_LIB=build_var/lib_$v.so timeout 120 python scripts/decomp_probe.py c3 3x1 | sed "s/^/$v c3 /"
+    RTN_LIB=build_var/lib_$v.so timeout 120 python scripts/decomp_probe.py c2 3x1 | sed "s/^/$v c2 /"
   done
-done > gpurun_out/ab25.txt 2>&1
+done > gpurun_out/ab26.txt 2>&1
