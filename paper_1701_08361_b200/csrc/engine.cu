@@ -763,8 +763,12 @@ void Engine::enq_image(const float2* est, float2* img, float scale, bool apply_s
 
 void Engine::enq_cr_fused(int it, float tol, const DeferRed& dr) {
   const int rho_skip = (dims_.grp && !dims_.count_rho) ? plan_.G * plan_.G : 0;
-  launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, static_cast<const float2*>(ar_),
-           partials_, st_, cr_, it, tol, rho_skip, dims_.grp, plan_.G, dr);
+  if (dims_.grp || dr.grp)
+    launch_k(k_cr_fused<true>, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, static_cast<const float2*>(ar_),
+             partials_, st_, cr_, it, tol, rho_skip, dims_.grp, plan_.G, dr);
+  else
+    launch_k(k_cr_fused<false>, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, static_cast<const float2*>(ar_),
+             partials_, st_, cr_, it, tol, rho_skip, 0, plan_.G, dr);
 }
 
 bool Engine::fused_crA() const { return fused_crA_ && fused_cr_ && ops_->crA != nullptr && !dims_.grp; }
@@ -1234,7 +1238,7 @@ double Engine::time_kernel(const char* which, int reps) {
       launch_k(k_cr_xr, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_, partials_, st_, cr_, 1, 0.f, 0, 0);
     } else if (w == "cr_fused") {
       // a step's last recurrence: the deferred partials in, its own grid reduction out
-      launch_k(k_cr_fused, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_,
+      launch_k(k_cr_fused<false>, vec_grid_, kThreads, 0, s_, D_, xcg_, r_, p_, ap_,
                static_cast<const float2*>(ar_), partials_, st_, cr_, 1, 0.f, 0, 0, plan_.G, dr);
     } else if (w == "crA") {
       DeferRed d2 = dr;

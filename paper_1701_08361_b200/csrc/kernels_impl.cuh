@@ -154,22 +154,6 @@ __device__ void block_partial(double (&v)[K], double* out) {
   }
 }
 
-// the consumer half, one warp: lane l sums blocks l, l + 32, ... in order, then the
-// warp tree; every lane gets the totals. Identical in every block of the consumer.
-template <int K>
-__device__ __forceinline__ void warp_totals(const double* part, int nb, double (&tot)[K]) {
-  const int lane = threadIdx.x & 31;
-  double s[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) s[k] = 0.0;
-  for (int b = lane; b < nb; b += 32) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) s[k] += __ldcg(part + b * K + k);
-  }
-#pragma unroll
-  for (int k = 0; k < K; ++k) tot[k] = __shfl_sync(0xffffffffu, warp_sum(s[k]), 0);
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------------
@@ -1088,25 +1072,42 @@ __device__ __forceinline__ double grp_sum(const GroupScal& g, const double* cons
 // checks, the totals of the deferred reductions (DeferRed) -- the previous iteration's
 // tail (|ap|^2 for the denominator, |r|, the iteration count and the tolerance stop,
 // as cr_fused_tail) and this iteration's dots -- then the step coefficients (cr_coef).
-// Warp 0 loads and sums the partials, thread 0 decides (block 0 records), the block
+// The block loads and sums the partials, thread 0 decides (block 0 records), the block
 // reads the decision from shared memory. Returns false when the iteration must not run.
+// kGrp: the channel-group branch is compiled in (k_crA never runs on a group member).
+template <bool kGrp = true>
 __device__ inline bool cr_begin(DevState* st, const CrScalars& cr, int it, float tol, const DeferRed& dr, CrCoef& c) {
-  if (dr.grp) {
+  if (kGrp && dr.grp) {
     // channel group: k_grp_fin's member-order totals and decisions (the previous
     // iteration's tail, this application's dots), then the step coefficients; every block
     // of every member sums the same member partials in the same order
     __shared__ double g_c[2];
     __shared__ int g_ok;
-    double wt[3] = {0.0, 0.0, 0.0};
-    if (dr.grp == 2 && threadIdx.x < 32) {
-      // every member's per-block dot partials: each member's blocks in order (warp_totals),
-      // then the members in order
+    __shared__ double g_part[32][3];
+    __shared__ double g_tot[3];
+    if (dr.grp == 2) {
+      // every member's per-block dot partials: each member's blocks summed by the whole
+      // block (a stride per thread, the warp trees, thread 0 the warps in order), then
+      // the members in order
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
       for (int m = 0; m < dr.gs.A; ++m) {
-        double t[3];
-        warp_totals<3>(dr.gw[m], dr.gnw[m], t);
-        wt[0] += t[0];
-        wt[1] += t[1];
-        wt[2] += t[2];
+        double t[3] = {0.0, 0.0, 0.0};
+        for (int b = threadIdx.x; b < dr.gnw[m]; b += blockDim.x) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) t[k] += __ldcg(dr.gw[m] + 3 * b + k);
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double v = warp_sum(t[k]);
+          if (lane == 0) g_part[warp][k] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < 3) {
+          double u = 0.0;
+          for (int w = 0; w < (int)((blockDim.x + 31) >> 5); ++w) u += g_part[w][threadIdx.x];
+          g_tot[threadIdx.x] = m ? g_tot[threadIdx.x] + u : u;
+        }
+        __syncthreads();
       }
     }
     if (threadIdx.x == 0) {
@@ -1138,9 +1139,9 @@ __device__ inline bool cr_begin(DevState* st, const CrScalars& cr, int it, float
       }
       double a = 0.0, b = 0.0;
       if (ok) {
-        const double rar = dr.grp == 2 ? wt[0] : grp_sum(dr.gs, dr.gs.pcw, 3 * it + 0);
-        const double saa = dr.grp == 2 ? wt[1] : grp_sum(dr.gs, dr.gs.pcw, 3 * it + 1);
-        const double spa = dr.grp == 2 ? wt[2] : grp_sum(dr.gs, dr.gs.pcw, 3 * it + 2);
+        const double rar = dr.grp == 2 ? g_tot[0] : grp_sum(dr.gs, dr.gs.pcw, 3 * it + 0);
+        const double saa = dr.grp == 2 ? g_tot[1] : grp_sum(dr.gs, dr.gs.pcw, 3 * it + 1);
+        const double spa = dr.grp == 2 ? g_tot[2] : grp_sum(dr.gs, dr.gs.pcw, 3 * it + 2);
         if (rec) {
           cr.rar[it] = rar;
           cr.saa[it] = saa;
@@ -1390,7 +1391,7 @@ __global__ void RTNB_BOUNDS_N(RTNB_MINB_CRA) k_crA(Dims d, float2* __restrict__ 
     }
   }
   CrCoef c;
-  if (!cr_begin(st, cr, it, tol, dr, c)) return;
+  if (!cr_begin<false>(st, cr, it, tol, dr, c)) return;
   const float bf = (float)c.b, af = (float)c.a, naf = (float)(-c.a);
   double acc_ap = 0.0, acc_r = 0.0;
   if (colblk) {
@@ -1638,7 +1639,9 @@ __global__ void __launch_bounds__(kThreads) k_cr_pap(int D, float2* __restrict__
 //   |ap|^2 = b^2 |ap_prev|^2 + 2b Re<ap_prev, ar> + |ar|^2  from the exact norm of the
 //     previous ap and the application's dots (exact for it = 0);
 //   a = rar[it]/|ap|^2; x += a p; r -= a ap; rn[it+1] = |r|  (nlinv.cpp:205-220)
-// The exact |ap|^2 of this pass is reduced for the next iteration.
+// The exact |ap|^2 of this pass is reduced for the next iteration. kGrp: the channel-group
+// branches are compiled in (a single engine launches k_cr_fused<false>).
+template <bool kGrp>
 __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict__ x, float2* __restrict__ r,
                                                        float2* __restrict__ p, float2* __restrict__ ap,
                                                        const float2* __restrict__ ar, double* partials,
@@ -1646,7 +1649,7 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
                                                        int rho_skip, int grp, int G, DeferRed dr) {
   pdl_enter();
   CrCoef c;
-  if (!cr_begin(st, cr, it, tol, dr, c)) return;
+  if (!cr_begin<kGrp>(st, cr, it, tol, dr, c)) return;
   const float bf = (float)c.b, af = (float)c.a, naf = (float)(-c.a);
   double acc_ap = 0.0, acc_r = 0.0;
   // rho entries outside the window are exactly zero in every vector: skip them
@@ -1698,7 +1701,7 @@ __global__ void __launch_bounds__(kThreads) k_cr_fused(int D, float2* __restrict
     return;
   }
   if (grid_reduce<2>(v, partials, &st->counter, tot) && threadIdx.x == 0) {
-    if (grp) {
+    if (kGrp && grp) {
       cr.pcr[2 * it + 0] = tot[0];
       cr.pcr[2 * it + 1] = tot[1];
       return;
