@@ -407,7 +407,8 @@ void Engine::alloc() {
   const int L2w = dims_.L * dims_.L;
   nbr_ = std::min(static_cast<int>((G2 + ops_->NT - 1) / ops_->NT),
                   env_int("RTN_RHO_BLOCKS", std::clamp(L2w / 512, 16, 148)));
-  const int max_grid = std::max({vec_grid_, plan_.J * ((plan_.G + ops_->LPB - 1) / ops_->LPB) + nbr_ + 8, 4 * 148});
+  // (8 x 148: the largest k_rho_sum grid RTN_RHO_SUM_BLOCKS may ask for)
+  const int max_grid = std::max({vec_grid_, plan_.J * ((plan_.G + ops_->LPB - 1) / ops_->LPB) + nbr_ + 8, 8 * 148});
   // grid_reduce<K> writes K doubles per block; K <= kMaxReduce
   check_cuda(cudaMalloc(&partials_, sizeof(double) * kMaxReduce * max_grid), "partials");
   if (ops_->colsT_box_rows > 0) encode_psf_map(&tmP_, P_, plan_.G, ops_->LPB, ops_->colsT_box_rows);
@@ -431,7 +432,7 @@ void Engine::alloc() {
     check_cuda(cudaMalloc(&kpart_, sizeof(double) * 3 * plan_.J * ops_->cluster_ctas), "cluster partials");
     // 32 window entries (x J channel terms) per block
     rho_grid_ = std::max(1, std::min(static_cast<int>((L * L + kRhoTile - 1) / kRhoTile), 4 * 148));
-    if (const char* e = std::getenv("RTN_RHO_SUM_BLOCKS")) rho_grid_ = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("RTN_RHO_SUM_BLOCKS")) rho_grid_ = std::clamp(std::atoi(e), 1, 8 * 148);
   }
   // alpha schedule and budget split are data independent (nlinv.cpp:295-313)
   float alpha = plan_.alpha0;
